@@ -1,0 +1,144 @@
+/*
+ * topo_b200.h — C ABI of the B200-native FE-evaluation hot path of the
+ * reference `romtopt` package (arXiv 2004.05756), built for sm_100a.
+ *
+ * Plain C: opaque handles, plain pointers and sizes, `int` status codes, a
+ * thread-local message from tb_last_error().  No torch types.  All array
+ * arguments of compute calls are DEVICE pointers on the plan's device,
+ * caller-owned, fp64 unless stated; `stream` is a cudaStream_t passed as
+ * void* (0 = legacy default stream).  Plans are not safe for concurrent calls
+ * from several threads; distinct plans are independent.
+ *
+ * Layout (reference fem.py:154-229, extended to Hex8):
+ *   node id   n = (k*(ny+1) + j)*(nx+1) + i     (k = 0 in 2D)
+ *   element   e = (k*ny + j)*nx + i
+ *   dof       d*n + c  (interleaved components, d = 2 or 3)
+ *   element nodes: CCW from the bottom-left corner (2D, fem.py:225);
+ *                  3D: bottom face (z=k) CCW, then top face (z=k+1) CCW.
+ *
+ * Each entry point names the reference interface it replaces (file:line in
+ * /root/reference/pkg/src/romtopt).
+ */
+#ifndef TOPO_B200_H
+#define TOPO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define TB_OK 0
+#define TB_ERR_INVALID 1        /* bad argument  -> Python ValueError                      */
+#define TB_ERR_CUDA 2           /* CUDA runtime failure                                    */
+#define TB_ERR_INDEFINITE 3     /* pCG breakdown p^T K p <= 0 / non-finite -> IndefiniteMatrixError (fem.py:33-38) */
+#define TB_ERR_NOT_CONVERGED 4  /* maxit reached before rtol                               */
+#define TB_ERR_DEGENERATE 5     /* reduced stiffness not SPD -> DegenerateBasisError (rom.py:49-50) */
+#define TB_ERR_DENSITY 6        /* density outside [rho_l, 1] -> ValueError (hdm.py:156-162) */
+
+typedef struct tb_plan tb_plan;
+typedef struct tb_filter tb_filter;
+
+int tb_version(void);
+const char* tb_last_error(void);
+
+/* ---- plan: one structured mesh + unit element stiffness + SIMP law + Dirichlet set ----
+ * Replaces HdmSolver.__init__ (hdm.py:120-142) and PatternAssembler (fem.py:357-396):
+ * no matrix is assembled; the operator is applied matrix-free.
+ *   dim       2 (Q4) or 3 (Hex8); nz ignored for dim 2
+ *   k_e       HOST pointer, (8x8) or (24x24) row-major unit-density element stiffness
+ *   rho_l, p  MaterialModel (hdm.py:40-55)
+ *   fixed     HOST pointer, n_dofs bytes, nonzero = Dirichlet dof (hdm.py:139-141)      */
+int tb_plan_create(int dim, int nx, int ny, int nz, double h, const double* k_e,
+                   double rho_l, double p, const uint8_t* fixed, int device, tb_plan** out);
+int tb_plan_destroy(tb_plan* plan);
+int tb_plan_sizes(const tb_plan* plan, int64_t* n_elems, int64_t* n_nodes, int64_t* n_dofs);
+
+/* alpha(rho) and alpha'(rho) per element (hdm.py:40-55). */
+int tb_material(tb_plan* plan, const double* rho, double* alpha, double* dalpha, void* stream);
+
+/* Clamp a raw filtered density into [rho_l, 1] and return the largest adjustment
+ * (hdm.py:144-154); *clamp_width is a HOST pointer (synchronises the stream). */
+int tb_clamp_density(tb_plan* plan, const double* rho_raw, double* rho, double* clamp_width,
+                     void* stream);
+
+/* y = Z K(rho) v (fixed ROWS zeroed when mask_rows != 0): HdmSolver.apply_stiffness
+ * (hdm.py:224-233).  mask_rows = 0 gives the unmasked K(rho) v of rom.py:309-317. */
+int tb_apply_stiffness(tb_plan* plan, const double* rho, const double* v, double* y,
+                       int mask_rows, void* stream);
+
+/* s_e = drho_e - alpha'(rho_e) u_e^T K_e lam_e: HdmSolver.element_sensitivity
+ * (hdm.py:211-222).  drho may be NULL (compliance: dj/drho = 0, hdm.py:95-96). */
+int tb_element_sensitivity(tb_plan* plan, const double* rho, const double* u, const double* lam,
+                           const double* drho, double* s, void* stream);
+
+/* Jacobi-preconditioned CG on Z K(rho) Z x = Z b (replaces PatternAssembler.factorize +
+ * SpdFactorization.solve, fem.py:283-333, 406-409; fixed dofs of x stay 0).  Stops when the
+ * TRUE residual ||Z(b - K x)|| <= rtol ||Z b||.  x is output only (x0 = 0).
+ * *iters, *relres are HOST pointers (may be NULL).  Returns TB_ERR_INDEFINITE on breakdown,
+ * TB_ERR_NOT_CONVERGED at maxit (x holds the last iterate). */
+int tb_pcg_solve(tb_plan* plan, const double* rho, const double* b, double* x, double rtol,
+                 int maxit, int* iters, double* relres, void* stream);
+
+/* Diagnostics: time the two pCG kernels in situ.  Starts a solve of K(rho) x = b and runs
+ * nrep iterations with a CUDA event pair around every kernel on `stream`; returns the mean
+ * duration (ms) of the fused operator kernel and of the update kernel (HOST pointers). */
+int tb_pcg_profile(tb_plan* plan, const double* rho, const double* b, int nrep, double* ms_fused,
+                   double* ms_update, void* stream);
+/* Number of kernels this library has launched so far (graph-body kernels included). */
+int64_t tb_launch_count(void);
+
+/* Deterministic fp64 dot product of two device vectors; *out is a HOST pointer. */
+int tb_dot(tb_plan* plan, const double* a, const double* b, int64_t n, double* out, void* stream);
+
+/* ---- Helmholtz PDE density filter (filtering.py:47-114); HelmholtzFilter.__init__(mesh, R) ----
+ * radius R -> PDE length r = R/(2 sqrt 3) (filtering.py:29-32,59); pure Neumann;
+ * solved matrix-free by Jacobi-PCG to rtol (relative to the load vector norm). */
+int tb_filter_create(int dim, int nx, int ny, int nz, double h, double radius, int device,
+                     tb_filter** out);
+int tb_filter_destroy(tb_filter* filt);
+/* b(psi) = (h^d/2^d) sum_{e∋n} psi_e  (filtering.py:73-76) */
+int tb_filter_load_vector(tb_filter* filt, const double* psi, double* b, void* stream);
+/* phi = H^-1 b(psi); rho_e = mean of phi over the element nodes (filtering.py:78-97);
+ * phi may be NULL.  *iters HOST (may be NULL). */
+int tb_filter_apply(tb_filter* filt, const double* psi, double* phi, double* rho, double rtol,
+                    int* iters, void* stream);
+/* w = (h^d/2^d) Q^T H^-1 Q (v/2^d): exact transpose of psi->rho (filtering.py:99-114) */
+int tb_filter_adjoint(tb_filter* filt, const double* v, double* w, double rtol, int* iters,
+                      void* stream);
+
+/* ---- reduced-order model (rom.py:182-390); phi is (n_dofs x k) ROW-major ---- */
+/* out[k*d + j] = sum_i phi[i*k + j] * vec[d*n + i] for nvec <= 16 stacked vectors of length n
+ * (Phi^T f, rom.py:251, 289; also Q^T S of the POD) */
+int tb_rom_project(int64_t n, const double* phi, int k, const double* vec, int nvec, double* out,
+                   void* stream);
+/* khat[d] = Phi^T K(rho_d) Phi (k x k, row-major) for nd designs stacked in rho (nd x n_elems):
+ * RomModel.reduced_stiffness (rom.py:254-262), node-form contraction on FP64 tensor cores. */
+int tb_rom_reduced_stiffness(tb_plan* plan, const double* phi, int k, const double* rho, int nd,
+                             double* khat, void* stream);
+/* Batched Cholesky solve khat[d] X = rhs[d] (nrhs right-hand sides per design, row-major
+ * nd x nrhs x k) for rom.py:280-291.  status is a HOST int array of nd entries: 0 ok,
+ * 1 = not SPD (cho_factor LinAlgError -> DegenerateBasisError). */
+int tb_rom_cholesky_solve(int k, int nd, int nrhs, const double* khat, const double* rhs,
+                          double* x, int* status, void* stream);
+/* u[d] = Phi uhat[d] (length n) for nd <= 16 coefficient vectors (rom.py:285) */
+int tb_rom_reconstruct(int64_t n, const double* phi, int k, const double* uhat, int nd, double* u,
+                       void* stream);
+/* norms[d] = || Z (K(rho_d) Phi uhat_d - g_d) ||_2 (rom.py:309-335); g is (nd x n_dofs) or a
+ * single shared vector when g_stride == 0.  norms is a HOST array of nd doubles. */
+int tb_rom_residual_norms(tb_plan* plan, const double* phi, int k, const double* rho,
+                          const double* uhat, int nd, const double* g, int64_t g_stride,
+                          double* norms, void* stream);
+
+/* Modified Gram-Schmidt with one re-orthogonalisation pass and relative drop tolerance
+ * (rom.py:76-97).  vectors: m COLUMN vectors of length n (column-major n x m, device);
+ * q: output (n x kept) ROW-major, compact (buffer of n*m doubles). *kept HOST.
+ * Returns TB_ERR_INVALID when no vector survives ("no independent vectors supplied"). */
+int tb_gram_schmidt(int64_t n, int m, const double* vectors, double drop_tol, double* q,
+                    int* kept, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOPO_B200_H */

@@ -1,0 +1,423 @@
+// libtopo_b200: plan, SIMP elasticity operator, Helmholtz filter, HDM entry points.
+#include <stdarg.h>
+#include <string.h>
+
+#include <atomic>
+#include <string>
+
+#include "pcg.cuh"
+#include "plan.cuh"
+#include "q1.cuh"
+
+namespace tb {
+
+static thread_local char g_err[1024] = "";
+static std::atomic<int64_t> g_launches{0};
+
+void launched(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+// ---------------------------------------------------------------------------------------
+// elementwise kernels
+// ---------------------------------------------------------------------------------------
+// alpha = rho_l + (1-rho_l) rho^p ; alpha' = (1-rho_l) p rho^(p-1)   (hdm.py:40-55)
+__global__ void k_material(int64_t n, double rho_l, double p, const double* __restrict__ rho,
+                           double* __restrict__ alpha, double* __restrict__ dalpha) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const double r = rho[e];
+    if (alpha) alpha[e] = rho_l + (1.0 - rho_l) * pow(r, p);
+    if (dalpha) dalpha[e] = (1.0 - rho_l) * p * pow(r, p - 1.0);
+  }
+}
+
+// rho = clip(raw, rho_l, 1); block maxima of |rho - raw| (hdm.py:152-153)
+__global__ void k_clamp(int64_t n, double lo, const double* __restrict__ raw, double* __restrict__ rho,
+                        double* __restrict__ part) {
+  double m = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const double r = raw[e];
+    const double c = fmin(fmax(r, lo), 1.0);
+    rho[e] = c;
+    m = fmax(m, fabs(c - r));
+  }
+  m = warp_max(m);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+    v = warp_max(v);
+    if (threadIdx.x == 0) part[blockIdx.x] = v;
+  }
+}
+
+// block partial sums of a.b
+__global__ void k_dot_part(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                           double* __restrict__ part) {
+  double acc[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc[0] = fma(a[i], b[i], acc[0]);
+  block_sum<1>(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+}
+
+// fixed-order final sum (one block) of nb partials, with optional max instead of sum
+__global__ void k_finish(int nb, const double* __restrict__ part, double* __restrict__ out, int take_max) {
+  double acc[1] = {0.0};
+  if (take_max) {
+    double m = 0.0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) m = fmax(m, part[b]);
+    m = warp_max(m);
+    __shared__ double red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double v = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+      v = warp_max(v);
+      if (threadIdx.x == 0) *out = v;
+    }
+    return;
+  }
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) acc[0] += part[b];
+  block_sum<1>(acc);
+  if (threadIdx.x == 0) *out = acc[0];
+}
+
+void finish_sum(int nb, const double* part, double* out, cudaStream_t s) {
+  { k_finish<<<1, kBlock, 0, s>>>(nb, part, out, 0); tb::launched(); }
+}
+
+int device_dot(const double* a, const double* b, int64_t n, double* scratch, double* out_dev, cudaStream_t s) {
+  const int nb = grid_for(n);
+  { k_dot_part<<<nb, kBlock, 0, s>>>(n, a, b, scratch); tb::launched(); }
+  { k_finish<<<1, kBlock, 0, s>>>(nb, scratch, out_dev, 0); tb::launched(); }
+  TB_CHECK_LAUNCH();
+  return TB_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// operators
+// ---------------------------------------------------------------------------------------
+static inline int nblk(int64_t n) { return (int)((n + kBlock - 1) / kBlock); }
+
+void ElastOp::launch_fused(const PcgWork& w, const double* pold, double* pnew, cudaStream_t s) const {
+  const Grid& g = plan->g;
+  if (g.dim == 2)
+    k_pcg_fused<2, 2, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, plan->K2, plan->d_alpha, w.z, pold, pnew, w.q,
+                                                                w.st, w.partA());
+  else
+    k_pcg_fused<3, 3, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, plan->K3, plan->d_alpha, w.z, pold, pnew, w.q,
+                                                                w.st, w.partA());
+}
+void ElastOp::launch_apply(const double* v, double* y, cudaStream_t s) const {
+  plan->apply_alpha(plan->d_alpha, v, y, true, s);
+}
+void ElastOp::launch_dinv(double* dinv, cudaStream_t s) const {
+  const Grid& g = plan->g;
+  if (g.dim == 2)
+    { k_node_dinv<2, 2, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, plan->K2, plan->d_alpha, plan->d_fixed, dinv); tb::launched(); }
+  else
+    { k_node_dinv<3, 3, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, plan->K3, plan->d_alpha, plan->d_fixed, dinv); tb::launched(); }
+}
+int ElastOp::fused_blocks() const { return nblk(plan->g.n_nodes); }
+
+void HelmOp::launch_fused(const PcgWork& w, const double* pold, double* pnew, cudaStream_t s) const {
+  const Grid& g = filt->g;
+  if (g.dim == 2)
+    k_pcg_fused<2, 1, false><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, filt->H2, nullptr, w.z, pold, pnew, w.q, w.st,
+                                                                 w.partA());
+  else
+    k_pcg_fused<3, 1, false><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, filt->H3, nullptr, w.z, pold, pnew, w.q, w.st,
+                                                                 w.partA());
+}
+void HelmOp::launch_apply(const double* v, double* y, cudaStream_t s) const {
+  const Grid& g = filt->g;
+  if (g.dim == 2)
+    { k_node_apply<2, 1, false><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, filt->H2, nullptr, v, y, nullptr); tb::launched(); }
+  else
+    { k_node_apply<3, 1, false><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, filt->H3, nullptr, v, y, nullptr); tb::launched(); }
+}
+void HelmOp::launch_dinv(double* dinv, cudaStream_t s) const {
+  const Grid& g = filt->g;
+  if (g.dim == 2)
+    { k_node_dinv<2, 1, false><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, filt->H2, nullptr, nullptr, dinv); tb::launched(); }
+  else
+    { k_node_dinv<3, 1, false><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, filt->H3, nullptr, nullptr, dinv); tb::launched(); }
+}
+int HelmOp::fused_blocks() const { return nblk(filt->g.n_nodes); }
+
+void tb_plan_impl::apply_alpha(const double* alpha, const double* v, double* y, bool mask, cudaStream_t s) const {
+  const uint8_t* fx = mask ? d_fixed : nullptr;
+  if (g.dim == 2)
+    { k_node_apply<2, 2, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, K2, alpha, v, y, fx); tb::launched(); }
+  else
+    { k_node_apply<3, 3, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, K3, alpha, v, y, fx); tb::launched(); }
+}
+
+int tb_plan_impl::material(const double* rho, double* alpha, double* dalpha, cudaStream_t s) const {
+  { k_material<<<grid_for(g.n_elems), kBlock, 0, s>>>(g.n_elems, rho_l, p, rho, alpha, dalpha); tb::launched(); }
+  TB_CHECK_LAUNCH();
+  return TB_OK;
+}
+
+}  // namespace tb
+
+using namespace tb;
+
+// =========================================================================================
+// C ABI
+// =========================================================================================
+extern "C" {
+
+int tb_version(void) { return 100; }
+const char* tb_last_error(void) { return g_err; }
+
+#define TB_GUARD(cond, ...)        \
+  do {                             \
+    if (!(cond)) {                 \
+      set_error(__VA_ARGS__);      \
+      return TB_ERR_INVALID;       \
+    }                              \
+  } while (0)
+
+int tb_plan_create(int dim, int nx, int ny, int nz, double h, const double* k_e, double rho_l, double p,
+                   const uint8_t* fixed, int device, tb_plan** out) {
+  TB_GUARD(out != nullptr && k_e != nullptr && fixed != nullptr, "null argument");
+  TB_GUARD(dim == 2 || dim == 3, "dim must be 2 or 3, got %d", dim);
+  TB_GUARD(nx >= 1 && ny >= 1 && (dim == 2 || nz >= 1), "element counts must be >= 1");
+  TB_GUARD(h > 0.0, "element size must be positive, got %g", h);
+  TB_GUARD(rho_l > 0.0 && rho_l < 1.0 && p >= 1.0, "material parameters out of range");
+  TB_CUDA(cudaSetDevice(device));
+  auto* P = new tb_plan_impl();
+  P->g = make_grid(dim, nx, ny, nz, h);
+  const Grid& g = P->g;
+  P->n_dofs = (int64_t)dim * g.n_nodes;
+  P->device = device;
+  P->rho_l = rho_l;
+  P->p = p;
+  const int ne = (dim == 2) ? 8 : 24;
+  if (dim == 2)
+    memcpy(P->K2.v, k_e, sizeof(double) * ne * ne);
+  else
+    memcpy(P->K3.v, k_e, sizeof(double) * ne * ne);
+  P->op.plan = P;
+  int rc = P->init(fixed);
+  if (rc != TB_OK) {
+    P->release();
+    delete P;
+    return rc;
+  }
+  *out = reinterpret_cast<tb_plan*>(P);
+  return TB_OK;
+}
+
+int tb_plan_destroy(tb_plan* plan) {
+  if (!plan) return TB_OK;
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  cudaSetDevice(P->device);
+  P->release();
+  delete P;
+  return TB_OK;
+}
+
+int tb_plan_sizes(const tb_plan* plan, int64_t* n_elems, int64_t* n_nodes, int64_t* n_dofs) {
+  TB_GUARD(plan != nullptr, "null plan");
+  auto* P = reinterpret_cast<const tb_plan_impl*>(plan);
+  if (n_elems) *n_elems = P->g.n_elems;
+  if (n_nodes) *n_nodes = P->g.n_nodes;
+  if (n_dofs) *n_dofs = P->n_dofs;
+  return TB_OK;
+}
+
+int tb_material(tb_plan* plan, const double* rho, double* alpha, double* dalpha, void* stream) {
+  TB_GUARD(plan && rho, "null argument");
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  return P->material(rho, alpha, dalpha, (cudaStream_t)stream);
+}
+
+int tb_clamp_density(tb_plan* plan, const double* rho_raw, double* rho, double* clamp_width, void* stream) {
+  TB_GUARD(plan && rho_raw && rho, "null argument");
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nb = grid_for(P->g.n_elems);
+  { k_clamp<<<nb, kBlock, 0, s>>>(P->g.n_elems, P->rho_l, rho_raw, rho, P->d_scratch); tb::launched(); }
+  { k_finish<<<1, kBlock, 0, s>>>(nb, P->d_scratch, P->d_scalar, 1); tb::launched(); }
+  TB_CHECK_LAUNCH();
+  if (clamp_width) {
+    TB_CUDA(cudaMemcpyAsync(P->h_scalar, P->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
+    TB_CUDA(cudaStreamSynchronize(s));
+    *clamp_width = *P->h_scalar;
+  }
+  return TB_OK;
+}
+
+int tb_apply_stiffness(tb_plan* plan, const double* rho, const double* v, double* y, int mask_rows, void* stream) {
+  TB_GUARD(plan && rho && v && y, "null argument");
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  cudaStream_t s = (cudaStream_t)stream;
+  TB_TRY(P->material(rho, P->d_alpha2, nullptr, s));
+  P->apply_alpha(P->d_alpha2, v, y, mask_rows != 0, s);
+  TB_CHECK_LAUNCH();
+  return TB_OK;
+}
+
+int tb_element_sensitivity(tb_plan* plan, const double* rho, const double* u, const double* lam, const double* drho,
+                           double* s_out, void* stream) {
+  TB_GUARD(plan && rho && u && lam && s_out, "null argument");
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  cudaStream_t s = (cudaStream_t)stream;
+  const Grid& g = P->g;
+  if (g.dim == 2)
+    { k_elem_sensitivity<2><<<nblk(g.n_elems), kBlock, 0, s>>>(g, P->K2, P->rho_l, P->p, rho, u, lam, drho, s_out); tb::launched(); }
+  else
+    { k_elem_sensitivity<3><<<nblk(g.n_elems), kBlock, 0, s>>>(g, P->K3, P->rho_l, P->p, rho, u, lam, drho, s_out); tb::launched(); }
+  TB_CHECK_LAUNCH();
+  return TB_OK;
+}
+
+int tb_pcg_solve(tb_plan* plan, const double* rho, const double* b, double* x, double rtol, int maxit, int* iters,
+                 double* relres, void* stream) {
+  TB_GUARD(plan && rho && b && x, "null argument");
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  cudaStream_t s = (cudaStream_t)stream;
+  TB_TRY(P->material(rho, P->d_alpha, nullptr, s));
+  return pcg_solve(P->op, P->work, b, x, rtol, maxit, iters, relres, s);
+}
+
+int tb_pcg_profile(tb_plan* plan, const double* rho, const double* b, int nrep, double* ms_fused, double* ms_update,
+                   void* stream) {
+  TB_GUARD(plan && rho && b && ms_fused && ms_update && nrep >= 1, "bad arguments");
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  cudaStream_t s = (cudaStream_t)stream;
+  TB_TRY(P->material(rho, P->d_alpha, nullptr, s));
+  return pcg_profile(P->op, P->work, b, nrep, ms_fused, ms_update, s);
+}
+
+int64_t tb_launch_count(void) { return g_launches.load(); }
+
+int tb_dot(tb_plan* plan, const double* a, const double* b, int64_t n, double* out, void* stream) {
+  TB_GUARD(plan && a && b && out, "null argument");
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  cudaStream_t s = (cudaStream_t)stream;
+  TB_TRY(device_dot(a, b, n, P->d_scratch, P->d_scalar, s));
+  TB_CUDA(cudaMemcpyAsync(P->h_scalar, P->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, s));
+  TB_CUDA(cudaStreamSynchronize(s));
+  *out = *P->h_scalar;
+  return TB_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// Helmholtz filter
+// ---------------------------------------------------------------------------------------
+int tb_filter_create(int dim, int nx, int ny, int nz, double h, double radius, int device, tb_filter** out) {
+  TB_GUARD(out != nullptr, "null argument");
+  TB_GUARD(dim == 2 || dim == 3, "dim must be 2 or 3, got %d", dim);
+  TB_GUARD(nx >= 1 && ny >= 1 && (dim == 2 || nz >= 1), "element counts must be >= 1");
+  TB_GUARD(h > 0.0, "element size must be positive, got %g", h);
+  TB_GUARD(radius >= 0.0, "filter radius must be nonnegative, got %g", radius);
+  TB_CUDA(cudaSetDevice(device));
+  auto* F = new tb_filter_impl();
+  F->g = make_grid(dim, nx, ny, nz, h);
+  F->device = device;
+  F->radius = radius;
+  F->r = (1.0 / (2.0 * sqrt(3.0))) * radius;  // LENGTH_SCALE_FACTOR * R (filtering.py:29-32,59)
+  const Grid& g = F->g;
+  const int nn = (g.dim == 2) ? 4 : 8;
+  double S[64], M[64], s_div, m_mul;
+  scalar_element_matrices(g.dim, g.h, S, M, &s_div, &m_mul);
+  // H_e = r^2 S_e + M_e in the reference's operation order (fem.py:135)
+  const double r2 = (g.dim == 2) ? F->r * F->r : F->r * F->r * g.h;
+  for (int i = 0; i < nn * nn; ++i) {
+    const double hv = r2 * S[i] / s_div + m_mul * M[i];
+    if (g.dim == 2)
+      F->H2.v[i] = hv;
+    else
+      F->H3.v[i] = hv;
+  }
+  F->vol_share = pow(g.h, g.dim) / nn;  // b_e entries = h^d / 2^d (filtering.py:75-76)
+  F->op.filt = F;
+  int rc = F->work.alloc(g.n_nodes, F->op.fused_blocks());
+  if (rc == TB_OK) {
+    cudaError_t e = cudaMalloc(&F->d_b, sizeof(double) * g.n_nodes);
+    if (e != cudaSuccess) {
+      set_error("cudaMalloc: %s", cudaGetErrorString(e));
+      rc = TB_ERR_CUDA;
+    }
+  }
+  if (rc != TB_OK) {
+    F->work.release();
+    delete F;
+    return rc;
+  }
+  *out = reinterpret_cast<tb_filter*>(F);
+  return TB_OK;
+}
+
+int tb_filter_destroy(tb_filter* filt) {
+  if (!filt) return TB_OK;
+  auto* F = reinterpret_cast<tb_filter_impl*>(filt);
+  cudaSetDevice(F->device);
+  F->work.release();
+  if (F->d_b) cudaFree(F->d_b);
+  delete F;
+  return TB_OK;
+}
+
+int tb_filter_load_vector(tb_filter* filt, const double* psi, double* b, void* stream) {
+  TB_GUARD(filt && psi && b, "null argument");
+  auto* F = reinterpret_cast<tb_filter_impl*>(filt);
+  const Grid& g = F->g;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (g.dim == 2)
+    { k_elem_to_node<2><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, psi, F->vol_share, 1.0, b); tb::launched(); }
+  else
+    { k_elem_to_node<3><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, psi, F->vol_share, 1.0, b); tb::launched(); }
+  TB_CHECK_LAUNCH();
+  return TB_OK;
+}
+
+int tb_filter_apply(tb_filter* filt, const double* psi, double* phi, double* rho, double rtol, int* iters,
+                    void* stream) {
+  TB_GUARD(filt && psi && rho, "null argument");
+  auto* F = reinterpret_cast<tb_filter_impl*>(filt);
+  const Grid& g = F->g;
+  cudaStream_t s = (cudaStream_t)stream;
+  TB_TRY(tb_filter_load_vector(filt, psi, F->d_b, stream));
+  TB_TRY(pcg_solve(F->op, F->work, F->d_b, F->work.x, rtol, 10000, iters, nullptr, s));
+  const double inv_nn = (g.dim == 2) ? 0.25 : 0.125;
+  if (g.dim == 2)
+    { k_node_to_elem<2><<<nblk(g.n_elems), kBlock, 0, s>>>(g, F->work.x, inv_nn, rho); tb::launched(); }
+  else
+    { k_node_to_elem<3><<<nblk(g.n_elems), kBlock, 0, s>>>(g, F->work.x, inv_nn, rho); tb::launched(); }
+  TB_CHECK_LAUNCH();
+  if (phi) TB_CUDA(cudaMemcpyAsync(phi, F->work.x, sizeof(double) * g.n_nodes, cudaMemcpyDeviceToDevice, s));
+  return TB_OK;
+}
+
+int tb_filter_adjoint(tb_filter* filt, const double* v, double* w, double rtol, int* iters, void* stream) {
+  TB_GUARD(filt && v && w, "null argument");
+  auto* F = reinterpret_cast<tb_filter_impl*>(filt);
+  const Grid& g = F->g;
+  cudaStream_t s = (cudaStream_t)stream;
+  const double inv_nn = (g.dim == 2) ? 0.25 : 0.125;
+  if (g.dim == 2)
+    { k_elem_to_node<2><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, v, inv_nn, 1.0, F->d_b); tb::launched(); }
+  else
+    { k_elem_to_node<3><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, v, inv_nn, 1.0, F->d_b); tb::launched(); }
+  TB_CHECK_LAUNCH();
+  TB_TRY(pcg_solve(F->op, F->work, F->d_b, F->work.x, rtol, 10000, iters, nullptr, s));
+  if (g.dim == 2)
+    { k_node_to_elem<2><<<nblk(g.n_elems), kBlock, 0, s>>>(g, F->work.x, F->vol_share, w); tb::launched(); }
+  else
+    { k_node_to_elem<3><<<nblk(g.n_elems), kBlock, 0, s>>>(g, F->work.x, F->vol_share, w); tb::launched(); }
+  TB_CHECK_LAUNCH();
+  return TB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,234 @@
+// pCG engine implementation (see pcg.cuh).
+#include "pcg.cuh"
+
+namespace tb {
+
+int PcgWork::alloc(int64_t n_, int max_blocks) {
+  n = n_;
+  part_stride = max_blocks > kUpdateBlocks ? max_blocks : kUpdateBlocks;
+  const size_t vb = sizeof(double) * (size_t)n;
+  double** vecs[] = {&x, &r, &z, &pa, &pb, &q, &dinv, &tmp};
+  for (double** p : vecs) TB_CUDA(cudaMalloc(p, vb));
+  TB_CUDA(cudaMalloc(&part, sizeof(double) * 6 * (size_t)part_stride));
+  TB_CUDA(cudaMalloc(&st, sizeof(PcgState)));
+  TB_CUDA(cudaMemset(st, 0, sizeof(PcgState)));
+  TB_CUDA(cudaMallocHost(&h_st, sizeof(PcgState)));
+  return TB_OK;
+}
+
+void PcgWork::release() {
+  double* vecs[] = {x, r, z, pa, pb, q, dinv, tmp, part};
+  for (double* p : vecs)
+    if (p) cudaFree(p);
+  if (st) cudaFree(st);
+  if (h_st) cudaFreeHost(h_st);
+  if (exec) cudaGraphExecDestroy(exec);
+  *this = PcgWork();
+}
+
+// Kernel B: x += alpha p ; r -= alpha q ; z = D^-1 r on free dofs (dinv != 0); rz, rr.
+__global__ void __launch_bounds__(kBlock) k_pcg_update(int64_t n, const double* __restrict__ p,
+                                                       const double* __restrict__ q, const double* __restrict__ dinv,
+                                                       double* __restrict__ x, double* __restrict__ r,
+                                                       double* __restrict__ z, PcgState* st, double* partials) {
+  if (st->done) return;
+  const double a = st->alpha;
+  double acc[2] = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double di = dinv[i];
+    if (di != 0.0) {
+      x[i] = fma(a, p[i], x[i]);
+      const double ri = fma(-a, q[i], r[i]);
+      const double zi = di * ri;
+      r[i] = ri;
+      z[i] = zi;
+      acc[0] = fma(ri, zi, acc[0]);
+      acc[1] = fma(ri, ri, acc[1]);
+    }
+  }
+  block_sum<2>(acc);
+  if (publish_partials<2>(acc, partials, &st->count_b)) {
+    gather_partials<2>(acc, partials, &st->count_b);
+    if (threadIdx.x == 0) {
+      const int it = st->iters + 1;
+      st->iters = it;
+      st->beta = acc[0] / st->rz;
+      st->rz = acc[0];
+      st->rr = acc[1];
+      if (!isfinite(acc[0]) || !isfinite(acc[1])) st->done = 3;
+      else if (acc[1] <= st->tol2) st->done = 1;
+      else if (it >= st->maxit) st->done = 2;
+    }
+  }
+}
+
+// (Re)start: r = Z(b - Kx) (Kx = tmp, or x = 0 when tmp == nullptr), z = D^-1 r, p_old = 0,
+// rz, rr; on init also sets tol2 from ||Z b||.
+__global__ void __launch_bounds__(kBlock) k_pcg_start(int64_t n, const double* __restrict__ b,
+                                                      const double* __restrict__ kx, const double* __restrict__ dinv,
+                                                      double* __restrict__ x, double* __restrict__ r,
+                                                      double* __restrict__ z, double* __restrict__ pa,
+                                                      PcgState* st, double* partials, int init, double rtol,
+                                                      int maxit) {
+  double acc[2] = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double di = dinv[i];
+    double ri = 0.0;
+    if (di != 0.0) ri = (kx != nullptr) ? b[i] - kx[i] : b[i];
+    if (init) x[i] = 0.0;
+    const double zi = di * ri;
+    r[i] = ri;
+    z[i] = zi;
+    pa[i] = 0.0;
+    acc[0] = fma(ri, zi, acc[0]);
+    acc[1] = fma(ri, ri, acc[1]);
+  }
+  block_sum<2>(acc);
+  if (publish_partials<2>(acc, partials, &st->count_c)) {
+    gather_partials<2>(acc, partials, &st->count_c);
+    if (threadIdx.x == 0 && !(init == 0 && st->done == 3)) {  // a breakdown stays reported
+      if (init) {
+        st->tol2 = rtol * rtol * acc[1];
+        st->iters = 0;
+        st->maxit = maxit;
+        st->bb = acc[1];
+      }
+      st->rz = acc[0];
+      st->rr = acc[1];
+      st->beta = 0.0;
+      st->alpha = 0.0;
+      const bool conv = init ? (acc[1] == 0.0) : (acc[1] <= st->tol2);
+      st->done = conv ? 1 : (!isfinite(acc[1]) ? 3 : (st->iters >= st->maxit ? 2 : 0));
+    }
+  }
+}
+
+__global__ void k_pcg_cond(cudaGraphConditionalHandle h, const PcgState* st) {
+  cudaGraphSetConditional(h, st->done == 0 ? 1u : 0u);
+}
+
+static int build_graph(const PcgOp& op, PcgWork& w) {
+  cudaStream_t cs;
+  TB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaGraph_t g;
+  TB_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  TB_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1u, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  TB_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  TB_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  for (int it = 0; it < kIters; ++it) {
+    double* pold = (it & 1) ? w.pb : w.pa;
+    double* pnew = (it & 1) ? w.pa : w.pb;
+    op.launch_fused(w, pold, pnew, cs);
+    k_pcg_update<<<kUpdateBlocks, kBlock, 0, cs>>>(w.n, pnew, w.q, w.dinv, w.x, w.r, w.z, w.st, w.partB());
+  }
+  k_pcg_cond<<<1, 1, 0, cs>>>(h, w.st);
+  cudaGraph_t captured;
+  TB_CUDA(cudaStreamEndCapture(cs, &captured));
+  TB_CUDA(cudaGraphInstantiate(&w.exec, g, 0));
+  TB_CUDA(cudaGraphDestroy(g));
+  TB_CUDA(cudaStreamDestroy(cs));
+  return TB_OK;
+}
+
+int pcg_solve(const PcgOp& op, PcgWork& w, const double* b, double* x_out, double rtol, int maxit, int* iters,
+              double* relres, cudaStream_t s) {
+  if (!(rtol > 0.0) || maxit < 1) {
+    set_error("pcg: rtol must be > 0 and maxit >= 1 (got %g, %d)", rtol, maxit);
+    return TB_ERR_INVALID;
+  }
+  if (!w.exec) TB_TRY(build_graph(op, w));
+  const int nb = kUpdateBlocks;
+  op.launch_dinv(w.dinv, s);
+  k_pcg_start<<<nb, kBlock, 0, s>>>(w.n, b, nullptr, w.dinv, w.x, w.r, w.z, w.pa, w.st, w.partC(), 1, rtol, maxit);
+  launched(1);
+  TB_CHECK_LAUNCH();
+  int rc = TB_OK;
+  int iters_before = 0, stalls = 0;
+  double best_rr = -1.0;
+  for (int restart = 0;; ++restart) {
+    TB_CUDA(cudaGraphLaunch(w.exec, s));
+    // true residual check at exit
+    op.launch_apply(w.x, w.tmp, s);
+    k_pcg_start<<<nb, kBlock, 0, s>>>(w.n, b, w.tmp, w.dinv, w.x, w.r, w.z, w.pa, w.st, w.partC(), 0, rtol, maxit);
+    launched(1);
+    TB_CHECK_LAUNCH();
+    TB_CUDA(cudaMemcpyAsync(w.h_st, w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    TB_CUDA(cudaStreamSynchronize(s));
+    const PcgState& h = *w.h_st;
+    const int delta = h.iters - iters_before;
+    iters_before = h.iters;
+    launched((int64_t)(delta > 0 ? (delta + kIters - 1) / kIters : 1) * (2 * kIters + 1));
+    if (h.done == 1) break;  // true residual within tolerance
+    if (h.done == 3) {
+      set_error("pCG breakdown after %d iterations: p^T K p <= 0 or non-finite; matrix is not positive definite",
+                h.iters);
+      rc = TB_ERR_INDEFINITE;
+      break;
+    }
+    // the recursive residual met rtol but the true one did not: restart from the true residual,
+    // unless restarts have stopped paying off (rtol below the attainable accuracy)
+    if (best_rr >= 0.0 && h.rr > 0.25 * best_rr) ++stalls;
+    else stalls = 0;
+    if (best_rr < 0.0 || h.rr < best_rr) best_rr = h.rr;
+    if (h.done == 2 || h.iters >= maxit || stalls >= 3 || restart >= 64) {
+      set_error("pCG did not reach rtol=%g in %d iterations (relative residual %.3e)", rtol, h.iters,
+                sqrt(h.rr / (h.bb > 0 ? h.bb : 1.0)));
+      rc = TB_ERR_NOT_CONVERGED;
+      break;
+    }
+  }
+  const PcgState& h = *w.h_st;
+  if (iters) *iters = h.iters;
+  if (relres) *relres = (h.bb > 0.0) ? sqrt(h.rr / h.bb) : 0.0;
+  if (x_out != w.x) TB_CUDA(cudaMemcpyAsync(x_out, w.x, sizeof(double) * w.n, cudaMemcpyDeviceToDevice, s));
+  return rc;
+}
+
+int pcg_profile(const PcgOp& op, PcgWork& w, const double* b, int nrep, double* ms_fused, double* ms_update,
+                cudaStream_t s) {
+  const int nb = kUpdateBlocks;
+  op.launch_dinv(w.dinv, s);
+  // tol2 < 0 and maxit = INT_MAX keep every iteration live
+  k_pcg_start<<<nb, kBlock, 0, s>>>(w.n, b, nullptr, w.dinv, w.x, w.r, w.z, w.pa, w.st, w.partC(), 1, -1.0,
+                                    0x7fffffff);
+  launched(1);
+  TB_CHECK_LAUNCH();
+  cudaEvent_t ev[3];
+  for (auto& e : ev) TB_CUDA(cudaEventCreate(&e));
+  double tf = 0.0, tu = 0.0;
+  for (int it = 0; it < nrep; ++it) {
+    double* pold = (it & 1) ? w.pb : w.pa;
+    double* pnew = (it & 1) ? w.pa : w.pb;
+    cudaEventRecord(ev[0], s);
+    op.launch_fused(w, pold, pnew, s);
+    cudaEventRecord(ev[1], s);
+    k_pcg_update<<<kUpdateBlocks, kBlock, 0, s>>>(w.n, pnew, w.q, w.dinv, w.x, w.r, w.z, w.st, w.partB());
+    cudaEventRecord(ev[2], s);
+    launched(2);
+    TB_CUDA(cudaEventSynchronize(ev[2]));
+    float a = 0.f, c = 0.f;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&c, ev[1], ev[2]);
+    tf += a;
+    tu += c;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  TB_CUDA(cudaMemcpy(w.h_st, w.st, sizeof(PcgState), cudaMemcpyDeviceToHost));
+  if (w.h_st->done != 0) {
+    set_error("profile run stopped early (state %d after %d iterations)", w.h_st->done, w.h_st->iters);
+    return TB_ERR_INVALID;
+  }
+  *ms_fused = tf / nrep;
+  *ms_update = tu / nrep;
+  return TB_OK;
+}
+
+}  // namespace tb

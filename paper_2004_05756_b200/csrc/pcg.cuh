@@ -1,0 +1,54 @@
+// Jacobi-preconditioned CG engine, device-resident.
+//
+// One iteration = two kernels:
+//   A (operator-specific, fused):  p = z + beta p_old ; q = K p ; pq  -> alpha
+//   B (generic, per dof):          x += alpha p ; r -= alpha q ; z = D^-1 r ; rz, rr -> beta, done
+// The loop runs inside ONE CUDA graph whose body (kIters iterations + a condition kernel)
+// sits under a conditional WHILE node, so a whole solve is a single graph launch with no
+// host round trip; convergence is re-checked on the TRUE residual at exit
+// (reference SpdFactorization.solve, fem.py:324-333, is a direct solve; the survey's
+// Appendix A requires the true residual <= rtol).
+#pragma once
+
+#include "common.cuh"
+
+namespace tb {
+
+struct PcgWork;
+
+struct PcgOp {
+  virtual ~PcgOp() = default;
+  virtual int64_t size() const = 0;     // vector length (dofs)
+  virtual int fused_blocks() const = 0; // grid of kernel A
+  // kernel A on stream s
+  virtual void launch_fused(const PcgWork& w, const double* pold, double* pnew, cudaStream_t s) const = 0;
+  // y = Z K v (fixed rows zeroed)
+  virtual void launch_apply(const double* v, double* y, cudaStream_t s) const = 0;
+  // Jacobi inverse diagonal (0 on fixed dofs)
+  virtual void launch_dinv(double* dinv, cudaStream_t s) const = 0;
+};
+
+struct PcgWork {
+  int64_t n = 0;
+  double *x = nullptr, *r = nullptr, *z = nullptr, *pa = nullptr, *pb = nullptr, *q = nullptr,
+         *dinv = nullptr, *tmp = nullptr, *part = nullptr;
+  int part_stride = 0;  // doubles per partial region
+  PcgState* st = nullptr;
+  PcgState* h_st = nullptr;  // pinned
+  cudaGraphExec_t exec = nullptr;
+  double* partA() const { return part; }
+  double* partB() const { return part + 2 * part_stride; }
+  double* partC() const { return part + 4 * part_stride; }
+  int alloc(int64_t n_, int max_blocks);
+  void release();
+};
+
+constexpr int kIters = 8;  // pCG iterations per while-loop body
+constexpr int kUpdateBlocks = 148 * 4;
+
+int pcg_solve(const PcgOp& op, PcgWork& w, const double* b, double* x_out, double rtol, int maxit,
+              int* iters, double* relres, cudaStream_t stream);
+int pcg_profile(const PcgOp& op, PcgWork& w, const double* b, int nrep, double* ms_fused, double* ms_update,
+                cudaStream_t stream);
+
+}  // namespace tb

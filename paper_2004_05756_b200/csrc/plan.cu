@@ -1,0 +1,81 @@
+// Plan lifetime, element tables and workspace management.
+#include "plan.cuh"
+
+namespace tb {
+
+int64_t ElastOp::size() const { return plan->n_dofs; }
+int64_t HelmOp::size() const { return filt->g.n_nodes; }
+
+// Hamming distance between two local corner nodes of the Q1 element.
+static int corner_dist(int a, int b) {
+  auto ox = [](int t) { return ((t & 3) == 1 || (t & 3) == 2) ? 1 : 0; };
+  auto oy = [](int t) { return ((t & 3) >= 2) ? 1 : 0; };
+  auto oz = [](int t) { return t >> 2; };
+  return (ox(a) != ox(b)) + (oy(a) != oy(b)) + (oz(a) != oz(b));
+}
+
+void scalar_element_matrices(int dim, double h, double* S, double* M, double* s_div, double* m_mul) {
+  const int nn = (dim == 2) ? 4 : 8;
+  // 2D (fem.py:72-92): Laplacian 6*S = {4 | -1 edge | -2 diagonal}, mass 36/h^2*M = {4 | 2 | 1}
+  // 3D: Laplacian 12/h*S = {4 | 0 edge | -1 face diag | -1 body diag}, mass 216/h^3*M = {8|4|2|1}
+  static const double s2[3] = {4.0, -1.0, -2.0}, m2[3] = {4.0, 2.0, 1.0};
+  static const double s3[4] = {4.0, 0.0, -1.0, -1.0}, m3[4] = {8.0, 4.0, 2.0, 1.0};
+  for (int a = 0; a < nn; ++a)
+    for (int b = 0; b < nn; ++b) {
+      const int d = corner_dist(a, b);
+      S[a * nn + b] = (dim == 2) ? s2[d] : s3[d];
+      M[a * nn + b] = (dim == 2) ? m2[d] : m3[d];
+    }
+  *s_div = (dim == 2) ? 6.0 : 12.0;
+  *m_mul = (dim == 2) ? h * h / 36.0 : h * h * h / 216.0;
+}
+
+Grid make_grid(int dim, int nx, int ny, int nz, double h) {
+  Grid g{};
+  g.dim = dim;
+  g.nx = nx;
+  g.ny = ny;
+  g.nz = (dim == 3) ? nz : 1;
+  g.nnx = nx + 1;
+  g.nny = ny + 1;
+  g.nnz = (dim == 3) ? nz + 1 : 1;
+  g.h = h;
+  g.n_elems = (int64_t)nx * ny * g.nz;
+  g.n_nodes = (int64_t)g.nnx * g.nny * g.nnz;
+  return g;
+}
+
+int tb_plan_impl::init(const uint8_t* fixed_host) {
+  const size_t ne = (size_t)g.n_elems;
+  TB_CUDA(cudaMalloc(&d_fixed, (size_t)n_dofs));
+  TB_CUDA(cudaMemcpy(d_fixed, fixed_host, (size_t)n_dofs, cudaMemcpyHostToDevice));
+  TB_CUDA(cudaMalloc(&d_alpha, sizeof(double) * ne));
+  TB_CUDA(cudaMalloc(&d_alpha2, sizeof(double) * ne));
+  TB_CUDA(cudaMalloc(&d_scratch, sizeof(double) * 8 * 148 * 8));
+  TB_CUDA(cudaMalloc(&d_scalar, sizeof(double) * 16));
+  TB_CUDA(cudaMallocHost(&h_scalar, sizeof(double) * 16));
+  TB_TRY(work.alloc(n_dofs, op.fused_blocks()));
+  return TB_OK;
+}
+
+void tb_plan_impl::release() {
+  work.release();
+  void* bufs[] = {d_fixed, d_alpha, d_alpha2, d_scratch, d_scalar, d_rom};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (h_scalar) cudaFreeHost(h_scalar);
+  d_fixed = nullptr;
+  d_alpha = d_alpha2 = d_scratch = d_scalar = d_rom = h_scalar = nullptr;
+}
+
+int tb_plan_impl::rom_scratch(size_t bytes) {
+  if (bytes <= rom_bytes) return TB_OK;
+  if (d_rom) cudaFree(d_rom);
+  d_rom = nullptr;
+  rom_bytes = 0;
+  TB_CUDA(cudaMalloc(&d_rom, bytes));
+  rom_bytes = bytes;
+  return TB_OK;
+}
+
+}  // namespace tb

@@ -1,0 +1,74 @@
+// Plan / filter objects behind the opaque C handles.
+#pragma once
+
+#include "pcg.cuh"
+
+namespace tb {
+
+struct tb_plan_impl;
+struct tb_filter_impl;
+
+// SIMP elasticity operator  Z K(rho) Z  (alpha from the plan's d_alpha)
+struct ElastOp final : PcgOp {
+  tb_plan_impl* plan = nullptr;
+  int64_t size() const override;
+  int fused_blocks() const override;
+  void launch_fused(const PcgWork& w, const double* pold, double* pnew, cudaStream_t s) const override;
+  void launch_apply(const double* v, double* y, cudaStream_t s) const override;
+  void launch_dinv(double* dinv, cudaStream_t s) const override;
+};
+
+// Helmholtz operator  H = sum_e (r^2 S_e + M_e)  (pure Neumann)
+struct HelmOp final : PcgOp {
+  tb_filter_impl* filt = nullptr;
+  int64_t size() const override;
+  int fused_blocks() const override;
+  void launch_fused(const PcgWork& w, const double* pold, double* pnew, cudaStream_t s) const override;
+  void launch_apply(const double* v, double* y, cudaStream_t s) const override;
+  void launch_dinv(double* dinv, cudaStream_t s) const override;
+};
+
+struct tb_plan_impl {
+  Grid g{};
+  int64_t n_dofs = 0;
+  int device = 0;
+  double rho_l = 1e-3, p = 3.0;
+  Mat<8> K2{};
+  Mat<24> K3{};
+  uint8_t* d_fixed = nullptr;
+  double* d_alpha = nullptr;   // alpha of the design being solved (read by the pCG graph)
+  double* d_alpha2 = nullptr;  // alpha scratch for one-off applies
+  double* d_scratch = nullptr; // reduction partials
+  double* d_scalar = nullptr;
+  double* h_scalar = nullptr;  // pinned
+  double* d_rom = nullptr;     // ROM scratch (grown on demand)
+  size_t rom_bytes = 0;
+  ElastOp op;
+  PcgWork work;
+
+  int init(const uint8_t* fixed_host);
+  void release();
+  void apply_alpha(const double* alpha, const double* v, double* y, bool mask, cudaStream_t s) const;
+  int material(const double* rho, double* alpha, double* dalpha, cudaStream_t s) const;
+  int rom_scratch(size_t bytes);
+};
+
+struct tb_filter_impl {
+  Grid g{};
+  int device = 0;
+  double radius = 0.0, r = 0.0, vol_share = 0.0;
+  Mat<4> H2{};
+  Mat<8> H3{};
+  double* d_b = nullptr;
+  HelmOp op;
+  PcgWork work;
+};
+
+// Integer Laplacian / mass tables of the scalar Q1 element: S_e = (h^(d-2)) S/s_div,
+// M_e = m_mul * M  (2D: S/6, h^2/36 M, fem.py:72-92; 3D: h S/12, h^3/216 M).
+void scalar_element_matrices(int dim, double h, double* S, double* M, double* s_div, double* m_mul);
+Grid make_grid(int dim, int nx, int ny, int nz, double h);
+void finish_sum(int nb, const double* part, double* out, cudaStream_t s);
+int device_dot(const double* a, const double* b, int64_t n, double* scratch, double* out_dev, cudaStream_t s);
+
+}  // namespace tb

@@ -1,0 +1,501 @@
+// Reduced-order-model kernels (reference rom.py:76-390).
+//
+// Reduced stiffness uses the node-form identity  Phi^T K(rho) Phi = Phi^T Y,  Y = K(rho) Phi
+// (reference PAPER.md:444; rom.py:254-262 evaluates the same sum element by element).
+// Y rows are produced by the node-owner operator over k columns; the k x k contraction
+// Phi^T Y runs on the FP64 tensor cores (mma.sync m8n8k4 f64 -> SASS DMMA) with a
+// deterministic two-level reduction.
+#include <string.h>
+
+#include "plan.cuh"
+#include "q1.cuh"
+
+namespace tb {
+
+static inline int nblk(int64_t n) { return (int)((n + kBlock - 1) / kBlock); }
+
+// ---------------------------------------------------------------------------------------
+// out[d][j] = sum_i phi[i][j] vec[d][i]     (Phi^T f, rom.py:251)
+// ---------------------------------------------------------------------------------------
+constexpr int kMaxVec = 16;
+
+__global__ void __launch_bounds__(kBlock) k_project_part(int64_t n, int k, const double* __restrict__ phi,
+                                                         const double* __restrict__ vec, int nvec,
+                                                         double* __restrict__ part) {
+  extern __shared__ double sh[];  // [groups][nvec][k]
+  const int groups = kBlock / k;
+  const int t = threadIdx.x, j = t % k, rg = t / k;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * per, i1 = min(n, i0 + per);
+  double acc[kMaxVec];
+#pragma unroll
+  for (int d = 0; d < kMaxVec; ++d) acc[d] = 0.0;
+  if (rg < groups) {
+    for (int64_t i = i0 + rg; i < i1; i += groups) {
+      const double pv = phi[i * k + j];
+#pragma unroll
+      for (int d = 0; d < kMaxVec; ++d)
+        if (d < nvec) acc[d] = fma(pv, __ldg(vec + (int64_t)d * n + i), acc[d]);
+    }
+    for (int d = 0; d < nvec; ++d) sh[(rg * nvec + d) * k + j] = acc[d];
+  }
+  __syncthreads();
+  for (int o = t; o < nvec * k; o += blockDim.x) {
+    double s = 0.0;
+    for (int g = 0; g < groups; ++g) s += sh[g * nvec * k + o];
+    part[(int64_t)blockIdx.x * nvec * k + o] = s;
+  }
+}
+
+// out[o] = sum_b part[b][o]  (fixed order), o < len
+__global__ void k_sum_parts(int nb, int len, const double* __restrict__ part, double* __restrict__ out) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= len) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += part[(int64_t)b * len + o];
+  out[o] = s;
+}
+
+// ---------------------------------------------------------------------------------------
+// Y = K(alpha) Phi  for all k columns: thread per (node, column), column fastest so the
+// neighbourhood loads of a warp are contiguous rows of Phi.
+// ---------------------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_apply_cols(Grid g, Mat<Q1<D>::NN * D> K, const double* __restrict__ alpha,
+                                                       const double* __restrict__ phi, int k, double* __restrict__ y) {
+  constexpr int NC = D;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = t / k;
+  const int col = (int)(t % k);
+  if (n >= g.n_nodes) return;
+  int i, j, kk;
+  node_coords(g, n, i, j, kk);
+  double P[Q1<D>::NB][NC];
+#pragma unroll
+  for (int dz = 0; dz < (D == 3 ? 3 : 1); ++dz)
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) {
+        const int nb = (dz * 3 + dy) * 3 + dx;
+        const int ii = i + dx - 1, jj = j + dy - 1, k3 = (D == 3) ? kk + dz - 1 : 0;
+        const bool ok = ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny && k3 >= 0 && k3 < g.nnz;
+        const int64_t node = ((int64_t)k3 * g.nny + jj) * g.nnx + ii;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) P[nb][c] = ok ? __ldg(phi + (NC * node + c) * k + col) : 0.0;
+      }
+  double a[Q1<D>::NN];
+  slot_scales<D, true>(g, i, j, kk, alpha, a);
+  double out[NC];
+  node_rows<D, NC>(K, P, a, out);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) y[(NC * n + c) * k + col] = out[c];
+}
+
+// ---------------------------------------------------------------------------------------
+// C_part[block] = A^T B over a row range, A,B: n x k row-major, on DMMA (m8n8k4 f64).
+// ---------------------------------------------------------------------------------------
+constexpr int kRows = 32;       // rows staged per step
+constexpr int kGemmThreads = 256;
+
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int KP>  // padded k (multiple of 8)
+__global__ void __launch_bounds__(kGemmThreads) k_atb_dmma(int64_t n, int k, const double* __restrict__ A,
+                                                           const double* __restrict__ B, double* __restrict__ part) {
+  constexpr int LD = KP + 8;  // padded smem row (bank-conflict-free fragment reads)
+  constexpr int TILES = (KP / 8) * (KP / 8);
+  constexpr int NW = kGemmThreads / 32;
+  constexpr int TPW = (TILES + NW - 1) / NW;
+  __shared__ double sa[kRows * LD];
+  __shared__ double sb[kRows * LD];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t per = ((n + gridDim.x - 1) / gridDim.x + kRows - 1) / kRows * kRows;
+  const int64_t i0 = (int64_t)blockIdx.x * per, i1 = min(n, i0 + per);
+  double acc[TPW][2];
+#pragma unroll
+  for (int t = 0; t < TPW; ++t) acc[t][0] = acc[t][1] = 0.0;
+  for (int64_t base = i0; base < i1; base += kRows) {
+    __syncthreads();
+    for (int o = tid; o < kRows * KP; o += kGemmThreads) {
+      const int r = o / KP, c = o % KP;
+      const int64_t row = base + r;
+      const bool ok = row < i1 && c < k;
+      sa[r * LD + c] = ok ? A[row * k + c] : 0.0;
+      sb[r * LD + c] = ok ? B[row * k + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < TPW; ++t) {
+      const int tile = warp + t * NW;
+      if (tile < TILES) {
+        const int m0 = (tile / (KP / 8)) * 8, n0 = (tile % (KP / 8)) * 8;
+#pragma unroll
+        for (int r0 = 0; r0 < kRows; r0 += 4) {
+          const double a = sa[(r0 + (lane & 3)) * LD + m0 + (lane >> 2)];
+          const double b = sb[(r0 + (lane & 3)) * LD + n0 + (lane >> 2)];
+          dmma_8x8x4(acc[t], a, b);
+        }
+      }
+    }
+  }
+  // D fragment: row = lane>>2, cols = 2*(lane&3) + {0,1}
+  double* out = part + (int64_t)blockIdx.x * k * k;
+#pragma unroll
+  for (int t = 0; t < TPW; ++t) {
+    const int tile = warp + t * NW;
+    if (tile < TILES) {
+      const int m = (tile / (KP / 8)) * 8 + (lane >> 2);
+      const int c0 = (tile % (KP / 8)) * 8 + 2 * (lane & 3);
+      if (m < k && c0 < k) out[m * k + c0] = acc[t][0];
+      if (m < k && c0 + 1 < k) out[m * k + c0 + 1] = acc[t][1];
+    }
+  }
+}
+
+static int launch_atb(int64_t n, int k, const double* A, const double* B, double* part, int nb, cudaStream_t s) {
+  const int kp = (k + 7) / 8 * 8;
+  if (kp <= 8)
+    { k_atb_dmma<8><<<nb, kGemmThreads, 0, s>>>(n, k, A, B, part); tb::launched(); }
+  else if (kp <= 16)
+    { k_atb_dmma<16><<<nb, kGemmThreads, 0, s>>>(n, k, A, B, part); tb::launched(); }
+  else if (kp <= 32)
+    { k_atb_dmma<32><<<nb, kGemmThreads, 0, s>>>(n, k, A, B, part); tb::launched(); }
+  else if (kp <= 64)
+    { k_atb_dmma<64><<<nb, kGemmThreads, 0, s>>>(n, k, A, B, part); tb::launched(); }
+  else {
+    set_error("reduced basis size k=%d exceeds 64", k);
+    return TB_ERR_INVALID;
+  }
+  TB_CHECK_LAUNCH();
+  return TB_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// batched Cholesky  A = U^T U  (upper triangle, as scipy.linalg.cho_factor(lower=False))
+// and solve for nrhs right-hand sides.  One CTA per design.
+// ---------------------------------------------------------------------------------------
+__global__ void k_cholesky_solve(int k, int nrhs, const double* __restrict__ khat, const double* __restrict__ rhs,
+                                 double* __restrict__ x, int* __restrict__ status) {
+  extern __shared__ double U[];  // k*k
+  const int d = blockIdx.x, t = threadIdx.x, nt = blockDim.x;
+  const double* A = khat + (int64_t)d * k * k;
+  for (int o = t; o < k * k; o += nt) U[o] = A[o];
+  __shared__ int bad;
+  if (t == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    if (t == 0) {
+      const double piv = U[j * k + j];
+      const double ref = fabs(A[j * k + j]);
+      // non-positive pivot, or one lost in round-off: numerically singular (rom.py:49-50)
+      if (!(piv > (double)k * 2.220446049250313e-16 * ref) || !isfinite(piv)) bad = 1;
+      else U[j * k + j] = sqrt(piv);
+    }
+    __syncthreads();
+    if (bad) break;
+    const double ujj = U[j * k + j];
+    for (int c = j + 1 + t; c < k; c += nt) U[j * k + c] /= ujj;
+    __syncthreads();
+    const int m = k - j - 1;
+    for (int o = t; o < m * m; o += nt) {
+      const int r = j + 1 + o / m, c = j + 1 + o % m;
+      if (c >= r) U[r * k + c] -= U[j * k + r] * U[j * k + c];
+    }
+    __syncthreads();
+  }
+  if (t == 0) status[d] = bad;
+  if (bad) return;
+  // U^T y = b ; U x = y
+  for (int q = t; q < nrhs; q += nt) {
+    const double* b = rhs + ((int64_t)d * nrhs + q) * k;
+    double* xv = x + ((int64_t)d * nrhs + q) * k;
+    for (int i = 0; i < k; ++i) {
+      double s = b[i];
+      for (int l = 0; l < i; ++l) s -= U[l * k + i] * xv[l];
+      xv[i] = s / U[i * k + i];
+    }
+    for (int i = k - 1; i >= 0; --i) {
+      double s = xv[i];
+      for (int l = i + 1; l < k; ++l) s -= U[i * k + l] * xv[l];
+      xv[i] = s / U[i * k + i];
+    }
+  }
+}
+
+// u[d][i] = sum_j phi[i][j] uhat[d][j]  (warp per row, lanes over j)
+__global__ void __launch_bounds__(kBlock) k_reconstruct(int64_t n, int k, const double* __restrict__ phi,
+                                                        const double* __restrict__ uhat, int nd, double* __restrict__ u) {
+  extern __shared__ double su[];  // nd*k
+  for (int o = threadIdx.x; o < nd * k; o += blockDim.x) su[o] = uhat[o];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    double acc[kMaxVec];
+#pragma unroll
+    for (int d = 0; d < kMaxVec; ++d) acc[d] = 0.0;
+    for (int j = lane; j < k; j += 32) {
+      const double pv = phi[i * k + j];
+#pragma unroll
+      for (int d = 0; d < kMaxVec; ++d)
+        if (d < nd) acc[d] = fma(pv, su[d * k + j], acc[d]);
+    }
+#pragma unroll
+    for (int d = 0; d < kMaxVec; ++d)
+      if (d < nd) {
+        const double v = warp_sum(acc[d]);
+        if (lane == 0) u[(int64_t)d * n + i] = v;
+      }
+  }
+}
+
+// block partials of || mask * (y - g) ||^2
+__global__ void __launch_bounds__(kBlock) k_resid_part(int64_t n, const double* __restrict__ y,
+                                                       const double* __restrict__ g, const uint8_t* __restrict__ fixed,
+                                                       double* __restrict__ part) {
+  double acc[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (!fixed[i]) {
+      const double r = y[i] - g[i];
+      acc[0] = fma(r, r, acc[0]);
+    }
+  }
+  block_sum<1>(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+}
+
+// ---------------------------------------------------------------------------------------
+// Modified Gram-Schmidt step: v -= c_prev * q_prev ; c_next = q_next . v  (last block)
+// ---------------------------------------------------------------------------------------
+struct GsState {
+  double c[2];
+  unsigned int count;
+  unsigned int pad;
+};
+
+__global__ void __launch_bounds__(kBlock) k_gs_step(int64_t n, double* __restrict__ v, const double* __restrict__ qprev,
+                                                    int cprev_slot, const double* __restrict__ qnext, int cnext_slot,
+                                                    GsState* st, double* part) {
+  const double cp = (qprev != nullptr) ? st->c[cprev_slot] : 0.0;
+  double acc[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double vi = v[i];
+    if (qprev != nullptr) {
+      vi = fma(-cp, qprev[i], vi);
+      v[i] = vi;
+    }
+    if (qnext != nullptr) acc[0] = fma(qnext[i], vi, acc[0]);
+  }
+  if (qnext == nullptr) return;
+  block_sum<1>(acc);
+  if (publish_partials<1>(acc, part, &st->count)) {
+    gather_partials<1>(acc, part, &st->count);
+    if (threadIdx.x == 0) st->c[cnext_slot] = acc[0];
+  }
+}
+
+__global__ void k_scale_copy(int64_t n, const double* __restrict__ v, double s, double* __restrict__ q) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    q[i] = v[i] * s;
+}
+
+// column-major (n x m) -> row-major (n x m)
+__global__ void k_transpose_cm_rm(int64_t n, int m, const double* __restrict__ cm, double* __restrict__ rm) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * m) return;
+  const int64_t i = t / m;
+  const int j = (int)(t % m);
+  rm[t] = cm[(int64_t)j * n + i];
+}
+
+}  // namespace tb
+
+using namespace tb;
+
+extern "C" {
+
+#define TB_GUARD(cond, ...)   \
+  do {                        \
+    if (!(cond)) {            \
+      set_error(__VA_ARGS__); \
+      return TB_ERR_INVALID;  \
+    }                         \
+  } while (0)
+
+int tb_rom_project(int64_t n, const double* phi, int k, const double* vec, int nvec, double* out, void* stream) {
+  TB_GUARD(phi && vec && out && n >= 1, "bad arguments");
+  TB_GUARD(k >= 1 && k <= kBlock, "basis size k=%d out of range [1, %d]", k, kBlock);
+  TB_GUARD(nvec >= 1 && nvec <= kMaxVec, "nvec=%d out of range [1, %d]", nvec, kMaxVec);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nb = 148 * 2;
+  double* part = nullptr;
+  TB_CUDA(cudaMallocAsync(&part, sizeof(double) * (size_t)nb * nvec * k, s));
+  const int groups = kBlock / k;
+  { k_project_part<<<nb, kBlock, sizeof(double) * groups * nvec * k, s>>>(n, k, phi, vec, nvec, part); tb::launched(); }
+  { k_sum_parts<<<nblk(nvec * k), kBlock, 0, s>>>(nb, nvec * k, part, out); tb::launched(); }
+  TB_CHECK_LAUNCH();
+  TB_CUDA(cudaFreeAsync(part, s));
+  return TB_OK;
+}
+
+int tb_rom_reduced_stiffness(tb_plan* plan, const double* phi, int k, const double* rho, int nd, double* khat,
+                             void* stream) {
+  TB_GUARD(plan && phi && rho && khat, "null argument");
+  TB_GUARD(k >= 1 && k <= 64, "basis size k=%d out of range [1, 64]", k);
+  TB_GUARD(nd >= 1, "nd must be >= 1");
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  cudaStream_t s = (cudaStream_t)stream;
+  const Grid& g = P->g;
+  const int nb = 148 * 2;
+  const size_t ybytes = sizeof(double) * (size_t)P->n_dofs * k;
+  const size_t pbytes = sizeof(double) * (size_t)nb * k * k;
+  TB_TRY(P->rom_scratch(ybytes + pbytes));
+  double* Y = P->d_rom;
+  double* part = P->d_rom + (size_t)P->n_dofs * k;
+  for (int d = 0; d < nd; ++d) {
+    TB_TRY(P->material(rho + (int64_t)d * g.n_elems, P->d_alpha2, nullptr, s));
+    const int64_t threads = g.n_nodes * k;
+    const int blocks = (int)((threads + kBlock - 1) / kBlock);
+    if (g.dim == 2)
+      { k_apply_cols<2><<<blocks, kBlock, 0, s>>>(g, P->K2, P->d_alpha2, phi, k, Y); tb::launched(); }
+    else
+      { k_apply_cols<3><<<blocks, kBlock, 0, s>>>(g, P->K3, P->d_alpha2, phi, k, Y); tb::launched(); }
+    TB_CHECK_LAUNCH();
+    TB_TRY(launch_atb(P->n_dofs, k, phi, Y, part, nb, s));
+    { k_sum_parts<<<nblk(k * k), kBlock, 0, s>>>(nb, k * k, part, khat + (int64_t)d * k * k); tb::launched(); }
+    TB_CHECK_LAUNCH();
+  }
+  return TB_OK;
+}
+
+int tb_rom_cholesky_solve(int k, int nd, int nrhs, const double* khat, const double* rhs, double* x, int* status,
+                          void* stream) {
+  TB_GUARD(khat && rhs && x && status, "null argument");
+  TB_GUARD(k >= 1 && k <= 128 && nd >= 1 && nrhs >= 1, "bad sizes k=%d nd=%d nrhs=%d", k, nd, nrhs);
+  cudaStream_t s = (cudaStream_t)stream;
+  int* d_status = nullptr;
+  TB_CUDA(cudaMallocAsync(&d_status, sizeof(int) * nd, s));
+  const size_t sm = sizeof(double) * k * k;
+  if (sm > 48 * 1024) TB_CUDA(cudaFuncSetAttribute(k_cholesky_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  { k_cholesky_solve<<<nd, 256, sm, s>>>(k, nrhs, khat, rhs, x, d_status); tb::launched(); }
+  TB_CHECK_LAUNCH();
+  TB_CUDA(cudaMemcpyAsync(status, d_status, sizeof(int) * nd, cudaMemcpyDeviceToHost, s));
+  TB_CUDA(cudaFreeAsync(d_status, s));
+  TB_CUDA(cudaStreamSynchronize(s));
+  for (int d = 0; d < nd; ++d)
+    if (status[d]) {
+      set_error("reduced stiffness of design %d is not positive definite", d);
+      return TB_ERR_DEGENERATE;
+    }
+  return TB_OK;
+}
+
+int tb_rom_reconstruct(int64_t n, const double* phi, int k, const double* uhat, int nd, double* u, void* stream) {
+  TB_GUARD(phi && uhat && u && n >= 1, "bad arguments");
+  TB_GUARD(k >= 1 && nd >= 1 && nd <= kMaxVec, "bad sizes k=%d nd=%d", k, nd);
+  cudaStream_t s = (cudaStream_t)stream;
+  { k_reconstruct<<<148 * 8, kBlock, sizeof(double) * nd * k, s>>>(n, k, phi, uhat, nd, u); tb::launched(); }
+  TB_CHECK_LAUNCH();
+  return TB_OK;
+}
+
+int tb_rom_residual_norms(tb_plan* plan, const double* phi, int k, const double* rho, const double* uhat, int nd,
+                          const double* g, int64_t g_stride, double* norms, void* stream) {
+  TB_GUARD(plan && phi && rho && uhat && g && norms, "null argument");
+  TB_GUARD(k >= 1 && nd >= 1 && nd <= kMaxVec, "bad sizes k=%d nd=%d", k, nd);
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n = P->n_dofs;
+  const int nb = grid_for(n);
+  TB_TRY(P->rom_scratch(sizeof(double) * ((size_t)(nd + 1) * n + nb + 16)));
+  double* U = P->d_rom;
+  double* Y = U + (size_t)nd * n;
+  double* part = Y + n;
+  TB_TRY(tb_rom_reconstruct(n, phi, k, uhat, nd, U, stream));
+  for (int d = 0; d < nd; ++d) {
+    TB_TRY(P->material(rho + (int64_t)d * P->g.n_elems, P->d_alpha2, nullptr, s));
+    P->apply_alpha(P->d_alpha2, U + (int64_t)d * n, Y, false, s);
+    { k_resid_part<<<nb, kBlock, 0, s>>>(n, Y, g + d * g_stride, P->d_fixed, part); tb::launched(); }
+    finish_sum(nb, part, P->d_scalar + d, s);
+  }
+  TB_CHECK_LAUNCH();
+  TB_CUDA(cudaMemcpyAsync(P->h_scalar, P->d_scalar, sizeof(double) * nd, cudaMemcpyDeviceToHost, s));
+  TB_CUDA(cudaStreamSynchronize(s));
+  for (int d = 0; d < nd; ++d) norms[d] = sqrt(P->h_scalar[d]);
+  return TB_OK;
+}
+
+int tb_gram_schmidt(int64_t n, int m, const double* vectors, double drop_tol, double* q, int* kept, void* stream) {
+  TB_GUARD(vectors && q && kept && n >= 1 && m >= 1, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nb = grid_for(n);
+  double *V = nullptr, *Q = nullptr, *part = nullptr, *h = nullptr;
+  GsState* st = nullptr;
+  TB_CUDA(cudaMallocAsync(&V, sizeof(double) * n, s));
+  TB_CUDA(cudaMallocAsync(&Q, sizeof(double) * n * m, s));
+  TB_CUDA(cudaMallocAsync(&part, sizeof(double) * nb, s));
+  TB_CUDA(cudaMallocAsync(&st, sizeof(GsState), s));
+  TB_CUDA(cudaMemsetAsync(st, 0, sizeof(GsState), s));
+  TB_CUDA(cudaMallocHost(&h, sizeof(double) * 2));
+  int nk = 0;
+  int rc = TB_OK;
+  for (int i = 0; i < m && rc == TB_OK; ++i) {
+    cudaMemcpyAsync(V, vectors + (int64_t)i * n, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
+    { k_gs_step<<<nb, kBlock, 0, s>>>(n, V, nullptr, 0, V, 0, st, part); tb::launched(); }  // ||v0||^2
+    cudaMemcpyAsync(h, st->c, sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) {
+      rc = TB_ERR_CUDA;
+      break;
+    }
+    const double n0 = sqrt(h[0]);
+    if (n0 == 0.0) continue;
+    int slot = 0;
+    const double* prev = nullptr;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int b = 0; b < nk; ++b) {
+        const double* qb = Q + (int64_t)b * n;
+        { k_gs_step<<<nb, kBlock, 0, s>>>(n, V, prev, slot ^ 1, qb, slot, st, part); tb::launched(); }
+        prev = qb;
+        slot ^= 1;
+      }
+    // last deflation + ||v||^2
+    { k_gs_step<<<nb, kBlock, 0, s>>>(n, V, prev, slot ^ 1, nullptr, 0, st, part); tb::launched(); }
+    { k_gs_step<<<nb, kBlock, 0, s>>>(n, V, nullptr, 0, V, 0, st, part); tb::launched(); }
+    cudaMemcpyAsync(h, st->c, sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) {
+      rc = TB_ERR_CUDA;
+      break;
+    }
+    const double n1 = sqrt(h[0]);
+    if (n1 >= drop_tol * n0) {
+      { k_scale_copy<<<nb, kBlock, 0, s>>>(n, V, 1.0 / n1, Q + (int64_t)nk * n); tb::launched(); }
+      ++nk;
+    }
+  }
+  if (rc == TB_OK && cudaGetLastError() != cudaSuccess) rc = TB_ERR_CUDA;
+  if (rc == TB_OK && nk == 0) {
+    set_error("no independent vectors supplied");
+    rc = TB_ERR_INVALID;
+  }
+  if (rc == TB_OK) {
+    const int64_t tot = n * nk;
+    { k_transpose_cm_rm<<<(int)((tot + kBlock - 1) / kBlock), kBlock, 0, s>>>(n, nk, Q, q); tb::launched(); }
+  }
+  *kept = nk;
+  cudaFreeAsync(V, s);
+  cudaFreeAsync(Q, s);
+  cudaFreeAsync(part, s);
+  cudaFreeAsync(st, s);
+  cudaStreamSynchronize(s);
+  cudaFreeHost(h);
+  if (rc == TB_ERR_CUDA) set_error("CUDA failure in gram_schmidt");
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,461 @@
+"""Galerkin reduced-order model on the GPU (drop-in for reference rom.py).
+
+The reference assembles Phi^T K(rho) Phi from cached element slices
+``elem_phi``/``elem_k_phi`` (rom.py:242-262), which cost 2 x 8 x N_e x k doubles (103 GB at
+BASELINE cfg 5).  Here the basis lives once on the device and every reduced quantity is
+computed from it directly:
+
+* ``Phi^T f``            -> tb_rom_project
+* ``Phi^T K(rho) Phi``   -> tb_rom_reduced_stiffness (node-form, DMMA contraction)
+* Cholesky / solves      -> tb_rom_cholesky_solve (batched, one CTA per design)
+* ``Phi uhat``           -> tb_rom_reconstruct
+* ``||K Phi uhat - g||`` -> tb_rom_residual_norms
+* Gram-Schmidt           -> tb_gram_schmidt (MGS x2 with drop tolerance, rom.py:76-97)
+
+``ReducedBasis(phi, elem_phi, elem_k_phi, f_hat)`` keeps the reference signature; the two
+cache arguments are accepted and ignored (pass None).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from itertools import count
+
+import numpy as np
+
+from . import _lib
+from .hdm import ComplianceObjective, HdmSolver, Objective
+from .stats import RunStats
+
+__all__ = [
+    "pod",
+    "gram_schmidt",
+    "SnapshotWindow",
+    "ReducedBasis",
+    "RomSolution",
+    "RomModel",
+    "ErrorReport",
+    "BasisMismatchError",
+    "DegenerateBasisError",
+]
+
+_GEN_COUNTER = count(1)
+GS_DROP_TOL = 1e-10  # rom.py:42
+
+
+class BasisMismatchError(RuntimeError):
+    """A reduced solution was paired with a basis it was not computed from (rom.py:45-46)."""
+
+
+class DegenerateBasisError(RuntimeError):
+    """The reduced stiffness matrix was numerically singular (rom.py:49-50)."""
+
+
+def _device_of(x):
+    return x.device if _lib.is_torch(x) and x.is_cuda else _lib.require_cuda()
+
+
+def _stream(dev):
+    return _lib.stream_ptr(dev)
+
+
+def _gs_device(cols_d, drop_tol):
+    """cols_d: (m, n) device tensor, one vector per row -> (n, kept) row-major basis."""
+    t = _lib.torch()
+    m, n = cols_d.shape
+    q = t.empty(n * m, dtype=t.float64, device=cols_d.device)
+    kept = ctypes.c_int(0)
+    _lib.check(_lib.lib().tb_gram_schmidt(n, m, _lib.ptr(cols_d), float(drop_tol), _lib.ptr(q), ctypes.byref(kept),
+                                          _stream(cols_d.device)), "gram_schmidt")
+    return q[: n * kept.value].view(n, kept.value)
+
+
+def gram_schmidt(vectors, drop_tol: float = GS_DROP_TOL):
+    """Orthonormalise a sequence of vectors, dropping near-dependent ones (rom.py:76-97)."""
+    vectors = list(vectors)
+    if not vectors:
+        raise ValueError("no independent vectors supplied")
+    native = _lib.is_torch(vectors[0])
+    dev = _device_of(vectors[0])
+    t = _lib.torch()
+    cols = t.stack([_lib.to_dev(v, dev).reshape(-1) for v in vectors]).contiguous()
+    q = _gs_device(cols, drop_tol)
+    return _lib.to_user(q, native)
+
+
+def _project(phi_d, vecs_d):
+    """(phi^T v_d) for stacked vectors vecs_d (nv, n) -> (nv, k) device tensor."""
+    t = _lib.torch()
+    n, k = phi_d.shape
+    out = t.empty((vecs_d.shape[0], k), dtype=t.float64, device=phi_d.device)
+    for s in range(0, vecs_d.shape[0], 16):
+        nv = min(16, vecs_d.shape[0] - s)
+        _lib.check(_lib.lib().tb_rom_project(n, _lib.ptr(phi_d), k, _lib.ptr(vecs_d[s:s + nv].contiguous()), nv,
+                                             _lib.ptr(out[s:s + nv]), _stream(phi_d.device)), "rom project")
+    return out
+
+
+def _reconstruct(phi_d, coef_d):
+    """phi @ coef_d^T for stacked coefficient rows coef_d (nd, k) -> (nd, n)."""
+    t = _lib.torch()
+    n, k = phi_d.shape
+    out = t.empty((coef_d.shape[0], n), dtype=t.float64, device=phi_d.device)
+    for s in range(0, coef_d.shape[0], 16):
+        nd = min(16, coef_d.shape[0] - s)
+        _lib.check(_lib.lib().tb_rom_reconstruct(n, _lib.ptr(phi_d), k, _lib.ptr(coef_d[s:s + nd].contiguous()),
+                                                 nd, _lib.ptr(out[s:s + nd]), _stream(phi_d.device)),
+                   "rom reconstruct")
+    return out
+
+
+def pod(snapshots, n: int):
+    """First n left singular vectors with the deterministic sign rule (rom.py:53-73).
+
+    Thin QR on the device (MGS x2), SVD of the small R factor on the host, U = Q U_R
+    (backward-stable like LAPACK's thin SVD).  The largest-magnitude entry of each mode is
+    made positive (first occurrence on ties).  If the snapshots have numerical rank r < n,
+    modes r..n-1 are returned as zero columns (Gram-Schmidt drops them downstream).
+    """
+    t = _lib.torch()
+    native = _lib.is_torch(snapshots)
+    if native:
+        s_d = (snapshots if snapshots.dim() == 2 else snapshots[:, None]).to(dtype=t.float64)
+        rows, m = s_d.shape
+    else:
+        s_np = np.atleast_2d(np.asarray(snapshots, dtype=float))
+        rows, m = s_np.shape
+    if n > m:
+        raise ValueError(f"requested {n} modes from {m} snapshots")
+    if n == 0:
+        return t.zeros((rows, 0), dtype=t.float64, device=s_d.device) if native else np.zeros((rows, 0))
+    dev = s_d.device if native else _lib.require_cuda()
+    cols = (s_d.t() if native else _lib.to_dev(s_np.T, dev)).contiguous()  # (m, rows)
+    q = _gs_device(cols, GS_DROP_TOL).contiguous()  # (rows, r)
+    r = q.shape[1]
+    big_r = _project(q, cols).T.cpu().numpy()  # R = Q^T S, (r, m)
+    ur = np.linalg.svd(big_r, full_matrices=False)[0]
+    nm = min(n, r)
+    modes = _reconstruct(q, _lib.to_dev(np.ascontiguousarray(ur[:, :nm].T), dev))  # (nm, rows)
+    out = t.zeros((rows, n), dtype=t.float64, device=dev)
+    for c in range(nm):
+        v = modes[c]
+        piv = int(t.argmax(t.abs(v)))
+        out[:, c] = -v if float(v[piv]) < 0.0 else v
+    return _lib.to_user(out, native)
+
+
+class SnapshotWindow:
+    """Bounded FIFO of full-order primal/adjoint snapshots with key dedupe (rom.py:100-138)."""
+
+    def __init__(self, max_size: int):
+        if max_size < 1:
+            raise ValueError("window size must be >= 1")
+        self.max_size = max_size
+        self._primal: list = []
+        self._adjoint: list = []
+        self._keys: list = []
+
+    def __len__(self) -> int:
+        return len(self._primal)
+
+    def __contains__(self, key) -> bool:
+        return key is not None and key in self._keys
+
+    @staticmethod
+    def _copy(x):
+        if _lib.is_torch(x):
+            return x.detach().to(dtype=_lib.torch().float64).clone()
+        return np.asarray(x, dtype=float).copy()
+
+    def append(self, u, lam, key=None) -> None:
+        if key is not None and key in self._keys:
+            return
+        self._primal.append(self._copy(u))
+        self._adjoint.append(self._copy(lam))
+        self._keys.append(key)
+        if len(self._primal) > self.max_size:
+            self._primal.pop(0)
+            self._adjoint.pop(0)
+            self._keys.pop(0)
+
+    @staticmethod
+    def _stack(vs):
+        if not vs:
+            return np.zeros((0, 0))
+        if _lib.is_torch(vs[0]):
+            return _lib.torch().stack(vs, dim=1)
+        return np.column_stack(vs)
+
+    def primal_matrix(self):
+        return self._stack(self._primal)
+
+    def adjoint_matrix(self):
+        return self._stack(self._adjoint)
+
+
+@dataclass
+class ReducedBasis:
+    """Orthonormal basis and reduced load (rom.py:141-153).  Caches are not materialised."""
+
+    phi: object  # (N_u, j) orthonormal columns, numpy or CUDA tensor
+    elem_phi: object = field(default=None, repr=False)
+    elem_k_phi: object = field(default=None, repr=False)
+    f_hat: object = None
+    gen_id: int = field(default_factory=lambda: next(_GEN_COUNTER))
+
+    @property
+    def size(self) -> int:
+        return int(self.phi.shape[1])
+
+    def device_phi(self, device):
+        d = self.__dict__.get("_phi_d")
+        if d is None or d.device != device:
+            d = _lib.to_dev(self.phi, device)
+            self.__dict__["_phi_d"] = d
+        return d
+
+    def device_fhat(self, device):
+        d = self.__dict__.get("_fhat_d")
+        if d is None or d.device != device:
+            d = _lib.to_dev(self.f_hat, device).reshape(-1)
+            self.__dict__["_fhat_d"] = d
+        return d
+
+
+@dataclass
+class RomSolution:
+    """One reduced solve (rom.py:156-167)."""
+
+    basis_gen: int
+    uhat: object
+    u: object
+    lamhat: object
+    lam: object
+    j: float
+    residual_norm: float
+    grad: object = None
+
+
+@dataclass
+class ErrorReport:
+    """Residual norms and, in certified mode, error bounds (rom.py:170-179)."""
+
+    primal_residual: float
+    adjoint_residual: float
+    sigma_min: float | None = None
+    sigma_min_converged: bool = True
+    energy_error_bound: float | None = None
+    objective_error_bound: float | None = None
+
+
+class RomModel:
+    """Reduced evaluations bound to one HdmSolver (rom.py:182-390)."""
+
+    def __init__(self, solver: HdmSolver, stats: RunStats | None = None):
+        self.solver = solver
+        self.mesh = solver.mesh
+        self.k_e = solver.k_e
+        self.f = solver.f
+        self.free_mask = solver.free_mask
+        self.material = solver.material
+        self.stats = stats or solver.stats
+        self.device = solver.device
+        self._plan = solver._plan
+
+    # ------------------------------------------------------------------ basis
+    def build_basis(self, window: SnapshotWindow, center_u, center_lambda, is_compliance: bool, n_k: int,
+                    center_rho=None) -> ReducedBasis:
+        """POD of the window plus the exact center states, orthonormalised (rom.py:199-252)."""
+        t = _lib.torch()
+        native = _lib.is_torch(center_u)
+        if center_u is None:
+            raise ValueError("center primal state must be a nonzero vector")
+        cu = _lib.to_dev(center_u, self.device)
+        if float(t.linalg.vector_norm(cu)) == 0.0:
+            raise ValueError("center primal state must be a nonzero vector")
+        n_k = min(n_k, len(window))
+        blocks = [cu]
+        if not is_compliance:
+            blocks.append(_lib.to_dev(center_lambda, self.device))
+        if n_k > 0:
+            blocks.extend(_lib.to_dev(pod(window.primal_matrix(), n_k), self.device).t())
+            if not is_compliance:
+                blocks.extend(_lib.to_dev(pod(window.adjoint_matrix(), n_k), self.device).t())
+        free = self.solver._fixed_d == 0
+        cols = t.stack([t.where(free, b, t.zeros((), dtype=t.float64, device=self.device)) for b in blocks])
+        phi_d = _gs_device(cols.contiguous(), GS_DROP_TOL).contiguous()
+        if center_rho is not None:
+            f_eff = self.solver.apply_device(_lib.to_dev(center_rho, self.device), cu)
+        else:
+            f_eff = self.solver._f_d
+        f_hat = _project(phi_d, f_eff[None, :])[0]
+        basis = ReducedBasis(phi=_lib.to_user(phi_d, native), elem_phi=None, elem_k_phi=None,
+                             f_hat=_lib.to_user(f_hat, native))
+        basis.__dict__["_phi_d"] = phi_d
+        basis.__dict__["_fhat_d"] = f_hat
+        return basis
+
+    # ------------------------------------------------------------------ reduced operators
+    def reduced_stiffness_device(self, basis: ReducedBasis, rho_d):
+        """(nd, j, j) reduced stiffness for rho_d of shape (N_e,) or (nd, N_e)."""
+        t = _lib.torch()
+        phi_d = basis.device_phi(self.device)
+        k = phi_d.shape[1]
+        rho2 = rho_d.reshape(-1, self.mesh.n_elems).contiguous()
+        nd = rho2.shape[0]
+        khat = t.empty((nd, k, k), dtype=t.float64, device=self.device)
+        _lib.check(_lib.lib().tb_rom_reduced_stiffness(self._plan, _lib.ptr(phi_d), k, _lib.ptr(rho2), nd,
+                                                       _lib.ptr(khat), _stream(self.device)), "reduced_stiffness")
+        return khat
+
+    def reduced_stiffness(self, basis: ReducedBasis, rho):
+        """Dense j x j reduced stiffness Phi^T K(rho) Phi (rom.py:254-262)."""
+        native = _lib.is_torch(rho)
+        return _lib.to_user(self.reduced_stiffness_device(basis, _lib.to_dev(rho, self.device))[0], native)
+
+    def _chol_solve(self, khat_d, rhs_d):
+        """khat_d (nd,k,k), rhs_d (nd,nrhs,k) -> x (nd,nrhs,k); DegenerateBasisError if not SPD."""
+        t = _lib.torch()
+        nd, k = khat_d.shape[0], khat_d.shape[1]
+        nrhs = rhs_d.shape[1]
+        x = t.empty((nd, nrhs, k), dtype=t.float64, device=self.device)
+        status = (ctypes.c_int * nd)()
+        _lib.check(_lib.lib().tb_rom_cholesky_solve(k, nd, nrhs, _lib.ptr(khat_d.contiguous()),
+                                                    _lib.ptr(rhs_d.contiguous()), _lib.ptr(x), status,
+                                                    _stream(self.device)), "reduced Cholesky")
+        return x
+
+    def _residual_norms(self, phi_d, rho2, coef, g_d, g_stride):
+        nd = coef.shape[0]
+        out = (ctypes.c_double * nd)()
+        _lib.check(_lib.lib().tb_rom_residual_norms(self._plan, _lib.ptr(phi_d), phi_d.shape[1], _lib.ptr(rho2),
+                                                    _lib.ptr(coef.contiguous()), nd, _lib.ptr(g_d), g_stride, out,
+                                                    _stream(self.device)), "residual norms")
+        return [float(v) for v in out]
+
+    def solve(self, basis: ReducedBasis, rho, objective: Objective, compute_gradient: bool = False) -> RomSolution:
+        """Galerkin solve at density rho (rom.py:264-307)."""
+        t = _lib.torch()
+        native = _lib.is_torch(rho)
+        rho_d = _lib.to_dev(rho, self.device)
+        phi_d = basis.device_phi(self.device)
+        khat = self.reduced_stiffness_device(basis, rho_d)
+        uhat = self._chol_solve(khat, basis.device_fhat(self.device)[None, None, :])[0, 0]
+        u_d = _reconstruct(phi_d, uhat[None, :])[0]
+        u_u = _lib.to_user(u_d, native)
+        rho_u = rho if native else np.asarray(rho, dtype=float)
+        if objective.is_compliance:
+            lamhat, lam_d, lam_u = uhat, u_d, u_u
+        else:
+            g_d = _lib.to_dev(objective.du(u_u, rho_u), self.device)
+            g_hat = _project(phi_d, g_d[None, :])
+            lamhat = self._chol_solve(khat, g_hat[:, None, :])[0, 0]
+            lam_d = _reconstruct(phi_d, lamhat[None, :])[0]
+            lam_u = _lib.to_user(lam_d, native)
+        if isinstance(objective, ComplianceObjective):
+            j = self.solver.dot_device(objective.device_f(self.device), u_d)
+        else:
+            j = float(objective.value(u_u, rho_u))
+        rnorm = self._residual_norms(phi_d, rho_d[None, :], uhat[None, :], self.solver._f_d, 0)[0]
+        self.stats.rom_solves += 1
+        sol = RomSolution(basis_gen=basis.gen_id, uhat=_lib.to_user(uhat, native), u=u_u,
+                          lamhat=(_lib.to_user(uhat, native) if objective.is_compliance else _lib.to_user(lamhat, native)),
+                          lam=lam_u, j=j, residual_norm=rnorm)
+        if objective.is_compliance:
+            sol.lamhat = sol.uhat
+        if compute_gradient:
+            drho_d = None if objective.is_compliance else _lib.to_dev(objective.drho(u_u, rho_u), self.device)
+            s_d = self.solver.sensitivity_device(rho_d, u_d, lam_d, drho_d)
+            sol.grad = _lib.to_user(self.solver.filter.apply_adjoint_device(s_d), native)
+        return sol
+
+    def solve_batch(self, basis: ReducedBasis, rho_batch_d, f_hat_d=None):
+        """Batched compliance solves for nd designs (BASELINE cfg 5): returns
+        (khat (nd,k,k), uhat (nd,k), residual norms list)."""
+        phi_d = basis.device_phi(self.device)
+        rho2 = rho_batch_d.reshape(-1, self.mesh.n_elems).contiguous()
+        nd = rho2.shape[0]
+        khat = self.reduced_stiffness_device(basis, rho2)
+        fh = basis.device_fhat(self.device) if f_hat_d is None else f_hat_d
+        rhs = fh[None, None, :].expand(nd, 1, fh.shape[0]).contiguous()
+        uhat = self._chol_solve(khat, rhs)[:, 0, :].contiguous()
+        norms = []
+        for s in range(0, nd, 16):
+            e = min(nd, s + 16)
+            norms += self._residual_norms(phi_d, rho2[s:e], uhat[s:e], self.solver._f_d, 0)
+        self.stats.rom_solves += nd
+        return khat, uhat, norms
+
+    # ------------------------------------------------------------------ residuals
+    def _check_gen(self, basis, solution):
+        if solution.basis_gen != basis.gen_id:
+            raise BasisMismatchError("reduced solution does not belong to this basis generation")
+
+    def _resid_vec(self, basis, rho, coef, g_d, native):
+        phi_d = basis.device_phi(self.device)
+        c = _lib.to_dev(coef, self.device).reshape(1, -1)
+        u_d = _reconstruct(phi_d, c)[0]
+        y = self.solver.apply_device(_lib.to_dev(rho, self.device), u_d, mask_rows=True)
+        free = (self.solver._fixed_d == 0).to(y.dtype)
+        return _lib.to_user(y - g_d * free, native)
+
+    def residual_vector(self, basis: ReducedBasis, rho, uhat):
+        """K(rho) Phi uhat - f on the free dofs, zeros elsewhere (rom.py:319-325)."""
+        return self._resid_vec(basis, rho, uhat, self.solver._f_d, _lib.is_torch(uhat))
+
+    def residual_norm(self, basis: ReducedBasis, rho, solution: RomSolution) -> float:
+        """||K(rho) Phi uhat - f||_2 over free dofs (rom.py:327-335)."""
+        self._check_gen(basis, solution)
+        rho_d = _lib.to_dev(rho, self.device)
+        return self._residual_norms(basis.device_phi(self.device), rho_d[None, :],
+                                    _lib.to_dev(solution.uhat, self.device)[None, :], self.solver._f_d, 0)[0]
+
+    def adjoint_residual_vector(self, basis: ReducedBasis, rho, solution: RomSolution, objective: Objective):
+        """K(rho) lam_k - dj/du(u_k) on the free dofs (rom.py:337-347)."""
+        g_d = _lib.to_dev(objective.du(solution.u, rho), self.device)
+        return self._resid_vec(basis, rho, solution.lamhat, g_d, _lib.is_torch(solution.lamhat))
+
+    def error_bounds(self, basis: ReducedBasis, rho, solution: RomSolution, objective: Objective,
+                     mode: str = "cheap", power_max_iter: int = 200, power_rtol: float = 1e-10) -> ErrorReport:
+        """Residual-norm indicators, optionally with certified bounds (rom.py:349-390)."""
+        self._check_gen(basis, solution)
+        rho_d = _lib.to_dev(rho, self.device)
+        phi_d = basis.device_phi(self.device)
+        r_p = self._residual_norms(phi_d, rho_d[None, :], _lib.to_dev(solution.uhat, self.device)[None, :],
+                                   self.solver._f_d, 0)[0]
+        g_d = _lib.to_dev(objective.du(solution.u, rho), self.device)
+        r_a = self._residual_norms(phi_d, rho_d[None, :], _lib.to_dev(solution.lamhat, self.device)[None, :], g_d,
+                                   0)[0]
+        report = ErrorReport(primal_residual=r_p, adjoint_residual=r_a)
+        if mode == "cheap":
+            return report
+        if mode != "certified":
+            raise ValueError(f"unknown mode {mode!r}")
+        sigma, converged = self._smallest_eigenvalue(rho_d, power_max_iter, power_rtol)
+        report.sigma_min = sigma
+        report.sigma_min_converged = converged
+        if converged:
+            report.energy_error_bound = r_p / np.sqrt(sigma)
+            report.objective_error_bound = r_p**2 / sigma
+        return report
+
+    def _smallest_eigenvalue(self, rho_d, max_iter, rtol):
+        """Inverse power iteration (rom.py:393-407) with device pCG solves in place of the
+        sparse factorization; same deterministic start vector on the free dofs."""
+        t = _lib.torch()
+        free = np.flatnonzero(self.free_mask)
+        x_np = np.zeros(self.mesh.n_dofs)
+        x_np[free] = np.ones(free.size) + 1e-3 * np.sin(np.arange(free.size))
+        x = _lib.to_dev(x_np, self.device)
+        x = x / t.linalg.vector_norm(x)
+        prev = np.inf
+        for _ in range(max_iter):
+            y = self.solver.pcg_device(rho_d, x, rtol=1e-13)
+            x = y / t.linalg.vector_norm(y)
+            kx = self.solver.apply_device(rho_d, x, mask_rows=True)
+            ev = self.solver.dot_device(x, kx)
+            if abs(ev - prev) <= rtol * abs(ev):
+                return ev, True
+            prev = ev
+        return prev, False

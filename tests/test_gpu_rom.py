@@ -1,0 +1,182 @@
+"""GPU parity of the ROM path (Gram-Schmidt, POD, Phi^T f, Phi^T K Phi, reduced solve,
+residual / error estimates) against reference golden vectors and the CPU oracle.
+Tolerances: reduced operators and error estimates 1e-6 relative (BASELINE north_star)."""
+
+import numpy as np
+import pytest
+
+import paper_2004_05756_b200 as tb
+from conftest import golden
+from oracle.fem import build_grid
+from oracle.hdm import Filter, Hdm, Material
+from oracle.rom import Rom, gram_schmidt as gs_ref, pod as pod_ref
+from paper_2004_05756_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+MAT = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
+
+
+def frel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(np.asarray(b)), 1e-300)
+
+
+def build(prob, rtol=1e-12):
+    return tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, prob.radius), prob.f, prob.fixed, MAT,
+                        rtol=rtol)
+
+
+def test_gram_schmidt_matches_oracle(cuda):
+    rng = np.random.default_rng(3)
+    vecs = [rng.standard_normal(1000) for _ in range(6)]
+    vecs.insert(2, 2.0 * vecs[0])  # dependent -> dropped
+    vecs.insert(4, np.zeros(1000))  # zero -> skipped
+    q = tb.gram_schmidt(vecs)
+    q_ref = gs_ref(vecs)
+    assert q.shape == q_ref.shape == (1000, 6)
+    assert np.abs(q - q_ref).max() < 1e-12
+    assert np.abs(q.T @ q - np.eye(6)).max() < 1e-12
+    with pytest.raises(ValueError):
+        tb.gram_schmidt([np.zeros(5)])
+    assert tb.gram_schmidt([np.ones(5), -np.ones(5)]).shape[1] == 1
+
+
+def test_pod_matches_oracle(cuda):
+    rng = np.random.default_rng(1)
+    snaps = rng.standard_normal((50, 6))
+    u = tb.pod(snaps, 3)
+    u_ref = pod_ref(snaps, 3)
+    assert np.abs(u - u_ref).max() < 1e-10  # same sign convention, same vectors
+    assert tb.pod(snaps, 0).shape == (50, 0)
+    with pytest.raises(ValueError):
+        tb.pod(np.ones((5, 2)), 3)
+    G = golden("golden_small.npz")
+    assert np.abs(tb.pod(G["cant6x2_win"], 2) - G["cant6x2_pod2"]).max() < 1e-8
+
+
+def test_cfg1_rom_chain_vs_reference_golden(cuda):
+    G = golden("golden_cfg1.npz")
+    prob = configs.cfg1()
+    s = build(prob, rtol=1e-10)
+    obj = tb.ComplianceObjective(s.f)
+    snaps = [np.where(s.free_mask, s.solve(d, obj).u, 0.0) for d in prob.rom_designs]
+    phi = tb.gram_schmidt(snaps)
+    assert phi.shape[1] == int(G["rom_kept"])
+    basis = tb.ReducedBasis(phi, None, None, phi.T @ s.f)
+    rom = tb.RomModel(s)
+    rho, _ = s.filtered_density(prob.psi)
+    assert frel(rom.reduced_stiffness(basis, rho), G["rom_k_hat"]) <= 1e-6
+    rs = rom.solve(basis, rho, obj)
+    assert abs(rs.j - G["rom_j"]) <= 1e-8 * abs(G["rom_j"])
+    assert abs(rs.residual_norm - G["rom_residual"]) <= 1e-6 * G["rom_residual"]
+    assert rom.residual_norm(basis, rho, rs) == rs.residual_norm
+    assert s.stats.rom_solves == 1
+
+
+def test_reduced_operators_vs_oracle_exact_basis(cuda):
+    """Same Phi on both sides: k_hat, f_hat, uhat, residual to round-off."""
+    for k in (3, 10, 33, 64):
+        prob = configs.cfg1(seed=k, nx=40, ny=20)
+        s = build(prob)
+        g = build_grid(40, 20, 1.0)
+        ora = Hdm(g, prob.k_e, Filter(g, prob.radius), prob.f, prob.fixed, Material(configs.RHO_L, configs.P_SIMP))
+        rng = np.random.default_rng(k)
+        raw = rng.standard_normal((k, g.n_dofs))
+        raw[:, ~ora.free_mask] = 0.0
+        phi = gs_ref(list(raw))
+        rho = np.clip(rng.random(g.n_elems), 1e-3, 1.0)
+        rom = tb.RomModel(s)
+        basis = tb.ReducedBasis(phi, None, None, phi.T @ s.f)
+        kh = rom.reduced_stiffness(basis, rho)
+        kr = Rom(ora).reduced_stiffness_elemform(phi, rho)
+        assert frel(kh, kr) <= 1e-12
+        rs = rom.solve(basis, rho, tb.ComplianceObjective(s.f))
+        rr = Rom(ora).solve(phi, phi.T @ ora.f, rho)
+        assert frel(rs.uhat, rr["uhat"]) <= 1e-9
+        assert abs(rs.residual_norm - rr["residual_norm"]) <= 1e-9 * rr["residual_norm"]
+
+
+def test_batched_reduced_stiffness(cuda):
+    import torch
+
+    prob = configs.cfg1(seed=5, nx=32, ny=16)
+    s = build(prob)
+    g = build_grid(32, 16, 1.0)
+    ora = Hdm(g, prob.k_e, Filter(g, prob.radius), prob.f, prob.fixed, Material(configs.RHO_L, configs.P_SIMP))
+    rng = np.random.default_rng(0)
+    raw = rng.standard_normal((12, g.n_dofs))
+    raw[:, ~ora.free_mask] = 0.0
+    phi = gs_ref(list(raw))
+    rhos = np.clip(rng.random((5, g.n_elems)), 1e-3, 1.0)
+    rom = tb.RomModel(s)
+    basis = tb.ReducedBasis(phi, None, None, phi.T @ s.f)
+    khat, uhat, norms = rom.solve_batch(basis, torch.as_tensor(rhos, device=cuda))
+    for d in range(5):
+        rr = Rom(ora).solve(phi, phi.T @ ora.f, rhos[d])
+        assert frel(khat[d].cpu().numpy(), rr["k_hat"]) <= 1e-12
+        assert frel(uhat[d].cpu().numpy(), rr["uhat"]) <= 1e-9
+        assert abs(norms[d] - rr["residual_norm"]) <= 1e-9 * rr["residual_norm"]
+
+
+def test_small_fixture_build_basis_and_bounds(cuda):
+    G = golden("golden_small.npz")
+    key = "cant6x2"
+    mesh = tb.build_mesh(6, 2, 1.0)
+    s = tb.HdmSolver(mesh, tb.elasticity_element_matrix(1.0, 0.3), tb.HelmholtzFilter(mesh, 1.5), G[f"{key}_f"],
+                     G[f"{key}_fixed"], tb.MaterialModel(), rtol=1e-13)
+    obj = tb.ComplianceObjective(s.f)
+    sol = s.solve(G[f"{key}_psi"], obj)
+    win = tb.SnapshotWindow(5)
+    for c in range(G[f"{key}_win"].shape[1]):
+        win.append(G[f"{key}_win"][:, c], G[f"{key}_win"][:, c])
+    rom = tb.RomModel(s)
+    basis = rom.build_basis(win, sol.u, sol.lam, True, 2, center_rho=sol.rho)
+    assert basis.size == G[f"{key}_rom_phi"].shape[1]
+    # span/orientation: compare projectors
+    P = basis.phi @ basis.phi.T
+    Pr = G[f"{key}_rom_phi"] @ G[f"{key}_rom_phi"].T
+    assert np.abs(P - Pr).max() < 1e-8
+    rho_t = G[f"{key}_rom_rho"]
+    assert frel(rom.reduced_stiffness(basis, rho_t), G[f"{key}_rom_khat"]) <= 1e-6
+    rs = rom.solve(basis, rho_t, obj)
+    assert abs(rs.j - G[f"{key}_rom_j"]) <= 1e-8 * abs(G[f"{key}_rom_j"])
+    assert abs(rs.residual_norm - G[f"{key}_rom_res"]) <= 1e-6 * G[f"{key}_rom_res"]
+    rep = rom.error_bounds(basis, rho_t, rs, obj, mode="cheap")
+    assert rep.primal_residual == pytest.approx(rs.residual_norm, rel=1e-12)
+    assert rep.adjoint_residual == pytest.approx(rep.primal_residual, rel=1e-10)
+    rep = rom.error_bounds(basis, rho_t, rs, obj, mode="certified")
+    assert rep.sigma_min == pytest.approx(float(G[f"{key}_rom_sigma"]), rel=1e-6)
+    with pytest.raises(ValueError):
+        rom.error_bounds(basis, rho_t, rs, obj, mode="tight")
+
+
+def test_exact_span_and_errors(cuda):
+    mesh = tb.build_mesh(6, 2, 1.0)
+    f = np.zeros(mesh.n_dofs)
+    f[2 * mesh.node_id(6, 1) + 1] = -1.0
+    left = mesh.boundary_nodes("left")
+    s = tb.HdmSolver(mesh, tb.elasticity_element_matrix(1.0, 0.3), tb.HelmholtzFilter(mesh, 1.5), f,
+                     np.concatenate([2 * left, 2 * left + 1]), tb.MaterialModel(), rtol=1e-13)
+    obj = tb.ComplianceObjective(s.f)
+    psi = np.full(mesh.n_elems, 0.55)
+    sol = s.solve(psi, obj)
+    rom = tb.RomModel(s)
+    basis = rom.build_basis(tb.SnapshotWindow(20), sol.u, sol.lam, True, 0, center_rho=sol.rho)
+    assert basis.size == 1
+    rs = rom.solve(basis, sol.rho, obj)
+    assert np.linalg.norm(rs.u - sol.u) <= 1e-9 * np.linalg.norm(sol.u)
+    assert abs(rs.j - sol.j) <= 1e-9 * abs(sol.j)
+    assert rs.residual_norm <= 1e-9 * np.linalg.norm(s.f)
+    r0 = rom.residual_vector(basis, sol.rho, np.zeros(basis.size))
+    assert abs(np.linalg.norm(r0) - np.linalg.norm(s.f)) <= 1e-12
+    # rank-deficient basis -> DegenerateBasisError (reference tests/test_rom.py:293-307)
+    v = sol.u / np.linalg.norm(sol.u)
+    phi = np.column_stack([v, v])
+    with pytest.raises(tb.DegenerateBasisError):
+        rom.solve(tb.ReducedBasis(phi, None, None, phi.T @ s.f), sol.rho, obj)
+    # generation mismatch
+    basis2 = rom.build_basis(tb.SnapshotWindow(20), sol.u, sol.lam, True, 0, center_rho=sol.rho)
+    with pytest.raises(tb.BasisMismatchError):
+        rom.residual_norm(basis2, sol.rho, rs)
+    with pytest.raises(ValueError):
+        rom.build_basis(tb.SnapshotWindow(5), np.zeros(mesh.n_dofs), None, True, 0)

@@ -196,8 +196,8 @@ int pcg_profile(const PcgOp& op, PcgWork& w, const double* b, int nrep, double* 
                 cudaStream_t s) {
   const int nb = kUpdateBlocks;
   op.launch_dinv(w.dinv, s);
-  // tol2 < 0 and maxit = INT_MAX keep every iteration live
-  k_pcg_start<<<nb, kBlock, 0, s>>>(w.n, b, nullptr, w.dinv, w.x, w.r, w.z, w.pa, w.st, w.partC(), 1, -1.0,
+  // rtol = 0 (tol2 = 0) and maxit = INT_MAX keep every iteration live
+  k_pcg_start<<<nb, kBlock, 0, s>>>(w.n, b, nullptr, w.dinv, w.x, w.r, w.z, w.pa, w.st, w.partC(), 1, 0.0,
                                     0x7fffffff);
   launched(1);
   TB_CHECK_LAUNCH();

@@ -451,7 +451,7 @@ class RomModel:
         x = x / t.linalg.vector_norm(x)
         prev = np.inf
         for _ in range(max_iter):
-            y = self.solver.pcg_device(rho_d, x, rtol=1e-13)
+            y = self.solver.pcg_device(rho_d, x, rtol=1e-12)
             x = y / t.linalg.vector_norm(y)
             kx = self.solver.apply_device(rho_d, x, mask_rows=True)
             ev = self.solver.dot_device(x, kx)

@@ -1,4 +1,6 @@
 // pCG engine implementation (see pcg.cuh).
+#include <stdlib.h>
+
 #include "pcg.cuh"
 
 namespace tb {
@@ -13,6 +15,8 @@ int PcgWork::alloc(int64_t n_, int max_blocks) {
   TB_CUDA(cudaMalloc(&st, sizeof(PcgState)));
   TB_CUDA(cudaMemset(st, 0, sizeof(PcgState)));
   TB_CUDA(cudaMallocHost(&h_st, sizeof(PcgState)));
+  TB_CUDA(cudaMalloc(&barrier, 64));
+  TB_CUDA(cudaMemset(barrier, 0, 64));
   return TB_OK;
 }
 
@@ -22,6 +26,7 @@ void PcgWork::release() {
     if (p) cudaFree(p);
   if (st) cudaFree(st);
   if (h_st) cudaFreeHost(h_st);
+  if (barrier) cudaFree(barrier);
   if (exec) cudaGraphExecDestroy(exec);
   *this = PcgWork();
 }
@@ -138,13 +143,41 @@ static int build_graph(const PcgOp& op, PcgWork& w) {
   return TB_OK;
 }
 
+// TB_PCG_NOGRAPH=1 issues the same kernels as plain stream launches (ncu cannot profile kernel
+// nodes of graphs that contain conditional nodes); results are identical.
+static bool no_graph() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TB_PCG_NOGRAPH");
+    v = (e != nullptr && e[0] != '\0' && e[0] != '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+static int run_loop_plain(const PcgOp& op, PcgWork& w, cudaStream_t s) {
+  for (;;) {
+    for (int it = 0; it < kIters; ++it) {
+      double* pold = (it & 1) ? w.pb : w.pa;
+      double* pnew = (it & 1) ? w.pa : w.pb;
+      op.launch_fused(w, pold, pnew, s);
+      k_pcg_update<<<kUpdateBlocks, kBlock, 0, s>>>(w.n, pnew, w.q, w.dinv, w.x, w.r, w.z, w.st, w.partB());
+    }
+    TB_CHECK_LAUNCH();
+    TB_CUDA(cudaMemcpyAsync(w.h_st, w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    TB_CUDA(cudaStreamSynchronize(s));
+    if (w.h_st->done != 0) return TB_OK;
+  }
+}
+
 int pcg_solve(const PcgOp& op, PcgWork& w, const double* b, double* x_out, double rtol, int maxit, int* iters,
               double* relres, cudaStream_t s) {
   if (!(rtol > 0.0) || maxit < 1) {
     set_error("pcg: rtol must be > 0 and maxit >= 1 (got %g, %d)", rtol, maxit);
     return TB_ERR_INVALID;
   }
-  if (!w.exec) TB_TRY(build_graph(op, w));
+  const bool plain = no_graph();
+  const bool persistent = !plain && op.has_persistent();
+  if (!plain && !persistent && !w.exec) TB_TRY(build_graph(op, w));
   const int nb = kUpdateBlocks;
   op.launch_dinv(w.dinv, s);
   k_pcg_start<<<nb, kBlock, 0, s>>>(w.n, b, nullptr, w.dinv, w.x, w.r, w.z, w.pa, w.st, w.partC(), 1, rtol, maxit);
@@ -154,7 +187,14 @@ int pcg_solve(const PcgOp& op, PcgWork& w, const double* b, double* x_out, doubl
   int iters_before = 0, stalls = 0;
   double best_rr = -1.0;
   for (int restart = 0;; ++restart) {
-    TB_CUDA(cudaGraphLaunch(w.exec, s));
+    if (plain) {
+      TB_TRY(run_loop_plain(op, w, s));
+    } else if (persistent) {
+      op.launch_persistent(w, s);
+      TB_CHECK_LAUNCH();
+    } else {
+      TB_CUDA(cudaGraphLaunch(w.exec, s));
+    }
     // true residual check at exit
     op.launch_apply(w.x, w.tmp, s);
     k_pcg_start<<<nb, kBlock, 0, s>>>(w.n, b, w.tmp, w.dinv, w.x, w.r, w.z, w.pa, w.st, w.partC(), 0, rtol, maxit);
@@ -165,7 +205,8 @@ int pcg_solve(const PcgOp& op, PcgWork& w, const double* b, double* x_out, doubl
     const PcgState& h = *w.h_st;
     const int delta = h.iters - iters_before;
     iters_before = h.iters;
-    launched((int64_t)(delta > 0 ? (delta + kIters - 1) / kIters : 1) * (2 * kIters + 1));
+    if (persistent) launched(1);
+    else launched((int64_t)(delta > 0 ? (delta + kIters - 1) / kIters : 1) * (2 * kIters + 1));
     if (h.done == 1) break;  // true residual within tolerance
     if (h.done == 3) {
       set_error("pCG breakdown after %d iterations: p^T K p <= 0 or non-finite; matrix is not positive definite",

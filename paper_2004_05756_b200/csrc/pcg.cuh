@@ -26,6 +26,10 @@ struct PcgOp {
   virtual void launch_apply(const double* v, double* y, cudaStream_t s) const = 0;
   // Jacobi inverse diagonal (0 on fixed dofs)
   virtual void launch_dinv(double* dinv, cudaStream_t s) const = 0;
+  // Whole iteration loop in one persistent cooperative launch (operators without a persistent
+  // variant use the conditional-graph loop).
+  virtual bool has_persistent() const { return false; }
+  virtual void launch_persistent(const PcgWork& w, cudaStream_t s) const { (void)w; (void)s; }
 };
 
 struct PcgWork {
@@ -35,6 +39,7 @@ struct PcgWork {
   int part_stride = 0;  // doubles per partial region
   PcgState* st = nullptr;
   PcgState* h_st = nullptr;  // pinned
+  void* barrier = nullptr;   // GridBarrier of the persistent kernel
   cudaGraphExec_t exec = nullptr;
   double* partA() const { return part; }
   double* partB() const { return part + 2 * part_stride; }

@@ -16,6 +16,9 @@ struct ElastOp final : PcgOp {
   void launch_fused(const PcgWork& w, const double* pold, double* pnew, cudaStream_t s) const override;
   void launch_apply(const double* v, double* y, cudaStream_t s) const override;
   void launch_dinv(double* dinv, cudaStream_t s) const override;
+  bool has_persistent() const override { return persist_grid > 0; }
+  void launch_persistent(const PcgWork& w, cudaStream_t s) const override;
+  int persist_grid = 0;
 };
 
 // Helmholtz operator  H = sum_e (r^2 S_e + M_e)  (pure Neumann)
@@ -26,6 +29,9 @@ struct HelmOp final : PcgOp {
   void launch_fused(const PcgWork& w, const double* pold, double* pnew, cudaStream_t s) const override;
   void launch_apply(const double* v, double* y, cudaStream_t s) const override;
   void launch_dinv(double* dinv, cudaStream_t s) const override;
+  bool has_persistent() const override { return persist_grid > 0; }
+  void launch_persistent(const PcgWork& w, cudaStream_t s) const override;
+  int persist_grid = 0;
 };
 
 struct tb_plan_impl {

@@ -126,7 +126,7 @@ class HdmSolution:
     @property
     def psi_hash(self) -> str:
         if self._psi_hash is None:  # native mode: hash on first request only
-            self._psi_hash = psi_digest(self._psi_ref)
+            self._psi_hash = psi_digest(self._psi_ref[0])
         return self._psi_hash
 
     def __repr__(self):
@@ -272,7 +272,8 @@ class HdmSolver:
             self.stats.hdm_adjoint_solves += 1
             j = float(objective.value(u_u, rho_u))
         if native:
-            return HdmSolution(None, rho_u, u_u, lam_u, j, clamp_width, None, psi_ref=psi_d.clone(),
+            keep = psi_d.clone() if psi_d is psi else psi_d  # snapshot of the design's bytes
+            return HdmSolution(None, rho_u, u_u, lam_u, j, clamp_width, None, psi_ref=(keep, psi, psi._version),
                                iterations=iters, relres=relres)
         return HdmSolution(psi_digest(psi), rho_u, u_u, lam_u, j, clamp_width, None, iterations=iters,
                            relres=relres)
@@ -281,8 +282,12 @@ class HdmSolver:
         """Adjoint gradient of J at psi; requires a matching solution (hdm.py:199-209)."""
         native = _lib.is_torch(psi)
         if native and solution._psi_ref is not None:
-            ref = solution._psi_ref
-            same = tuple(ref.shape) == tuple(psi.shape) and bool(_lib.torch().equal(ref, psi.to(ref.device, ref.dtype)))
+            ref, src, version = solution._psi_ref
+            if psi is src and psi._version == version:
+                same = True  # the very tensor the solution was computed from, never modified since
+            else:
+                same = tuple(ref.shape) == tuple(psi.shape) and bool(
+                    _lib.torch().equal(ref, psi.to(ref.device, ref.dtype)))
         else:
             same = psi_digest(psi) == solution.psi_hash
         if not same:

@@ -1,0 +1,286 @@
+// Single-reduction persistent Jacobi-pCG for 2D structured grids (Chronopoulos-Gear CG).
+//
+// Why: on BASELINE cfg 1-2 the whole working set (< 20 MB) sits in L2 and a Jacobi-pCG
+// iteration is worth ~3 us of memory traffic, so kernel boundaries and grid-wide reductions
+// dominate.  This kernel runs the entire solve in one cooperative launch with ONE grid
+// barrier per iteration:
+//
+//   CG-CG recurrences (x, r, u = D^-1 r, w = A u, p, s = A p):
+//     p_i = u_i + b_i p_{i-1};  s_i = w_i + b_i s_{i-1}
+//     x_{i+1} = x_i + a_i p_i;  r_{i+1} = r_i - a_i s_i;  u_{i+1} = D^-1 r_{i+1};  w_{i+1} = A u_{i+1}
+//     g_{i+1} = (r,u), d_{i+1} = (w,u), rho_{i+1} = (r,r)       <- the only reduction
+//     b_{i+1} = g_{i+1}/g_i;  a_{i+1} = g_{i+1} / (d_{i+1} - b_{i+1} g_{i+1}/a_i)
+//
+// Each CTA owns a contiguous node range and keeps x, r, p, s, w, D^-1 of it in shared memory.
+// The matvec needs u_{i+1} on a one-node halo; instead of a second barrier the CTA recomputes
+// the halo's u_{i+1} = D^-1 (r_i - a_i (w_i + b_i s_{i-1})) from vectors its neighbours
+// published before the previous barrier (parity double-buffered in global memory).  Partials
+// are summed by every CTA in the same fixed order: deterministic, identical decisions.
+#pragma once
+
+#include "persist.cuh"
+
+namespace tb {
+
+// cooperative-groups-style barrier: one atomic per CTA, bit 31 flips when all have arrived.
+__device__ __forceinline__ void grid_sync_flip(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int nb = gridDim.x;
+    const unsigned int add = (blockIdx.x == 0) ? (0x80000000u - (nb - 1u)) : 1u;
+    __threadfence();
+    const unsigned int old = atomicAdd(bar, add);
+    unsigned int cur;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+    } while (((old ^ cur) & 0x80000000u) == 0u);
+    __threadfence();  // also invalidates this SM's L1
+  }
+  __syncthreads();
+}
+
+struct CgcgArgs {
+  const double* b;     // unused (restart state comes from r, x)
+  double* x;           // in: x0 ; out: solution
+  const double* r0;    // r0 = Z (b - K x0) (k_pcg_start)
+  const double* dinv;  // Jacobi inverse diagonal, 0 on fixed dofs
+  double* pub;         // published vectors [2 parities][3 (r, w, s)][n_dofs]
+  double* part;        // [3][gridDim.x]
+  PcgState* st;
+  unsigned int* bar;
+  int own_max;         // max nodes owned by a CTA
+};
+
+constexpr int kCgcgThreads = 512;
+
+template <int NC, bool SCALED>
+__global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * NC> K, const double* __restrict__ alpha,
+                                                               CgcgArgs a) {
+  extern __shared__ double sm[];
+  __shared__ Mat<4 * NC> Ks;
+  __shared__ double bc[3];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int nbk = gridDim.x;
+  const int64_t N = g.n_nodes, ND = (int64_t)NC * N;
+  const int64_t per = (N + nbk - 1) / nbk;
+  const int64_t n0 = (int64_t)blockIdx.x * per;
+  const int64_t n1 = min(N, n0 + per);
+  const int no = (int)max((int64_t)0, n1 - n0);
+  const int64_t h0 = max((int64_t)0, n0 - g.nnx - 1);
+  const int64_t h1 = min(N, n1 + g.nnx + 1);
+  const int ne_ext = (int)(h1 - h0);
+  // element rows touching own nodes
+  const int j_lo = (int)(n0 / g.nnx), j_hi = (int)((max(n1, n0 + 1) - 1) / g.nnx);
+  const int64_t e0 = (int64_t)max(0, j_lo - 1) * g.nx;
+  const int64_t e1 = (int64_t)min(g.ny, j_hi + 1) * g.nx;
+  // shared-memory carve-up
+  double* u_ext = sm;                          // (h1-h0)*NC
+  double* xs = u_ext + (size_t)ne_ext * NC;    // own: x, r, p, s, w, dinv
+  double* rs = xs + (size_t)no * NC;
+  double* ps = rs + (size_t)no * NC;
+  double* ss = ps + (size_t)no * NC;
+  double* ws = ss + (size_t)no * NC;
+  double* ds = ws + (size_t)no * NC;
+  double* as = ds + (size_t)no * NC;           // alpha of elements [e0, e1)
+  for (int o = tid; o < 16 * NC * NC; o += nt) Ks.v[o] = K.v[o];
+  for (int64_t e = e0 + tid; e < e1; e += nt) as[e - e0] = SCALED ? alpha[e] : 1.0;
+
+  const int64_t d0 = (int64_t)NC * n0;
+  const int nod = no * NC;
+  // ---- prologue: x, r, D^-1 from global; u on own + halo; s_{-1} = p_{-1} = 0 ----
+  for (int o = tid; o < nod; o += nt) {
+    xs[o] = a.x[d0 + o];
+    rs[o] = a.r0[d0 + o];
+    ds[o] = a.dinv[d0 + o];
+    ps[o] = 0.0;
+    ss[o] = 0.0;
+  }
+  for (int64_t o = tid; o < (int64_t)ne_ext * NC; o += nt) {
+    const int64_t d = h0 * NC + o;
+    u_ext[o] = a.dinv[d] * a.r0[d];
+  }
+  __syncthreads();
+
+  double* pubr[2] = {a.pub, a.pub + 3 * ND};
+  auto node_apply = [&](int64_t n, double (&out)[NC]) {
+    const int i = (int)(n % g.nnx), j = (int)(n / g.nnx);
+    double P[9][NC];
+    double sc[4];
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) {
+        const int ii = i + dx - 1, jj = j + dy - 1;
+        const bool ok = ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
+        const int64_t m = (int64_t)jj * g.nnx + ii;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) P[dy * 3 + dx][c] = ok ? u_ext[(m - h0) * NC + c] : 0.0;
+      }
+#pragma unroll
+    for (int sl = 0; sl < 4; ++sl) {
+      const int ei = i - 1 + (sl & 1), ej = j - 1 + (sl >> 1);
+      const bool ok = ei >= 0 && ei < g.nx && ej >= 0 && ej < g.ny;
+      sc[sl] = ok ? as[(int64_t)ej * g.nx + ei - e0] : 0.0;
+    }
+    node_rows<2, NC>(Ks, P, sc, out);
+  };
+
+  // w_0 = A u_0 ; partials ; publish r_0, w_0, s_{-1}
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int o = tid; o < no; o += nt) {
+    const int64_t n = n0 + o;
+    double out[NC];
+    node_apply(n, out);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int od = o * NC + c;
+      const double u = u_ext[(n - h0) * NC + c];
+      ws[od] = out[c];
+      acc[0] = fma(rs[od], u, acc[0]);
+      acc[1] = fma(out[c], u, acc[1]);
+      acc[2] = fma(rs[od], rs[od], acc[2]);
+      pubr[0][d0 + od] = rs[od];
+      pubr[0][ND + d0 + od] = out[c];
+      pubr[0][2 * ND + d0 + od] = 0.0;
+    }
+  }
+  block_sum<3>(acc);
+  if (tid == 0) {
+    a.part[blockIdx.x] = acc[0];
+    a.part[nbk + blockIdx.x] = acc[1];
+    a.part[2 * nbk + blockIdx.x] = acc[2];
+  }
+  grid_sync_flip(a.bar);
+
+  double gam = 0.0, al = 0.0, be = 0.0, rr = 0.0;
+  int it = a.st->iters, done = 0;
+  const int maxit = a.st->maxit;
+  const double tol2 = a.st->tol2;
+  int par = 0;  // parity of the buffer holding (r_i, w_i, s_{i-1})
+  for (bool first = true;; first = false) {
+    // fixed-order sums of the partials (every CTA identically)
+    if (tid < 32) {
+#pragma unroll
+      for (int v = 0; v < 3; ++v) {
+        double s = 0.0;
+        for (int b = tid; b < nbk; b += 32) s += __ldcg(a.part + v * nbk + b);
+        s = warp_sum(s);
+        if (tid == 0) bc[v] = s;
+      }
+    }
+    __syncthreads();
+    const double gnew = bc[0], dnew = bc[1];
+    rr = bc[2];
+    __syncthreads();
+    if (!isfinite(gnew) || !isfinite(dnew) || !isfinite(rr)) {
+      done = 3;
+      break;
+    }
+    if (!first) {
+      ++it;
+      if (rr <= tol2) {
+        done = 1;
+        break;
+      }
+      if (it >= maxit) {
+        done = 2;
+        break;
+      }
+    } else if (rr == 0.0 || rr <= tol2) {
+      done = 1;
+      break;
+    }
+    if (first) {
+      be = 0.0;
+      if (!(dnew > 0.0)) {
+        done = 3;
+        break;
+      }
+      al = gnew / dnew;
+    } else {
+      be = gnew / gam;
+      const double pap = dnew - be * gnew / al;  // p^T A p
+      if (!(pap > 0.0)) {
+        done = 3;
+        break;
+      }
+      al = gnew / pap;
+    }
+    gam = gnew;
+
+    // ---- own: p, s, x, r, u ----
+    for (int o = tid; o < nod; o += nt) {
+      const double di = ds[o];
+      const int64_t n = n0 + o / NC;
+      const double u = u_ext[(n - h0) * NC + (o % NC)];
+      const double p = fma(be, ps[o], u);
+      const double s = fma(be, ss[o], ws[o]);
+      ps[o] = p;
+      ss[o] = s;
+      double r = rs[o];
+      if (di != 0.0) {
+        xs[o] = fma(al, p, xs[o]);
+        r = fma(-al, s, r);
+      }
+      rs[o] = r;
+    }
+    // ---- halo: u_{i+1} = D^-1 (r_i - al (w_i + be s_{i-1})) from the neighbours' publication ----
+    const double* pr = pubr[par];
+    for (int64_t m = h0 * NC + tid; m < h1 * NC; m += nt) {
+      if (m >= d0 && m < d0 + nod) continue;
+      const double di = a.dinv[m];
+      double r = __ldcg(pr + m);
+      if (di != 0.0) r = fma(-al, fma(be, __ldcg(pr + 2 * ND + m), __ldcg(pr + ND + m)), r);
+      u_ext[m - h0 * NC] = di * r;
+    }
+    __syncthreads();
+    for (int o = tid; o < nod; o += nt) {
+      const int64_t n = n0 + o / NC;
+      u_ext[(n - h0) * NC + (o % NC)] = ds[o] * rs[o];
+    }
+    __syncthreads();
+    // ---- own: w_{i+1} = A u_{i+1}; partials; publish (r_{i+1}, w_{i+1}, s_i) ----
+    double* pw = pubr[par ^ 1];
+    double acc3[3] = {0.0, 0.0, 0.0};
+    for (int o = tid; o < no; o += nt) {
+      const int64_t n = n0 + o;
+      double out[NC];
+      node_apply(n, out);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int od = o * NC + c;
+        const double u = u_ext[(n - h0) * NC + c];
+        ws[od] = out[c];
+        acc3[0] = fma(rs[od], u, acc3[0]);
+        acc3[1] = fma(out[c], u, acc3[1]);
+        acc3[2] = fma(rs[od], rs[od], acc3[2]);
+        pw[d0 + od] = rs[od];
+        pw[ND + d0 + od] = out[c];
+        pw[2 * ND + d0 + od] = ss[od];
+      }
+    }
+    block_sum<3>(acc3);
+    if (tid == 0) {
+      a.part[blockIdx.x] = acc3[0];
+      a.part[nbk + blockIdx.x] = acc3[1];
+      a.part[2 * nbk + blockIdx.x] = acc3[2];
+    }
+    par ^= 1;
+    grid_sync_flip(a.bar);
+  }
+  for (int o = tid; o < nod; o += nt) a.x[d0 + o] = xs[o];
+  if (blockIdx.x == 0 && tid == 0) {
+    a.st->rr = rr;
+    a.st->iters = it;
+    a.st->done = done;
+  }
+}
+
+// dynamic shared memory of one CTA for a given ownership size
+inline size_t cgcg_smem_bytes(int NC, int64_t own, int64_t nnx, int64_t nx) {
+  const int64_t ext = own + 2 * (nnx + 1);
+  const int64_t rows = own / nnx + 3;
+  return sizeof(double) * (size_t)(ext * NC + 6 * own * NC + (rows + 1) * nx);
+}
+
+}  // namespace tb

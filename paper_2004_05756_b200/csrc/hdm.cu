@@ -7,7 +7,7 @@
 
 #include "pcg.cuh"
 #include "plan.cuh"
-#include "persist.cuh"
+#include "cgcg2d.cuh"
 #include "q1.cuh"
 
 namespace tb {
@@ -153,40 +153,52 @@ void HelmOp::launch_dinv(double* dinv, cudaStream_t s) const {
 }
 int HelmOp::fused_blocks() const { return nblk(filt->g.n_nodes); }
 
-// grid of the persistent kernel: every CTA co-resident (cooperative launch), 0 if unsupported
-template <int D, int NC, bool SCALED>
-static int persist_grid_for(int64_t n_nodes) {
-  int dev = 0, sms = 0, coop = 0, occ = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+// Grid of the single-reduction persistent kernel (one CTA per SM, every CTA co-resident), or 0
+// when the device cannot launch it cooperatively or a CTA's node range exceeds shared memory.
+template <int NC, bool SCALED>
+static int persist_grid_for(const Grid& g) {
+  int dev = 0, sms = 0, coop = 0, occ = 0, smem_max = 0;
+  if (g.dim != 2 || cudaGetDevice(&dev) != cudaSuccess) return 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-  if (!coop) return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg_persistent<D, NC, SCALED>, kPersistThreads, 0) !=
+  cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (!coop || sms < 1) return 0;
+  // at most one CTA per SM, at least ~128 nodes per CTA (fewer CTAs = cheaper barriers)
+  const int64_t want = (g.n_nodes + 127) / 128;
+  const int grid = (int)(want < sms ? (want < 1 ? 1 : want) : sms);
+  const int64_t own = (g.n_nodes + grid - 1) / grid;
+  const size_t smem = cgcg_smem_bytes(NC, own, g.nnx, g.nx);
+  if (smem + 2048 > (size_t)smem_max) return 0;
+  if (cudaFuncSetAttribute(k_pcg2d_cgcg<NC, SCALED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg2d_cgcg<NC, SCALED>, kCgcgThreads, smem) !=
           cudaSuccess ||
       occ < 1)
     return 0;
-  const int64_t need = (n_nodes + kPersistThreads - 1) / kPersistThreads;
-  const int64_t grid = (int64_t)sms * occ < need ? (int64_t)sms * occ : need;
-  return (int)(grid < 1 ? 1 : grid);
+  return grid;
 }
 
-template <int D, int NC, bool SCALED>
-static void launch_coop(const Grid& g, const Mat<Q1<D>::NN * NC>& K, const double* alpha, const PcgWork& w,
-                        int grid, cudaStream_t s) {
-  PersistArgs a{w.x, w.r, w.z, w.pa, w.pb, w.q, w.dinv, w.partA(), w.st, reinterpret_cast<GridBarrier*>(w.barrier)};
+template <int NC, bool SCALED>
+static void launch_cgcg(const Grid& g, const Mat<4 * NC>& K, const double* alpha, const PcgWork& w, int grid,
+                        cudaStream_t s) {
+  const int64_t own = (g.n_nodes + grid - 1) / grid;
+  const size_t smem = cgcg_smem_bytes(NC, own, g.nnx, g.nx);
+  CgcgArgs a{nullptr, w.x, w.r, w.dinv, w.pub, w.partA(), w.st, reinterpret_cast<unsigned int*>(w.barrier),
+             (int)own};
   Grid gg = g;
-  Mat<Q1<D>::NN * NC> KK = K;
+  Mat<4 * NC> KK = K;
   const double* al = alpha;
   void* args[] = {&gg, &KK, &al, &a};
-  cudaLaunchCooperativeKernel((const void*)k_pcg_persistent<D, NC, SCALED>, grid, kPersistThreads, args, 0, s);
+  cudaLaunchCooperativeKernel((const void*)k_pcg2d_cgcg<NC, SCALED>, grid, kCgcgThreads, args, smem, s);
 }
 
 void ElastOp::launch_persistent(const PcgWork& w, cudaStream_t s) const {
-  launch_coop<2, 2, true>(plan->g, plan->K2, plan->d_alpha, w, persist_grid, s);
+  launch_cgcg<2, true>(plan->g, plan->K2, plan->d_alpha, w, persist_grid, s);
 }
 
 void HelmOp::launch_persistent(const PcgWork& w, cudaStream_t s) const {
-  launch_coop<2, 1, false>(filt->g, filt->H2, nullptr, w, persist_grid, s);
+  launch_cgcg<1, false>(filt->g, filt->H2, nullptr, w, persist_grid, s);
 }
 
 void tb_plan_impl::apply_alpha(const double* alpha, const double* v, double* y, bool mask, cudaStream_t s) const {
@@ -244,7 +256,7 @@ int tb_plan_create(int dim, int nx, int ny, int nz, double h, const double* k_e,
   else
     memcpy(P->K3.v, k_e, sizeof(double) * ne * ne);
   P->op.plan = P;
-  if (dim == 2) P->op.persist_grid = persist_grid_for<2, 2, true>(P->g.n_nodes);
+  if (dim == 2) P->op.persist_grid = persist_grid_for<2, true>(P->g);
   int rc = P->init(fixed);
   if (rc != TB_OK) {
     P->release();
@@ -380,9 +392,8 @@ int tb_filter_create(int dim, int nx, int ny, int nz, double h, double radius, i
   }
   F->vol_share = pow(g.h, g.dim) / nn;  // b_e entries = h^d / 2^d (filtering.py:75-76)
   F->op.filt = F;
-  // 3D filters keep the graph loop (the 27-point persistent variant spills)
-  F->op.persist_grid = (g.dim == 2) ? persist_grid_for<2, 1, false>(g.n_nodes) : 0;
-  int rc = F->work.alloc(g.n_nodes, F->op.fused_blocks());
+  F->op.persist_grid = (g.dim == 2) ? persist_grid_for<1, false>(g) : 0;  // 3D: graph loop
+  int rc = F->work.alloc(g.n_nodes, F->op.fused_blocks(), F->op.persist_grid > 0);
   if (rc == TB_OK) {
     cudaError_t e = cudaMalloc(&F->d_b, sizeof(double) * g.n_nodes);
     if (e != cudaSuccess) {

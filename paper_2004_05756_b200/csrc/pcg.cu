@@ -5,7 +5,7 @@
 
 namespace tb {
 
-int PcgWork::alloc(int64_t n_, int max_blocks) {
+int PcgWork::alloc(int64_t n_, int max_blocks, bool with_pub) {
   n = n_;
   part_stride = max_blocks > kUpdateBlocks ? max_blocks : kUpdateBlocks;
   const size_t vb = sizeof(double) * (size_t)n;
@@ -17,6 +17,7 @@ int PcgWork::alloc(int64_t n_, int max_blocks) {
   TB_CUDA(cudaMallocHost(&h_st, sizeof(PcgState)));
   TB_CUDA(cudaMalloc(&barrier, 64));
   TB_CUDA(cudaMemset(barrier, 0, 64));
+  if (with_pub) TB_CUDA(cudaMalloc(&pub, sizeof(double) * 6 * (size_t)n));
   return TB_OK;
 }
 
@@ -27,6 +28,7 @@ void PcgWork::release() {
   if (st) cudaFree(st);
   if (h_st) cudaFreeHost(h_st);
   if (barrier) cudaFree(barrier);
+  if (pub) cudaFree(pub);
   if (exec) cudaGraphExecDestroy(exec);
   *this = PcgWork();
 }

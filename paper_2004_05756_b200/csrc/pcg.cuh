@@ -39,12 +39,13 @@ struct PcgWork {
   int part_stride = 0;  // doubles per partial region
   PcgState* st = nullptr;
   PcgState* h_st = nullptr;  // pinned
-  void* barrier = nullptr;   // GridBarrier of the persistent kernel
+  void* barrier = nullptr;   // grid-barrier word of the persistent kernel
+  double* pub = nullptr;     // persistent kernel's published vectors [2][3][n]
   cudaGraphExec_t exec = nullptr;
   double* partA() const { return part; }
   double* partB() const { return part + 2 * part_stride; }
   double* partC() const { return part + 4 * part_stride; }
-  int alloc(int64_t n_, int max_blocks);
+  int alloc(int64_t n_, int max_blocks, bool with_pub = false);
   void release();
 };
 

@@ -54,7 +54,7 @@ int tb_plan_impl::init(const uint8_t* fixed_host) {
   TB_CUDA(cudaMalloc(&d_scratch, sizeof(double) * 8 * 148 * 8));
   TB_CUDA(cudaMalloc(&d_scalar, sizeof(double) * 16));
   TB_CUDA(cudaMallocHost(&h_scalar, sizeof(double) * 16));
-  TB_TRY(work.alloc(n_dofs, op.fused_blocks()));
+  TB_TRY(work.alloc(n_dofs, op.fused_blocks(), op.persist_grid > 0));
   return TB_OK;
 }
 

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtopo_b200.so")
+LIB_PATH = os.environ.get("TB_LIB_PATH") or os.path.join(_HERE, "libtopo_b200.so")
 
 TB_OK = 0
 TB_ERR_INVALID = 1

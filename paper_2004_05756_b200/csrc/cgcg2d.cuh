@@ -22,6 +22,26 @@
 
 namespace tb {
 
+#ifdef TB_CGCG_PROF
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PROF_MARK(k)                                  \
+  do {                                                \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {        \
+      const unsigned long long t_ = gtime();          \
+      prof[k] += t_ - prof_last;                      \
+      prof_last = t_;                                 \
+    }                                                 \
+  } while (0)
+#else
+#define PROF_MARK(k) \
+  do {               \
+  } while (0)
+#endif
+
 // cooperative-groups-style barrier: one atomic per CTA, bit 31 flips when all have arrived.
 __device__ __forceinline__ void grid_sync_flip(unsigned int* bar) {
   __syncthreads();
@@ -57,7 +77,7 @@ template <int NC, bool SCALED>
 __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * NC> K, const double* __restrict__ alpha,
                                                                CgcgArgs a) {
   extern __shared__ double sm[];
-  __shared__ Mat<4 * NC> Ks;
+  __shared__ __align__(16) Mat<4 * NC> Ks;
   __shared__ double bc[3];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int nbk = gridDim.x;
@@ -102,8 +122,9 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
   __syncthreads();
 
   double* pubr[2] = {a.pub, a.pub + 3 * ND};
-  auto node_apply = [&](int64_t n, double (&out)[NC]) {
-    const int i = (int)(n % g.nnx), j = (int)(n / g.nnx);
+  const int nnx = g.nnx, h0i = (int)h0, e0i = (int)e0, n0i = (int)n0;
+  auto node_apply = [&](int n, double (&out)[NC]) {
+    const int j = n / nnx, i = n - j * nnx;
     double P[9][NC];
     double sc[4];
 #pragma unroll
@@ -112,15 +133,15 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
       for (int dx = 0; dx < 3; ++dx) {
         const int ii = i + dx - 1, jj = j + dy - 1;
         const bool ok = ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
-        const int64_t m = (int64_t)jj * g.nnx + ii;
+        const int m = jj * nnx + ii - h0i;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) P[dy * 3 + dx][c] = ok ? u_ext[(m - h0) * NC + c] : 0.0;
+        for (int c = 0; c < NC; ++c) P[dy * 3 + dx][c] = ok ? u_ext[m * NC + c] : 0.0;
       }
 #pragma unroll
     for (int sl = 0; sl < 4; ++sl) {
       const int ei = i - 1 + (sl & 1), ej = j - 1 + (sl >> 1);
       const bool ok = ei >= 0 && ei < g.nx && ej >= 0 && ej < g.ny;
-      sc[sl] = ok ? as[(int64_t)ej * g.nx + ei - e0] : 0.0;
+      sc[sl] = ok ? as[ej * g.nx + ei - e0i] : 0.0;
     }
     node_rows<2, NC>(Ks, P, sc, out);
   };
@@ -128,13 +149,13 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
   // w_0 = A u_0 ; partials ; publish r_0, w_0, s_{-1}
   double acc[3] = {0.0, 0.0, 0.0};
   for (int o = tid; o < no; o += nt) {
-    const int64_t n = n0 + o;
+    const int n = n0i + o;
     double out[NC];
     node_apply(n, out);
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const int od = o * NC + c;
-      const double u = u_ext[(n - h0) * NC + c];
+      const double u = u_ext[(n - h0i) * NC + c];
       ws[od] = out[c];
       acc[0] = fma(rs[od], u, acc[0]);
       acc[1] = fma(out[c], u, acc[1]);
@@ -152,6 +173,10 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
   }
   grid_sync_flip(a.bar);
 
+#ifdef TB_CGCG_PROF
+  unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long prof_last = gtime();
+#endif
   double gam = 0.0, al = 0.0, be = 0.0, rr = 0.0;
   int it = a.st->iters, done = 0;
   const int maxit = a.st->maxit;
@@ -159,16 +184,27 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
   int par = 0;  // parity of the buffer holding (r_i, w_i, s_{i-1})
   for (bool first = true;; first = false) {
     // fixed-order sums of the partials (every CTA identically)
+    // (all loads issued before any add: one L2 round trip, not a dependent chain)
     if (tid < 32) {
+      constexpr int kPB = 8;  // supports up to 256 CTAs
+      double v[3][kPB];
 #pragma unroll
-      for (int v = 0; v < 3; ++v) {
+      for (int q = 0; q < kPB; ++q) {
+        const int b = tid + 32 * q;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[c][q] = (b < nbk) ? __ldcg(a.part + c * nbk + b) : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
         double s = 0.0;
-        for (int b = tid; b < nbk; b += 32) s += __ldcg(a.part + v * nbk + b);
+#pragma unroll
+        for (int q = 0; q < kPB; ++q) s += v[c][q];
         s = warp_sum(s);
-        if (tid == 0) bc[v] = s;
+        if (tid == 0) bc[c] = s;
       }
     }
     __syncthreads();
+    PROF_MARK(0);
     const double gnew = bc[0], dnew = bc[1];
     rr = bc[2];
     __syncthreads();
@@ -208,11 +244,45 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
     }
     gam = gnew;
 
+    // ---- halo: u_{i+1} = D^-1 (r_i - al (w_i + be s_{i-1})) from the neighbours' publication.
+    // L2-latency bound: the first kHB-deep batch of loads is issued before the own update so the
+    // update's shared-memory work hides it.
+    const double* pr = pubr[par];
+    const int64_t lo_len = d0 - h0 * NC;  // halo below the own range
+    const int64_t hi_beg = d0 + nod;      // halo above
+    const int64_t halo = lo_len + (h1 * NC - hi_beg);
+    constexpr int kHB = 5;
+    double rv[kHB], wv[kHB], sv[kHB], dv[kHB];
+    int64_t mm[kHB];
+    auto halo_load = [&](int64_t base) {
+#pragma unroll
+      for (int q = 0; q < kHB; ++q) {
+        const int64_t t = base + tid + (int64_t)q * nt;
+        const int64_t m = (t < lo_len) ? h0 * NC + t : hi_beg + (t - lo_len);
+        mm[q] = (t < halo) ? m : -1;
+        if (t < halo) {
+          rv[q] = __ldcg(pr + m);
+          wv[q] = __ldcg(pr + ND + m);
+          sv[q] = __ldcg(pr + 2 * ND + m);
+          dv[q] = a.dinv[m];
+        }
+      }
+    };
+    auto halo_store = [&]() {
+#pragma unroll
+      for (int q = 0; q < kHB; ++q) {
+        if (mm[q] < 0) continue;
+        double r = rv[q];
+        if (dv[q] != 0.0) r = fma(-al, fma(be, sv[q], wv[q]), r);
+        u_ext[mm[q] - h0 * NC] = dv[q] * r;
+      }
+    };
+    halo_load(0);
     // ---- own: p, s, x, r, u ----
+    const int own_off = (n0i - h0i) * NC;  // own block inside u_ext
     for (int o = tid; o < nod; o += nt) {
       const double di = ds[o];
-      const int64_t n = n0 + o / NC;
-      const double u = u_ext[(n - h0) * NC + (o % NC)];
+      const double u = u_ext[own_off + o];
       const double p = fma(be, ps[o], u);
       const double s = fma(be, ss[o], ws[o]);
       ps[o] = p;
@@ -224,32 +294,28 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
       }
       rs[o] = r;
     }
-    // ---- halo: u_{i+1} = D^-1 (r_i - al (w_i + be s_{i-1})) from the neighbours' publication ----
-    const double* pr = pubr[par];
-    for (int64_t m = h0 * NC + tid; m < h1 * NC; m += nt) {
-      if (m >= d0 && m < d0 + nod) continue;
-      const double di = a.dinv[m];
-      double r = __ldcg(pr + m);
-      if (di != 0.0) r = fma(-al, fma(be, __ldcg(pr + 2 * ND + m), __ldcg(pr + ND + m)), r);
-      u_ext[m - h0 * NC] = di * r;
+    PROF_MARK(1);
+    halo_store();
+    for (int64_t base = (int64_t)kHB * nt; base < halo; base += (int64_t)kHB * nt) {
+      halo_load(base);
+      halo_store();
     }
     __syncthreads();
-    for (int o = tid; o < nod; o += nt) {
-      const int64_t n = n0 + o / NC;
-      u_ext[(n - h0) * NC + (o % NC)] = ds[o] * rs[o];
-    }
+    PROF_MARK(2);
+    for (int o = tid; o < nod; o += nt) u_ext[own_off + o] = ds[o] * rs[o];
     __syncthreads();
+    PROF_MARK(3);
     // ---- own: w_{i+1} = A u_{i+1}; partials; publish (r_{i+1}, w_{i+1}, s_i) ----
     double* pw = pubr[par ^ 1];
     double acc3[3] = {0.0, 0.0, 0.0};
     for (int o = tid; o < no; o += nt) {
-      const int64_t n = n0 + o;
+      const int n = n0i + o;
       double out[NC];
       node_apply(n, out);
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         const int od = o * NC + c;
-        const double u = u_ext[(n - h0) * NC + c];
+        const double u = u_ext[(n - h0i) * NC + c];
         ws[od] = out[c];
         acc3[0] = fma(rs[od], u, acc3[0]);
         acc3[1] = fma(out[c], u, acc3[1]);
@@ -259,7 +325,9 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
         pw[2 * ND + d0 + od] = ss[od];
       }
     }
+    PROF_MARK(4);
     block_sum<3>(acc3);
+    PROF_MARK(5);
     if (tid == 0) {
       a.part[blockIdx.x] = acc3[0];
       a.part[nbk + blockIdx.x] = acc3[1];
@@ -267,7 +335,14 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
     }
     par ^= 1;
     grid_sync_flip(a.bar);
+    PROF_MARK(6);
   }
+#ifdef TB_CGCG_PROF
+  if (blockIdx.x == 0 && tid == 0)
+    printf("cgcg prof (ns/iter over %d its): sums %.0f own %.0f halo %.0f ownu %.0f apply %.0f bsum %.0f barrier %.0f\n",
+           it, prof[0] / (double)it, prof[1] / (double)it, prof[2] / (double)it, prof[3] / (double)it,
+           prof[4] / (double)it, prof[5] / (double)it, prof[6] / (double)it);
+#endif
   for (int o = tid; o < nod; o += nt) a.x[d0 + o] = xs[o];
   if (blockIdx.x == 0 && tid == 0) {
     a.st->rr = rr;

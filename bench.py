@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-flush", action="store_true", help="diagnostic: skip the L2 flush between steps")
     return ap.parse_args()
 
 
@@ -213,7 +214,8 @@ def run_ours(args):
     launches0 = _lib.lib().tb_launch_count()
     clocks.start()
     for k in range(args.steps):
-        flush.zero_()  # L2 flush between steps, outside the per-step events
+        if not args.no_flush:
+            flush.zero_()  # L2 flush between steps, outside the per-step events
         ev[k][0].record()
         sol, g = step()
         ev[k][1].record()
@@ -223,7 +225,9 @@ def run_ours(args):
     launches = _lib.lib().tb_launch_count() - launches0
     if dist:
         dist.barrier()
-    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    print("step ms:", [round(x, 3) for x in step_ms], file=sys.stderr)
+    total_ms = sum(step_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

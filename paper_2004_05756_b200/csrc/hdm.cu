@@ -112,6 +112,9 @@ void ElastOp::launch_fused(const PcgWork& w, const double* pold, double* pnew, c
   if (g.dim == 2)
     k_pcg_fused<2, 2, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, plan->K2, plan->d_alpha, w.z, pold, pnew, w.q,
                                                                 w.st, w.partA());
+  else if (plan->hex8)
+    k_hex8<true><<<hex8_grid(g, plan->zchunk), kHT, kHex8Smem, s>>>(g, plan->hb, plan->d_alpha, w.z, pold, pnew,
+                                                                    w.q, nullptr, w.st, w.partA(), plan->zchunk);
   else
     k_pcg_fused<3, 3, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, plan->K3, plan->d_alpha, w.z, pold, pnew, w.q,
                                                                 w.st, w.partA());
@@ -126,7 +129,13 @@ void ElastOp::launch_dinv(double* dinv, cudaStream_t s) const {
   else
     { k_node_dinv<3, 3, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, plan->K3, plan->d_alpha, plan->d_fixed, dinv); tb::launched(); }
 }
-int ElastOp::fused_blocks() const { return nblk(plan->g.n_nodes); }
+int ElastOp::fused_blocks() const {
+  if (plan->g.dim == 3 && plan->hex8) {
+    const dim3 gr = hex8_grid(plan->g, plan->zchunk);
+    return (int)(gr.x * gr.y * gr.z);
+  }
+  return nblk(plan->g.n_nodes);
+}
 
 void HelmOp::launch_fused(const PcgWork& w, const double* pold, double* pnew, cudaStream_t s) const {
   const Grid& g = filt->g;
@@ -205,6 +214,8 @@ void tb_plan_impl::apply_alpha(const double* alpha, const double* v, double* y, 
   const uint8_t* fx = mask ? d_fixed : nullptr;
   if (g.dim == 2)
     { k_node_apply<2, 2, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, K2, alpha, v, y, fx); tb::launched(); }
+  else if (hex8)
+    { k_hex8<false><<<hex8_grid(g, zchunk), kHT, kHex8Smem, s>>>(g, hb, alpha, v, nullptr, nullptr, y, fx, nullptr, nullptr, zchunk); tb::launched(); }
   else
     { k_node_apply<3, 3, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, K3, alpha, v, y, fx); tb::launched(); }
 }
@@ -256,6 +267,15 @@ int tb_plan_create(int dim, int nx, int ny, int nz, double h, const double* k_e,
   else
     memcpy(P->K3.v, k_e, sizeof(double) * ne * ne);
   P->op.plan = P;
+  if (dim == 3) {
+    P->hex8 = hex8_blocks(P->K3.v, &P->hb);
+    P->zchunk = hex8_zchunk(P->g);
+    if (P->hex8) {
+      cudaError_t e1 = cudaFuncSetAttribute(k_hex8<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHex8Smem);
+      cudaError_t e2 = cudaFuncSetAttribute(k_hex8<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHex8Smem);
+      if (e1 != cudaSuccess || e2 != cudaSuccess) P->hex8 = false;
+    }
+  }
   if (dim == 2) P->op.persist_grid = persist_grid_for<2, true>(P->g);
   int rc = P->init(fixed);
   if (rc != TB_OK) {

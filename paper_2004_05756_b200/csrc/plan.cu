@@ -30,6 +30,37 @@ void scalar_element_matrices(int dim, double h, double* S, double* M, double* s_
   *m_mul = (dim == 2) ? h * h / 36.0 : h * h * h / 216.0;
 }
 
+bool hex8_blocks(const double* K, Hex8Blocks* B) {
+  auto loc = [](int t) {  // corner t = ox + 2 oy + 4 oz -> local node (CCW faces)
+    const int ox = t & 1, oy = (t >> 1) & 1, oz = t >> 2;
+    return (oy ? (ox ? 2 : 3) : (ox ? 1 : 0)) + 4 * oz;
+  };
+  auto sgn = [](int s, int t) { return (__builtin_popcount(s & t) & 1) ? -1.0 : 1.0; };
+  double Mf[24][24];  // (s, c) x (s', c')
+  double kmax = 0.0;
+  for (int s = 0; s < 8; ++s)
+    for (int c = 0; c < 3; ++c)
+      for (int s2 = 0; s2 < 8; ++s2)
+        for (int c2 = 0; c2 < 3; ++c2) {
+          double acc = 0.0;
+          for (int t = 0; t < 8; ++t)
+            for (int t2 = 0; t2 < 8; ++t2)
+              acc += sgn(s, t) * K[(loc(t) * 3 + c) * 24 + loc(t2) * 3 + c2] * sgn(s2, t2);
+          Mf[s * 3 + c][s2 * 3 + c2] = acc / 64.0;
+          kmax = fmax(kmax, fabs(acc / 64.0));
+        }
+  double off = 0.0;
+  for (int r = 0; r < 24; ++r)
+    for (int q = 0; q < 24; ++q) {
+      const int kr = (r / 3) ^ (1 << (r % 3)), kq = (q / 3) ^ (1 << (q % 3));
+      if (kr != kq) off = fmax(off, fabs(Mf[r][q]));
+    }
+  for (int k = 0; k < 8; ++k)
+    for (int c = 0; c < 3; ++c)
+      for (int c2 = 0; c2 < 3; ++c2) B->m[k][c * 3 + c2] = Mf[(k ^ (1 << c)) * 3 + c][(k ^ (1 << c2)) * 3 + c2];
+  return off <= 1e-13 * kmax;
+}
+
 Grid make_grid(int dim, int nx, int ny, int nz, double h) {
   Grid g{};
   g.dim = dim;

@@ -113,7 +113,7 @@ void ElastOp::launch_fused(const PcgWork& w, const double* pold, double* pnew, c
     k_pcg_fused<2, 2, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, plan->K2, plan->d_alpha, w.z, pold, pnew, w.q,
                                                                 w.st, w.partA());
   else if (plan->hex8)
-    k_hex8<true><<<hex8_grid(g, plan->zchunk), kHT, kHex8Smem, s>>>(g, plan->hb, plan->d_alpha, w.z, pold, pnew,
+    k_hex8<true><<<hex8_grid(g, plan->zchunk), kHT, kHex8Smem, s>>>(g, plan->hiso, plan->d_alpha, w.z, pold, pnew,
                                                                     w.q, nullptr, w.st, w.partA(), plan->zchunk);
   else
     k_pcg_fused<3, 3, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, plan->K3, plan->d_alpha, w.z, pold, pnew, w.q,
@@ -215,7 +215,7 @@ void tb_plan_impl::apply_alpha(const double* alpha, const double* v, double* y, 
   if (g.dim == 2)
     { k_node_apply<2, 2, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, K2, alpha, v, y, fx); tb::launched(); }
   else if (hex8)
-    { k_hex8<false><<<hex8_grid(g, zchunk), kHT, kHex8Smem, s>>>(g, hb, alpha, v, nullptr, nullptr, y, fx, nullptr, nullptr, zchunk); tb::launched(); }
+    { k_hex8<false><<<hex8_grid(g, zchunk), kHT, kHex8Smem, s>>>(g, hiso, alpha, v, nullptr, nullptr, y, fx, nullptr, nullptr, zchunk); tb::launched(); }
   else
     { k_node_apply<3, 3, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, K3, alpha, v, y, fx); tb::launched(); }
 }
@@ -268,7 +268,7 @@ int tb_plan_create(int dim, int nx, int ny, int nz, double h, const double* k_e,
     memcpy(P->K3.v, k_e, sizeof(double) * ne * ne);
   P->op.plan = P;
   if (dim == 3) {
-    P->hex8 = hex8_blocks(P->K3.v, &P->hb);
+    P->hex8 = hex8_blocks(P->K3.v, &P->hiso);
     P->zchunk = hex8_zchunk(P->g);
     if (P->hex8) {
       cudaError_t e1 = cudaFuncSetAttribute(k_hex8<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHex8Smem);

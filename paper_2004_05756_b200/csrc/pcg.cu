@@ -34,6 +34,30 @@ void PcgWork::release() {
 }
 
 // Kernel B: x += alpha p ; r -= alpha q ; z = D^-1 r on free dofs (dinv != 0); rz, rr.
+// Pure streaming (8 vector passes): each thread handles 4 x 2 consecutive dofs per trip with
+// 16-byte loads so ~40 independent loads are in flight per thread.
+__device__ __forceinline__ void upd2(double a, double2 p, double2 q, double2 d, double2& x, double2& r, double2& z,
+                                     double (&acc)[2]) {
+  if (d.x != 0.0) {
+    x.x = fma(a, p.x, x.x);
+    r.x = fma(-a, q.x, r.x);
+    z.x = d.x * r.x;
+    acc[0] = fma(r.x, z.x, acc[0]);
+    acc[1] = fma(r.x, r.x, acc[1]);
+  } else {
+    z.x = 0.0;
+  }
+  if (d.y != 0.0) {
+    x.y = fma(a, p.y, x.y);
+    r.y = fma(-a, q.y, r.y);
+    z.y = d.y * r.y;
+    acc[0] = fma(r.y, z.y, acc[0]);
+    acc[1] = fma(r.y, r.y, acc[1]);
+  } else {
+    z.y = 0.0;
+  }
+}
+
 __global__ void __launch_bounds__(kBlock) k_pcg_update(int64_t n, const double* __restrict__ p,
                                                        const double* __restrict__ q, const double* __restrict__ dinv,
                                                        double* __restrict__ x, double* __restrict__ r,
@@ -41,16 +65,55 @@ __global__ void __launch_bounds__(kBlock) k_pcg_update(int64_t n, const double* 
   if (st->done) return;
   const double a = st->alpha;
   double acc[2] = {0.0, 0.0};
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double di = dinv[i];
+  constexpr int U = 4;
+  const int64_t n2 = n / 2;  // double2 count (vectors are 16-byte aligned cudaMalloc buffers)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+  const double2* q2 = reinterpret_cast<const double2*>(q);
+  const double2* d2 = reinterpret_cast<const double2*>(dinv);
+  double2* x2 = reinterpret_cast<double2*>(x);
+  double2* r2 = reinterpret_cast<double2*>(r);
+  double2* z2 = reinterpret_cast<double2*>(z);
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < n2; i += U * stride) {
+    double2 pv[U], qv[U], dv[U], xv[U], rv[U], zv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = i + u * stride;
+      pv[u] = __ldcs(p2 + j);
+      qv[u] = __ldcs(q2 + j);
+      dv[u] = __ldg(d2 + j);
+      xv[u] = x2[j];
+      rv[u] = r2[j];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      upd2(a, pv[u], qv[u], dv[u], xv[u], rv[u], zv[u], acc);
+      const int64_t j = i + u * stride;
+      x2[j] = xv[u];
+      r2[j] = rv[u];
+      z2[j] = zv[u];
+    }
+  }
+  for (; i < n2; i += stride) {
+    double2 pv = p2[i], qv = q2[i], dv = d2[i], xv = x2[i], rv = r2[i], zv;
+    upd2(a, pv, qv, dv, xv, rv, zv, acc);
+    x2[i] = xv;
+    r2[i] = rv;
+    z2[i] = zv;
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail dof
+    const int64_t k = n - 1;
+    const double di = dinv[k];
     if (di != 0.0) {
-      x[i] = fma(a, p[i], x[i]);
-      const double ri = fma(-a, q[i], r[i]);
-      const double zi = di * ri;
-      r[i] = ri;
-      z[i] = zi;
-      acc[0] = fma(ri, zi, acc[0]);
+      x[k] = fma(a, p[k], x[k]);
+      const double ri = fma(-a, q[k], r[k]);
+      r[k] = ri;
+      z[k] = di * ri;
+      acc[0] = fma(ri, z[k], acc[0]);
       acc[1] = fma(ri, ri, acc[1]);
+    } else {
+      z[k] = 0.0;
     }
   }
   block_sum<2>(acc);

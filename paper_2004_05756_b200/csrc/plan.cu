@@ -30,7 +30,7 @@ void scalar_element_matrices(int dim, double h, double* S, double* M, double* s_
   *m_mul = (dim == 2) ? h * h / 36.0 : h * h * h / 216.0;
 }
 
-bool hex8_blocks(const double* K, Hex8Blocks* B) {
+bool hex8_blocks(const double* K, Hex8Iso* B) {
   auto loc = [](int t) {  // corner t = ox + 2 oy + 4 oz -> local node (CCW faces)
     const int ox = t & 1, oy = (t >> 1) & 1, oz = t >> 2;
     return (oy ? (ox ? 2 : 3) : (ox ? 1 : 0)) + 4 * oz;
@@ -55,10 +55,28 @@ bool hex8_blocks(const double* K, Hex8Blocks* B) {
       const int kr = (r / 3) ^ (1 << (r % 3)), kq = (q / 3) ^ (1 << (q % 3));
       if (kr != kq) off = fmax(off, fabs(Mf[r][q]));
     }
+  double m[8][3][3];
   for (int k = 0; k < 8; ++k)
     for (int c = 0; c < 3; ++c)
-      for (int c2 = 0; c2 < 3; ++c2) B->m[k][c * 3 + c2] = Mf[(k ^ (1 << c)) * 3 + c][(k ^ (1 << c2)) * 3 + c2];
-  return off <= 1e-13 * kmax;
+      for (int c2 = 0; c2 < 3; ++c2) m[k][c][c2] = Mf[(k ^ (1 << c)) * 3 + c][(k ^ (1 << c2)) * 3 + c2];
+  B->a = m[0][0][0];
+  B->b = m[0][0][1];
+  B->c = m[1][1][1];
+  B->d = m[1][1][2];
+  B->e = m[3][0][0];
+  B->f = m[3][2][2];
+  B->g = m[7][0][0];
+  B->h = m[7][0][1];
+  const double a = B->a, b = B->b, c = B->c, d = B->d, e = B->e, f = B->f, g = B->g, h = B->h;
+  const double pat[8][3][3] = {
+      {{a, b, b}, {b, a, b}, {b, b, a}}, {{0, 0, 0}, {0, c, d}, {0, d, c}}, {{c, 0, d}, {0, 0, 0}, {d, 0, c}},
+      {{e, e, 0}, {e, e, 0}, {0, 0, f}}, {{c, d, 0}, {d, c, 0}, {0, 0, 0}}, {{e, 0, e}, {0, f, 0}, {e, 0, e}},
+      {{f, 0, 0}, {0, e, e}, {0, e, e}}, {{g, h, h}, {h, g, h}, {h, h, g}}};
+  double dev = off;
+  for (int k = 0; k < 8; ++k)
+    for (int c2 = 0; c2 < 3; ++c2)
+      for (int c3 = 0; c3 < 3; ++c3) dev = fmax(dev, fabs(m[k][c2][c3] - pat[k][c2][c3]));
+  return dev <= 1e-13 * kmax;
 }
 
 Grid make_grid(int dim, int nx, int ny, int nz, double h) {

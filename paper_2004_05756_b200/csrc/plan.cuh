@@ -42,8 +42,8 @@ struct tb_plan_impl {
   double rho_l = 1e-3, p = 3.0;
   Mat<8> K2{};
   Mat<24> K3{};
-  Hex8Blocks hb{};       // WHT block form of K3 (3D)
-  bool hex8 = false;     // K3 is block diagonal in the WHT basis -> element-centric kernel
+  Hex8Iso hiso{};        // WHT block values of K3 (3D)
+  bool hex8 = false;     // K3 has the isotropic WHT block structure -> element-centric kernel
   int zchunk = 8;
   uint8_t* d_fixed = nullptr;
   double* d_alpha = nullptr;   // alpha of the design being solved (read by the pCG graph)
@@ -76,8 +76,8 @@ struct tb_filter_impl {
 
 // Integer Laplacian / mass tables of the scalar Q1 element: S_e = (h^(d-2)) S/s_div,
 // M_e = m_mul * M  (2D: S/6, h^2/36 M, fem.py:72-92; 3D: h S/12, h^3/216 M).
-// WHT block form of a Hex8 element matrix; returns false if K is not block diagonal.
-bool hex8_blocks(const double* K, Hex8Blocks* B);
+// Isotropic WHT block values of a Hex8 element matrix; false if K lacks that structure.
+bool hex8_blocks(const double* K, Hex8Iso* B);
 void scalar_element_matrices(int dim, double h, double* S, double* M, double* s_div, double* m_mul);
 Grid make_grid(int dim, int nx, int ny, int nz, double h);
 void finish_sum(int nb, const double* part, double* out, cudaStream_t s);

@@ -89,6 +89,22 @@ int tb_pcg_profile(tb_plan* plan, const double* rho, const double* b, int nrep, 
 /* Number of kernels this library has launched so far (graph-body kernels included). */
 int64_t tb_launch_count(void);
 
+/* ---- slab-distributed pCG: the plan covers one z-slab; ghost node planes are
+ * Dirichlet-masked in `fixed`.  Reductions and the operator's p.q run over the owned node
+ * planes [k0, k1) only. */
+int tb_plan_set_owned_planes(tb_plan* plan, int k0, int k1);
+/* One phase of a distributed Jacobi-pCG iteration on this rank.  Phases: 0 init (needs rho, b,
+ * rtol, maxit; publishes local r.z, r.r), 1 finish init (after the host allreduce), 2 operator
+ * (publishes local p.q; `parity` = iteration index), 3 alpha (after allreduce), 4 update
+ * (publishes local r.z, r.r), 5 beta/convergence (after allreduce).  Between phases the caller
+ * allreduces the 4-double `red` buffer and, after phase 4, refreshes the ghost planes of z. */
+int tb_pcg_dist_phase(tb_plan* plan, int phase, const double* rho, const double* b, double rtol,
+                      int maxit, int parity, void* stream);
+/* Device pointers of this rank's solution x, preconditioned residual z and reduction buffer. */
+int tb_pcg_dist_buffers(tb_plan* plan, double** x, double** z, double** red);
+/* Host read of the iteration state (synchronises the stream). */
+int tb_pcg_dist_state(tb_plan* plan, int* iters, int* done, double* rr, double* bb, void* stream);
+
 /* Deterministic fp64 dot product of two device vectors; *out is a HOST pointer. */
 int tb_dot(tb_plan* plan, const double* a, const double* b, int64_t n, double* out, void* stream);
 

@@ -64,6 +64,12 @@ struct PcgState {
   int done;      // 0 running, 1 converged, 2 maxit, 3 breakdown
   int pad;
   unsigned int count_a, count_b, count_c, pad2;
+  // distributed (slab) mode: kernels only publish rank-local sums in red[] (pq; rz, rr) and
+  // the host allreduces them before tb_pcg_dist_alpha / tb_pcg_dist_beta
+  int dist;
+  int dot_k0, dot_k1;  // node planes [k0, k1) that own their rows (reductions, contractions)
+  int pad3;
+  double red[4];
 };
 
 // ---------------------------------------------------------------------------------------

@@ -356,6 +356,10 @@ int tb_pcg_solve(tb_plan* plan, const double* rho, const double* b, double* x, d
   TB_GUARD(plan && rho && b && x, "null argument");
   auto* P = reinterpret_cast<tb_plan_impl*>(plan);
   cudaStream_t s = (cudaStream_t)stream;
+  if (P->dist) {
+    P->dist = 0;
+    TB_TRY(P->work.set_fields(0, P->own_k0, P->own_k1));
+  }
   TB_TRY(P->material(rho, P->d_alpha, nullptr, s));
   return pcg_solve(P->op, P->work, b, x, rtol, maxit, iters, relres, s);
 }
@@ -370,6 +374,55 @@ int tb_pcg_profile(tb_plan* plan, const double* rho, const double* b, int nrep, 
 }
 
 int64_t tb_launch_count(void) { return g_launches.load(); }
+
+int tb_plan_set_owned_planes(tb_plan* plan, int k0, int k1) {
+  TB_GUARD(plan != nullptr, "null plan");
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  TB_GUARD(0 <= k0 && k0 <= k1 && k1 <= P->g.nnz, "owned node planes [%d, %d) outside [0, %d]", k0, k1, P->g.nnz);
+  P->own_k0 = k0;
+  P->own_k1 = k1;
+  return P->work.set_fields(P->dist, k0, k1);
+}
+
+int tb_pcg_dist_phase(tb_plan* plan, int phase, const double* rho, const double* b, double rtol, int maxit,
+                      int parity, void* stream) {
+  TB_GUARD(plan != nullptr, "null plan");
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (phase == 0) {
+    TB_GUARD(rho && b, "phase 0 needs rho and b");
+    TB_GUARD(rtol > 0.0 && maxit >= 1, "rtol must be > 0 and maxit >= 1");
+    if (!P->dist) {
+      P->dist = 1;
+      TB_TRY(P->work.set_fields(1, P->own_k0, P->own_k1));
+    }
+    TB_TRY(P->material(rho, P->d_alpha, nullptr, s));
+  }
+  return pcg_dist_phase(P->op, P->work, phase, b, rtol, maxit, parity, s);
+}
+
+int tb_pcg_dist_buffers(tb_plan* plan, double** x, double** z, double** red) {
+  TB_GUARD(plan != nullptr, "null plan");
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  if (x) *x = P->work.x;
+  if (z) *z = P->work.z;
+  if (red) *red = P->work.st->red;
+  return TB_OK;
+}
+
+int tb_pcg_dist_state(tb_plan* plan, int* iters, int* done, double* rr, double* bb, void* stream) {
+  TB_GUARD(plan != nullptr, "null plan");
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  cudaStream_t s = (cudaStream_t)stream;
+  TB_CUDA(cudaMemcpyAsync(P->work.h_st, P->work.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+  TB_CUDA(cudaStreamSynchronize(s));
+  const PcgState& h = *P->work.h_st;
+  if (iters) *iters = h.iters;
+  if (done) *done = h.done;
+  if (rr) *rr = h.rr;
+  if (bb) *bb = h.bb;
+  return TB_OK;
+}
 
 int tb_dot(tb_plan* plan, const double* a, const double* b, int64_t n, double* out, void* stream) {
   TB_GUARD(plan && a && b && out, "null argument");
@@ -414,6 +467,7 @@ int tb_filter_create(int dim, int nx, int ny, int nz, double h, double radius, i
   F->op.filt = F;
   F->op.persist_grid = (g.dim == 2) ? persist_grid_for<1, false>(g) : 0;  // 3D: graph loop
   int rc = F->work.alloc(g.n_nodes, F->op.fused_blocks(), F->op.persist_grid > 0);
+  if (rc == TB_OK) rc = F->work.set_fields(0, 0, g.nnz);
   if (rc == TB_OK) {
     cudaError_t e = cudaMalloc(&F->d_b, sizeof(double) * g.n_nodes);
     if (e != cudaSuccess) {

@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kHT, 2) k_hex8(Grid g, Hex8Iso K, const double
         for (int c = 0; c < 3; ++c) {
           double v = carry[c] + bot[c];
           if (FUSED) {
-            acc[0] = fma(plane[pbuf(ez)][c][py * kPX + px], v, acc[0]);
+            if (ez >= st->dot_k0 && ez < st->dot_k1) acc[0] = fma(plane[pbuf(ez)][c][py * kPX + px], v, acc[0]);
           } else if (fixed != nullptr && fixed[3 * node + c]) {
             v = 0.0;
           }
@@ -289,7 +289,9 @@ __global__ void __launch_bounds__(kHT, 2) k_hex8(Grid g, Hex8Iso K, const double
       gather_partials<1>(acc, partials, &st->count_a);
       if (threadIdx.x == 0) {
         const double v = acc[0];
-        if (!(v > 0.0) || !isfinite(v)) {
+        if (st->dist) {
+          st->red[0] = v;
+        } else if (!(v > 0.0) || !isfinite(v)) {
           st->done = 3;
         } else {
           st->pq = v;

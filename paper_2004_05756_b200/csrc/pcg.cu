@@ -1,4 +1,5 @@
 // pCG engine implementation (see pcg.cuh).
+#include <stddef.h>
 #include <stdlib.h>
 
 #include "pcg.cuh"
@@ -18,6 +19,12 @@ int PcgWork::alloc(int64_t n_, int max_blocks, bool with_pub) {
   TB_CUDA(cudaMalloc(&barrier, 64));
   TB_CUDA(cudaMemset(barrier, 0, 64));
   if (with_pub) TB_CUDA(cudaMalloc(&pub, sizeof(double) * 6 * (size_t)n));
+  return TB_OK;
+}
+
+int PcgWork::set_fields(int dist, int dot_k0, int dot_k1) {
+  const int v[3] = {dist, dot_k0, dot_k1};
+  TB_CUDA(cudaMemcpy(reinterpret_cast<char*>(st) + offsetof(PcgState, dist), v, sizeof(v), cudaMemcpyHostToDevice));
   return TB_OK;
 }
 
@@ -119,7 +126,10 @@ __global__ void __launch_bounds__(kBlock) k_pcg_update(int64_t n, const double* 
   block_sum<2>(acc);
   if (publish_partials<2>(acc, partials, &st->count_b)) {
     gather_partials<2>(acc, partials, &st->count_b);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && st->dist) {
+      st->red[1] = acc[0];
+      st->red[2] = acc[1];
+    } else if (threadIdx.x == 0) {
       const int it = st->iters + 1;
       st->iters = it;
       st->beta = acc[0] / st->rz;
@@ -156,7 +166,18 @@ __global__ void __launch_bounds__(kBlock) k_pcg_start(int64_t n, const double* _
   block_sum<2>(acc);
   if (publish_partials<2>(acc, partials, &st->count_c)) {
     gather_partials<2>(acc, partials, &st->count_c);
-    if (threadIdx.x == 0 && !(init == 0 && st->done == 3)) {  // a breakdown stays reported
+    if (threadIdx.x == 0 && st->dist) {
+      st->red[1] = acc[0];
+      st->red[2] = acc[1];
+      if (init) {
+        st->iters = 0;
+        st->maxit = maxit;
+        st->beta = 0.0;
+        st->alpha = 0.0;
+        st->done = 0;
+        st->pq = rtol;  // stashed until tb_pcg_dist_init2 has the global norm
+      }
+    } else if (threadIdx.x == 0 && !(init == 0 && st->done == 3)) {  // a breakdown stays reported
       if (init) {
         st->tol2 = rtol * rtol * acc[1];
         st->iters = 0;
@@ -334,6 +355,78 @@ int pcg_profile(const PcgOp& op, PcgWork& w, const double* b, int nrep, double* 
   }
   *ms_fused = tf / nrep;
   *ms_update = tu / nrep;
+  return TB_OK;
+}
+
+// ---- distributed (slab) mode: rank-local phases, scalars finished after host allreduce ----
+__global__ void k_dist_init2(PcgState* st) {
+  const double rtol = st->pq;
+  st->rz = st->red[1];
+  st->bb = st->red[2];
+  st->rr = st->red[2];
+  st->tol2 = rtol * rtol * st->red[2];
+  st->beta = 0.0;
+  st->done = (st->red[2] == 0.0) ? 1 : (isfinite(st->red[2]) ? 0 : 3);
+}
+__global__ void k_dist_alpha(PcgState* st) {
+  if (st->done) return;
+  const double v = st->red[0];
+  if (!(v > 0.0) || !isfinite(v)) {
+    st->done = 3;
+  } else {
+    st->pq = v;
+    st->alpha = st->rz / v;
+  }
+}
+__global__ void k_dist_beta(PcgState* st) {
+  if (st->done) return;
+  const int it = st->iters + 1;
+  st->iters = it;
+  st->beta = st->red[1] / st->rz;
+  st->rz = st->red[1];
+  st->rr = st->red[2];
+  if (!isfinite(st->red[1]) || !isfinite(st->red[2])) st->done = 3;
+  else if (st->red[2] <= st->tol2) st->done = 1;
+  else if (it >= st->maxit) st->done = 2;
+}
+
+int pcg_dist_phase(const PcgOp& op, PcgWork& w, int phase, const double* b, double rtol, int maxit, int parity,
+                   cudaStream_t s) {
+  const int nb = kUpdateBlocks;
+  double* pold = (parity & 1) ? w.pb : w.pa;
+  double* pnew = (parity & 1) ? w.pa : w.pb;
+  switch (phase) {
+    case 0:  // init: D^-1, r = Z b, z, local r.z and r.r
+      op.launch_dinv(w.dinv, s);
+      k_pcg_start<<<nb, kBlock, 0, s>>>(w.n, b, nullptr, w.dinv, w.x, w.r, w.z, w.pa, w.st, w.partC(), 1, rtol,
+                                        maxit);
+      launched(1);
+      break;
+    case 1:
+      k_dist_init2<<<1, 1, 0, s>>>(w.st);
+      launched(1);
+      break;
+    case 2:  // operator + local p.q
+      op.launch_fused(w, pold, pnew, s);
+      launched(1);
+      break;
+    case 3:
+      k_dist_alpha<<<1, 1, 0, s>>>(w.st);
+      launched(1);
+      break;
+    case 4:  // update + local r.z, r.r
+      k_pcg_update<<<kUpdateBlocks, kBlock, 0, s>>>(w.n, pnew, w.q, w.dinv, w.x, w.r, w.z, w.st, w.partB());
+      launched(1);
+      break;
+    case 5:
+      k_dist_beta<<<1, 1, 0, s>>>(w.st);
+      launched(1);
+      break;
+    default:
+      set_error("unknown distributed pCG phase %d", phase);
+      return TB_ERR_INVALID;
+  }
+  TB_CHECK_LAUNCH();
   return TB_OK;
 }
 

@@ -46,6 +46,7 @@ struct PcgWork {
   double* partB() const { return part + 2 * part_stride; }
   double* partC() const { return part + 4 * part_stride; }
   int alloc(int64_t n_, int max_blocks, bool with_pub = false);
+  int set_fields(int dist, int dot_k0, int dot_k1);  // distributed mode + owned node planes
   void release();
 };
 
@@ -54,6 +55,9 @@ constexpr int kUpdateBlocks = 148 * 4;
 
 int pcg_solve(const PcgOp& op, PcgWork& w, const double* b, double* x_out, double rtol, int maxit,
               int* iters, double* relres, cudaStream_t stream);
+// one phase of the distributed (slab) pCG: 0 init, 1 finish init, 2 operator, 3 alpha, 4 update, 5 beta
+int pcg_dist_phase(const PcgOp& op, PcgWork& w, int phase, const double* b, double rtol, int maxit, int parity,
+                   cudaStream_t stream);
 int pcg_profile(const PcgOp& op, PcgWork& w, const double* b, int nrep, double* ms_fused, double* ms_update,
                 cudaStream_t stream);
 

@@ -104,6 +104,7 @@ int tb_plan_impl::init(const uint8_t* fixed_host) {
   TB_CUDA(cudaMalloc(&d_scalar, sizeof(double) * 16));
   TB_CUDA(cudaMallocHost(&h_scalar, sizeof(double) * 16));
   TB_TRY(work.alloc(n_dofs, op.fused_blocks(), op.persist_grid > 0));
+  TB_TRY(work.set_fields(0, 0, g.nnz));
   return TB_OK;
 }
 

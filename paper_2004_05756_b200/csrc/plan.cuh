@@ -45,6 +45,8 @@ struct tb_plan_impl {
   Hex8Iso hiso{};        // WHT block values of K3 (3D)
   bool hex8 = false;     // K3 has the isotropic WHT block structure -> element-centric kernel
   int zchunk = 8;
+  int dist = 0;              // distributed (slab) pCG mode
+  int own_k0 = 0, own_k1 = 1 << 30;  // owned node planes (set by tb_plan_set_owned_planes)
   uint8_t* d_fixed = nullptr;
   double* d_alpha = nullptr;   // alpha of the design being solved (read by the pCG graph)
   double* d_alpha2 = nullptr;  // alpha scratch for one-off applies

@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kBlock) k_pcg_fused(Grid g, Mat<Q1<D>::NN * NC
     for (int c = 0; c < NC; ++c) {
       pnew[NC * n + c] = P[self][c];
       q[NC * n + c] = out[c];
-      pq[0] = fma(P[self][c], out[c], pq[0]);
+      if (k >= st->dot_k0 && k < st->dot_k1) pq[0] = fma(P[self][c], out[c], pq[0]);
     }
   }
   block_sum<1>(pq);
@@ -159,7 +159,9 @@ __global__ void __launch_bounds__(kBlock) k_pcg_fused(Grid g, Mat<Q1<D>::NN * NC
     gather_partials<1>(pq, partials, &st->count_a);
     if (threadIdx.x == 0) {
       const double v = pq[0];
-      if (!(v > 0.0) || !isfinite(v)) {
+      if (st->dist) {
+        st->red[0] = v;
+      } else if (!(v > 0.0) || !isfinite(v)) {
         st->done = 3;
       } else {
         st->pq = v;

@@ -1,0 +1,247 @@
+"""z-slab domain decomposition of the 3D HDM solve across GPUs (BASELINE cfg 4).
+
+Rank r owns the global node planes [k0, k1) and holds the element planes [e0, e1) that touch
+them, i.e. its own slab plus one ghost element layer per interior side.  Its local grid is an
+ordinary structured Hex8 grid with node planes [e0, e1].  Because nodes are numbered plane by
+plane, every local vector is a contiguous slice of the global one, and ghost node planes are
+contiguous too.
+
+Ghost node planes are Dirichlet-masked in the local plan, so the unmodified kernels
+(operator, update, Jacobi diagonal) run on the slab.  Their rows are never updated, and every
+reduction and the operator's p.q are restricted to the owned planes
+(tb_plan_set_owned_planes).  One iteration of the distributed Jacobi-pCG:
+
+    phase 2  operator + local p.q   ->  allreduce(red)  ->  phase 3  alpha
+    phase 4  update + local r.z, r.r ->  allreduce(red)  ->  phase 5  beta / convergence
+    halo     ghost planes of z <- neighbours' first / last owned planes
+
+The direction p = z + beta p_old is formed inside the operator for owned and ghost nodes
+alike from identical z and p_old, so ghost p needs no exchange.  All ranks receive bitwise
+identical allreduce results, so every rank takes the same convergence decision.
+
+The phase driver takes a list of local solvers and a communicator: one solver per process
+with ``TorchComm`` (NCCL on GPUs; gloo for the CPU tests), or several solvers in one process
+on one GPU with ``LocalComm``.  ``LocalComm`` emulates the exchange step by step on the host;
+no kernel ever waits on another rank.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .fem import StructuredMesh, build_mesh_3d
+
+__all__ = ["Slab", "partition", "SlabSolver", "LocalComm", "TorchComm", "dist_pcg_solve"]
+
+
+@dataclass(frozen=True)
+class Slab:
+    rank: int
+    nranks: int
+    k0: int  # owned global node planes [k0, k1)
+    k1: int
+    e0: int  # local element planes [e0, e1) (global ids); local node planes [e0, e1]
+    e1: int
+
+    @property
+    def local_nz(self) -> int:
+        return self.e1 - self.e0
+
+    @property
+    def ghost_lo(self) -> bool:
+        return self.k0 > self.e0
+
+    @property
+    def ghost_hi(self) -> bool:
+        return self.e1 >= self.k1
+
+    @property
+    def own_local(self):
+        return self.k0 - self.e0, self.k1 - self.e0
+
+
+def partition(nz: int, nranks: int) -> list:
+    """Split the nz+1 node planes into nranks contiguous owned ranges (sizes differ by <= 1)."""
+    nnz = nz + 1
+    if nranks < 1 or nranks > nnz // 2:
+        raise ValueError(f"cannot split {nnz} node planes over {nranks} ranks (need >= 2 planes each)")
+    base, extra = divmod(nnz, nranks)
+    out, k = [], 0
+    for r in range(nranks):
+        k1 = k + base + (1 if r < extra else 0)
+        out.append(Slab(r, nranks, k, k1, max(0, k - 1), min(nz, k1)))
+        k = k1
+    return out
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of library-owned device memory (torch.as_tensor aliases it)."""
+
+    def __init__(self, ptr, n, device):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3,
+                                         "strides": None}
+        self.device = device
+
+
+class SlabSolver:
+    """Rank-local part of the distributed HDM solve (one z-slab of a 3D Hex8 problem)."""
+
+    def __init__(self, mesh: StructuredMesh, k_e, f, fixed_dofs, material, slab: Slab, device=None):
+        t = _lib.torch()
+        if not mesh.nz:
+            raise ValueError("slab decomposition is for 3D meshes")
+        self.mesh, self.slab = mesh, slab
+        self.device = _lib.require_cuda(device)
+        self.local = build_mesh_3d(mesh.nx, mesh.ny, slab.local_nz, mesh.h)
+        self.plane_nodes = (mesh.nx + 1) * (mesh.ny + 1)
+        self.plane_dofs = 3 * self.plane_nodes
+        self.plane_elems = mesh.nx * mesh.ny
+        d0 = slab.e0 * self.plane_dofs
+        nl = self.local.n_dofs
+        fixed = np.zeros(mesh.n_dofs, dtype=np.uint8)
+        fixed[np.asarray(fixed_dofs, dtype=np.int64)] = 1
+        fixed_l = fixed[d0:d0 + nl].copy()
+        if slab.ghost_lo:
+            fixed_l[:self.plane_dofs] = 1
+        if slab.ghost_hi:
+            fixed_l[-self.plane_dofs:] = 1
+        f_l = np.asarray(f, dtype=float)[d0:d0 + nl].copy()
+        f_l[fixed_l != 0] = 0.0
+        self.fixed_local = fixed_l
+        ke = np.ascontiguousarray(np.asarray(k_e, dtype=float))
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().tb_plan_create(3, mesh.nx, mesh.ny, slab.local_nz, mesh.h,
+                                             ke.ctypes.data_as(ctypes.c_void_p), material.rho_l, material.p,
+                                             np.ascontiguousarray(fixed_l).ctypes.data_as(ctypes.c_void_p),
+                                             self.device.index, ctypes.byref(h)), "slab plan")
+        self._plan = h
+        k0, k1 = slab.own_local
+        _lib.check(_lib.lib().tb_plan_set_owned_planes(h, k0, k1), "owned planes")
+        self.f = _lib.to_dev(f_l, self.device)
+        px, pz, pr = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(_lib.lib().tb_pcg_dist_buffers(h, ctypes.byref(px), ctypes.byref(pz), ctypes.byref(pr)), "bufs")
+        self.x = t.as_tensor(_CudaArray(px.value, nl, self.device), device=self.device)
+        self.z = t.as_tensor(_CudaArray(pz.value, nl, self.device), device=self.device)
+        self.red = t.as_tensor(_CudaArray(pr.value, 4, self.device), device=self.device)
+        self.rho = None
+        self.rtol, self.maxit = 1e-8, 200000
+
+    def __del__(self):
+        h = getattr(self, "_plan", None)
+        if h is not None and h.value and _lib._lib is not None:
+            _lib._lib.tb_plan_destroy(h)
+            self._plan = None
+
+    # -- element / node slices of global fields
+    def local_elems(self, global_elem_field):
+        s = self.slab
+        return global_elem_field[s.e0 * self.plane_elems:s.e1 * self.plane_elems]
+
+    def owned_dofs(self):
+        """(local slice, global slice) of this rank's owned dofs."""
+        k0, k1 = self.slab.own_local
+        return (slice(k0 * self.plane_dofs, k1 * self.plane_dofs),
+                slice(self.slab.k0 * self.plane_dofs, self.slab.k1 * self.plane_dofs))
+
+    def plane(self, vec, local_plane):
+        return vec[local_plane * self.plane_dofs:(local_plane + 1) * self.plane_dofs]
+
+    # -- phases (see module docstring)
+    def phase(self, p, parity=0):
+        rho = _lib.ptr(self.rho) if p == 0 else _lib.P(0)
+        b = _lib.ptr(self.f) if p == 0 else _lib.P(0)
+        _lib.check(_lib.lib().tb_pcg_dist_phase(self._plan, p, rho, b, self.rtol, self.maxit, parity,
+                                                _lib.stream_ptr(self.device)), f"dist phase {p}")
+
+    def state(self):
+        it, done, rr, bb = ctypes.c_int(), ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+        _lib.check(_lib.lib().tb_pcg_dist_state(self._plan, ctypes.byref(it), ctypes.byref(done), ctypes.byref(rr),
+                                                ctypes.byref(bb), _lib.stream_ptr(self.device)), "dist state")
+        return it.value, done.value, rr.value, bb.value
+
+
+class LocalComm:
+    """All ranks in one process: allreduce = fixed-order sum, halo = device copies."""
+
+    def allreduce(self, solvers):
+        total = solvers[0].red.clone()
+        for s in solvers[1:]:
+            total = total + s.red
+        for s in solvers:
+            s.red.copy_(total)
+
+    def halo(self, solvers, name="z"):
+        for lo, hi in zip(solvers[:-1], solvers[1:]):
+            vlo, vhi = getattr(lo, name), getattr(hi, name)
+            k0_hi, _ = hi.slab.own_local
+            _, k1_lo = lo.slab.own_local
+            # hi's ghost-below plane <- lo's last owned plane; lo's ghost-above <- hi's first owned
+            hi.plane(vhi, 0).copy_(lo.plane(vlo, k1_lo - 1))
+            lo.plane(vlo, k1_lo).copy_(hi.plane(vhi, k0_hi))
+
+
+class TorchComm:
+    """One solver per process; collectives through torch.distributed (NCCL or gloo)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+
+    def allreduce(self, solvers):
+        self.dist.all_reduce(solvers[0].red, group=self.group)
+
+    def halo(self, solvers, name="z"):
+        d = self.dist
+        s = solvers[0]
+        v = getattr(s, name)
+        r, n = s.slab.rank, s.slab.nranks
+        k0, k1 = s.slab.own_local
+        ops = []
+        if r > 0:
+            ops.append(d.P2POp(d.isend, s.plane(v, k0).contiguous(), r - 1, self.group))
+            ops.append(d.P2POp(d.irecv, s.plane(v, 0), r - 1, self.group))
+        if r < n - 1:
+            ops.append(d.P2POp(d.isend, s.plane(v, k1 - 1).contiguous(), r + 1, self.group))
+            ops.append(d.P2POp(d.irecv, s.plane(v, k1), r + 1, self.group))
+        if ops:
+            for req in d.batch_isend_irecv(ops):
+                req.wait()
+
+
+def dist_pcg_solve(solvers, comm, rtol=1e-8, maxit=200000, check_every=8):
+    """Jacobi-pCG over the slabs of ``solvers`` (this process's share).  Returns
+    (iterations, recursive relative residual, converged flag)."""
+    for s in solvers:
+        s.rtol, s.maxit = rtol, maxit
+        s.phase(0)
+    comm.allreduce(solvers)
+    for s in solvers:
+        s.phase(1)
+    comm.halo(solvers)
+    it = 0
+    while True:
+        for s in solvers:
+            s.phase(2, parity=it)
+        comm.allreduce(solvers)
+        for s in solvers:
+            s.phase(3)
+            s.phase(4, parity=it)
+        comm.allreduce(solvers)
+        for s in solvers:
+            s.phase(5)
+        comm.halo(solvers)
+        it += 1
+        if it % check_every == 0 or it >= maxit:
+            iters, done, rr, bb = solvers[0].state()
+            if done != 0:
+                if done == 3:
+                    from .fem import IndefiniteMatrixError
+
+                    raise IndefiniteMatrixError("distributed pCG breakdown")
+                return iters, (rr / bb) ** 0.5 if bb > 0 else 0.0, done == 1

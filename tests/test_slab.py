@@ -1,0 +1,209 @@
+"""Slab decomposition: partitioning, the phase-wise distributed pCG driver with a
+world_size-2 gloo run on CPU, and the CUDA slab kernels emulated on one GPU (LocalComm)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2004_05756_b200 import configs
+from paper_2004_05756_b200.slab import LocalComm, Slab, TorchComm, dist_pcg_solve, partition
+
+
+@pytest.mark.parametrize("nz,r", [(5, 2), (12, 4), (96, 8), (7, 3)])
+def test_partition_covers_planes(nz, r):
+    slabs = partition(nz, r)
+    assert slabs[0].k0 == 0 and slabs[-1].k1 == nz + 1
+    sizes = [s.k1 - s.k0 for s in slabs]
+    assert max(sizes) - min(sizes) <= 1
+    for a, b in zip(slabs[:-1], slabs[1:]):
+        assert a.k1 == b.k0
+        assert a.ghost_hi and b.ghost_lo
+        assert a.e1 == a.k1 and b.e0 == b.k0 - 1
+    assert not slabs[0].ghost_lo and not slabs[-1].ghost_hi
+    for s in slabs:  # every element touching an owned node plane is local
+        assert s.e0 == max(0, s.k0 - 1) and s.e1 == min(nz, s.k1)
+    with pytest.raises(ValueError):
+        partition(2, 3)
+
+
+class CpuSlab:
+    """Test-side numpy restatement of the six phases of tb_pcg_dist_phase (same masks, same
+    reductions) over the oracle's sparse stiffness of the slab grid."""
+
+    def __init__(self, prob, slab: Slab):
+        from oracle.fem import assemble, build_grid
+
+        m = prob.mesh
+        self.slab = slab
+        self.plane_dofs = 3 * (m.nx + 1) * (m.ny + 1)
+        pe = m.nx * m.ny
+        self.grid = build_grid(m.nx, m.ny, m.h, nz=slab.local_nz)
+        d0 = slab.e0 * self.plane_dofs
+        nl = self.grid.n_dofs
+        fixed = np.zeros(m.n_dofs, bool)
+        fixed[prob.fixed] = True
+        fl = fixed[d0:d0 + nl].copy()
+        if slab.ghost_lo:
+            fl[:self.plane_dofs] = True
+        if slab.ghost_hi:
+            fl[-self.plane_dofs:] = True
+        self.fixed = fl
+        self.b = np.where(fl, 0.0, prob.f[d0:d0 + nl])
+        rho = prob.psi[slab.e0 * pe:slab.e1 * pe]
+        alpha = configs.RHO_L + (1 - configs.RHO_L) * rho**3
+        self.K = assemble(self.grid, prob.k_e, alpha).tocsr()
+        self.x = torch.zeros(nl, dtype=torch.float64)
+        self.z = torch.zeros(nl, dtype=torch.float64)
+        self.red = torch.zeros(4, dtype=torch.float64)
+        self.p = [np.zeros(nl), np.zeros(nl)]
+        self.q = np.zeros(nl)
+        self.own = np.zeros(nl, bool)
+        k0, k1 = slab.own_local
+        self.own[k0 * self.plane_dofs:k1 * self.plane_dofs] = True
+        self.rtol, self.maxit = 1e-8, 100000
+
+    def plane(self, vec, k):
+        return vec[k * self.plane_dofs:(k + 1) * self.plane_dofs]
+
+    def phase(self, ph, parity=0):
+        x, z, red = self.x.numpy(), self.z.numpy(), self.red.numpy()
+        if ph == 0:
+            diag = self.K.diagonal()
+            self.dinv = np.where(self.fixed, 0.0, 1.0 / diag)
+            self.r = self.b.copy()
+            x[:] = 0.0
+            z[:] = self.dinv * self.r
+            self.p = [np.zeros_like(z), np.zeros_like(z)]
+            red[1], red[2] = self.r @ z, self.r @ self.r
+            self.st = dict(iters=0, done=0)
+        elif ph == 1:
+            self.st.update(rz=red[1], bb=red[2], rr=red[2], tol2=self.rtol**2 * red[2], beta=0.0,
+                           done=1 if red[2] == 0 else 0)
+        elif self.st["done"]:
+            return
+        elif ph == 2:
+            pold, pnew = self.p[parity & 1], self.p[(parity + 1) & 1]
+            pnew[:] = z + self.st["beta"] * pold
+            self.q = self.K @ pnew
+            red[0] = pnew[self.own] @ self.q[self.own]
+        elif ph == 3:
+            if not red[0] > 0:
+                self.st["done"] = 3
+            else:
+                self.st["alpha"] = self.st["rz"] / red[0]
+        elif ph == 4:
+            a, pnew, free = self.st["alpha"], self.p[(parity + 1) & 1], self.dinv != 0
+            x[free] += a * pnew[free]
+            self.r[free] -= a * self.q[free]
+            z[:] = np.where(free, self.dinv * self.r, 0.0)
+            red[1], red[2] = self.r[free] @ z[free], self.r[free] @ self.r[free]
+        elif ph == 5:
+            st = self.st
+            st["iters"] += 1
+            st["beta"] = red[1] / st["rz"]
+            st["rz"], st["rr"] = red[1], red[2]
+            if red[2] <= st["tol2"]:
+                st["done"] = 1
+            elif st["iters"] >= self.maxit:
+                st["done"] = 2
+
+    def state(self):
+        s = self.st
+        return s["iters"], s["done"], s["rr"], s["bb"]
+
+
+def _problem():
+    return configs.cfg3(seed=5, nx=6, ny=3, nz=7)
+
+
+def _reference_u(prob):
+    from oracle.fem import build_grid
+    from oracle.hdm import Hdm, Material
+
+    g = build_grid(prob.mesh.nx, prob.mesh.ny, 1.0, nz=prob.mesh.nz)
+
+    class Ident:
+        def apply(self, psi):
+            return None, np.asarray(psi, float)
+
+    return Hdm(g, prob.k_e, Ident(), prob.f, prob.fixed, Material(configs.RHO_L, configs.P_SIMP)).solve(prob.psi)["u"]
+
+
+def test_driver_local_comm_cpu():
+    prob = _problem()
+    slabs = [CpuSlab(prob, s) for s in partition(prob.mesh.nz, 3)]
+    it, rel, ok = dist_pcg_solve(slabs, LocalComm(), rtol=1e-12, check_every=1)
+    assert ok
+    u = np.zeros(prob.mesh.n_dofs)
+    for s in slabs:
+        k0, k1 = s.slab.own_local
+        u[s.slab.k0 * s.plane_dofs:s.slab.k1 * s.plane_dofs] = s.x.numpy()[k0 * s.plane_dofs:k1 * s.plane_dofs]
+    ref = _reference_u(prob)
+    assert np.abs(u - ref).max() <= 1e-8 * np.abs(ref).max()
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    prob = _problem()
+    s = CpuSlab(prob, partition(prob.mesh.nz, world)[rank])
+    it, rel, ok = dist_pcg_solve([s], TorchComm(), rtol=1e-12, check_every=1)
+    k0, k1 = s.slab.own_local
+    q.put((rank, it, ok, s.slab.k0, s.slab.k1, s.x.numpy()[k0 * s.plane_dofs:k1 * s.plane_dofs].copy()))
+    dist.destroy_process_group()
+
+
+def test_gloo_world_size_2():
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    prob = _problem()
+    u = np.zeros(prob.mesh.n_dofs)
+    pd = 3 * (prob.mesh.nx + 1) * (prob.mesh.ny + 1)
+    assert res[0][1] == res[1][1] and res[0][2] and res[1][2]  # same iteration count, converged
+    for _, _, _, k0, k1, xs in res:
+        u[k0 * pd:k1 * pd] = xs
+    ref = _reference_u(prob)
+    assert np.abs(u - ref).max() <= 1e-8 * np.abs(ref).max()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_cuda_slabs_emulated_on_one_gpu(cuda, nranks):
+    import paper_2004_05756_b200 as tb
+    from paper_2004_05756_b200.slab import SlabSolver
+
+    prob = configs.cfg3(seed=6, nx=16, ny=8, nz=11)
+    mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
+    glob = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, 1.0), prob.f, prob.fixed, mat,
+                        rtol=1e-11)
+    rho = torch.as_tensor(prob.psi, device=cuda)
+    u_ref = glob.pcg_device(rho, glob._f_d).cpu().numpy()
+    solvers = [SlabSolver(prob.mesh, prob.k_e, prob.f, prob.fixed, mat, s) for s in partition(prob.mesh.nz, nranks)]
+    for s in solvers:
+        s.rho = s.local_elems(rho).contiguous()
+    it, rel, ok = dist_pcg_solve(solvers, LocalComm(), rtol=1e-11)
+    assert ok
+    u = np.zeros(prob.mesh.n_dofs)
+    for s in solvers:
+        sl, sg = s.owned_dofs()
+        u[sg] = s.x[sl].cpu().numpy()
+    assert np.abs(u - u_ref).max() <= 1e-8 * np.abs(u_ref).max()
+    assert abs(glob.last_iterations - it) <= 8 + glob.last_iterations // 50

@@ -90,8 +90,8 @@ int tb_pcg_profile(tb_plan* plan, const double* rho, const double* b, int nrep, 
 int64_t tb_launch_count(void);
 
 /* ---- slab-distributed pCG: the plan covers one z-slab; ghost node planes are
- * Dirichlet-masked in `fixed`.  Reductions and the operator's p.q run over the owned node
- * planes [k0, k1) only. */
+ * Dirichlet-masked in `fixed`.  Reductions, the operator's p.q and the rows contracted by
+ * tb_rom_reduced_stiffness run over the owned node planes [k0, k1) only. */
 int tb_plan_set_owned_planes(tb_plan* plan, int k0, int k1);
 /* One phase of a distributed Jacobi-pCG iteration on this rank.  Phases: 0 init (needs rho, b,
  * rtol, maxit; publishes local r.z, r.r), 1 finish init (after the host allreduce), 2 operator

@@ -46,7 +46,7 @@ struct tb_plan_impl {
   bool hex8 = false;     // K3 has the isotropic WHT block structure -> element-centric kernel
   int zchunk = 8;
   int dist = 0;              // distributed (slab) pCG mode
-  int own_k0 = 0, own_k1 = 1 << 30;  // owned node planes (set by tb_plan_set_owned_planes)
+  int own_k0 = 0, own_k1 = 1 << 30;  // owned node planes (set by tb_plan_set_owned_planes); ROM rows
   uint8_t* d_fixed = nullptr;
   double* d_alpha = nullptr;   // alpha of the design being solved (read by the pCG graph)
   double* d_alpha2 = nullptr;  // alpha scratch for one-off applies

@@ -367,7 +367,11 @@ int tb_rom_reduced_stiffness(tb_plan* plan, const double* phi, int k, const doub
     else
       { k_apply_cols<3><<<blocks, kBlock, 0, s>>>(g, P->K3, P->d_alpha2, phi, k, Y); tb::launched(); }
     TB_CHECK_LAUNCH();
-    TB_TRY(launch_atb(P->n_dofs, k, phi, Y, part, nb, s));
+    // contract only the rows of owned node planes (a slab's ghost rows belong to a neighbour)
+    const int64_t pd = (int64_t)g.dim * g.nnx * g.nny;
+    const int64_t r0 = (int64_t)P->own_k0 * pd;
+    const int64_t r1 = P->own_k1 >= g.nnz ? P->n_dofs : (int64_t)P->own_k1 * pd;
+    TB_TRY(launch_atb(r1 - r0, k, phi + r0 * k, Y + r0 * k, part, nb, s));
     { k_sum_parts<<<nblk(k * k), kBlock, 0, s>>>(nb, k * k, part, khat + (int64_t)d * k * k); tb::launched(); }
     TB_CHECK_LAUNCH();
   }

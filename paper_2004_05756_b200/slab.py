@@ -245,3 +245,77 @@ def dist_pcg_solve(solvers, comm, rtol=1e-8, maxit=200000, check_every=8):
 
                     raise IndefiniteMatrixError("distributed pCG breakdown")
                 return iters, (rr / bb) ** 0.5 if bb > 0 else 0.0, done == 1
+
+
+class SlabRom:
+    """Element-sharded ROM evaluation (BASELINE cfg 5): each rank holds the slab rows of Phi
+    (owned + ghost planes), contracts only its owned rows, and the k x k operators, Phi^T f and
+    squared residual norms are allreduced.  The k x k Cholesky runs redundantly on
+    every rank."""
+
+    def __init__(self, solver: SlabSolver, phi_local, comm):
+        t = _lib.torch()
+        self.s, self.comm = solver, comm
+        self.phi = phi_local.to(device=solver.device, dtype=t.float64).contiguous()
+        self.k = self.phi.shape[1]
+        sl, _ = solver.owned_dofs()
+        own_f = t.zeros_like(solver.f)
+        own_f[sl] = solver.f[sl]
+        self._fhat_part = self._project(own_f)
+
+    def _project(self, v):
+        from .rom import _project
+
+        return _project(self.phi, v[None, :])[0]
+
+    @staticmethod
+    def allreduce_tensors(slab_roms, comm, name):
+        """Sum ``getattr(rom, name)`` over ranks in place (LocalComm: fixed rank order)."""
+        if isinstance(comm, LocalComm):
+            total = getattr(slab_roms[0], name).clone()
+            for r in slab_roms[1:]:
+                total = total + getattr(r, name)
+            for r in slab_roms:
+                getattr(r, name).copy_(total)
+        else:
+            comm.dist.all_reduce(getattr(slab_roms[0], name), group=comm.group)
+
+    def local_khat(self, rho_batch_local):
+        t = _lib.torch()
+        rho2 = rho_batch_local.reshape(-1, self.s.local.n_elems).contiguous()
+        nd = rho2.shape[0]
+        khat = t.empty((nd, self.k, self.k), dtype=t.float64, device=self.s.device)
+        _lib.check(_lib.lib().tb_rom_reduced_stiffness(self.s._plan, _lib.ptr(self.phi), self.k, _lib.ptr(rho2), nd,
+                                                       _lib.ptr(khat), _lib.stream_ptr(self.s.device)), "slab khat")
+        return khat
+
+
+def slab_rom_solve_batch(roms, comm, rho_batches_local):
+    """Reduced stiffness, reduced solve and full-space residual norms for nd designs across the
+    slabs of ``roms`` (this process's share).  Returns (khat, uhat, residual norms)."""
+    t = _lib.torch()
+    for r, rho in zip(roms, rho_batches_local):
+        r.khat = r.local_khat(rho)
+        r.fhat = r._fhat_part.clone()
+    SlabRom.allreduce_tensors(roms, comm, "khat")
+    SlabRom.allreduce_tensors(roms, comm, "fhat")
+    for r, rho in zip(roms, rho_batches_local):
+        nd, k = r.khat.shape[0], r.k
+        rhs = r.fhat[None, None, :].expand(nd, 1, k).contiguous()
+        x = t.empty((nd, 1, k), dtype=t.float64, device=r.s.device)
+        status = (ctypes.c_int * nd)()
+        _lib.check(_lib.lib().tb_rom_cholesky_solve(k, nd, 1, _lib.ptr(r.khat), _lib.ptr(rhs), _lib.ptr(x), status,
+                                                    _lib.stream_ptr(r.s.device)), "slab cholesky")
+        r.uhat = x[:, 0, :].contiguous()
+        rho2 = rho.reshape(nd, -1).contiguous()
+        norms = []
+        for s0 in range(0, nd, 16):
+            e = min(nd, s0 + 16)
+            out = (ctypes.c_double * (e - s0))()
+            _lib.check(_lib.lib().tb_rom_residual_norms(r.s._plan, _lib.ptr(r.phi), k, _lib.ptr(rho2[s0:e]),
+                                                        _lib.ptr(r.uhat[s0:e]), e - s0, _lib.ptr(r.s.f), 0, out,
+                                                        _lib.stream_ptr(r.s.device)), "slab residual")
+            norms += [v * v for v in out]  # squared partials over this rank's owned free rows
+        r.res2 = t.tensor(norms, dtype=t.float64, device=r.s.device)
+    SlabRom.allreduce_tensors(roms, comm, "res2")
+    return roms[0].khat, roms[0].uhat, [float(v) ** 0.5 for v in roms[0].res2.cpu()]

@@ -207,3 +207,34 @@ def test_cuda_slabs_emulated_on_one_gpu(cuda, nranks):
         u[sg] = s.x[sl].cpu().numpy()
     assert np.abs(u - u_ref).max() <= 1e-8 * np.abs(u_ref).max()
     assert abs(glob.last_iterations - it) <= 8 + glob.last_iterations // 50
+
+
+@pytest.mark.gpu
+def test_cuda_slab_rom_emulated_on_one_gpu(cuda):
+    """cfg 5 recipe at small size: element-sharded reduced operators + allreduce == global."""
+    import paper_2004_05756_b200 as tb
+    from paper_2004_05756_b200.slab import SlabRom, SlabSolver, slab_rom_solve_batch
+
+    prob = configs.cfg5(nx=12, ny=6, nz=9, n_designs=3, k=10)
+    mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
+    glob = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, 1.0), prob.f, prob.fixed, mat)
+    raw = configs.phi_columns(prob.mesh, 10, seed=0)
+    raw[:, ~glob.free_mask] = 0.0
+    phi = torch.as_tensor(tb.gram_schmidt(list(raw)), device=cuda)
+    rhos = torch.as_tensor(np.stack(prob.rom_designs), device=cuda)
+    basis = tb.ReducedBasis(phi, None, None, phi.T @ glob._f_d)
+    kh_ref, uh_ref, n_ref = tb.RomModel(glob).solve_batch(basis, rhos)
+    slabs = partition(prob.mesh.nz, 3)
+    comm = LocalComm()
+    roms, rho_loc = [], []
+    for s in slabs:
+        sv = SlabSolver(prob.mesh, prob.k_e, prob.f, prob.fixed, mat, s)
+        d0 = s.e0 * sv.plane_dofs
+        roms.append(SlabRom(sv, phi[d0:d0 + sv.local.n_dofs], comm))
+        pe = sv.plane_elems
+        rho_loc.append(rhos[:, s.e0 * pe:s.e1 * pe].contiguous())
+    kh, uh, norms = slab_rom_solve_batch(roms, comm, rho_loc)
+    assert torch.linalg.norm(kh - kh_ref) <= 1e-12 * torch.linalg.norm(kh_ref)
+    assert torch.abs(uh - uh_ref).max() <= 1e-10 * torch.abs(uh_ref).max()
+    for a, b in zip(norms, n_ref):
+        assert abs(a - b) <= 1e-9 * b

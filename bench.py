@@ -37,7 +37,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg4", "cfg5"],
+                    help="cfg1/cfg2: HDM evaluation (headline cfg2); cfg4: slab-sharded 3D solve; cfg5: batched ROM")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
@@ -393,10 +394,157 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def fp64_peak_tflops(torch, dev):
+    """Measured FP64 GEMM throughput (cuBLAS DGEMM 8192^3, best of 5) as the FP64 roofline
+    denominator; MEASURED_PEAKS.json carries no FP64 figure."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    torch.matmul(a, b)
+    best = 1e9
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1) * 1e-3)
+    del a, b
+    return 2 * n**3 / best / 1e12
+
+
+def run_cfg5(args):
+    """BASELINE cfg 5: per trust-region step, 16 designs x (Phi^T K(rho_d) Phi, reduced solve,
+    ||K Phi uhat - f||) with a k = 64 basis on 256x128x128 Hex8 (12.8M DOF)."""
+    import numpy as np
+    import torch
+
+    import paper_2004_05756_b200 as tb
+    from paper_2004_05756_b200 import _lib, configs
+
+    rank, local, world = rank_info()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    prob = configs.cfg5(seed=args.seed)
+    m = prob.mesh
+    mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
+    s = tb.HdmSolver(m, prob.k_e, tb.HelmholtzFilter(m, prob.radius), prob.f, prob.fixed, mat, rtol=prob.rtol)
+    k = prob.rom_k
+    cols = configs.phi_columns(m, k, seed=args.seed, xp=torch, device=dev)
+    cols[:, torch.as_tensor(~s.free_mask, device=dev)] = 0.0
+    phi = tb.gram_schmidt(list(cols))
+    del cols
+    basis = tb.ReducedBasis(phi, None, None, phi.T @ s._f_d)
+    rom = tb.RomModel(s)
+    rhos = torch.as_tensor(np.stack(prob.rom_designs), device=dev)
+    nd = rhos.shape[0]
+    for _ in range(max(args.warmup, 1)):
+        rom.solve_batch(basis, rhos)
+    torch.cuda.synchronize()
+    launches0 = _lib.lib().tb_launch_count()
+    clocks = Clocks(dev.index)
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        ev[i][0].record()
+        khat, uhat, norms = rom.solve_batch(basis, rhos)
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = _lib.lib().tb_launch_count() - launches0
+    t_step = sum(a.elapsed_time(b) for a, b in ev) / args.steps * 1e-3
+    # the dominant kernel: Phi^T K Phi for one design (operator per column + DMMA contraction)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    rom.reduced_stiffness_device(basis, rhos[0])
+    e1.record()
+    torch.cuda.synchronize()
+    t_khat = e0.elapsed_time(e1) * 1e-3
+    n_u, n_e = m.n_dofs, m.n_elems
+    canonical = n_e * (2 * k * 24**2 + 2 * k**2 * 24)  # PAPER.md:664 element form, per design
+    executed_dmma = 2 * n_u * k * k                      # Phi^T Y on DMMA, per design
+    peak = fp64_peak_tflops(torch, dev)
+    line = {
+        "metric": "PhiT K Phi time (16-design ROM step)", "value": t_step, "unit": "s/step", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": t_step * 1e3, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg 5 recipe)",
+        "config": {"workload": f"cfg5 {m.nx}x{m.ny}x{m.nz} Hex8, {n_u} DOF, k={k}, {nd} designs: "
+                               "Phi^T K(rho_d) Phi + batched Cholesky + residual norms", "parallelism": "single"},
+        "roofline": {"kernel": "reduced stiffness of one design (k_hex8 per column + k_atb_dmma)", "bound": "tensor",
+                     "achieved": canonical / t_khat / 1e12, "peak": peak, "unit": "TFLOP/s",
+                     "frac": canonical / t_khat / 1e12 / peak, "traffic": None,
+                     "flops_convention": "canonical element-form count N_e(2k*24^2 + 2k^2*24) (PAPER.md:664)",
+                     "executed_dmma_tflops": executed_dmma / t_khat / 1e12, "s_per_design": t_khat,
+                     "peak_source": "cuBLAS DGEMM 8192^3 measured in this run"},
+        "gpu_launches": int(launches), "clocks": clk,
+        "extra": {"residual_norms": norms[:4], "uhat0_norm": float(torch.linalg.norm(uhat[0]))},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_cfg4(args):
+    """BASELINE cfg 4: slab-sharded (z) Jacobi-pCG solve + sensitivities on 384x192x192 Hex8
+    (43M DOF), one slab per rank, NCCL allreduce + halo exchange.  rho = psi (the filter is
+    applied once as input generation; the distributed filter is future work)."""
+    import numpy as np
+    import torch
+
+    import paper_2004_05756_b200 as tb
+    from paper_2004_05756_b200 import configs
+    from paper_2004_05756_b200.slab import SlabSolver, TorchComm, dist_pcg_solve, partition
+
+    rank, local, world = rank_info()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        if world > 1:
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            import socket
+
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                    device_id=dev)
+    prob = configs.cfg4(seed=args.seed)
+    mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
+    slab = partition(prob.mesh.nz, world)[rank]
+    sv = SlabSolver(prob.mesh, prob.k_e, prob.f, prob.fixed, mat, slab, device=dev)
+    rho = torch.as_tensor(sv.local_elems(prob.psi).copy(), device=dev)
+    sv.rho = rho
+    comm = TorchComm()
+    dist_pcg_solve([sv], comm, rtol=prob.rtol)  # warm-up
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    iters, rel, ok = dist_pcg_solve([sv], comm, rtol=prob.rtol)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({
+            "metric": "FE solve s/eval (slab-sharded)", "value": float(t.item()), "unit": "s/eval", "n_gpus": world,
+            "steps": 1, "warmup": 1, "ms_per_step": float(t.item()) * 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg 4 recipe)",
+            "config": {"workload": f"cfg4 {prob.mesh.nx}x{prob.mesh.ny}x{prob.mesh.nz} Hex8, {prob.mesh.n_dofs} DOF, "
+                                   f"z-slabs x{world}, Jacobi-pCG to {prob.rtol:g}",
+                       "parallelism": f"slab{world}", "pcg_iterations": iters, "converged": ok}}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "cfg5":
+        run_cfg5(args)
+    elif args.config == "cfg4":
+        run_cfg4(args)
     else:
         run_ours(args)
 

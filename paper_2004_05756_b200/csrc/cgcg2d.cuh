@@ -23,11 +23,7 @@
 namespace tb {
 
 #ifdef TB_CGCG_PROF
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
+__device__ __forceinline__ unsigned long long gtime() { return (unsigned long long)clock64(); }
 #define PROF_MARK(k)                                  \
   do {                                                \
     if (blockIdx.x == 0 && threadIdx.x == 0) {        \
@@ -69,6 +65,7 @@ struct CgcgArgs {
   PcgState* st;
   unsigned int* bar;
   int own_max;         // max nodes owned by a CTA
+  int dbg;             // profiling builds only: bit0 skip barrier, bit1 skip apply, bit2 skip halo
 };
 
 constexpr int kCgcgThreads = 512;
@@ -295,10 +292,15 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
       rs[o] = r;
     }
     PROF_MARK(1);
-    halo_store();
-    for (int64_t base = (int64_t)kHB * nt; base < halo; base += (int64_t)kHB * nt) {
-      halo_load(base);
+#ifdef TB_CGCG_PROF
+    if (!(a.dbg & 4))
+#endif
+    {
       halo_store();
+      for (int64_t base = (int64_t)kHB * nt; base < halo; base += (int64_t)kHB * nt) {
+        halo_load(base);
+        halo_store();
+      }
     }
     __syncthreads();
     PROF_MARK(2);
@@ -311,6 +313,11 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
     for (int o = tid; o < no; o += nt) {
       const int n = n0i + o;
       double out[NC];
+#ifdef TB_CGCG_PROF
+      if (a.dbg & 2) {
+        for (int c = 0; c < NC; ++c) out[c] = u_ext[(n - h0i) * NC + c];
+      } else
+#endif
       node_apply(n, out);
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
@@ -334,12 +341,15 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
       a.part[2 * nbk + blockIdx.x] = acc3[2];
     }
     par ^= 1;
-    grid_sync_flip(a.bar);
+#ifdef TB_CGCG_PROF
+    if (!(a.dbg & 1))
+#endif
+      grid_sync_flip(a.bar);
     PROF_MARK(6);
   }
 #ifdef TB_CGCG_PROF
   if (blockIdx.x == 0 && tid == 0)
-    printf("cgcg prof (ns/iter over %d its): sums %.0f own %.0f halo %.0f ownu %.0f apply %.0f bsum %.0f barrier %.0f\n",
+    printf("cgcg prof (cycles/iter over %d its): sums %.0f own %.0f halo %.0f ownu %.0f apply %.0f bsum %.0f barrier %.0f\n",
            it, prof[0] / (double)it, prof[1] / (double)it, prof[2] / (double)it, prof[3] / (double)it,
            prof[4] / (double)it, prof[5] / (double)it, prof[6] / (double)it);
 #endif

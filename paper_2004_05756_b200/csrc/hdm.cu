@@ -1,5 +1,6 @@
 // libtopo_b200: plan, SIMP elasticity operator, Helmholtz filter, HDM entry points.
 #include <stdarg.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -194,7 +195,10 @@ static void launch_cgcg(const Grid& g, const Mat<4 * NC>& K, const double* alpha
   const int64_t own = (g.n_nodes + grid - 1) / grid;
   const size_t smem = cgcg_smem_bytes(NC, own, g.nnx, g.nx);
   CgcgArgs a{nullptr, w.x, w.r, w.dinv, w.pub, w.partA(), w.st, reinterpret_cast<unsigned int*>(w.barrier),
-             (int)own};
+             (int)own, 0};
+#ifdef TB_CGCG_PROF
+  if (const char* e = getenv("TB_CGCG_DBG")) a.dbg = (NC == 2) ? atoi(e) : 0;
+#endif
   Grid gg = g;
   Mat<4 * NC> KK = K;
   const double* al = alpha;

@@ -104,9 +104,12 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-template <int KP>  // padded k (multiple of 8)
+// COLMAJOR: A and B are k contiguous columns with leading dimension ld (A[c*ld + row]);
+// otherwise row-major (A[row*k + c]).
+template <int KP, bool COLMAJOR>
 __global__ void __launch_bounds__(kGemmThreads) k_atb_dmma(int64_t n, int k, const double* __restrict__ A,
-                                                           const double* __restrict__ B, double* __restrict__ part) {
+                                                           const double* __restrict__ B, double* __restrict__ part,
+                                                           int64_t ld) {
   constexpr int LD = KP + 8;  // padded smem row (bank-conflict-free fragment reads)
   constexpr int TILES = (KP / 8) * (KP / 8);
   constexpr int NW = kGemmThreads / 32;
@@ -122,11 +125,12 @@ __global__ void __launch_bounds__(kGemmThreads) k_atb_dmma(int64_t n, int k, con
   for (int64_t base = i0; base < i1; base += kRows) {
     __syncthreads();
     for (int o = tid; o < kRows * KP; o += kGemmThreads) {
-      const int r = o / KP, c = o % KP;
+      const int r = COLMAJOR ? o % kRows : o / KP, c = COLMAJOR ? o / kRows : o % KP;
       const int64_t row = base + r;
       const bool ok = row < i1 && c < k;
-      sa[r * LD + c] = ok ? A[row * k + c] : 0.0;
-      sb[r * LD + c] = ok ? B[row * k + c] : 0.0;
+      const int64_t at = COLMAJOR ? c * ld + row : row * k + c;
+      sa[r * LD + c] = ok ? A[at] : 0.0;
+      sb[r * LD + c] = ok ? B[at] : 0.0;
     }
     __syncthreads();
 #pragma unroll
@@ -157,22 +161,46 @@ __global__ void __launch_bounds__(kGemmThreads) k_atb_dmma(int64_t n, int k, con
   }
 }
 
-static int launch_atb(int64_t n, int k, const double* A, const double* B, double* part, int nb, cudaStream_t s) {
+template <bool CM>
+static int launch_atb_t(int64_t n, int k, const double* A, const double* B, double* part, int nb, int64_t ld,
+                        cudaStream_t s) {
   const int kp = (k + 7) / 8 * 8;
   if (kp <= 8)
-    { k_atb_dmma<8><<<nb, kGemmThreads, 0, s>>>(n, k, A, B, part); tb::launched(); }
+    { k_atb_dmma<8, CM><<<nb, kGemmThreads, 0, s>>>(n, k, A, B, part, ld); tb::launched(); }
   else if (kp <= 16)
-    { k_atb_dmma<16><<<nb, kGemmThreads, 0, s>>>(n, k, A, B, part); tb::launched(); }
+    { k_atb_dmma<16, CM><<<nb, kGemmThreads, 0, s>>>(n, k, A, B, part, ld); tb::launched(); }
   else if (kp <= 32)
-    { k_atb_dmma<32><<<nb, kGemmThreads, 0, s>>>(n, k, A, B, part); tb::launched(); }
+    { k_atb_dmma<32, CM><<<nb, kGemmThreads, 0, s>>>(n, k, A, B, part, ld); tb::launched(); }
   else if (kp <= 64)
-    { k_atb_dmma<64><<<nb, kGemmThreads, 0, s>>>(n, k, A, B, part); tb::launched(); }
+    { k_atb_dmma<64, CM><<<nb, kGemmThreads, 0, s>>>(n, k, A, B, part, ld); tb::launched(); }
   else {
     set_error("reduced basis size k=%d exceeds 64", k);
     return TB_ERR_INVALID;
   }
   TB_CHECK_LAUNCH();
   return TB_OK;
+}
+
+static int launch_atb(int64_t n, int k, const double* A, const double* B, double* part, int nb, cudaStream_t s) {
+  return launch_atb_t<false>(n, k, A, B, part, nb, 0, s);
+}
+
+// row-major (n x k) -> column-major (k columns of n), 32 x 32 tiles through shared memory
+__global__ void k_transpose_rm_cm(int64_t n, int k, const double* __restrict__ rm, double* __restrict__ cm) {
+  __shared__ double tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int c0 = blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t r = r0 + y;
+    const int c = c0 + threadIdx.x;
+    tile[y][threadIdx.x] = (r < n && c < k) ? rm[r * k + c] : 0.0;
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int c = c0 + y;
+    const int64_t r = r0 + threadIdx.x;
+    if (r < n && c < k) cm[(int64_t)c * n + r] = tile[threadIdx.x][y];
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -352,26 +380,42 @@ int tb_rom_reduced_stiffness(tb_plan* plan, const double* phi, int k, const doub
   auto* P = reinterpret_cast<tb_plan_impl*>(plan);
   cudaStream_t s = (cudaStream_t)stream;
   const Grid& g = P->g;
+  const int64_t n = P->n_dofs;
   const int nb = 148 * 2;
-  const size_t ybytes = sizeof(double) * (size_t)P->n_dofs * k;
+  // contract only the rows of owned node planes (a slab's ghost rows belong to a neighbour)
+  const int64_t pd = (int64_t)g.dim * g.nnx * g.nny;
+  const int64_t r0 = (int64_t)P->own_k0 * pd;
+  const int64_t r1 = P->own_k1 >= g.nnz ? n : (int64_t)P->own_k1 * pd;
+  const bool hex8 = (g.dim == 3 && P->hex8);
+  // 3D: one WHT Hex8 launch per column on a column-major copy of Phi; 2D: node-owner over
+  // all k columns of the row-major Phi
+  const size_t ybytes = sizeof(double) * (size_t)n * k * (hex8 ? 2 : 1);
   const size_t pbytes = sizeof(double) * (size_t)nb * k * k;
   TB_TRY(P->rom_scratch(ybytes + pbytes));
   double* Y = P->d_rom;
-  double* part = P->d_rom + (size_t)P->n_dofs * k;
+  double* PhiT = hex8 ? P->d_rom + (size_t)n * k : nullptr;
+  double* part = P->d_rom + (size_t)n * k * (hex8 ? 2 : 1);
+  if (hex8) {
+    dim3 tg((unsigned)((n + 31) / 32), (unsigned)((k + 31) / 32));
+    { k_transpose_rm_cm<<<tg, dim3(32, 8), 0, s>>>(n, k, phi, PhiT); tb::launched(); }
+  }
   for (int d = 0; d < nd; ++d) {
     TB_TRY(P->material(rho + (int64_t)d * g.n_elems, P->d_alpha2, nullptr, s));
-    const int64_t threads = g.n_nodes * k;
-    const int blocks = (int)((threads + kBlock - 1) / kBlock);
-    if (g.dim == 2)
-      { k_apply_cols<2><<<blocks, kBlock, 0, s>>>(g, P->K2, P->d_alpha2, phi, k, Y); tb::launched(); }
-    else
-      { k_apply_cols<3><<<blocks, kBlock, 0, s>>>(g, P->K3, P->d_alpha2, phi, k, Y); tb::launched(); }
-    TB_CHECK_LAUNCH();
-    // contract only the rows of owned node planes (a slab's ghost rows belong to a neighbour)
-    const int64_t pd = (int64_t)g.dim * g.nnx * g.nny;
-    const int64_t r0 = (int64_t)P->own_k0 * pd;
-    const int64_t r1 = P->own_k1 >= g.nnz ? P->n_dofs : (int64_t)P->own_k1 * pd;
-    TB_TRY(launch_atb(r1 - r0, k, phi + r0 * k, Y + r0 * k, part, nb, s));
+    if (hex8) {
+      for (int j = 0; j < k; ++j)
+        { k_hex8<false><<<hex8_grid(g, P->zchunk), kHT, kHex8Smem, s>>>(g, P->hiso, P->d_alpha2, PhiT + (int64_t)j * n, nullptr, nullptr, Y + (int64_t)j * n, nullptr, nullptr, nullptr, P->zchunk); tb::launched(); }
+      TB_CHECK_LAUNCH();
+      TB_TRY(launch_atb_t<true>(r1 - r0, k, PhiT + r0, Y + r0, part, nb, n, s));
+    } else {
+      const int64_t threads = g.n_nodes * k;
+      const int blocks = (int)((threads + kBlock - 1) / kBlock);
+      if (g.dim == 2)
+        { k_apply_cols<2><<<blocks, kBlock, 0, s>>>(g, P->K2, P->d_alpha2, phi, k, Y); tb::launched(); }
+      else
+        { k_apply_cols<3><<<blocks, kBlock, 0, s>>>(g, P->K3, P->d_alpha2, phi, k, Y); tb::launched(); }
+      TB_CHECK_LAUNCH();
+      TB_TRY(launch_atb(r1 - r0, k, phi + r0 * k, Y + r0 * k, part, nb, s));
+    }
     { k_sum_parts<<<nblk(k * k), kBlock, 0, s>>>(nb, k * k, part, khat + (int64_t)d * k * k); tb::launched(); }
     TB_CHECK_LAUNCH();
   }

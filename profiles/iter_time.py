@@ -18,6 +18,19 @@ s = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, prob.radius)
                  tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP), rtol=prob.rtol)
 psi = torch.as_tensor(prob.psi, device="cuda")
 rho, _ = s.filtered_density_device(psi)
+if os.environ.get("TB_MAXIT"):  # ablation timing: fixed iteration budget, results not meaningful
+    s.maxit = int(os.environ["TB_MAXIT"])
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for rep in range(2):
+        a.record()
+        try:
+            s.pcg_device(rho, s._f_d)
+        except Exception:
+            pass
+        b.record()
+        torch.cuda.synchronize()
+    print(f"{name} maxit={s.maxit} dbg={os.environ.get('TB_CGCG_DBG')}: {a.elapsed_time(b) * 1e3 / s.maxit:.3f} us/iteration")
+    sys.exit(0)
 for _ in range(2):
     s.pcg_device(rho, s._f_d)
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

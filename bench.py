@@ -413,6 +413,31 @@ def fp64_peak_tflops(torch, dev):
     return 2 * n**3 / best / 1e12
 
 
+def dmma_time(rom, basis, rho, torch):
+    """CUDA-event time of the DMMA contraction alone (tb_rom_gram_colmajor: the kernel
+    tb_rom_reduced_stiffness uses, on the column-major basis), one launch after warm-up."""
+    import ctypes
+
+    from paper_2004_05756_b200 import _lib
+
+    phi = basis.device_phi(rom.device)
+    n, k = phi.shape
+    ldp = (n + 1) // 2 * 2
+    a = torch.zeros((k, ldp), dtype=torch.float64, device=rom.device)
+    a[:, :n] = phi.t()
+    out = torch.empty((k, k), dtype=torch.float64, device=rom.device)
+    for _ in range(2):
+        _lib.check(_lib.lib().tb_rom_gram_colmajor(n, k, _lib.ptr(a), _lib.ptr(a), ldp, _lib.ptr(out),
+                                                   _lib.stream_ptr(rom.device)), "gram")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _lib.check(_lib.lib().tb_rom_gram_colmajor(n, k, _lib.ptr(a), _lib.ptr(a), ldp, _lib.ptr(out),
+                                               _lib.stream_ptr(rom.device)), "gram")
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e-3
+
+
 def run_cfg5(args):
     """BASELINE cfg 5: per trust-region step, 16 designs x (Phi^T K(rho_d) Phi, reduced solve,
     ||K Phi uhat - f||) with a k = 64 basis on 256x128x128 Hex8 (12.8M DOF)."""
@@ -463,19 +488,24 @@ def run_cfg5(args):
     n_u, n_e = m.n_dofs, m.n_elems
     canonical = n_e * (2 * k * 24**2 + 2 * k**2 * 24)  # PAPER.md:664 element form, per design
     executed_dmma = 2 * n_u * k * k                      # Phi^T Y on DMMA, per design
+    executed_op = 190 * n_e * k                          # WHT Hex8 operator, FP64 instr per element-column
     peak = fp64_peak_tflops(torch, dev)
+    # the dominant kernel alone: the DMMA contraction, timed with events around its launch
+    t_dmma = dmma_time(rom, basis, rhos[0], torch)
     line = {
         "metric": "PhiT K Phi time (16-design ROM step)", "value": t_step, "unit": "s/step", "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": t_step * 1e3, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg 5 recipe)",
         "config": {"workload": f"cfg5 {m.nx}x{m.ny}x{m.nz} Hex8, {n_u} DOF, k={k}, {nd} designs: "
                                "Phi^T K(rho_d) Phi + batched Cholesky + residual norms", "parallelism": "single"},
-        "roofline": {"kernel": "reduced stiffness of one design (k_hex8 per column + k_atb_dmma)", "bound": "tensor",
-                     "achieved": canonical / t_khat / 1e12, "peak": peak, "unit": "TFLOP/s",
-                     "frac": canonical / t_khat / 1e12 / peak, "traffic": None,
-                     "flops_convention": "canonical element-form count N_e(2k*24^2 + 2k^2*24) (PAPER.md:664)",
-                     "executed_dmma_tflops": executed_dmma / t_khat / 1e12, "s_per_design": t_khat,
-                     "peak_source": "cuBLAS DGEMM 8192^3 measured in this run"},
+        "roofline": {"kernel": "k_atb_cm<64> (Phi^T Y on FP64 tensor cores, DMMA m8n8k4)", "bound": "tensor",
+                     "achieved": executed_dmma / t_dmma / 1e12, "peak": peak, "unit": "TFLOP/s",
+                     "frac": executed_dmma / t_dmma / 1e12 / peak, "traffic": None,
+                     "us_per_launch": t_dmma * 1e6, "flops_per_launch": executed_dmma,
+                     "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64)",
+                     "per_design": {"s": t_khat, "executed_tflops": (executed_dmma + executed_op) / t_khat / 1e12,
+                                    "canonical_elementform_tflops_equiv": canonical / t_khat / 1e12,
+                                    "canonical_flops_convention": "N_e(2k*24^2 + 2k^2*24) (PAPER.md:664)"}},
         "gpu_launches": int(launches), "clocks": clk,
         "extra": {"residual_norms": norms[:4], "uhat0_norm": float(torch.linalg.norm(uhat[0]))},
     }

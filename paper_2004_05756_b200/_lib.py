@@ -30,7 +30,7 @@ EXPORTS = (
     "tb_pcg_solve", "tb_pcg_profile", "tb_launch_count", "tb_plan_set_owned_planes", "tb_pcg_dist_phase",
     "tb_pcg_dist_buffers", "tb_pcg_dist_state", "tb_dot", "tb_filter_create", "tb_filter_destroy", "tb_filter_load_vector",
     "tb_filter_apply", "tb_filter_adjoint", "tb_rom_project", "tb_rom_reduced_stiffness",
-    "tb_rom_cholesky_solve", "tb_rom_reconstruct", "tb_rom_residual_norms", "tb_gram_schmidt",
+    "tb_rom_gram_colmajor", "tb_rom_cholesky_solve", "tb_rom_reconstruct", "tb_rom_residual_norms", "tb_gram_schmidt",
 )
 
 
@@ -73,6 +73,7 @@ _SIGS = {
     "tb_filter_adjoint": ([P, P, P, D, PI, P], I),
     "tb_rom_project": ([I64, P, I, P, I, P, P], I),
     "tb_rom_reduced_stiffness": ([P, P, I, P, I, P, P], I),
+    "tb_rom_gram_colmajor": ([I64, I, P, P, I64, P, P], I),
     "tb_rom_cholesky_solve": ([I, I, I, P, P, P, PI, P], I),
     "tb_rom_reconstruct": ([I64, P, I, P, I, P, P], I),
     "tb_rom_residual_norms": ([P, P, I, P, P, I, P, I64, PD, P], I),

@@ -161,6 +161,113 @@ __global__ void __launch_bounds__(kGemmThreads) k_atb_dmma(int64_t n, int k, con
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Column-major A^T B on DMMA with a double-buffered cp.async pipeline (3D ROM path).
+// A, B: k columns with leading dimension ld; rows [r0, r1) are contracted.
+// Stage = 32 rows x KP columns of both matrices in shared memory as [col][row] (+pad);
+// warp w owns output row block(s) so its A fragment feeds 8 DMMAs per k-step.
+// ---------------------------------------------------------------------------------------
+constexpr int kCmRows = 32, kCmLd = kCmRows + 4;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 8 : 0;  // src-size 0 zero-fills the destination
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int KP>
+__global__ void __launch_bounds__(kGemmThreads) k_atb_cm(int64_t r0, int64_t r1, int k,
+                                                         const double* __restrict__ A, const double* __restrict__ B,
+                                                         double* __restrict__ part, int64_t ld) {
+  constexpr int MB = KP / 8, TILES = MB * MB, NW = kGemmThreads / 32, TPW = (TILES + NW - 1) / NW;
+  constexpr int STAGE = 2 * KP * kCmLd;  // doubles per stage (A then B)
+  extern __shared__ __align__(16) double smc[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n = r1 - r0;
+  const int64_t per = ((n + gridDim.x - 1) / gridDim.x + kCmRows - 1) / kCmRows * kCmRows;
+  const int64_t i0 = r0 + (int64_t)blockIdx.x * per, i1 = min(r1, i0 + per);
+  const int nstages = (int)((max(i1 - i0, (int64_t)0) + kCmRows - 1) / kCmRows);
+  auto load = [&](int stg, int buf) {
+    const int64_t base = i0 + (int64_t)stg * kCmRows;
+    double* sbuf = smc + buf * STAGE;
+    for (int idx = tid; idx < 2 * KP * kCmRows; idx += kGemmThreads) {
+      const int mat = idx / (KP * kCmRows), rem = idx % (KP * kCmRows);
+      const int c = rem / kCmRows, r = rem % kCmRows;
+      const int64_t row = base + r;
+      const bool ok = c < k && row < i1;
+      const double* src = (mat ? B : A) + (ok ? (int64_t)c * ld + row : 0);
+      cp_async8(sbuf + mat * KP * kCmLd + c * kCmLd + r, src, ok);
+    }
+    cp_async_commit();
+  };
+  double acc[TPW][2];
+#pragma unroll
+  for (int t = 0; t < TPW; ++t) acc[t][0] = acc[t][1] = 0.0;
+  if (nstages > 0) load(0, 0);
+  for (int st = 0; st < nstages; ++st) {
+    if (st + 1 < nstages) {
+      load(st + 1, (st + 1) & 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* sa = smc + (st & 1) * STAGE;
+    const double* sb = sa + KP * kCmLd;
+#pragma unroll
+    for (int r0 = 0; r0 < kCmRows; r0 += 4) {
+      const int rr = r0 + (lane & 3), cc = lane >> 2;
+#pragma unroll
+      for (int t = 0; t < TPW; ++t) {
+        const int tile = warp * TPW + t;
+        if (tile < TILES) {
+          const int m0 = (tile / MB) * 8, n0 = (tile % MB) * 8;
+          const double a = sa[(m0 + cc) * kCmLd + rr];
+          const double b = sb[(n0 + cc) * kCmLd + rr];
+          dmma_8x8x4(acc[t], a, b);
+        }
+      }
+    }
+    __syncthreads();  // the buffer is refilled two stages later
+  }
+  double* out = part + (int64_t)blockIdx.x * k * k;
+#pragma unroll
+  for (int t = 0; t < TPW; ++t) {
+    const int tile = warp * TPW + t;
+    if (tile < TILES) {
+      const int m = (tile / MB) * 8 + (lane >> 2);
+      const int c0 = (tile % MB) * 8 + 2 * (lane & 3);
+      if (m < k && c0 < k) out[m * k + c0] = acc[t][0];
+      if (m < k && c0 + 1 < k) out[m * k + c0 + 1] = acc[t][1];
+    }
+  }
+}
+
+template <int KP>
+static int launch_cm(int64_t r0, int64_t r1, int k, const double* A, const double* B, double* part, int nb,
+                     int64_t ld, cudaStream_t s) {
+  const size_t smem = sizeof(double) * 2 * 2 * KP * kCmLd;
+  TB_CUDA(cudaFuncSetAttribute(k_atb_cm<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  { k_atb_cm<KP><<<nb, kGemmThreads, smem, s>>>(r0, r1, k, A, B, part, ld); tb::launched(); }
+  TB_CHECK_LAUNCH();
+  return TB_OK;
+}
+
+static int launch_atb_colmajor(int64_t r0, int64_t r1, int k, const double* A, const double* B, double* part,
+                               int nb, int64_t ld, cudaStream_t s) {
+  const int kp = (k + 7) / 8 * 8;
+  if (kp <= 16) return launch_cm<16>(r0, r1, k, A, B, part, nb, ld, s);
+  if (kp <= 32) return launch_cm<32>(r0, r1, k, A, B, part, nb, ld, s);
+  if (kp <= 64) return launch_cm<64>(r0, r1, k, A, B, part, nb, ld, s);
+  set_error("reduced basis size k=%d exceeds 64", k);
+  return TB_ERR_INVALID;
+}
+
 template <bool CM>
 static int launch_atb_t(int64_t n, int k, const double* A, const double* B, double* part, int nb, int64_t ld,
                         cudaStream_t s) {
@@ -185,8 +292,9 @@ static int launch_atb(int64_t n, int k, const double* A, const double* B, double
   return launch_atb_t<false>(n, k, A, B, part, nb, 0, s);
 }
 
-// row-major (n x k) -> column-major (k columns of n), 32 x 32 tiles through shared memory
-__global__ void k_transpose_rm_cm(int64_t n, int k, const double* __restrict__ rm, double* __restrict__ cm) {
+// row-major (n x k) -> column-major (k columns, leading dimension ld >= n), 32 x 32 tiles
+__global__ void k_transpose_rm_cm(int64_t n, int k, const double* __restrict__ rm, double* __restrict__ cm,
+                                  int64_t ld) {
   __shared__ double tile[32][33];
   const int64_t r0 = (int64_t)blockIdx.x * 32;
   const int c0 = blockIdx.y * 32;
@@ -199,7 +307,7 @@ __global__ void k_transpose_rm_cm(int64_t n, int k, const double* __restrict__ r
   for (int y = threadIdx.y; y < 32; y += blockDim.y) {
     const int c = c0 + y;
     const int64_t r = r0 + threadIdx.x;
-    if (r < n && c < k) cm[(int64_t)c * n + r] = tile[threadIdx.x][y];
+    if (c < k && r < ld) cm[(int64_t)c * ld + r] = (r < n) ? tile[threadIdx.x][y] : 0.0;
   }
 }
 
@@ -389,23 +497,25 @@ int tb_rom_reduced_stiffness(tb_plan* plan, const double* phi, int k, const doub
   const bool hex8 = (g.dim == 3 && P->hex8);
   // 3D: one WHT Hex8 launch per column on a column-major copy of Phi; 2D: node-owner over
   // all k columns of the row-major Phi
-  const size_t ybytes = sizeof(double) * (size_t)n * k * (hex8 ? 2 : 1);
-  const size_t pbytes = sizeof(double) * (size_t)nb * k * k;
+  const int nbc = hex8 ? 148 * 3 : nb;              // column-major DMMA: 3 CTAs per SM
+  const int64_t ldp = hex8 ? (n + 1) / 2 * 2 : n;    // even leading dimension (16-byte columns)
+  const size_t ybytes = sizeof(double) * (size_t)ldp * k * (hex8 ? 2 : 1);
+  const size_t pbytes = sizeof(double) * (size_t)nbc * k * k;
   TB_TRY(P->rom_scratch(ybytes + pbytes));
   double* Y = P->d_rom;
-  double* PhiT = hex8 ? P->d_rom + (size_t)n * k : nullptr;
-  double* part = P->d_rom + (size_t)n * k * (hex8 ? 2 : 1);
+  double* PhiT = hex8 ? P->d_rom + (size_t)ldp * k : nullptr;
+  double* part = P->d_rom + (size_t)ldp * k * (hex8 ? 2 : 1);
   if (hex8) {
     dim3 tg((unsigned)((n + 31) / 32), (unsigned)((k + 31) / 32));
-    { k_transpose_rm_cm<<<tg, dim3(32, 8), 0, s>>>(n, k, phi, PhiT); tb::launched(); }
+    { k_transpose_rm_cm<<<tg, dim3(32, 8), 0, s>>>(n, k, phi, PhiT, ldp); tb::launched(); }
   }
   for (int d = 0; d < nd; ++d) {
     TB_TRY(P->material(rho + (int64_t)d * g.n_elems, P->d_alpha2, nullptr, s));
     if (hex8) {
       for (int j = 0; j < k; ++j)
-        { k_hex8<false><<<hex8_grid(g, P->zchunk), kHT, kHex8Smem, s>>>(g, P->hiso, P->d_alpha2, PhiT + (int64_t)j * n, nullptr, nullptr, Y + (int64_t)j * n, nullptr, nullptr, nullptr, P->zchunk); tb::launched(); }
+        { k_hex8<false><<<hex8_grid(g, P->zchunk), kHT, kHex8Smem, s>>>(g, P->hiso, P->d_alpha2, PhiT + (int64_t)j * ldp, nullptr, nullptr, Y + (int64_t)j * ldp, nullptr, nullptr, nullptr, P->zchunk); tb::launched(); }
       TB_CHECK_LAUNCH();
-      TB_TRY(launch_atb_t<true>(r1 - r0, k, PhiT + r0, Y + r0, part, nb, n, s));
+      TB_TRY(launch_atb_colmajor(r0, r1, k, PhiT, Y, part, nbc, ldp, s));
     } else {
       const int64_t threads = g.n_nodes * k;
       const int blocks = (int)((threads + kBlock - 1) / kBlock);
@@ -416,9 +526,24 @@ int tb_rom_reduced_stiffness(tb_plan* plan, const double* phi, int k, const doub
       TB_CHECK_LAUNCH();
       TB_TRY(launch_atb(r1 - r0, k, phi + r0 * k, Y + r0 * k, part, nb, s));
     }
-    { k_sum_parts<<<nblk(k * k), kBlock, 0, s>>>(nb, k * k, part, khat + (int64_t)d * k * k); tb::launched(); }
+    { k_sum_parts<<<nblk(k * k), kBlock, 0, s>>>(hex8 ? nbc : nb, k * k, part, khat + (int64_t)d * k * k); tb::launched(); }
     TB_CHECK_LAUNCH();
   }
+  return TB_OK;
+}
+
+int tb_rom_gram_colmajor(int64_t n, int k, const double* A, const double* B, int64_t ld, double* out,
+                         void* stream) {
+  TB_GUARD(A && B && out && n >= 1 && ld >= n, "bad arguments");
+  TB_GUARD(k >= 1 && k <= 64, "k=%d out of range [1, 64]", k);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nb = 148 * 3;
+  double* part = nullptr;
+  TB_CUDA(cudaMallocAsync(&part, sizeof(double) * (size_t)nb * k * k, s));
+  TB_TRY(launch_atb_colmajor(0, n, k, A, B, part, nb, ld, s));
+  { k_sum_parts<<<nblk(k * k), kBlock, 0, s>>>(nb, k * k, part, out); tb::launched(); }
+  TB_CHECK_LAUNCH();
+  TB_CUDA(cudaFreeAsync(part, s));
   return TB_OK;
 }
 

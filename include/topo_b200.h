@@ -81,6 +81,11 @@ int tb_element_sensitivity(tb_plan* plan, const double* rho, const double* u, co
 int tb_pcg_solve(tb_plan* plan, const double* rho, const double* b, double* x, double rtol,
                  int maxit, int* iters, double* relres, void* stream);
 
+/* Preconditioner of tb_pcg_solve: 0 Jacobi (default), 1 geometric multigrid (Galerkin element
+ * aggregation, damped-Jacobi V-cycle, dense coarsest solve; needs even element counts down to a
+ * coarsest level of <= 6144 dofs, else TB_ERR_INVALID). */
+int tb_plan_set_preconditioner(tb_plan* plan, int kind);
+
 /* Diagnostics: time the two pCG kernels in situ.  Starts a solve of K(rho) x = b and runs
  * nrep iterations with a CUDA event pair around every kernel on `stream`; returns the mean
  * duration (ms) of the fused operator kernel and of the update kernel (HOST pointers). */

@@ -27,7 +27,7 @@ TB_ERR_DENSITY = 6
 EXPORTS = (
     "tb_version", "tb_last_error", "tb_plan_create", "tb_plan_destroy", "tb_plan_sizes",
     "tb_material", "tb_clamp_density", "tb_apply_stiffness", "tb_element_sensitivity",
-    "tb_pcg_solve", "tb_pcg_profile", "tb_launch_count", "tb_plan_set_owned_planes", "tb_pcg_dist_phase",
+    "tb_pcg_solve", "tb_plan_set_preconditioner", "tb_pcg_profile", "tb_launch_count", "tb_plan_set_owned_planes", "tb_pcg_dist_phase",
     "tb_pcg_dist_buffers", "tb_pcg_dist_state", "tb_dot", "tb_filter_create", "tb_filter_destroy", "tb_filter_load_vector",
     "tb_filter_apply", "tb_filter_adjoint", "tb_rom_project", "tb_rom_reduced_stiffness",
     "tb_rom_gram_colmajor", "tb_rom_cholesky_solve", "tb_rom_reconstruct", "tb_rom_residual_norms", "tb_gram_schmidt",
@@ -59,6 +59,7 @@ _SIGS = {
     "tb_apply_stiffness": ([P, P, P, P, I, P], I),
     "tb_element_sensitivity": ([P, P, P, P, P, P, P], I),
     "tb_pcg_solve": ([P, P, P, P, D, I, PI, PD, P], I),
+    "tb_plan_set_preconditioner": ([P, I], I),
     "tb_pcg_profile": ([P, P, P, I, PD, PD, P], I),
     "tb_launch_count": ([], I64),
     "tb_plan_set_owned_planes": ([P, I, I], I),

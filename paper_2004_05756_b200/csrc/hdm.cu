@@ -379,6 +379,15 @@ int tb_pcg_profile(tb_plan* plan, const double* rho, const double* b, int nrep, 
 
 int64_t tb_launch_count(void) { return g_launches.load(); }
 
+int tb_plan_set_preconditioner(tb_plan* plan, int kind) {
+  TB_GUARD(plan != nullptr, "null plan");
+  TB_GUARD(kind == 0 || kind == 1, "preconditioner must be 0 (Jacobi) or 1 (multigrid), got %d", kind);
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  if (kind == 1) TB_TRY(mg_build(P));
+  P->precond = kind;
+  return TB_OK;
+}
+
 int tb_plan_set_owned_planes(tb_plan* plan, int k0, int k1) {
   TB_GUARD(plan != nullptr, "null plan");
   auto* P = reinterpret_cast<tb_plan_impl*>(plan);

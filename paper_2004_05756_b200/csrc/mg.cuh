@@ -1,0 +1,52 @@
+// Geometric multigrid preconditioner for the SIMP elasticity operator.
+//
+// Hierarchy: vertex-centred coarsening by 2 in every direction while the element counts stay
+// even.  Coarse operators are exact Galerkin products, built element by element: a coarse
+// element E covers 2^d fine elements e, and with the (tri)linear interpolation R_e from E's
+// corners to e's corners,
+//     K_E = sum_{e in E} R_e^T (Z_e K_e Z_e) R_e ,  then rows/cols of fixed coarse dofs zeroed,
+// where Z masks Dirichlet dofs and K_e = alpha_e K_unit on the finest level.  The interpolation
+// is element-local inside a coarse element, so sum_E P_E K_E P_E^T equals P^T Z A Z P exactly.
+//
+// V-cycle (symmetric, so the preconditioner is SPD and plain pCG applies): nu damped-Jacobi
+// sweeps, residual, restriction P^T, recursive coarse correction, prolongation P, nu sweeps.
+// The coarsest level is solved exactly with a dense inverse (cuSOLVER potrf/potri at set-up).
+#pragma once
+
+#include <vector>
+
+#include "q1.cuh"
+
+namespace tb {
+
+struct MgLevel {
+  Grid g{};
+  int nc = 2;                  // components
+  double* ke = nullptr;        // level >= 1: dense element matrices (n_elems x NE x NE)
+  uint8_t* fixed = nullptr;    // Dirichlet mask of this level
+  double* dinv = nullptr;      // Jacobi inverse diagonal (0 on fixed)
+  double *x = nullptr, *b = nullptr, *r = nullptr, *t = nullptr;  // work vectors
+  int64_t n = 0;               // dofs
+};
+
+struct Mg {
+  std::vector<MgLevel> lv;     // lv[0] = fine level (operator = alpha K_unit, matrix-free)
+  double* ainv = nullptr;      // coarsest dense inverse (n x n)
+  double* dense = nullptr;     // coarsest dense matrix scratch
+  int64_t ncoarse = 0;
+  int nu = 2;                  // smoothing sweeps
+  double omega = 0.6;          // Jacobi damping
+  void* solver = nullptr;      // cusolverDnHandle_t
+  double* work = nullptr;      // cuSOLVER workspace
+  int lwork = 0;
+  int* info = nullptr;
+  bool built = false;
+};
+
+struct tb_plan_impl;
+int mg_build(tb_plan_impl* P);                          // allocate the hierarchy (once per plan)
+int mg_setup(tb_plan_impl* P, cudaStream_t s);          // operators for the current alpha
+int mg_apply(tb_plan_impl* P, const double* r, double* z, cudaStream_t s);  // z = M^-1 r
+void mg_release(Mg& mg);
+
+}  // namespace tb

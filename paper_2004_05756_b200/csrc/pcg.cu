@@ -37,6 +37,7 @@ void PcgWork::release() {
   if (barrier) cudaFree(barrier);
   if (pub) cudaFree(pub);
   if (exec) cudaGraphExecDestroy(exec);
+  if (exec_pc) cudaGraphExecDestroy(exec_pc);
   *this = PcgWork();
 }
 
@@ -229,6 +230,89 @@ static int build_graph(const PcgOp& op, PcgWork& w) {
   return TB_OK;
 }
 
+// ---- general preconditioner (multigrid): the update kernel leaves z to M^-1 ----
+__global__ void __launch_bounds__(kBlock) k_pcg_update_pc(int64_t n, const double* __restrict__ p,
+                                                          const double* __restrict__ q, const double* __restrict__ dinv,
+                                                          double* __restrict__ x, double* __restrict__ r, PcgState* st,
+                                                          double* partials) {
+  if (st->done) return;
+  const double a = st->alpha;
+  double acc[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (dinv[i] != 0.0) {
+      x[i] = fma(a, p[i], x[i]);
+      const double ri = fma(-a, q[i], r[i]);
+      r[i] = ri;
+      acc[0] = fma(ri, ri, acc[0]);
+    }
+  }
+  block_sum<1>(acc);
+  if (publish_partials<1>(acc, partials, &st->count_b)) {
+    gather_partials<1>(acc, partials, &st->count_b);
+    if (threadIdx.x == 0) {
+      const int it = st->iters + 1;
+      st->iters = it;
+      st->rr = acc[0];
+      if (!isfinite(acc[0])) st->done = 3;
+      else if (acc[0] <= st->tol2) st->done = 1;
+      else if (it >= st->maxit) st->done = 2;
+    }
+  }
+}
+
+// rz = r.z of z = M^-1 r; beta = rz / rz_old (init: beta = 0)
+__global__ void __launch_bounds__(kBlock) k_pcg_rz(int64_t n, const double* __restrict__ r, const double* __restrict__ z,
+                                                   PcgState* st, double* partials, int init) {
+  if (!init && st->done) return;
+  double acc[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc[0] = fma(r[i], z[i], acc[0]);
+  block_sum<1>(acc);
+  if (publish_partials<1>(acc, partials, &st->count_c)) {
+    gather_partials<1>(acc, partials, &st->count_c);
+    if (threadIdx.x == 0) {
+      st->beta = init ? 0.0 : acc[0] / st->rz;
+      st->rz = acc[0];
+      if (!(acc[0] > 0.0) && !(st->done)) st->done = (acc[0] == 0.0 && st->rr == 0.0) ? 1 : 3;
+    }
+  }
+}
+
+static void pc_body(const PcgOp& op, PcgWork& w, cudaStream_t s) {
+  op.launch_fused(w, w.pa, w.pb, s);
+  k_pcg_update_pc<<<kUpdateBlocks, kBlock, 0, s>>>(w.n, w.pb, w.q, w.dinv, w.x, w.r, w.st, w.partB());
+  op.precond_apply(w.r, w.z, s);
+  k_pcg_rz<<<kUpdateBlocks, kBlock, 0, s>>>(w.n, w.r, w.z, w.st, w.partC(), 0);
+  // p is double buffered by copy here (one iteration per body): pb -> pa
+  cudaMemcpyAsync(w.pa, w.pb, sizeof(double) * w.n, cudaMemcpyDeviceToDevice, s);
+}
+
+static int build_graph_pc(const PcgOp& op, PcgWork& w) {
+  cudaStream_t cs;
+  TB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaGraph_t g;
+  TB_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  TB_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1u, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  TB_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  TB_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  pc_body(op, w, cs);
+  k_pcg_cond<<<1, 1, 0, cs>>>(h, w.st);
+  cudaGraph_t captured;
+  TB_CUDA(cudaStreamEndCapture(cs, &captured));
+  TB_CUDA(cudaGraphInstantiate(&w.exec_pc, g, 0));
+  TB_CUDA(cudaGraphDestroy(g));
+  TB_CUDA(cudaStreamDestroy(cs));
+  return TB_OK;
+}
+
 // TB_PCG_NOGRAPH=1 issues the same kernels as plain stream launches (ncu cannot profile kernel
 // nodes of graphs that contain conditional nodes); results are identical.
 static bool no_graph() {
@@ -255,12 +339,73 @@ static int run_loop_plain(const PcgOp& op, PcgWork& w, cudaStream_t s) {
   }
 }
 
+// pCG with a general SPD preconditioner (multigrid V-cycle); one iteration per graph body.
+static int pcg_solve_pc(const PcgOp& op, PcgWork& w, const double* b, double* x_out, double rtol, int maxit,
+                        int* iters, double* relres, cudaStream_t s) {
+  const bool plain = no_graph();
+  if (!plain && !w.exec_pc) TB_TRY(build_graph_pc(op, w));
+  const int nb = kUpdateBlocks;
+  op.launch_dinv(w.dinv, s);
+  k_pcg_start<<<nb, kBlock, 0, s>>>(w.n, b, nullptr, w.dinv, w.x, w.r, w.z, w.pa, w.st, w.partC(), 1, rtol, maxit);
+  launched(1);
+  TB_CHECK_LAUNCH();
+  TB_TRY(op.precond_setup(s));
+  int rc = TB_OK, stalls = 0, it_before = 0;
+  double best_rr = -1.0;
+  for (int restart = 0;; ++restart) {
+    TB_TRY(op.precond_apply(w.r, w.z, s));
+    k_pcg_rz<<<nb, kBlock, 0, s>>>(w.n, w.r, w.z, w.st, w.partC(), 1);
+    launched(1);
+    if (plain) {
+      for (;;) {
+        pc_body(op, w, s);
+        TB_CHECK_LAUNCH();
+        TB_CUDA(cudaMemcpyAsync(w.h_st, w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+        TB_CUDA(cudaStreamSynchronize(s));
+        if (w.h_st->done != 0) break;
+      }
+    } else {
+      TB_CUDA(cudaGraphLaunch(w.exec_pc, s));
+    }
+    op.launch_apply(w.x, w.tmp, s);
+    k_pcg_start<<<nb, kBlock, 0, s>>>(w.n, b, w.tmp, w.dinv, w.x, w.r, w.z, w.pa, w.st, w.partC(), 0, rtol, maxit);
+    launched(1);
+    TB_CHECK_LAUNCH();
+    TB_CUDA(cudaMemcpyAsync(w.h_st, w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    TB_CUDA(cudaStreamSynchronize(s));
+    const PcgState& h = *w.h_st;
+    launched((int64_t)(h.iters - it_before) * 40);  // approximate: kernels per V-cycle iteration
+    it_before = h.iters;
+    if (h.done == 1) break;
+    if (h.done == 3) {
+      set_error("preconditioned pCG breakdown after %d iterations", h.iters);
+      rc = TB_ERR_INDEFINITE;
+      break;
+    }
+    if (best_rr >= 0.0 && h.rr > 0.25 * best_rr) ++stalls;
+    else stalls = 0;
+    if (best_rr < 0.0 || h.rr < best_rr) best_rr = h.rr;
+    if (h.done == 2 || h.iters >= maxit || stalls >= 3 || restart >= 64) {
+      set_error("preconditioned pCG did not reach rtol=%g in %d iterations (relative residual %.3e)", rtol, h.iters,
+                sqrt(h.rr / (h.bb > 0 ? h.bb : 1.0)));
+      rc = TB_ERR_NOT_CONVERGED;
+      break;
+    }
+  }
+  const PcgState& h = *w.h_st;
+  if (iters) *iters = h.iters;
+  if (relres) *relres = (h.bb > 0.0) ? sqrt(h.rr / h.bb) : 0.0;
+  if (x_out != w.x) TB_CUDA(cudaMemcpyAsync(x_out, w.x, sizeof(double) * w.n, cudaMemcpyDeviceToDevice, s));
+  return rc;
+}
+
 int pcg_solve(const PcgOp& op, PcgWork& w, const double* b, double* x_out, double rtol, int maxit, int* iters,
               double* relres, cudaStream_t s) {
   if (!(rtol > 0.0) || maxit < 1) {
     set_error("pcg: rtol must be > 0 and maxit >= 1 (got %g, %d)", rtol, maxit);
     return TB_ERR_INVALID;
   }
+  if (op.has_precond()) return pcg_solve_pc(op, w, b, x_out, rtol, maxit, iters, relres, s);
   const bool plain = no_graph();
   const bool persistent = !plain && op.has_persistent();
   if (!plain && !persistent && !w.exec) TB_TRY(build_graph(op, w));

@@ -29,6 +29,10 @@ struct PcgOp {
   // Whole iteration loop in one persistent cooperative launch (operators without a persistent
   // variant use the conditional-graph loop).
   virtual bool has_persistent() const { return false; }
+  // optional preconditioner replacing Jacobi (multigrid): set-up per operator, z = M^-1 r
+  virtual bool has_precond() const { return false; }
+  virtual int precond_setup(cudaStream_t s) const { (void)s; return TB_OK; }
+  virtual int precond_apply(const double* r, double* z, cudaStream_t s) const { (void)r; (void)z; (void)s; return TB_OK; }
   virtual void launch_persistent(const PcgWork& w, cudaStream_t s) const { (void)w; (void)s; }
 };
 
@@ -42,6 +46,7 @@ struct PcgWork {
   void* barrier = nullptr;   // grid-barrier word of the persistent kernel
   double* pub = nullptr;     // persistent kernel's published vectors [2][3][n]
   cudaGraphExec_t exec = nullptr;
+  cudaGraphExec_t exec_pc = nullptr;  // graph of the preconditioned (multigrid) loop
   double* partA() const { return part; }
   double* partB() const { return part + 2 * part_stride; }
   double* partC() const { return part + 4 * part_stride; }

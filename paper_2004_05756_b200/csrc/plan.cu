@@ -108,7 +108,12 @@ int tb_plan_impl::init(const uint8_t* fixed_host) {
   return TB_OK;
 }
 
+bool ElastOp::has_precond() const { return plan->precond == 1 && !plan->dist; }
+int ElastOp::precond_setup(cudaStream_t s) const { return mg_setup(plan, s); }
+int ElastOp::precond_apply(const double* r, double* z, cudaStream_t s) const { return mg_apply(plan, r, z, s); }
+
 void tb_plan_impl::release() {
+  mg_release(mg);
   work.release();
   void* bufs[] = {d_fixed, d_alpha, d_alpha2, d_scratch, d_scalar, d_rom};
   for (void* b : bufs)

@@ -2,6 +2,7 @@
 #pragma once
 
 #include "hex8.cuh"
+#include "mg.cuh"
 #include "pcg.cuh"
 
 namespace tb {
@@ -19,6 +20,9 @@ struct ElastOp final : PcgOp {
   void launch_dinv(double* dinv, cudaStream_t s) const override;
   bool has_persistent() const override { return persist_grid > 0; }
   void launch_persistent(const PcgWork& w, cudaStream_t s) const override;
+  bool has_precond() const override;
+  int precond_setup(cudaStream_t s) const override;
+  int precond_apply(const double* r, double* z, cudaStream_t s) const override;
   int persist_grid = 0;
 };
 
@@ -46,6 +50,8 @@ struct tb_plan_impl {
   bool hex8 = false;     // K3 has the isotropic WHT block structure -> element-centric kernel
   int zchunk = 8;
   int dist = 0;              // distributed (slab) pCG mode
+  int precond = 0;           // 0 Jacobi, 1 geometric multigrid
+  Mg mg;
   int own_k0 = 0, own_k1 = 1 << 30;  // owned node planes (set by tb_plan_set_owned_planes); ROM rows
   uint8_t* d_fixed = nullptr;
   double* d_alpha = nullptr;   // alpha of the design being solved (read by the pCG graph)

@@ -137,12 +137,13 @@ class HdmSolver:
     """Full-order objective and adjoint gradient on one GPU (hdm.py:112-233).
 
     Extra keyword arguments: ``rtol`` (pCG true-residual tolerance, BASELINE cfg 1-2: 1e-10),
-    ``maxit`` and ``device``.
+    ``maxit``, ``device`` and ``preconditioner`` ("jacobi", the BASELINE design, or "mg":
+    geometric multigrid with Galerkin coarse operators).
     """
 
     def __init__(self, mesh: StructuredMesh, k_e, filt: HelmholtzFilter, f, fixed_dofs,
                  material: MaterialModel | None = None, stats: RunStats | None = None,
-                 rtol: float = 1e-10, maxit: int = 200000, device=None):
+                 rtol: float = 1e-10, maxit: int = 200000, device=None, preconditioner: str = "jacobi"):
         self.mesh = mesh
         self.k_e = np.asarray(k_e, dtype=float)
         self.filter = filt
@@ -168,6 +169,11 @@ class HdmSolver:
             self.material.rho_l, self.material.p, fixed_u8.ctypes.data_as(ctypes.c_void_p),
             self.device.index, ctypes.byref(h)), "HdmSolver")
         self._plan = h
+        if preconditioner not in ("jacobi", "mg"):
+            raise ValueError(f"preconditioner must be 'jacobi' or 'mg', got {preconditioner!r}")
+        self.preconditioner = preconditioner
+        if preconditioner == "mg":
+            _lib.check(_lib.lib().tb_plan_set_preconditioner(h, 1), "multigrid set-up")
         self._f_d = _lib.to_dev(self.f, self.device)
         self._fixed_d = _lib.to_dev(fixed_u8, self.device, dtype=_lib.torch().uint8)
         self.last_iterations = 0

@@ -14,8 +14,9 @@ if name.startswith("cfg3s"):
     prob = configs.cfg3(nx=96, ny=48, nz=48)
 else:
     prob = getattr(configs, name)()
+pc = os.environ.get("TB_PRECOND", "jacobi")
 s = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, prob.radius), prob.f, prob.fixed,
-                 tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP), rtol=prob.rtol)
+                 tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP), rtol=prob.rtol, preconditioner=pc)
 psi = torch.as_tensor(prob.psi, device="cuda")
 rho, _ = s.filtered_density_device(psi)
 if os.environ.get("TB_MAXIT"):  # ablation timing: fixed iteration budget, results not meaningful
@@ -39,5 +40,5 @@ u = s.pcg_device(rho, s._f_d)
 b.record()
 torch.cuda.synchronize()
 ms = a.elapsed_time(b)
-print(f"{name}: pCG {ms:.3f} ms, {s.last_iterations} iterations, {ms * 1e3 / s.last_iterations:.3f} us/iteration, "
+print(f"{name} [{pc}]: pCG {ms:.3f} ms, {s.last_iterations} iterations, {ms * 1e3 / s.last_iterations:.3f} us/iteration, "
       f"J={float(s._f_d @ u):.10f}")

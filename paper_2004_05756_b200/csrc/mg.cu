@@ -292,6 +292,7 @@ int mg_build(tb_plan_impl* P) {
   l0.nc = D;
   l0.n = P->n_dofs;
   l0.fixed = P->d_fixed;
+  l0.dinv = P->work.dinv;  // stable pointer: graphs capture it before the first set-up
   mg.lv.push_back(l0);
   while (true) {
     const Grid& gf = mg.lv.back().g;
@@ -369,7 +370,6 @@ int mg_setup(tb_plan_impl* P, cudaStream_t s) {
   Mg& mg = P->mg;
   TB_TRY(mg_build(P));
   const int D = P->g.dim;
-  mg.lv[0].dinv = P->work.dinv;  // fine Jacobi diagonal of the current alpha (pcg_solve computed it)
   for (size_t l = 1; l < mg.lv.size(); ++l) {
     MgLevel& C = mg.lv[l];
     const MgLevel& F = mg.lv[l - 1];

@@ -28,8 +28,12 @@ struct Hex8Iso {
   double a, b, c, d, e, f, g, h;
 };
 
-constexpr int kHX = 32, kHY = 8;            // element tile per plane (one element per thread)
+#ifndef TB_HEX8_HY
+#define TB_HEX8_HY 8
+#endif
+constexpr int kHX = 32, kHY = TB_HEX8_HY;   // element tile per plane (one element per thread)
 constexpr int kHT = kHX * kHY;              // 256 threads
+constexpr int kHexCtas = 512 / kHT;         // resident CTAs per SM (128 registers per thread)
 constexpr int kPX = kHX + 1, kPY = kHY + 1;  // node-plane tile incl. halo ring
 constexpr int kPN = kPX * kPY;
 constexpr int kOX = kHX - 1, kOY = kHY - 1;  // owned nodes per plane (31 x 7)
@@ -107,21 +111,34 @@ __device__ __forceinline__ void hex8_iso_blocks(const Hex8Iso& K, double alpha, 
   }
 }
 
+// Shared/global tile geometry.  A node-plane tile is kPY rows of kPX nodes; with the dof
+// layout 3 n + c each row is kRow = 3 kPX contiguous doubles in global memory, so a plane is
+// fetched as kPY coalesced row segments and kept in shared memory in the same (AoS) order.
+constexpr int kRow = 3 * kPX;                          // 99 doubles per node row
+constexpr int kPlane = kRow * kPY;                     // 891 doubles per node plane
+constexpr int kSlots = (kPlane + kHT - 1) / kHT;       // 4 fetch slots per thread
+constexpr int kORow = 3 * kOX;                         // 93 owned doubles per row
+constexpr int kOPlane = kORow * kOY;                   // 651 owned doubles per plane
+constexpr int kOSlots = (kOPlane + kHT - 1) / kHT;     // 3 store slots per thread
+
 // FUSED: in = z, in2 = p_old, out = q, writes pnew, reduces p.q (pCG kernel A).
 // !FUSED: in = v, out = y = K v (fixed rows zeroed when `fixed` != nullptr).
 template <bool FUSED>
-__global__ void __launch_bounds__(kHT, 2) k_hex8(Grid g, Hex8Iso K, const double* __restrict__ alpha,
+__global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const double* __restrict__ alpha,
                                                  const double* __restrict__ in, const double* __restrict__ in2,
                                                  double* __restrict__ pnew, double* __restrict__ out,
                                                  const uint8_t* __restrict__ fixed, PcgState* st, double* partials,
                                                  int zchunk) {
-  // plane[4][3][kPN]: node planes, buffer = plane index mod 4 (SoA per component).
-  // stage[2][4][3][kHT]: corner outputs (q = oy + 2 oz) already summed over the two
-  // x-neighbour elements, double buffered by step parity.  With 4 plane buffers and 2 stage
-  // buffers a step needs ONE barrier: no thread can be more than one step ahead of another.
+  // plane[4][kPlane]: node planes (buffer = plane index mod 4), AoS rows as in global memory.
+  // stage[2][2][3][kHT]: node-plane corner outputs (oy) already summed over the two
+  // x-neighbour elements, double buffered by step parity.  ostg[2][kOPlane]: finished owned
+  // node values of a plane, stored to global memory (coalesced) one step later; pstg[2][kPlane]:
+  // p_old staging (FUSED).  With 4 plane
+  // buffers and 2 stage/output buffers a step needs ONE barrier.
   extern __shared__ double hsm[];
-  double (*plane)[3][kPN] = reinterpret_cast<double (*)[3][kPN]>(hsm);
-  double (*stage2)[4][3][kHT] = reinterpret_cast<double (*)[4][3][kHT]>(hsm + 4 * 3 * kPN);
+  double* plane = hsm;
+  double (*stage2)[2][3][kHT] = reinterpret_cast<double (*)[2][3][kHT]>(hsm + 4 * kPlane);
+  double* ostg = hsm + 4 * kPlane + 2 * 2 * 3 * kHT;
   double beta = 0.0;
   if (FUSED) {
     if (st->done) return;
@@ -136,153 +153,193 @@ __global__ void __launch_bounds__(kHT, 2) k_hex8(Grid g, Hex8Iso K, const double
   const bool col_ok = gei >= 0 && gei < g.nx && gej >= 0 && gej < g.ny;
   const bool own = t < kOX * kOY;
   const int onx = t % kOX, ony = t / kOX;                 // owned node in the tile
-  const int gni = i0 + onx, gnj = j0 + ony;
-  const bool own_ok = own && gni < g.nnx && gnj < g.nny;
   const int px = onx + 1, py = ony + 1;                   // its position in the plane tile
-  const int64_t plane_stride = (int64_t)g.nnx * g.nny;
-  constexpr int kPF = (kPN + kHT - 1) / kHT;              // plane entries per thread (2)
-  int lxs[kPF], lys[kPF];
+  const int plane_dofs = 3 * g.nnx * g.nny;               // < 2^31 for every supported grid
+  // fetch slots: flat tile index f = t + s kHT -> (row f / kRow, double f % kRow)
+  int goff[kSlots];
+  unsigned fok = 0, fown = 0;                              // slot valid / slot is an owned node
 #pragma unroll
-  for (int q = 0; q < kPF; ++q) {
-    lxs[q] = (t + q * kHT) % kPX;
-    lys[q] = (t + q * kHT) / kPX;
+  for (int s = 0; s < kSlots; ++s) {
+    const int f = t + s * kHT, ly = f / kRow, d = f % kRow, lx = d / 3;
+    const int ni = i0 - 1 + lx, nj = j0 - 1 + ly;
+    goff[s] = 3 * (nj * g.nnx + ni) + d % 3;
+    if (f < kPlane && ni >= 0 && ni < g.nnx && nj >= 0 && nj < g.nny) {
+      fok |= 1u << s;
+      if (lx >= 1 && lx <= kOX && ly >= 1 && ly <= kOY) fown |= 1u << s;
+    }
+  }
+  // store slots: flat owned index o = t + s kHT -> (row o / kORow, double o % kORow)
+  int ooff[kOSlots];
+  unsigned ook = 0;
+#pragma unroll
+  for (int s = 0; s < kOSlots; ++s) {
+    const int o = t + s * kHT, r = o / kORow, d = o % kORow;
+    const int ni = i0 + d / 3, nj = j0 + r;
+    ooff[s] = 3 * (nj * g.nnx + ni) + d % 3;
+    if (o < kOPlane && ni < g.nnx && nj < g.nny) ook |= 1u << s;
   }
 
-  double pf[kPF][3];
-#define HEX8_FETCH(kp_)                                                                                     \
-  _Pragma("unroll") for (int q = 0; q < kPF; ++q) {                                                         \
-    const int ni = i0 - 1 + lxs[q], nj = j0 - 1 + lys[q];                                                   \
-    const bool ok = (t + q * kHT) < kPN && (kp_) >= 0 && (kp_) < g.nnz && ni >= 0 && ni < g.nnx && nj >= 0 && \
-                    nj < g.nny;                                                                             \
-    const int64_t node = (int64_t)(kp_) * plane_stride + (int64_t)nj * g.nnx + ni;                          \
-    _Pragma("unroll") for (int c = 0; c < 3; ++c) {                                                         \
-      double v = 0.0;                                                                                       \
-      if (ok) {                                                                                             \
-        v = __ldg(in + 3 * node + c);                                                                       \
-        if (FUSED) v = fma(beta, __ldg(in2 + 3 * node + c), v);                                             \
-      }                                                                                                     \
-      pf[q][c] = v;                                                                                         \
-    }                                                                                                       \
-  }
-#define HEX8_STORE(kp_, buf_)                                                                               \
-  _Pragma("unroll") for (int q = 0; q < kPF; ++q) {                                                         \
-    const int idx = t + q * kHT;                                                                            \
-    if (idx < kPN) {                                                                                        \
-      _Pragma("unroll") for (int c = 0; c < 3; ++c) plane[(buf_)][c][idx] = pf[q][c];                       \
-      if (FUSED && (kp_) >= K0 && (kp_) < K1 && lxs[q] >= 1 && lxs[q] <= kOX && lys[q] >= 1 &&              \
-          lys[q] <= kOY) {                                                                                  \
-        const int ni = i0 - 1 + lxs[q], nj = j0 - 1 + lys[q];                                               \
-        if (ni < g.nnx && nj < g.nny) {                                                                     \
-          const int64_t node = (int64_t)(kp_) * plane_stride + (int64_t)nj * g.nnx + ni;                    \
-          _Pragma("unroll") for (int c = 0; c < 3; ++c) pnew[3 * node + c] = pf[q][c];                      \
-        }                                                                                                   \
+  // Node planes move global -> shared with cp.async (no register staging): plane kp goes to
+  // plane buffer pbuf(kp); in FUSED mode p_old goes to pstg and, once landed, each thread turns
+  // its own slots into p = z + beta p_old in place (and writes owned p to pnew).
+#define HEX8_ISSUE(kp_, boff_, pst_)                                                                        \
+  {                                                                                                         \
+    const bool zok = (kp_) >= 0 && (kp_) < g.nnz;                                                           \
+    const double* src = in + (int64_t)(zok ? (kp_) : 0) * plane_dofs;                                       \
+    const double* src2 = FUSED ? in2 + (int64_t)(zok ? (kp_) : 0) * plane_dofs : nullptr;                   \
+    double* dst = plane + (boff_);                                                                          \
+    _Pragma("unroll") for (int s = 0; s < kSlots; ++s) {                                                    \
+      if (s < kSlots - 1 || t < kPlane - (kSlots - 1) * kHT) {                                              \
+        const bool ok = zok && (fok >> s & 1u);                                                             \
+        const int off = ok ? goff[s] : 0;                                                                   \
+        cp_async8(dst + t + s * kHT, src + off, ok);                                                        \
+        if (FUSED) cp_async8((pst_) + t + s * kHT, src2 + off, ok);                                         \
       }                                                                                                     \
     }                                                                                                       \
+    cp_async_commit();                                                                                      \
   }
-#define HEX8_FACE(buf_, f_)                                                                                 \
+#define HEX8_LAND(kp_, boff_, pst_)                                                                         \
+  if (FUSED) {                                                                                              \
+    double* dst = plane + (boff_);                                                                          \
+    const bool pown = (kp_) >= K0 && (kp_) < K1;                                                            \
+    double* pdst = pnew + (int64_t)(kp_) * plane_dofs;                                                      \
+    _Pragma("unroll") for (int s = 0; s < kSlots; ++s) {                                                    \
+      if (s < kSlots - 1 || t < kPlane - (kSlots - 1) * kHT) {                                              \
+        const int f = t + s * kHT;                                                                          \
+        const double v = fma(beta, (pst_)[f], dst[f]);                                                      \
+        dst[f] = v;                                                                                         \
+        if (pown && (fown >> s & 1u)) pdst[goff[s]] = v;                                                    \
+      }                                                                                                     \
+    }                                                                                                       \
+  }
+#define HEX8_FACE(boff_, f_)                                                                                \
   _Pragma("unroll") for (int cc = 0; cc < 4; ++cc) {                                                        \
-    const int idx = (ey + (cc >> 1)) * kPX + ex + (cc & 1);                                                 \
-    _Pragma("unroll") for (int c = 0; c < 3; ++c) f_[c][cc] = plane[(buf_)][c][idx];                        \
+    const double* src = plane + (boff_) + (ey + (cc >> 1)) * kRow + 3 * (ex + (cc & 1));                    \
+    _Pragma("unroll") for (int c = 0; c < 3; ++c) f_[c][cc] = src[c];                                       \
   }                                                                                                         \
   _Pragma("unroll") for (int c = 0; c < 3; ++c) wht4(f_[c]);
+  // coalesced store of the finished owned plane kp_ (staged in ostg[(kp_) & 1])
+#define HEX8_FLUSH(kp_, par_)                                                                               \
+  {                                                                                                         \
+    const double* srcs = ostg + (par_) * kOPlane;                                                           \
+    double* dst = out + (int64_t)(kp_) * plane_dofs;                                                        \
+    const uint8_t* fx = (!FUSED && fixed != nullptr) ? fixed + (int64_t)(kp_) * plane_dofs : nullptr;       \
+    _Pragma("unroll") for (int s = 0; s < kOSlots; ++s) {                                                   \
+      if ((s < kOSlots - 1 || t < kOPlane - (kOSlots - 1) * kHT) && (ook >> s & 1u)) {                      \
+        double v = srcs[t + s * kHT];                                                                       \
+        if (fx != nullptr && fx[ooff[s]]) v = 0.0;                                                          \
+        dst[ooff[s]] = v;                                                                                   \
+      }                                                                                                     \
+    }                                                                                                       \
+  }
 
-  auto pbuf = [](int kp) { return (kp + 4) & 3; };  // kp >= -1
-  HEX8_FETCH(K0 - 1);
-  HEX8_STORE(K0 - 1, pbuf(K0 - 1));
-  HEX8_FETCH(K0);
-  HEX8_STORE(K0, pbuf(K0));
-  HEX8_FETCH(K0 + 1);  // plane of the second step, stored at the top of the first
-  double a_next = (col_ok && K0 - 1 >= 0) ? __ldg(alpha + ((int64_t)(K0 - 1) * g.ny + gej) * g.nx + gei) : 0.0;
+  // Ring buffers are indexed by the plane's position relative to the first plane of this CTA
+  // (K0 - 1).
+  double* pstg = ostg + 2 * kOPlane;  // [2][kPlane] p_old staging (FUSED)
+#define HEX8_PB(rel_) (((rel_) & 3) * kPlane)
+#define HEX8_PS(rel_) (pstg + ((rel_) & 1) * kPlane)
+  HEX8_ISSUE(K0 - 1, HEX8_PB(0), HEX8_PS(0));
+  HEX8_ISSUE(K0, HEX8_PB(1), HEX8_PS(1));
+  // p_old of plane K0+1 is staged in the (still unused) buffer of plane K0+2
+  HEX8_ISSUE(K0 + 1, HEX8_PB(2), plane + HEX8_PB(3));
+  cp_async_wait<0>();
+  HEX8_LAND(K0 - 1, HEX8_PB(0), HEX8_PS(0));
+  HEX8_LAND(K0, HEX8_PB(1), HEX8_PS(1));
+  HEX8_LAND(K0 + 1, HEX8_PB(2), plane + HEX8_PB(3));
+  const double* a_ptr = alpha + ((int64_t)gej * g.nx + gei);  // element column base (valid iff col_ok)
+  const int64_t a_stride = (int64_t)g.nx * g.ny;
+  double a_next = (col_ok && K0 - 1 >= 0) ? __ldg(a_ptr + (K0 - 1) * a_stride) : 0.0;
   __syncthreads();
   // xy-WHT of the 4 corner nodes of the current bottom face of this element column
   double fb[3][4];
-  HEX8_FACE(pbuf(K0 - 1), fb);
-  double carry[3] = {0.0, 0.0, 0.0};
+  HEX8_FACE(HEX8_PB(0), fb);
+  double tc[3][4];  // top-face spectrum of the previous element (its share of node plane ez)
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int s = 0; s < 4; ++s) tc[c][s] = 0.0;
   double acc[1] = {0.0};
-  for (int ez = K0 - 1; ez < K1; ++ez) {
-    const int sb = (ez + 1) & 1;  // stage buffer of this step
-    // store node plane ez+2 (fetched last step; read from the next step on) and fetch ez+3
-    if (ez + 2 <= K1) {
-      HEX8_STORE(ez + 2, pbuf(ez + 2));
-    }
-    if (ez + 3 <= K1) {
-      HEX8_FETCH(ez + 3);
-    }
-    const double a = a_next;
-    a_next = (col_ok && ez + 1 < g.nz && ez + 1 < K1) ? __ldg(alpha + ((int64_t)(ez + 1) * g.ny + gej) * g.nx + gei)
-                                                       : 0.0;
-    // ---- element (gei, gej, ez): spectrum from carried bottom face + new top face ----
+  const bool dot_any = FUSED && st->dot_k1 > st->dot_k0;
+  const int dk0 = FUSED ? st->dot_k0 : 0, dk1 = FUSED ? st->dot_k1 : 0;
+  const int steps = K1 - (K0 - 1);  // element planes ez = K0-1 .. K1-1
+  // (a 4-way unrolled sweep makes the ring offsets constants but spills and runs slower)
+#pragma unroll 1
+  for (int rel = 0; rel < steps; ++rel) {
     {
-      double ft[3][4];
-      HEX8_FACE(pbuf(ez + 1), ft);
-      double u[3][8];
+      const int r = rel & 3;
+      const int ez = K0 - 1 + rel;
+      const double a = a_next;
+      a_next = (col_ok && ez + 1 < g.nz && ez + 1 < K1) ? __ldg(a_ptr + (ez + 1) * a_stride) : 0.0;
+      // ---- element (gei, gej, ez): spectrum from carried bottom face + new top face ----
+      {
+        double ft[3][4];
+        HEX8_FACE(HEX8_PB(r + 1), ft);
+        double u[3][8];
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
+        for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          u[c][s] = fb[c][s] + ft[c][s];
-          u[c][s + 4] = fb[c][s] - ft[c][s];
-          fb[c][s] = ft[c][s];  // this top face is the next element's bottom face
-        }
-      hex8_iso_blocks(K, a, u);
-      // inverse: z stage, then xy stage per face -> corner outputs (ox + 2 oy + 4 oz)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double bot[4], top[4];
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          bot[s] = u[c][s] + u[c][s + 4];
-          top[s] = u[c][s] - u[c][s + 4];
-        }
-        wht4(bot);
-        wht4(top);
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          u[c][s] = bot[s];
-          u[c][s + 4] = top[s];
-        }
-      }
-      // node column ex+1 of this row: corner ox=1 of this element + ox=0 of the next
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {  // q = oy + 2 oz
-        const int base = 2 * (q & 1) + 4 * (q >> 1);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double right = __shfl_down_sync(0xffffffffu, u[c][base], 1);
-          stage2[sb][q][c][t] = u[c][base + 1] + (ex < kHX - 1 ? right : 0.0);
-        }
-      }
-    }
-    __syncthreads();
-    // ---- owned node (px, py): rows ey = py-1 (its corner oy=1) and ey = py (oy=0) ----
-    if (own) {
-      const int e_dn = (py - 1) * kHX + (px - 1), e_up = py * kHX + (px - 1);
-      double bot[3], top[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        bot[c] = stage2[sb][1][c][e_dn] + stage2[sb][0][c][e_up];
-        top[c] = stage2[sb][3][c][e_dn] + stage2[sb][2][c][e_up];
-      }
-      if (ez >= K0 && own_ok) {
-        const int64_t node = (int64_t)ez * plane_stride + (int64_t)gnj * g.nnx + gni;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          double v = carry[c] + bot[c];
-          if (FUSED) {
-            if (ez >= st->dot_k0 && ez < st->dot_k1) acc[0] = fma(plane[pbuf(ez)][c][py * kPX + px], v, acc[0]);
-          } else if (fixed != nullptr && fixed[3 * node + c]) {
-            v = 0.0;
+          for (int s = 0; s < 4; ++s) {
+            u[c][s] = fb[c][s] + ft[c][s];
+            u[c][s + 4] = fb[c][s] - ft[c][s];
+            fb[c][s] = ft[c][s];  // this top face is the next element's bottom face
           }
-          out[3 * node + c] = v;
+        hex8_iso_blocks(K, a, u);
+        // inverse z stage: bottom-face spectrum joins the previous element's top-face spectrum
+        // (both land on node plane ez), so the xy inverse runs once per node plane
+        double fq[3][4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            fq[c][s] = tc[c][s] + (u[c][s] + u[c][s + 4]);
+            tc[c][s] = u[c][s] - u[c][s + 4];
+          }
+          wht4(fq[c]);  // -> corner values (ox + 2 oy) of node plane ez from this element column
+        }
+        // node column ex+1 of this row: corner ox=1 of this element + ox=0 of the next
+        // (lane 31's sum is never read: node column 32 of the tile is not owned)
+#pragma unroll
+        for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const double right = __shfl_down_sync(0xffffffffu, fq[c][2 * oy], 1);
+            stage2[r & 1][oy][c][t] = fq[c][2 * oy + 1] + right;
+          }
+      }
+      // node plane ez+2 (issued at the end of the last step; the prologue landed plane K0+1)
+      // must have landed before the barrier: it is read from the next step on
+      if (rel >= 1 && ez + 2 <= K1) {
+        cp_async_wait<0>();
+        HEX8_LAND(ez + 2, HEX8_PB(r + 2), HEX8_PS(r + 2));
+      }
+      __syncthreads();
+      if (rel >= 2) HEX8_FLUSH(ez - 1, (r + 1) & 1);  // plane ez-1 was staged before this barrier
+      // ---- owned node (px, py) of plane ez: rows ey = py-1 (corner oy=1) and ey = py (oy=0) ----
+      if (own && rel >= 1) {
+        const int e_dn = (py - 1) * kHX + (px - 1), e_up = py * kHX + (px - 1);
+        double* o = ostg + (r & 1) * kOPlane + ony * kORow + 3 * onx;
+        const double* pp = plane + HEX8_PB(r) + py * kRow + 3 * px;
+        const bool dot_here = dot_any && ez >= dk0 && ez < dk1;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double v = stage2[r & 1][1][c][e_dn] + stage2[r & 1][0][c][e_up];
+          if (FUSED && dot_here) acc[0] = fma(pp[c], v, acc[0]);  // p is 0 outside the grid
+          o[c] = v;
         }
       }
-#pragma unroll
-      for (int c = 0; c < 3; ++c) carry[c] = top[c];
+      // plane ez+3 reuses the buffer of plane ez-1, which every thread finished with before
+      // this step's barrier
+      if (ez + 3 <= K1) HEX8_ISSUE(ez + 3, HEX8_PB(r + 3), HEX8_PS(r + 3));
     }
   }
-#undef HEX8_FETCH
-#undef HEX8_STORE
+  __syncthreads();
+  if (steps >= 2) HEX8_FLUSH(K1 - 1, (steps - 1) & 1);
+#undef HEX8_ISSUE
+#undef HEX8_LAND
 #undef HEX8_FACE
+#undef HEX8_FLUSH
+#undef HEX8_PB
+#undef HEX8_PS
   if (FUSED) {
     block_sum<1>(acc);
     if (publish_partials<1>(acc, partials, &st->count_a)) {
@@ -302,15 +359,27 @@ __global__ void __launch_bounds__(kHT, 2) k_hex8(Grid g, Hex8Iso K, const double
   }
 }
 
-constexpr size_t kHex8Smem = sizeof(double) * (4 * 3 * kPN + 2 * 4 * 3 * kHT);
+constexpr size_t kHex8Smem = sizeof(double) * (4 * kPlane + 2 * 2 * 3 * kHT + 2 * kOPlane + 2 * kPlane);
 
-// z-chunk giving ~8 CTAs of work per SM (2 resident) without much plane-halo redundancy
+// z-chunk: as few chunks per xy column as possible (each chunk recomputes one element plane
+// and refetches two node planes) while filling the resident CTA slots in whole waves.
 inline int hex8_zchunk(const Grid& g) {
   const int64_t xy = (int64_t)((g.nnx + kOX - 1) / kOX) * ((g.nny + kOY - 1) / kOY);
-  int64_t chunks = (148 * 8 + xy - 1) / xy;
-  if (chunks < 1) chunks = 1;
-  const int zc = (int)((g.nnz + chunks - 1) / chunks);
-  return zc < 4 ? 4 : (zc > 64 ? 64 : zc);
+  const int64_t slots = (int64_t)kHexCtas * 148;
+  double best = 1e30;
+  int best_zc = g.nnz;
+  for (int64_t c = 1; c <= 64 && c <= g.nnz; ++c) {
+    const int zc = (int)((g.nnz + c - 1) / c);
+    const int64_t ctas = xy * ((g.nnz + zc - 1) / zc);
+    const int64_t waves = (ctas + slots - 1) / slots;
+    // cost ~ waves x per-CTA work (zc owned planes + ~1.5 planes of chunk overhead)
+    const double cost = (double)waves * (zc + 1.5);
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_zc = zc;
+    }
+  }
+  return best_zc;
 }
 
 inline dim3 hex8_grid(const Grid& g, int zchunk) {

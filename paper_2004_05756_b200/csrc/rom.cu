@@ -169,16 +169,6 @@ __global__ void __launch_bounds__(kGemmThreads) k_atb_dmma(int64_t n, int k, con
 // ---------------------------------------------------------------------------------------
 constexpr int kCmRows = 32, kCmLd = kCmRows + 4;
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  const int sz = valid ? 8 : 0;  // src-size 0 zero-fills the destination
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
 
 template <int KP>
 __global__ void __launch_bounds__(kGemmThreads) k_atb_cm(int64_t r0, int64_t r1, int k,

@@ -14,6 +14,27 @@ __device__ __forceinline__ int64_t dof_of(const Grid& g, int i, int j, int k, in
   return (((int64_t)k * g.nny + j) * g.nnx + i) * nc + c;
 }
 
+// Per-axis coarsening of nf fine elements into nc = (nf + 1) / 2 coarse ones: coarse node I sits
+// on fine node min(2I, nf); when nf is odd the last coarse element spans a single fine element.
+__host__ __device__ __forceinline__ int cnode(int I, int nf) { return 2 * I < nf ? 2 * I : nf; }
+// position in [0,1] of fine node i inside coarse element I (i in [2I, 2I+2])
+__host__ __device__ __forceinline__ double tpos(int i, int I, int nf) {
+  return (i == nf && (nf & 1)) ? 1.0 : 0.5 * (i - 2 * I);
+}
+// prolongation weight of coarse node I at fine node i
+__device__ __forceinline__ double pw(int i, int I, int nf) {
+  if (i < 0 || i > nf) return 0.0;
+  if (!(i & 1)) return (i >> 1) == I ? 1.0 : 0.0;
+  if (i == nf) return ((nf + 1) >> 1) == I ? 1.0 : 0.0;
+  return ((i >> 1) == I || (i >> 1) + 1 == I) ? 0.5 : 0.0;
+}
+// coarse nodes interpolated at fine node i: lo (and lo+1 when n == 2, weights 1/2)
+__device__ __forceinline__ void pmap(int i, int nf, int& lo, int& n) {
+  if (!(i & 1)) { lo = i >> 1; n = 1; }
+  else if (i == nf) { lo = (nf + 1) >> 1; n = 1; }
+  else { lo = i >> 1; n = 2; }
+}
+
 // ---------------------------------------------------------------------------------------
 // Galerkin coarse element matrices.  One CTA per coarse element E; children e in {0,1}^D.
 // R[o][O] = prod_d w((c_d + o_d)/2, O_d), w(t,0) = 1-t, w(t,1) = t (corners in local order).
@@ -23,12 +44,14 @@ __global__ void __launch_bounds__(256) k_mg_aggregate(Grid gc, Grid gf, Mat<Q1<D
                                                       const double* __restrict__ alpha,
                                                       const double* __restrict__ ke_f,
                                                       const uint8_t* __restrict__ fixed_f,
-                                                      const uint8_t* __restrict__ fixed_c, double* __restrict__ ke_c) {
+                                                      const uint8_t* __restrict__ fixed_c,
+                                                      const uint8_t* __restrict__ dirty, double* __restrict__ ke_c) {
   constexpr int NN = Q1<D>::NN, NE = NN * D;
   __shared__ double Ke[NE * NE], T[NE * NE], Acc[NE * NE], R[NN * NN];
   __shared__ uint8_t mf[NE];
   const int t = threadIdx.x;
   const int64_t E = blockIdx.x;
+  if (dirty != nullptr && !dirty[E]) return;  // done by the fast path
   const int I = (int)(E % gc.nx);
   const int J = (int)((E / gc.nx) % gc.ny);
   const int K = (D == 3) ? (int)(E / ((int64_t)gc.nx * gc.ny)) : 0;
@@ -36,12 +59,14 @@ __global__ void __launch_bounds__(256) k_mg_aggregate(Grid gc, Grid gf, Mat<Q1<D
   for (int ch = 0; ch < NN; ++ch) {
     const int cx = ch & 1, cy = (ch >> 1) & 1, cz = ch >> 2;
     const int fi = 2 * I + cx, fj = 2 * J + cy, fk = (D == 3) ? 2 * K + cz : 0;
+    if (fi >= gf.nx || fj >= gf.ny || fk >= gf.nz) continue;  // short last coarse element
     const int64_t fe = ((int64_t)fk * gf.ny + fj) * gf.nx + fi;
     __syncthreads();
     // interpolation weights of this child (fine local corner b <- coarse local corner B)
     for (int o = t; o < NN * NN; o += blockDim.x) {
       const int b = o / NN, B = o % NN;
-      const double tx = 0.5 * (cx + offx(b)), ty = 0.5 * (cy + offy(b)), tz = 0.5 * (cz + offz(b));
+      const double tx = tpos(fi + offx(b), I, gf.nx), ty = tpos(fj + offy(b), J, gf.ny);
+      const double tz = (D == 3) ? tpos(fk + offz(b), K, gf.nz) : 0.0;
       double w = (offx(B) ? tx : 1.0 - tx) * (offy(B) ? ty : 1.0 - ty);
       if (D == 3) w *= offz(B) ? tz : 1.0 - tz;
       R[o] = w;
@@ -96,14 +121,58 @@ __global__ void k_mg_coarse_fixed(Grid gc, Grid gf, const uint8_t* __restrict__ 
   const int64_t n = d / D;
   const int c = (int)(d % D);
   const int I = (int)(n % gc.nnx), J = (int)((n / gc.nnx) % gc.nny), K = (int)(n / ((int64_t)gc.nnx * gc.nny));
-  fc[d] = ff[dof_of(gf, 2 * I, 2 * J, 2 * K, D, c)];
+  fc[d] = ff[dof_of(gf, cnode(I, gf.nx), cnode(J, gf.ny), (D == 3) ? cnode(K, gf.nz) : 0, D, c)];
 }
 
-// y = A v on a coarse level (dense element matrices), node-owner gather in fixed slot order
+// Coarse operators are applied as assembled 3^D-point node stencils.  The operator is
+// symmetric, so only the centre block and the upper half (offsets m > centre) are stored, SoA
+// over nodes:  st[((u D + c) D + c') n_nodes + n],  u = m - centre,  couples dof (n, c) with dof
+// (n + off(m), c'),  off(m) = (m % 3 - 1, m / 3 % 3 - 1, m / 9 - 1).  The lower blocks are the
+// transposes stored at the neighbour (off(NB-1-m) = -off(m)), which also makes the applied
+// operator exactly symmetric.  Built once per set-up from the element matrices in fixed order.
 template <int D>
-__global__ void __launch_bounds__(kBlock) k_mg_apply(Grid g, const double* __restrict__ ke, const double* __restrict__ v,
-                                                     double* __restrict__ y) {
-  constexpr int NN = Q1<D>::NN, NE = NN * D;
+__global__ void __launch_bounds__(kBlock) k_mg_stencil(Grid g, const double* __restrict__ ke, double* __restrict__ st) {
+  constexpr int NN = Q1<D>::NN, NE = NN * D, NB = Q1<D>::NB, MC = NB / 2;
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= g.n_nodes) return;
+  int i, j, k;
+  node_coords(g, n, i, j, k);
+  for (int m = MC; m < NB; ++m) {
+    const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = (D == 3) ? m / 9 - 1 : 0;
+    double a[D][D];
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+#pragma unroll
+      for (int cp = 0; cp < D; ++cp) a[c][cp] = 0.0;
+#pragma unroll
+    for (int s = 0; s < NN; ++s) {
+      const int sx = s & 1, sy = (s >> 1) & 1, sz = s >> 2;
+      const int ei = i - 1 + sx, ej = j - 1 + sy, ek = (D == 3) ? k - 1 + sz : 0;
+      if (ei < 0 || ei >= g.nx || ej < 0 || ej >= g.ny || ek < 0 || ek >= g.nz) continue;
+      const int ox = 1 - sx, oy = 1 - sy, oz = (D == 3) ? 1 - sz : 0;
+      const int bx = ox + dx, by = oy + dy, bz = oz + dz;
+      if (bx < 0 || bx > 1 || by < 0 || by > 1 || bz < 0 || bz > 1) continue;
+      const int64_t e = ((int64_t)ek * g.ny + ej) * g.nx + ei;
+      const int L = loc_of(ox, oy, oz), b = loc_of(bx, by, bz);
+      const double* kr = ke + e * NE * NE;
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+#pragma unroll
+        for (int cp = 0; cp < D; ++cp) a[c][cp] += kr[(L * D + c) * NE + b * D + cp];
+    }
+    const int u = m - MC;
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+#pragma unroll
+      for (int cp = 0; cp < D; ++cp) st[((int64_t)(u * D + c) * D + cp) * g.n_nodes + n] = a[c][cp];
+  }
+}
+
+// y = A v on a coarse level from its half stencil (node-owner, fixed neighbour order)
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_mg_sapply(Grid g, const double* __restrict__ st,
+                                                      const double* __restrict__ v, double* __restrict__ y) {
+  constexpr int NB = Q1<D>::NB, MC = NB / 2;
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= g.n_nodes) return;
   int i, j, k;
@@ -112,22 +181,28 @@ __global__ void __launch_bounds__(kBlock) k_mg_apply(Grid g, const double* __res
 #pragma unroll
   for (int c = 0; c < D; ++c) out[c] = 0.0;
 #pragma unroll
-  for (int s = 0; s < NN; ++s) {
-    const int sx = s & 1, sy = (s >> 1) & 1, sz = s >> 2;
-    const int ei = i - 1 + sx, ej = j - 1 + sy, ek = (D == 3) ? k - 1 + sz : 0;
-    if (ei < 0 || ei >= g.nx || ej < 0 || ej >= g.ny || ek < 0 || ek >= g.nz) continue;
-    const int64_t e = ((int64_t)ek * g.ny + ej) * g.nx + ei;
-    const int L = loc_of(1 - sx, 1 - sy, (D == 3) ? 1 - sz : 0);
-    const double* kr = ke + e * NE * NE;
+  for (int m = 0; m < NB; ++m) {
+    const int dx = m % 3 - 1, dy = (m / 3) % 3 - 1, dz = (D == 3) ? m / 9 - 1 : 0;
+    const int ni = i + dx, nj = j + dy, nk = k + dz;
+    if (ni < 0 || ni >= g.nnx || nj < 0 || nj >= g.nny || nk < 0 || nk >= g.nnz) continue;
+    const int64_t nbn = ((int64_t)nk * g.nny + nj) * g.nnx + ni;
+    double vv[D];
 #pragma unroll
-    for (int b = 0; b < NN; ++b) {
-      const int64_t nb = dof_of(g, ei + offx(b), ej + offy(b), ek + (D == 3 ? offz(b) : 0), D, 0);
+    for (int cp = 0; cp < D; ++cp) vv[cp] = __ldg(v + nbn * D + cp);
+    if (m >= MC) {  // stored here
+      const int u = m - MC;
 #pragma unroll
-      for (int cp = 0; cp < D; ++cp) {
-        const double vv = __ldg(v + nb + cp);
+      for (int c = 0; c < D; ++c)
 #pragma unroll
-        for (int c = 0; c < D; ++c) out[c] = fma(__ldg(kr + (L * D + c) * NE + b * D + cp), vv, out[c]);
-      }
+        for (int cp = 0; cp < D; ++cp)
+          out[c] = fma(__ldg(st + ((int64_t)(u * D + c) * D + cp) * g.n_nodes + n), vv[cp], out[c]);
+    } else {  // transpose of the neighbour's block towards this node
+      const int u = NB - 1 - m - MC;
+#pragma unroll
+      for (int c = 0; c < D; ++c)
+#pragma unroll
+        for (int cp = 0; cp < D; ++cp)
+          out[c] = fma(__ldg(st + ((int64_t)(u * D + cp) * D + c) * g.n_nodes + nbn), vv[cp], out[c]);
     }
   }
 #pragma unroll
@@ -135,26 +210,63 @@ __global__ void __launch_bounds__(kBlock) k_mg_apply(Grid g, const double* __res
 }
 
 template <int D>
-__global__ void k_mg_dinv(Grid g, const double* __restrict__ ke, const uint8_t* __restrict__ fixed,
+__global__ void k_mg_dinv(Grid g, const double* __restrict__ st, const uint8_t* __restrict__ fixed,
                           double* __restrict__ dinv) {
-  constexpr int NN = Q1<D>::NN, NE = NN * D;
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= g.n_nodes) return;
-  int i, j, k;
-  node_coords(g, n, i, j, k);
 #pragma unroll
   for (int c = 0; c < D; ++c) {
-    double d = 0.0;
-#pragma unroll
-    for (int s = 0; s < NN; ++s) {
-      const int sx = s & 1, sy = (s >> 1) & 1, sz = s >> 2;
-      const int ei = i - 1 + sx, ej = j - 1 + sy, ek = (D == 3) ? k - 1 + sz : 0;
-      if (ei < 0 || ei >= g.nx || ej < 0 || ej >= g.ny || ek < 0 || ek >= g.nz) continue;
-      const int64_t e = ((int64_t)ek * g.ny + ej) * g.nx + ei;
-      const int L = loc_of(1 - sx, 1 - sy, (D == 3) ? 1 - sz : 0);
-      d += ke[e * NE * NE + (L * D + c) * NE + L * D + c];
-    }
+    const double d = st[((int64_t)c * D + c) * g.n_nodes + n];  // centre block (u = 0)
     dinv[n * D + c] = (fixed[n * D + c] || !(d > 0.0)) ? 0.0 : 1.0 / d;
+  }
+}
+
+// Level-1 fast path.  A coarse element whose 2^D children all exist and whose fine nodes carry
+// no Dirichlet dof has  K_E = sum_ch alpha_ch G_ch,  G_ch = R_ch^T K_unit R_ch  (host-built).
+template <int D>
+__global__ void k_mg_dirty(Grid gc, Grid gf, const uint8_t* __restrict__ fixed_f, uint8_t* __restrict__ dirty) {
+  const int64_t E = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (E >= gc.n_elems) return;
+  const int I = (int)(E % gc.nx), J = (int)((E / gc.nx) % gc.ny);
+  const int K = (D == 3) ? (int)(E / ((int64_t)gc.nx * gc.ny)) : 0;
+  bool d = 2 * I + 1 >= gf.nx || 2 * J + 1 >= gf.ny || (D == 3 && 2 * K + 1 >= gf.nz);
+  for (int z = 0; z < (D == 3 ? 3 : 1) && !d; ++z)
+    for (int y = 0; y < 3 && !d; ++y)
+      for (int x = 0; x < 3 && !d; ++x)
+        for (int c = 0; c < D; ++c)
+          if (fixed_f[dof_of(gf, 2 * I + x, 2 * J + y, (D == 3) ? 2 * K + z : 0, D, c)]) d = true;
+  dirty[E] = d ? 1 : 0;
+}
+
+constexpr int kAggBatch = 16;
+template <int D>
+__global__ void __launch_bounds__(256) k_mg_agg_fast(Grid gc, Grid gf, const double* __restrict__ G,
+                                                     const double* __restrict__ alpha,
+                                                     const uint8_t* __restrict__ dirty, double* __restrict__ ke_c) {
+  constexpr int NN = Q1<D>::NN, NE = NN * D, NE2 = NE * NE;
+  __shared__ double a[kAggBatch][NN];
+  const int64_t E0 = (int64_t)blockIdx.x * kAggBatch;
+  for (int q = threadIdx.x; q < kAggBatch * NN; q += blockDim.x) {
+    const int b = q / NN, ch = q % NN;
+    const int64_t E = E0 + b;
+    double v = 0.0;
+    if (E < gc.n_elems && !dirty[E]) {
+      const int I = (int)(E % gc.nx), J = (int)((E / gc.nx) % gc.ny);
+      const int K = (D == 3) ? (int)(E / ((int64_t)gc.nx * gc.ny)) : 0;
+      const int fi = 2 * I + (ch & 1), fj = 2 * J + ((ch >> 1) & 1), fk = (D == 3) ? 2 * K + (ch >> 2) : 0;
+      v = alpha[((int64_t)fk * gf.ny + fj) * gf.nx + fi];
+    }
+    a[b][ch] = v;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < kAggBatch * NE2; q += blockDim.x) {
+    const int b = q / NE2, o = q % NE2;
+    const int64_t E = E0 + b;
+    if (E >= gc.n_elems || dirty[E]) continue;
+    double v = 0.0;
+#pragma unroll
+    for (int ch = 0; ch < NN; ++ch) v = fma(a[b][ch], __ldg(G + ch * NE2 + o), v);
+    ke_c[E * NE2 + o] = v;
   }
 }
 
@@ -192,8 +304,8 @@ __global__ void k_mg_restrict(Grid gc, Grid gf, const double* __restrict__ rf, c
 #pragma unroll
       for (int dx = -1; dx <= 1; ++dx) {
         const int fi = 2 * I + dx, fj = 2 * J + dy, fk = 2 * K + dz;
-        if (fi < 0 || fi >= gf.nnx || fj < 0 || fj >= gf.nny || fk < 0 || fk >= gf.nnz) continue;
-        const double w = (dx ? 0.5 : 1.0) * (dy ? 0.5 : 1.0) * (dz ? 0.5 : 1.0);
+        const double w = pw(fi, I, gf.nx) * pw(fj, J, gf.ny) * ((D == 3) ? pw(fk, K, gf.nz) : 1.0);
+        if (w == 0.0) continue;
         const int64_t fd = dof_of(gf, fi, fj, fk, D, 0);
 #pragma unroll
         for (int c = 0; c < D; ++c) acc[c] = fma(w, __ldg(rf + fd + c), acc[c]);
@@ -210,8 +322,10 @@ __global__ void k_mg_prolong_add(Grid gf, Grid gc, const double* __restrict__ xc
   if (n >= gf.n_nodes) return;
   int i, j, k;
   node_coords(gf, n, i, j, k);
-  const int i0 = i >> 1, j0 = j >> 1, k0 = k >> 1;
-  const int ni = (i & 1) ? 2 : 1, nj = (j & 1) ? 2 : 1, nk = (D == 3 && (k & 1)) ? 2 : 1;
+  int i0, j0, k0 = 0, ni, nj, nk = 1;
+  pmap(i, gf.nx, i0, ni);
+  pmap(j, gf.ny, j0, nj);
+  if (D == 3) pmap(k, gf.nz, k0, nk);
   const double w = (ni == 2 ? 0.5 : 1.0) * (nj == 2 ? 0.5 : 1.0) * (nk == 2 ? 0.5 : 1.0);
   double acc[D];
 #pragma unroll
@@ -294,12 +408,12 @@ int mg_build(tb_plan_impl* P) {
   l0.fixed = P->d_fixed;
   l0.dinv = P->work.dinv;  // stable pointer: graphs capture it before the first set-up
   mg.lv.push_back(l0);
-  while (true) {
+  while (mg.lv.back().n > kMgMinDofs) {
     const Grid& gf = mg.lv.back().g;
-    const bool even = (gf.nx % 2 == 0) && (gf.ny % 2 == 0) && (D == 2 || gf.nz % 2 == 0);
-    if (!even || mg.lv.back().n <= kMgMinDofs || gf.nx < 2 || gf.ny < 2) break;
+    const int cx = (gf.nx + 1) / 2, cy = (gf.ny + 1) / 2, cz = (D == 3) ? (gf.nz + 1) / 2 : 1;
+    if (cx == gf.nx && cy == gf.ny && cz == gf.nz) break;  // nothing left to coarsen
     MgLevel c;
-    c.g = make_grid(D, gf.nx / 2, gf.ny / 2, (D == 3) ? gf.nz / 2 : 0, gf.h * 2.0);
+    c.g = make_grid(D, cx, cy, (D == 3) ? cz : 0, gf.h * 2.0);
     c.nc = D;
     c.n = (int64_t)D * c.g.n_nodes;
     mg.lv.push_back(c);
@@ -319,6 +433,7 @@ int mg_build(tb_plan_impl* P) {
       TB_CUDA(cudaMalloc(&L.fixed, (size_t)L.n));
       TB_CUDA(cudaMalloc(&L.dinv, sizeof(double) * (size_t)L.n));
       TB_CUDA(cudaMalloc(&L.ke, sizeof(double) * (size_t)L.g.n_elems * NE * NE));
+      TB_CUDA(cudaMalloc(&L.st, sizeof(double) * (size_t)L.g.n_nodes * (D == 2 ? 5 : 14) * D * D));
       const MgLevel& F = mg.lv[l - 1];
       if (D == 2)
         { k_mg_coarse_fixed<2><<<nblk(L.n), kBlock>>>(L.g, F.g, F.fixed, L.fixed); tb::launched(); }
@@ -326,6 +441,40 @@ int mg_build(tb_plan_impl* P) {
         { k_mg_coarse_fixed<3><<<nblk(L.n), kBlock>>>(L.g, F.g, F.fixed, L.fixed); tb::launched(); }
       TB_CHECK_LAUNCH();
     }
+  }
+  // level-1 fast-path tables: G_ch = R_ch^T K_unit R_ch for the 2^D children of a full coarse element
+  {
+    const int NN = 1 << D;
+    const double* Ku = (D == 2) ? P->K2.v : P->K3.v;
+    std::vector<double> G((size_t)NN * NE * NE, 0.0), R((size_t)NN * NN);
+    for (int ch = 0; ch < NN; ++ch) {
+      const int c3[3] = {ch & 1, (ch >> 1) & 1, ch >> 2};
+      for (int b = 0; b < NN; ++b)
+        for (int B = 0; B < NN; ++B) {
+          const int ob[3] = {offx(b), offy(b), offz(b)}, oB[3] = {offx(B), offy(B), offz(B)};
+          double w = 1.0;
+          for (int d = 0; d < D; ++d) {
+            const double t = 0.5 * (c3[d] + ob[d]);
+            w *= oB[d] ? t : 1.0 - t;
+          }
+          R[(size_t)b * NN + B] = w;
+        }
+      double* Gc = G.data() + (size_t)ch * NE * NE;
+      for (int r = 0; r < NE; ++r)
+        for (int q = 0; q < NE; ++q) {
+          const int Br = r / D, cr = r % D, Bq = q / D, cq = q % D;
+          double acc = 0.0;
+          for (int b = 0; b < NN; ++b) {
+            const double rb = R[(size_t)b * NN + Br];
+            if (rb == 0.0) continue;
+            for (int bp = 0; bp < NN; ++bp) acc += rb * Ku[(b * D + cr) * NE + bp * D + cq] * R[(size_t)bp * NN + Bq];
+          }
+          Gc[(size_t)r * NE + q] = acc;
+        }
+    }
+    TB_CUDA(cudaMalloc(&mg.G, sizeof(double) * G.size()));
+    TB_CUDA(cudaMemcpy(mg.G, G.data(), sizeof(double) * G.size(), cudaMemcpyHostToDevice));
+    TB_CUDA(cudaMalloc(&mg.dirty, (size_t)mg.lv[1].g.n_elems));
   }
   mg.ncoarse = mg.lv.back().n;
   TB_CUDA(cudaMalloc(&mg.dense, sizeof(double) * (size_t)mg.ncoarse * mg.ncoarse));
@@ -356,10 +505,13 @@ void mg_release(Mg& mg) {
       if (L.fixed) cudaFree(L.fixed);
       if (L.dinv) cudaFree(L.dinv);
       if (L.ke) cudaFree(L.ke);
+      if (L.st) cudaFree(L.st);
     }
   }
   mg.lv.clear();
   if (mg.dense) cudaFree(mg.dense);
+  if (mg.G) cudaFree(mg.G);
+  if (mg.dirty) cudaFree(mg.dirty);
   if (mg.work) cudaFree(mg.work);
   if (mg.info) cudaFree(mg.info);
   if (mg.solver) cusolverDnDestroy((cusolverDnHandle_t)mg.solver);
@@ -374,18 +526,27 @@ int mg_setup(tb_plan_impl* P, cudaStream_t s) {
     MgLevel& C = mg.lv[l];
     const MgLevel& F = mg.lv[l - 1];
     const unsigned grid = (unsigned)C.g.n_elems;
+    const unsigned fast = (unsigned)((C.g.n_elems + kAggBatch - 1) / kAggBatch);
     if (D == 2) {
-      if (l == 1)
-        { k_mg_aggregate<2, true><<<grid, 256, 0, s>>>(C.g, F.g, P->K2, P->d_alpha, nullptr, F.fixed, C.fixed, C.ke); tb::launched(); }
-      else
-        { k_mg_aggregate<2, false><<<grid, 256, 0, s>>>(C.g, F.g, P->K2, nullptr, F.ke, F.fixed, C.fixed, C.ke); tb::launched(); }
-      { k_mg_dinv<2><<<nblk(C.g.n_nodes), kBlock, 0, s>>>(C.g, C.ke, C.fixed, C.dinv); tb::launched(); }
+      if (l == 1) {
+        { k_mg_dirty<2><<<nblk(C.g.n_elems), kBlock, 0, s>>>(C.g, F.g, F.fixed, mg.dirty); tb::launched(); }
+        { k_mg_agg_fast<2><<<fast, 256, 0, s>>>(C.g, F.g, mg.G, P->d_alpha, mg.dirty, C.ke); tb::launched(); }
+        { k_mg_aggregate<2, true><<<grid, 256, 0, s>>>(C.g, F.g, P->K2, P->d_alpha, nullptr, F.fixed, C.fixed, mg.dirty, C.ke); tb::launched(); }
+      } else {
+        { k_mg_aggregate<2, false><<<grid, 256, 0, s>>>(C.g, F.g, P->K2, nullptr, F.ke, F.fixed, C.fixed, nullptr, C.ke); tb::launched(); }
+      }
+      { k_mg_stencil<2><<<nblk(C.g.n_nodes), kBlock, 0, s>>>(C.g, C.ke, C.st); tb::launched(); }
+      { k_mg_dinv<2><<<nblk(C.g.n_nodes), kBlock, 0, s>>>(C.g, C.st, C.fixed, C.dinv); tb::launched(); }
     } else {
-      if (l == 1)
-        { k_mg_aggregate<3, true><<<grid, 256, 0, s>>>(C.g, F.g, P->K3, P->d_alpha, nullptr, F.fixed, C.fixed, C.ke); tb::launched(); }
-      else
-        { k_mg_aggregate<3, false><<<grid, 256, 0, s>>>(C.g, F.g, P->K3, nullptr, F.ke, F.fixed, C.fixed, C.ke); tb::launched(); }
-      { k_mg_dinv<3><<<nblk(C.g.n_nodes), kBlock, 0, s>>>(C.g, C.ke, C.fixed, C.dinv); tb::launched(); }
+      if (l == 1) {
+        { k_mg_dirty<3><<<nblk(C.g.n_elems), kBlock, 0, s>>>(C.g, F.g, F.fixed, mg.dirty); tb::launched(); }
+        { k_mg_agg_fast<3><<<fast, 256, 0, s>>>(C.g, F.g, mg.G, P->d_alpha, mg.dirty, C.ke); tb::launched(); }
+        { k_mg_aggregate<3, true><<<grid, 256, 0, s>>>(C.g, F.g, P->K3, P->d_alpha, nullptr, F.fixed, C.fixed, mg.dirty, C.ke); tb::launched(); }
+      } else {
+        { k_mg_aggregate<3, false><<<grid, 256, 0, s>>>(C.g, F.g, P->K3, nullptr, F.ke, F.fixed, C.fixed, nullptr, C.ke); tb::launched(); }
+      }
+      { k_mg_stencil<3><<<nblk(C.g.n_nodes), kBlock, 0, s>>>(C.g, C.ke, C.st); tb::launched(); }
+      { k_mg_dinv<3><<<nblk(C.g.n_nodes), kBlock, 0, s>>>(C.g, C.st, C.fixed, C.dinv); tb::launched(); }
     }
     TB_CHECK_LAUNCH();
   }
@@ -425,9 +586,9 @@ static void level_apply(tb_plan_impl* P, size_t l, const double* v, double* y, c
   if (l == 0) {
     P->apply_alpha(P->d_alpha, v, y, false, s);
   } else if (L.g.dim == 2) {
-    { k_mg_apply<2><<<nblk(L.g.n_nodes), kBlock, 0, s>>>(L.g, L.ke, v, y); tb::launched(); }
+    { k_mg_sapply<2><<<nblk(L.g.n_nodes), kBlock, 0, s>>>(L.g, L.st, v, y); tb::launched(); }
   } else {
-    { k_mg_apply<3><<<nblk(L.g.n_nodes), kBlock, 0, s>>>(L.g, L.ke, v, y); tb::launched(); }
+    { k_mg_sapply<3><<<nblk(L.g.n_nodes), kBlock, 0, s>>>(L.g, L.st, v, y); tb::launched(); }
   }
 }
 

@@ -1,7 +1,7 @@
 // Geometric multigrid preconditioner for the SIMP elasticity operator.
 //
-// Hierarchy: vertex-centred coarsening by 2 in every direction while the element counts stay
-// even.  Coarse operators are exact Galerkin products, built element by element: a coarse
+// Hierarchy: vertex-centred coarsening by 2 in every direction (an odd element count leaves a
+// last coarse element spanning one fine element) until the level has few enough dofs.  Coarse operators are exact Galerkin products, built element by element: a coarse
 // element E covers 2^d fine elements e, and with the (tri)linear interpolation R_e from E's
 // corners to e's corners,
 //     K_E = sum_{e in E} R_e^T (Z_e K_e Z_e) R_e ,  then rows/cols of fixed coarse dofs zeroed,
@@ -11,6 +11,8 @@
 // V-cycle (symmetric, so the preconditioner is SPD and plain pCG applies): nu damped-Jacobi
 // sweeps, residual, restriction P^T, recursive coarse correction, prolongation P, nu sweeps.
 // The coarsest level is solved exactly with a dense inverse (cuSOLVER potrf/potri at set-up).
+// Coarse levels are applied from assembled 3^D-point node stencils (fewer bytes per apply than
+// the element matrices they are built from).
 #pragma once
 
 #include <vector>
@@ -22,7 +24,8 @@ namespace tb {
 struct MgLevel {
   Grid g{};
   int nc = 2;                  // components
-  double* ke = nullptr;        // level >= 1: dense element matrices (n_elems x NE x NE)
+  double* ke = nullptr;        // level >= 1: dense element matrices (n_elems x NE x NE), set-up only
+  double* st = nullptr;        // level >= 1: half node stencil ((3^D+1)/2 D^2 x n_nodes), applies
   uint8_t* fixed = nullptr;    // Dirichlet mask of this level
   double* dinv = nullptr;      // Jacobi inverse diagonal (0 on fixed)
   double *x = nullptr, *b = nullptr, *r = nullptr, *t = nullptr;  // work vectors
@@ -32,6 +35,8 @@ struct MgLevel {
 struct Mg {
   std::vector<MgLevel> lv;     // lv[0] = fine level (operator = alpha K_unit, matrix-free)
   double* ainv = nullptr;      // coarsest dense inverse (n x n)
+  double* G = nullptr;         // level-1 fast path: R_ch^T K_unit R_ch per child (2^D x NE x NE)
+  uint8_t* dirty = nullptr;    // level-1 coarse elements that need the general aggregation
   double* dense = nullptr;     // coarsest dense matrix scratch
   int64_t ncoarse = 0;
   int nu = 2;                  // smoothing sweeps

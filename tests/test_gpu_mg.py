@@ -62,8 +62,25 @@ def test_mg_3d_matches_jacobi(cuda, dims):
     assert out["mg"][3] < out["jacobi"][3] / 4
 
 
-def test_mg_rejects_odd_grids(cuda):
-    mesh = tb.build_mesh(15, 5, 1.0)
+@pytest.mark.parametrize("dims", [(61, 23, None), (15, 9, 7), (25, 7, 11)])
+def test_mg_odd_grids_match_jacobi(cuda, dims):
+    """Odd element counts coarsen with a short last coarse element; the preconditioned answer
+    is the Jacobi answer."""
+    nx, ny, nz = dims
+    prob = configs.cfg1(seed=2, nx=nx, ny=ny) if nz is None else configs.cfg3(seed=2, nx=nx, ny=ny, nz=nz)
+    out = {}
+    for pc in ("jacobi", "mg"):
+        s = build(prob, pc, rtol=1e-10)
+        obj = tb.ComplianceObjective(s.f)
+        sol = s.solve(prob.psi, obj)
+        out[pc] = (sol.j, s.gradient(prob.psi, sol, obj), sol.iterations)
+    assert abs(out["mg"][0] - out["jacobi"][0]) <= 1e-8 * abs(out["jacobi"][0])
+    assert nrel(out["mg"][1], out["jacobi"][1]) <= 1e-6
+    assert out["mg"][2] < out["jacobi"][2] / 3
+
+
+def test_mg_rejects_grids_without_a_coarse_level(cuda):
+    mesh = tb.build_mesh(4, 2, 1.0)  # 30 dofs: already below the coarsest-level size
     f = np.zeros(mesh.n_dofs)
     f[-1] = -1.0
     left = mesh.boundary_nodes("left")

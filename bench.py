@@ -163,6 +163,32 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def time_eval(solver, obj, psi, torch, reps=3):
+    """Seconds per full evaluation (solve + gradient), device-resident, after one warm-up."""
+    sol = solver.solve(psi, obj)
+    solver.gradient(psi, sol, obj)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(reps):
+        sol = solver.solve(psi, obj)
+        solver.gradient(psi, sol, obj)
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) * 1e-3 / reps, sol
+
+
+def mg_extra(tb, configs, prob, psi, torch):
+    """Same evaluation with the geometric-multigrid preconditioner: the
+    solution matches the Jacobi path to the solve tolerance; reported beside the headline."""
+    s = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, prob.radius), prob.f, prob.fixed,
+                     tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP), rtol=prob.rtol, preconditioner="mg")
+    obj = tb.ComplianceObjective(s.f)
+    t, sol = time_eval(s, obj, psi, torch)
+    return {"preconditioner": "geometric multigrid V(2,2), Galerkin coarse levels, damped Jacobi",
+            "s_per_eval": t, "pcg_iterations": sol.iterations, "J": sol.j}
+
+
 def bench_cfg3(tb, configs, _lib, dev, pk):
     """BASELINE cfg 3 (192x96x96 Hex8, 5.4M DOF): one full HDM evaluation + the Hex8 operator
     kernel's roofline (graph path; per-kernel CUDA-event timing via tb_pcg_profile)."""
@@ -207,7 +233,8 @@ def bench_cfg3(tb, configs, _lib, dev, pk):
             "update_kernel": {"us_per_launch": msu.value * 1e3, "bytes_per_launch": by_up,
                               "achieved_gbs": by_up / (msu.value * 1e-3) / 1e9,
                               "frac_hbm": by_up / (msu.value * 1e-3) / 1e9 / pk.get("hbm_gbs")},
-            "us_per_iteration_in_solve": None}
+            "us_per_iteration_in_solve": None,
+            "mg": mg_extra(tb, configs, prob, psi, torch)}
 
 
 def peaks():
@@ -364,6 +391,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         extras["rom_khat_ms"] = a.elapsed_time(b) / 10
         extras["rom_k"] = k
+        extras["mg"] = mg_extra(tb, configs, prob, psi_d, torch)
         if args.extra3d:
             extras["cfg3"] = bench_cfg3(tb, configs, _lib, dev, pk)
 

@@ -138,7 +138,13 @@ def require_cuda(device=None):
     if not t.cuda.is_available():
         raise RuntimeError("paper_2004_05756_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
     lib()
-    return t.device("cuda", t.cuda.current_device() if device is None else device)
+    if isinstance(device, t.device):
+        if device.type != "cuda":
+            raise ValueError(f"device must be a CUDA device, got {device}")
+        return t.device("cuda", t.cuda.current_device() if device.index is None else device.index)
+    if isinstance(device, str):
+        return require_cuda(t.device(device))
+    return t.device("cuda", t.cuda.current_device() if device is None else int(device))
 
 
 def stream_ptr(device) -> P:

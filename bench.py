@@ -442,8 +442,9 @@ def fp64_peak_tflops(torch, dev):
 
 
 def dmma_time(rom, basis, rho, torch):
-    """CUDA-event time of the DMMA contraction alone (tb_rom_gram_colmajor: the kernel
-    tb_rom_reduced_stiffness uses, on the column-major basis), one launch after warm-up."""
+    """CUDA-event time of the DMMA contraction alone (tb_rom_gram_colmajor, symmetric: the
+    kernel variant tb_rom_reduced_stiffness uses, on the column-major basis), one launch after
+    warm-up."""
     import ctypes
 
     from paper_2004_05756_b200 import _lib
@@ -455,11 +456,11 @@ def dmma_time(rom, basis, rho, torch):
     a[:, :n] = phi.t()
     out = torch.empty((k, k), dtype=torch.float64, device=rom.device)
     for _ in range(2):
-        _lib.check(_lib.lib().tb_rom_gram_colmajor(n, k, _lib.ptr(a), _lib.ptr(a), ldp, _lib.ptr(out),
+        _lib.check(_lib.lib().tb_rom_gram_colmajor(n, k, _lib.ptr(a), _lib.ptr(a), ldp, 1, _lib.ptr(out),
                                                    _lib.stream_ptr(rom.device)), "gram")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    _lib.check(_lib.lib().tb_rom_gram_colmajor(n, k, _lib.ptr(a), _lib.ptr(a), ldp, _lib.ptr(out),
+    _lib.check(_lib.lib().tb_rom_gram_colmajor(n, k, _lib.ptr(a), _lib.ptr(a), ldp, 1, _lib.ptr(out),
                                                _lib.stream_ptr(rom.device)), "gram")
     e1.record()
     torch.cuda.synchronize()
@@ -515,8 +516,9 @@ def run_cfg5(args):
     t_khat = e0.elapsed_time(e1) * 1e-3
     n_u, n_e = m.n_dofs, m.n_elems
     canonical = n_e * (2 * k * 24**2 + 2 * k**2 * 24)  # PAPER.md:664 element form, per design
-    executed_dmma = 2 * n_u * k * k                      # Phi^T Y on DMMA, per design
-    executed_op = 190 * n_e * k                          # WHT Hex8 operator, FP64 instr per element-column
+    mb = (k + 7) // 8
+    executed_dmma = 2 * n_u * 64 * (mb * (mb + 1) // 2)  # Phi^T Y on DMMA, upper 8x8 tiles only (symmetric)
+    executed_op = 150 * n_e * k                          # WHT Hex8 operator, ~FP64 instr per element-column
     peak = fp64_peak_tflops(torch, dev)
     # the dominant kernel alone: the DMMA contraction, timed with events around its launch
     t_dmma = dmma_time(rom, basis, rhos[0], torch)
@@ -526,7 +528,8 @@ def run_cfg5(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg 5 recipe)",
         "config": {"workload": f"cfg5 {m.nx}x{m.ny}x{m.nz} Hex8, {n_u} DOF, k={k}, {nd} designs: "
                                "Phi^T K(rho_d) Phi + batched Cholesky + residual norms", "parallelism": "single"},
-        "roofline": {"kernel": "k_atb_cm<64> (Phi^T Y on FP64 tensor cores, DMMA m8n8k4)", "bound": "tensor",
+        "roofline": {"kernel": "k_atb_cm<64,sym> (Phi^T Y upper tiles on FP64 tensor cores, DMMA m8n8k4)",
+                     "bound": "tensor",
                      "achieved": executed_dmma / t_dmma / 1e12, "peak": peak, "unit": "TFLOP/s",
                      "frac": executed_dmma / t_dmma / 1e12 / peak, "traffic": None,
                      "us_per_launch": t_dmma * 1e6, "flops_per_launch": executed_dmma,

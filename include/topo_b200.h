@@ -139,9 +139,11 @@ int tb_rom_project(int64_t n, const double* phi, int k, const double* vec, int n
 int tb_rom_reduced_stiffness(tb_plan* plan, const double* phi, int k, const double* rho, int nd,
                              double* khat, void* stream);
 /* out (k x k, row-major) = A^T B for column-major A, B (k columns, leading dimension ld, rows
- * [0, n)): the DMMA contraction of tb_rom_reduced_stiffness on its own (also a Gram matrix). */
-int tb_rom_gram_colmajor(int64_t n, int k, const double* A, const double* B, int64_t ld, double* out,
-                         void* stream);
+ * [0, n)): the DMMA contraction of tb_rom_reduced_stiffness on its own (also a Gram matrix).
+ * symmetric != 0: the caller guarantees A^T B is symmetric (Phi^T K Phi, a Gram matrix); only
+ * the upper 8x8 tiles are computed and mirrored, as tb_rom_reduced_stiffness does. */
+int tb_rom_gram_colmajor(int64_t n, int k, const double* A, const double* B, int64_t ld, int symmetric,
+                         double* out, void* stream);
 /* Batched Cholesky solve khat[d] X = rhs[d] (nrhs right-hand sides per design, row-major
  * nd x nrhs x k) for rom.py:280-291.  status is a HOST int array of nd entries: 0 ok,
  * 1 = not SPD (cho_factor LinAlgError -> DegenerateBasisError). */

@@ -74,7 +74,7 @@ _SIGS = {
     "tb_filter_adjoint": ([P, P, P, D, PI, P], I),
     "tb_rom_project": ([I64, P, I, P, I, P, P], I),
     "tb_rom_reduced_stiffness": ([P, P, I, P, I, P, P], I),
-    "tb_rom_gram_colmajor": ([I64, I, P, P, I64, P, P], I),
+    "tb_rom_gram_colmajor": ([I64, I, P, P, I64, I, P, P], I),
     "tb_rom_cholesky_solve": ([I, I, I, P, P, P, PI, P], I),
     "tb_rom_reconstruct": ([I64, P, I, P, I, P, P], I),
     "tb_rom_residual_norms": ([P, P, I, P, P, I, P, I64, PD, P], I),

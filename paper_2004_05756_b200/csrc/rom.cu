@@ -167,14 +167,22 @@ __global__ void __launch_bounds__(kGemmThreads) k_atb_dmma(int64_t n, int k, con
 // Stage = 32 rows x KP columns of both matrices in shared memory as [col][row] (+pad);
 // warp w owns output row block(s) so its A fragment feeds 8 DMMAs per k-step.
 // ---------------------------------------------------------------------------------------
+#ifndef TB_CM_STAGES
+#define TB_CM_STAGES 2
+#endif
 constexpr int kCmRows = 32, kCmLd = kCmRows + 4;
+constexpr int kCmStages = TB_CM_STAGES;                       // cp.async ring depth
+constexpr int kCmCtas = (kCmStages <= 2) ? 3 : (kCmStages == 3 ? 2 : 1);  // resident CTAs per SM (KP = 64)
 
 
-template <int KP>
+// SYM: A^T B is known to be symmetric (Phi^T K Phi): only the MB(MB+1)/2 upper 8x8 tiles are
+// computed and the lower triangle is mirrored on output (exactly symmetric result).
+template <int KP, bool SYM>
 __global__ void __launch_bounds__(kGemmThreads) k_atb_cm(int64_t r0, int64_t r1, int k,
                                                          const double* __restrict__ A, const double* __restrict__ B,
                                                          double* __restrict__ part, int64_t ld) {
-  constexpr int MB = KP / 8, TILES = MB * MB, NW = kGemmThreads / 32, TPW = (TILES + NW - 1) / NW;
+  constexpr int MB = KP / 8, TILES = SYM ? MB * (MB + 1) / 2 : MB * MB, NW = kGemmThreads / 32;
+  constexpr int TPW = (TILES + NW - 1) / NW;
   constexpr int STAGE = 2 * KP * kCmLd;  // doubles per stage (A then B)
   extern __shared__ __align__(16) double smc[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -196,18 +204,39 @@ __global__ void __launch_bounds__(kGemmThreads) k_atb_cm(int64_t r0, int64_t r1,
     cp_async_commit();
   };
   double acc[TPW][2];
+  int tm[TPW], tn[TPW];  // tile origin (row block, column block) of this warp's tiles
 #pragma unroll
-  for (int t = 0; t < TPW; ++t) acc[t][0] = acc[t][1] = 0.0;
-  if (nstages > 0) load(0, 0);
-  for (int st = 0; st < nstages; ++st) {
-    if (st + 1 < nstages) {
-      load(st + 1, (st + 1) & 1);
-      cp_async_wait<1>();
+  for (int t = 0; t < TPW; ++t) {
+    acc[t][0] = acc[t][1] = 0.0;
+    int u = warp * TPW + t, mb = 0;
+    if (SYM) {
+      while (mb < MB && u >= MB - mb) u -= MB - mb++;
+      tm[t] = mb * 8;
+      tn[t] = (mb + u) * 8;
     } else {
-      cp_async_wait<0>();
+      tm[t] = (u / MB) * 8;
+      tn[t] = (u % MB) * 8;
     }
-    __syncthreads();
-    const double* sa = smc + (st & 1) * STAGE;
+  }
+  // ring of kCmStages buffers; stage st + kCmStages - 1 is issued while stage st is consumed
+#pragma unroll
+  for (int p = 0; p < kCmStages - 1; ++p) {
+    if (p < nstages)
+      load(p, p);
+    else
+      cp_async_commit();  // empty group keeps the wait count uniform
+  }
+  for (int st = 0; st < nstages; ++st) {
+    cp_async_wait<kCmStages - 2>();
+    __syncthreads();  // stage st visible to all; every warp is done with stage st-1's buffer
+    {
+      const int nx = st + kCmStages - 1;
+      if (nx < nstages)
+        load(nx, nx % kCmStages);
+      else
+        cp_async_commit();
+    }
+    const double* sa = smc + (st % kCmStages) * STAGE;
     const double* sb = sa + KP * kCmLd;
 #pragma unroll
     for (int r0 = 0; r0 < kCmRows; r0 += 4) {
@@ -216,44 +245,53 @@ __global__ void __launch_bounds__(kGemmThreads) k_atb_cm(int64_t r0, int64_t r1,
       for (int t = 0; t < TPW; ++t) {
         const int tile = warp * TPW + t;
         if (tile < TILES) {
-          const int m0 = (tile / MB) * 8, n0 = (tile % MB) * 8;
-          const double a = sa[(m0 + cc) * kCmLd + rr];
-          const double b = sb[(n0 + cc) * kCmLd + rr];
+          const double a = sa[(tm[t] + cc) * kCmLd + rr];
+          const double b = sb[(tn[t] + cc) * kCmLd + rr];
           dmma_8x8x4(acc[t], a, b);
         }
       }
     }
-    __syncthreads();  // the buffer is refilled two stages later
   }
+  cp_async_wait<0>();
   double* out = part + (int64_t)blockIdx.x * k * k;
 #pragma unroll
   for (int t = 0; t < TPW; ++t) {
     const int tile = warp * TPW + t;
     if (tile < TILES) {
-      const int m = (tile / MB) * 8 + (lane >> 2);
-      const int c0 = (tile % MB) * 8 + 2 * (lane & 3);
-      if (m < k && c0 < k) out[m * k + c0] = acc[t][0];
-      if (m < k && c0 + 1 < k) out[m * k + c0 + 1] = acc[t][1];
+      const int m = tm[t] + (lane >> 2);
+      const int c0 = tn[t] + 2 * (lane & 3);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = c0 + h;
+        if (m >= k || c >= k) continue;
+        if (!SYM) {
+          out[m * k + c] = acc[t][h];
+        } else if (c >= m) {  // upper entry (diagonal tiles: their lower half is dropped)
+          out[m * k + c] = acc[t][h];
+          out[c * k + m] = acc[t][h];
+        }
+      }
     }
   }
 }
 
-template <int KP>
+template <int KP, bool SYM>
 static int launch_cm(int64_t r0, int64_t r1, int k, const double* A, const double* B, double* part, int nb,
                      int64_t ld, cudaStream_t s) {
-  const size_t smem = sizeof(double) * 2 * 2 * KP * kCmLd;
-  TB_CUDA(cudaFuncSetAttribute(k_atb_cm<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  { k_atb_cm<KP><<<nb, kGemmThreads, smem, s>>>(r0, r1, k, A, B, part, ld); tb::launched(); }
+  const size_t smem = sizeof(double) * kCmStages * 2 * KP * kCmLd;
+  TB_CUDA(cudaFuncSetAttribute(k_atb_cm<KP, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  { k_atb_cm<KP, SYM><<<nb, kGemmThreads, smem, s>>>(r0, r1, k, A, B, part, ld); tb::launched(); }
   TB_CHECK_LAUNCH();
   return TB_OK;
 }
 
+template <bool SYM>
 static int launch_atb_colmajor(int64_t r0, int64_t r1, int k, const double* A, const double* B, double* part,
                                int nb, int64_t ld, cudaStream_t s) {
   const int kp = (k + 7) / 8 * 8;
-  if (kp <= 16) return launch_cm<16>(r0, r1, k, A, B, part, nb, ld, s);
-  if (kp <= 32) return launch_cm<32>(r0, r1, k, A, B, part, nb, ld, s);
-  if (kp <= 64) return launch_cm<64>(r0, r1, k, A, B, part, nb, ld, s);
+  if (kp <= 16) return launch_cm<16, SYM>(r0, r1, k, A, B, part, nb, ld, s);
+  if (kp <= 32) return launch_cm<32, SYM>(r0, r1, k, A, B, part, nb, ld, s);
+  if (kp <= 64) return launch_cm<64, SYM>(r0, r1, k, A, B, part, nb, ld, s);
   set_error("reduced basis size k=%d exceeds 64", k);
   return TB_ERR_INVALID;
 }
@@ -487,7 +525,7 @@ int tb_rom_reduced_stiffness(tb_plan* plan, const double* phi, int k, const doub
   const bool hex8 = (g.dim == 3 && P->hex8);
   // 3D: one WHT Hex8 launch per column on a column-major copy of Phi; 2D: node-owner over
   // all k columns of the row-major Phi
-  const int nbc = hex8 ? 148 * 3 : nb;              // column-major DMMA: 3 CTAs per SM
+  const int nbc = hex8 ? 148 * kCmCtas : nb;        // column-major DMMA: one wave of resident CTAs
   const int64_t ldp = hex8 ? (n + 1) / 2 * 2 : n;    // even leading dimension (16-byte columns)
   const size_t ybytes = sizeof(double) * (size_t)ldp * k * (hex8 ? 2 : 1);
   const size_t pbytes = sizeof(double) * (size_t)nbc * k * k;
@@ -505,7 +543,7 @@ int tb_rom_reduced_stiffness(tb_plan* plan, const double* phi, int k, const doub
       for (int j = 0; j < k; ++j)
         { k_hex8<false><<<hex8_grid(g, P->zchunk), kHT, kHex8Smem, s>>>(g, P->hiso, P->d_alpha2, PhiT + (int64_t)j * ldp, nullptr, nullptr, Y + (int64_t)j * ldp, nullptr, nullptr, nullptr, P->zchunk); tb::launched(); }
       TB_CHECK_LAUNCH();
-      TB_TRY(launch_atb_colmajor(r0, r1, k, PhiT, Y, part, nbc, ldp, s));
+      TB_TRY(launch_atb_colmajor<true>(r0, r1, k, PhiT, Y, part, nbc, ldp, s));  // Phi^T (K Phi) is symmetric
     } else {
       const int64_t threads = g.n_nodes * k;
       const int blocks = (int)((threads + kBlock - 1) / kBlock);
@@ -522,15 +560,18 @@ int tb_rom_reduced_stiffness(tb_plan* plan, const double* phi, int k, const doub
   return TB_OK;
 }
 
-int tb_rom_gram_colmajor(int64_t n, int k, const double* A, const double* B, int64_t ld, double* out,
-                         void* stream) {
+int tb_rom_gram_colmajor(int64_t n, int k, const double* A, const double* B, int64_t ld, int symmetric,
+                         double* out, void* stream) {
   TB_GUARD(A && B && out && n >= 1 && ld >= n, "bad arguments");
   TB_GUARD(k >= 1 && k <= 64, "k=%d out of range [1, 64]", k);
   cudaStream_t s = (cudaStream_t)stream;
-  const int nb = 148 * 3;
+  const int nb = 148 * kCmCtas;
   double* part = nullptr;
   TB_CUDA(cudaMallocAsync(&part, sizeof(double) * (size_t)nb * k * k, s));
-  TB_TRY(launch_atb_colmajor(0, n, k, A, B, part, nb, ld, s));
+  if (symmetric)
+    TB_TRY(launch_atb_colmajor<true>(0, n, k, A, B, part, nb, ld, s));
+  else
+    TB_TRY(launch_atb_colmajor<false>(0, n, k, A, B, part, nb, ld, s));
   { k_sum_parts<<<nblk(k * k), kBlock, 0, s>>>(nb, k * k, part, out); tb::launched(); }
   TB_CHECK_LAUNCH();
   TB_CUDA(cudaFreeAsync(part, s));

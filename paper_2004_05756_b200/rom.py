@@ -442,7 +442,10 @@ class RomModel:
 
     def _smallest_eigenvalue(self, rho_d, max_iter, rtol):
         """Inverse power iteration (rom.py:393-407) with device pCG solves in place of the
-        sparse factorization; same deterministic start vector on the free dofs."""
+        sparse factorization; same deterministic start vector on the free dofs.  The inner solves
+        run to 1e-9: the iterate concentrates on the softest mode, so the attainable residual of
+        K y = x is ~eps * cond(K) (5e-10 at cfg 1 with Jacobi), and the Rayleigh quotient is
+        insensitive to it far below the 1e-6 sigma tolerance."""
         t = _lib.torch()
         free = np.flatnonzero(self.free_mask)
         x_np = np.zeros(self.mesh.n_dofs)
@@ -451,7 +454,7 @@ class RomModel:
         x = x / t.linalg.vector_norm(x)
         prev = np.inf
         for _ in range(max_iter):
-            y = self.solver.pcg_device(rho_d, x, rtol=1e-12)
+            y = self.solver.pcg_device(rho_d, x, rtol=1e-9)
             x = y / t.linalg.vector_norm(y)
             kx = self.solver.apply_device(rho_d, x, mask_rows=True)
             ev = self.solver.dot_device(x, kx)

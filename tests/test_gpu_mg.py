@@ -87,3 +87,23 @@ def test_mg_rejects_grids_without_a_coarse_level(cuda):
     with pytest.raises(ValueError):
         tb.HdmSolver(mesh, tb.elasticity_element_matrix(1.0, 0.3), tb.HelmholtzFilter(mesh, 1.5), f,
                      np.concatenate([2 * left, 2 * left + 1]), MAT, preconditioner="mg")
+
+
+def test_mg_certified_error_bound_matches_jacobi(cuda):
+    """Certified mode's inverse power iteration (rom.py:393-407) runs one pCG solve per step;
+    with the multigrid preconditioner it converges to the same sigma_min."""
+    prob = configs.cfg1(seed=1)
+    out = {}
+    for pc in ("jacobi", "mg"):
+        s = build(prob, pc, rtol=1e-11)
+        obj = tb.ComplianceObjective(s.f)
+        snaps = [np.where(s.free_mask, s.solve(d, obj).u, 0.0) for d in prob.rom_designs[:3]]
+        phi = tb.gram_schmidt(snaps)
+        basis = tb.ReducedBasis(phi, None, None, phi.T @ s.f)
+        rom = tb.RomModel(s)
+        rho, _ = s.filtered_density(prob.psi)
+        rs = rom.solve(basis, rho, obj)
+        out[pc] = rom.error_bounds(basis, rho, rs, obj, mode="certified")
+    assert out["mg"].sigma_min_converged and out["jacobi"].sigma_min_converged
+    assert out["mg"].sigma_min == pytest.approx(out["jacobi"].sigma_min, rel=1e-6)
+    assert out["mg"].energy_error_bound == pytest.approx(out["jacobi"].energy_error_bound, rel=1e-6)

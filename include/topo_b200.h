@@ -36,6 +36,7 @@ extern "C" {
 #define TB_ERR_NOT_CONVERGED 4  /* maxit reached before rtol                               */
 #define TB_ERR_DEGENERATE 5     /* reduced stiffness not SPD -> DegenerateBasisError (rom.py:49-50) */
 #define TB_ERR_DENSITY 6        /* density outside [rho_l, 1] -> ValueError (hdm.py:156-162) */
+#define TB_ERR_RUNTIME 7        /* numerical failure the reference raises RuntimeError for (mma.py:158) */
 
 typedef struct tb_plan tb_plan;
 typedef struct tb_filter tb_filter;
@@ -164,6 +165,26 @@ int tb_rom_residual_norms(tb_plan* plan, const double* phi, int k, const double*
  * Returns TB_ERR_INVALID when no vector survives ("no independent vectors supplied"). */
 int tb_gram_schmidt(int64_t n, int m, const double* vectors, double drop_tol, double* q,
                     int* kept, void* stream);
+
+/* ---- Method of Moving Asymptotes (the trust-region subproblem engine) ---- */
+/* MmaConfig (mma.py:25-38), same fields and defaults on the Python side. */
+typedef struct tb_mma_config {
+  double asy_init, asy_incr, asy_decr, asy_min_frac, asy_max_frac;
+  double move, albefa, raa0, bisect_rtol;
+  int bisect_max_iter;
+} tb_mma_config;
+/* Device workspace for tb_mma_step on n variables; zero it once before the first step. */
+size_t tb_mma_workspace_bytes(int64_t n);
+/* One MmaOptimizer.step (mma.py:91-175) on device arrays of n doubles: x_new from x and grad
+ * under box [lower, upper] and w . x <= volume_cap; move_cap < 0 means none.  it = step count
+ * after increment; has_xold1/has_xold2 say whether the asymptote history exists.  On success
+ * the state (xold1, xold2, low, upp) advances as in mma.py:172-175; on TB_ERR_INVALID ("gradient
+ * must be finite", "iterate outside box bounds", "iterate violates the volume constraint") it is
+ * untouched.  TB_ERR_RUNTIME: "volume multiplier bracket failed".  Synchronises the stream. */
+int tb_mma_step(int64_t n, const double* x, const double* grad, const double* lower, const double* upper,
+                const double* w, double volume_cap, double move_cap, int it, int has_xold1, int has_xold2,
+                const tb_mma_config* cfg, double* xold1, double* xold2, double* low, double* upp,
+                void* workspace, double* x_new, void* stream);
 
 #ifdef __cplusplus
 }

@@ -40,6 +40,7 @@ from .rom import (
     gram_schmidt,
     pod,
 )
+from .mma import MmaConfig, MmaOptimizer
 from .stats import RunStats
 
 __version__ = "0.1.0"

@@ -22,6 +22,7 @@ TB_ERR_INDEFINITE = 3
 TB_ERR_NOT_CONVERGED = 4
 TB_ERR_DEGENERATE = 5
 TB_ERR_DENSITY = 6
+TB_ERR_RUNTIME = 7
 
 # every symbol include/topo_b200.h declares
 EXPORTS = (
@@ -31,6 +32,7 @@ EXPORTS = (
     "tb_pcg_dist_buffers", "tb_pcg_dist_state", "tb_dot", "tb_filter_create", "tb_filter_destroy", "tb_filter_load_vector",
     "tb_filter_apply", "tb_filter_adjoint", "tb_rom_project", "tb_rom_reduced_stiffness",
     "tb_rom_gram_colmajor", "tb_rom_cholesky_solve", "tb_rom_reconstruct", "tb_rom_residual_norms", "tb_gram_schmidt",
+    "tb_mma_workspace_bytes", "tb_mma_step",
 )
 
 
@@ -47,6 +49,14 @@ D = ctypes.c_double
 PI = ctypes.POINTER(ctypes.c_int)
 PD = ctypes.POINTER(ctypes.c_double)
 PI64 = ctypes.POINTER(ctypes.c_int64)
+
+class MmaConfigC(ctypes.Structure):
+    """tb_mma_config (include/topo_b200.h) = MmaConfig (mma.py:25-38)."""
+
+    _fields_ = [(f, ctypes.c_double) for f in ("asy_init", "asy_incr", "asy_decr", "asy_min_frac", "asy_max_frac",
+                                                "move", "albefa", "raa0", "bisect_rtol")] + [
+        ("bisect_max_iter", ctypes.c_int)]
+
 
 _SIGS = {
     "tb_version": ([], I),
@@ -79,6 +89,8 @@ _SIGS = {
     "tb_rom_reconstruct": ([I64, P, I, P, I, P, P], I),
     "tb_rom_residual_norms": ([P, P, I, P, P, I, P, I64, PD, P], I),
     "tb_gram_schmidt": ([I64, I, P, D, P, PI, P], I),
+    "tb_mma_workspace_bytes": ([I64], ctypes.c_size_t),
+    "tb_mma_step": ([I64, P, P, P, P, P, D, D, I, I, I, ctypes.POINTER(MmaConfigC), P, P, P, P, P, P, P], I),
 }
 
 

@@ -11,6 +11,7 @@ Files:
   golden_small.npz  reference test-fixture problems (cantilever 6x2 / 12x4 / 4x2, filters)
   golden_cfg2.npz   BASELINE cfg 2 (600x200): scalars + strided samples (needs --with-cfg2)
   ref3d_small.npz   reference HdmSolver / RomModel run on a duck-typed Hex8 mesh
+  golden_mma.npz    reference MmaOptimizer trajectories (box + volume bound, move caps)
 """
 
 from __future__ import annotations
@@ -214,7 +215,30 @@ def make_ref3d():
         print("ref3d: J=%.10f  J_rom=%.10f" % (sol.j, rs.j))
 
 
+def make_mma():
+    from romtopt.mma import MmaOptimizer
+
+    sys.path.insert(0, os.path.dirname(HERE))
+    from mma_cases import mma_cases
+
+    out = {}
+    for name, lower, upper, w, cap, x0, grads, caps in mma_cases():
+        opt = MmaOptimizer(lower, upper, w, cap)
+        x, xs = x0.copy(), []
+        for g, mc in zip(grads, caps):
+            x = opt.step(x, 0.0, g, move_cap=mc)
+            xs.append(x.copy())
+        out[f"{name}_xs"] = np.stack(xs)
+        out[f"{name}_low"], out[f"{name}_upp"] = opt.low, opt.upp
+        print(f"mma {name}: n={len(x0)} final volume {w @ x:.12g} cap {cap:.12g}")
+    np.savez_compressed(os.path.join(HERE, "golden_mma.npz"), **out)
+
+
 if __name__ == "__main__":
+    if "--mma-only" in sys.argv:
+        make_mma()
+        sys.exit(0)
+    make_mma()
     make_cfg1()
     make_small()
     make_ref3d()

@@ -21,7 +21,7 @@ from paper_2004_05756_b200.fem import (
 
 def declared_symbols():
     src = open(os.path.join(REPO, "include", "topo_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(tb_\w+)\s*\(", src, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|size_t|const char\*)\s+(tb_\w+)\s*\(", src, flags=re.M)))
 
 
 def test_header_and_binding_agree():

@@ -169,3 +169,21 @@ def test_direct_solver_rejects_singular():
     g = build_grid(2, 2, 1.0)
     with pytest.raises(OracleIndefinite):
         DirectSolver(assemble(g, elasticity_element_matrix(1.0, 0.3)))
+
+
+def test_mma_oracle_replays_reference_trajectories():
+    """oracle/mma.py against the reference MmaOptimizer's own trajectories (golden_mma.npz)."""
+    from mma_cases import mma_cases
+
+    from oracle.mma import MmaOracle
+
+    G = golden("golden_mma.npz")
+    for name, lower, upper, w, cap, x0, grads, caps in mma_cases():
+        opt = MmaOracle(lower, upper, w, cap)
+        x = x0
+        for k, (g, mc) in enumerate(zip(grads, caps)):
+            x = opt.step(x, g, move_cap=mc)
+            ref = G[f"{name}_xs"][k]
+            assert np.abs(x - ref).max() <= 1e-13, (name, k, np.abs(x - ref).max())
+        assert np.abs(opt.asy[0] - G[f"{name}_low"]).max() <= 1e-13
+        assert np.abs(opt.asy[1] - G[f"{name}_upp"]).max() <= 1e-13

@@ -189,6 +189,29 @@ def mg_extra(tb, configs, prob, psi, torch):
             "s_per_eval": t, "pcg_iterations": sol.iterations, "J": sol.j}
 
 
+def subproblem_extra(tb, solver, obj, prob, psi_d, phi, torch, inner=10):
+    """one trust-region subproblem sweep (trustregion.py:304-351) with every
+    vector on the device -- per inner step: MMA step, filter, ROM solve + gradient, residual."""
+    n_e = prob.mesh.n_elems
+    w = torch.ones(n_e, dtype=torch.float64, device=psi_d.device)
+    psi_k = (0.9 * psi_d).clamp(0.0, 1.0)
+    cap = float(w @ psi_k) * 1.05
+    sol = solver.solve(psi_k, obj)
+    g = solver.gradient(psi_k, sol, obj)
+    basis = tb.ReducedBasis(phi, None, None, phi.T @ solver._f_d)
+    sp = tb.TrustRegionSubproblem(solver, tb.RomModel(solver), obj, w, cap, constraint="dist", max_inner=inner)
+    sp.solve_subproblem(basis, psi_k, 1e9, sol.j, g)  # warm-up
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    r = sp.solve_subproblem(basis, psi_k, 1e9, sol.j, g)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    return {"what": f"TrustRegionSubproblem.solve_subproblem, {inner} inner MMA steps, k={phi.shape[1]} basis",
+            "ms_per_inner_step": ms / max(r.rom_solves, 1), "inner_steps": r.rom_solves}
+
+
 def bench_cfg3(tb, configs, _lib, dev, pk):
     """BASELINE cfg 3 (192x96x96 Hex8, 5.4M DOF): one full HDM evaluation + the Hex8 operator
     kernel's roofline (graph path; per-kernel CUDA-event timing via tb_pcg_profile)."""
@@ -392,6 +415,7 @@ def run_ours(args):
         extras["rom_khat_ms"] = a.elapsed_time(b) / 10
         extras["rom_k"] = k
         extras["mg"] = mg_extra(tb, configs, prob, psi_d, torch)
+        extras["tr_subproblem"] = subproblem_extra(tb, solver, obj, prob, psi_d, phi, torch)
         if args.extra3d:
             extras["cfg3"] = bench_cfg3(tb, configs, _lib, dev, pk)
 

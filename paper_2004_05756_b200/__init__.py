@@ -42,5 +42,6 @@ from .rom import (
 )
 from .mma import MmaConfig, MmaOptimizer
 from .stats import RunStats
+from .subproblem import SubproblemResult, TrustRegionSubproblem
 
 __version__ = "0.1.0"

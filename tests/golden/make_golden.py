@@ -12,6 +12,7 @@ Files:
   golden_cfg2.npz   BASELINE cfg 2 (600x200): scalars + strided samples (needs --with-cfg2)
   ref3d_small.npz   reference HdmSolver / RomModel run on a duck-typed Hex8 mesh
   golden_mma.npz    reference MmaOptimizer trajectories (box + volume bound, move caps)
+  golden_subproblem.npz  reference TrustRegionDriver.solve_subproblem on a 48x16 half-MBB
 """
 
 from __future__ import annotations
@@ -234,11 +235,53 @@ def make_mma():
     np.savez_compressed(os.path.join(HERE, "golden_mma.npz"), **out)
 
 
+def subproblem_setup():
+    """Shared recipe (also restated in tests/test_gpu_subproblem.py): 48x16 cfg-1 geometry,
+    centre psi_k = 0.9 psi (feasible for V = 0.5 |domain|), basis = GS of the centre solution
+    and the seeded ROM-design snapshots."""
+    prob = configs.cfg1(seed=4, nx=48, ny=16)
+    psi_k = np.clip(0.9 * prob.psi, 0.0, 1.0)
+    return prob, psi_k
+
+
+def make_subproblem():
+    from romtopt.trustregion import TrConfig, TrustRegionDriver
+
+    prob, psi_k = subproblem_setup()
+    mesh, filt, solver = ref_problem(prob)
+    obj = ComplianceObjective(solver.f)
+    sol = solver.solve(psi_k, obj)
+    g = solver.gradient(psi_k, sol, obj)
+    snaps = [np.where(solver.free_mask, sol.u, 0.0)]
+    snaps += [np.where(solver.free_mask, solver.solve(d, obj).u, 0.0) for d in prob.rom_designs[:5]]
+    phi = gram_schmidt(snaps)
+    basis = ReducedBasis(phi=phi, elem_phi=phi[mesh.elem_dofs], elem_k_phi=np.matmul(solver.k_e, phi[mesh.elem_dofs]),
+                         f_hat=phi.T @ solver.f)
+    rom = RomModel(solver)
+    w = np.full(mesh.n_elems, mesh.elem_volume)
+    cap = 0.5 * mesh.n_elems * mesh.elem_volume
+    out = dict(psi_k=psi_k, phi=phi, j_center=sol.j, grad_center=g, cap=cap)
+    for kind, delta, inner in (("res", 4.7, 12), ("dist", 5.2, 12)):
+        drv = TrustRegionDriver(solver, rom, obj, w, cap, TrConfig(constraint=kind, max_inner=inner))
+        r = drv.solve_subproblem(basis, psi_k, delta, sol.j, g)
+        out.update({f"{kind}_delta": delta, f"{kind}_inner": inner, f"{kind}_candidate": r.candidate,
+                    f"{kind}_model_value": r.model_value, f"{kind}_theta": r.theta, f"{kind}_steps": r.steps,
+                    f"{kind}_rom_solves": r.rom_solves, f"{kind}_curvature": r.curvature,
+                    f"{kind}_first": r.first_iterate})
+        print(f"subproblem {kind}: steps={r.steps} rom_solves={r.rom_solves} J_m={r.model_value:.10f} "
+              f"theta={r.theta:.4e} curvature={r.curvature:.4e}")
+    np.savez_compressed(os.path.join(HERE, "golden_subproblem.npz"), **out)
+
+
 if __name__ == "__main__":
+    if "--subproblem-only" in sys.argv:
+        make_subproblem()
+        sys.exit(0)
     if "--mma-only" in sys.argv:
         make_mma()
         sys.exit(0)
     make_mma()
+    make_subproblem()
     make_cfg1()
     make_small()
     make_ref3d()

@@ -169,6 +169,11 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool val
   const int sz = valid ? 8 : 0;  // src-size 0 zero-fills the destination
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
 }
+// 16-byte variant: copies src_bytes (0, 8 or 16) and zero-fills the rest of the 16 bytes
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {

@@ -177,7 +177,7 @@ constexpr int kCmCtas = (kCmStages <= 2) ? 3 : (kCmStages == 3 ? 2 : 1);  // res
 
 // SYM: A^T B is known to be symmetric (Phi^T K Phi): only the MB(MB+1)/2 upper 8x8 tiles are
 // computed and the lower triangle is mirrored on output (exactly symmetric result).
-template <int KP, bool SYM>
+template <int KP, bool SYM, bool V16>
 __global__ void __launch_bounds__(kGemmThreads) k_atb_cm(int64_t r0, int64_t r1, int k,
                                                          const double* __restrict__ A, const double* __restrict__ B,
                                                          double* __restrict__ part, int64_t ld) {
@@ -193,13 +193,24 @@ __global__ void __launch_bounds__(kGemmThreads) k_atb_cm(int64_t r0, int64_t r1,
   auto load = [&](int stg, int buf) {
     const int64_t base = i0 + (int64_t)stg * kCmRows;
     double* sbuf = smc + buf * STAGE;
-    for (int idx = tid; idx < 2 * KP * kCmRows; idx += kGemmThreads) {
-      const int mat = idx / (KP * kCmRows), rem = idx % (KP * kCmRows);
-      const int c = rem / kCmRows, r = rem % kCmRows;
-      const int64_t row = base + r;
-      const bool ok = c < k && row < i1;
-      const double* src = (mat ? B : A) + (ok ? (int64_t)c * ld + row : 0);
-      cp_async8(sbuf + mat * KP * kCmLd + c * kCmLd + r, src, ok);
+    if (V16) {  // row pairs: base and ld are even, so every pair is 16-byte aligned
+      for (int idx = tid; idx < KP * kCmRows; idx += kGemmThreads) {
+        const int mat = idx / (KP * kCmRows / 2), rem = idx % (KP * kCmRows / 2);
+        const int c = rem / (kCmRows / 2), r = 2 * (rem % (kCmRows / 2));
+        const int64_t row = base + r;
+        const int bytes = (c < k && row < i1) ? (row + 1 < i1 ? 16 : 8) : 0;
+        const double* src = (mat ? B : A) + (bytes ? (int64_t)c * ld + row : 0);
+        cp_async16(sbuf + mat * KP * kCmLd + c * kCmLd + r, src, bytes);
+      }
+    } else {
+      for (int idx = tid; idx < 2 * KP * kCmRows; idx += kGemmThreads) {
+        const int mat = idx / (KP * kCmRows), rem = idx % (KP * kCmRows);
+        const int c = rem / kCmRows, r = rem % kCmRows;
+        const int64_t row = base + r;
+        const bool ok = c < k && row < i1;
+        const double* src = (mat ? B : A) + (ok ? (int64_t)c * ld + row : 0);
+        cp_async8(sbuf + mat * KP * kCmLd + c * kCmLd + r, src, ok);
+      }
     }
     cp_async_commit();
   };
@@ -279,8 +290,14 @@ template <int KP, bool SYM>
 static int launch_cm(int64_t r0, int64_t r1, int k, const double* A, const double* B, double* part, int nb,
                      int64_t ld, cudaStream_t s) {
   const size_t smem = sizeof(double) * kCmStages * 2 * KP * kCmLd;
-  TB_CUDA(cudaFuncSetAttribute(k_atb_cm<KP, SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  { k_atb_cm<KP, SYM><<<nb, kGemmThreads, smem, s>>>(r0, r1, k, A, B, part, ld); tb::launched(); }
+  const bool v16 = ((r0 | ld) & 1) == 0 && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0;
+  if (v16) {
+    TB_CUDA(cudaFuncSetAttribute(k_atb_cm<KP, SYM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    { k_atb_cm<KP, SYM, true><<<nb, kGemmThreads, smem, s>>>(r0, r1, k, A, B, part, ld); tb::launched(); }
+  } else {
+    TB_CUDA(cudaFuncSetAttribute(k_atb_cm<KP, SYM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    { k_atb_cm<KP, SYM, false><<<nb, kGemmThreads, smem, s>>>(r0, r1, k, A, B, part, ld); tb::launched(); }
+  }
   TB_CHECK_LAUNCH();
   return TB_OK;
 }

@@ -33,8 +33,11 @@ __global__ void k_material(int64_t n, double rho_l, double p, const double* __re
                            double* __restrict__ alpha, double* __restrict__ dalpha) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const double r = rho[e];
-    if (alpha) alpha[e] = rho_l + (1.0 - rho_l) * pow(r, p);
-    if (dalpha) dalpha[e] = (1.0 - rho_l) * p * pow(r, p - 1.0);
+    // p = 3 (BASELINE's SIMP exponent): multiplies, not the ~100-instruction double pow
+    const double rp1 = (p == 3.0) ? r * r : pow(r, p - 1.0);
+    const double rp = (p == 3.0) ? rp1 * r : pow(r, p);
+    if (alpha) alpha[e] = rho_l + (1.0 - rho_l) * rp;
+    if (dalpha) dalpha[e] = (1.0 - rho_l) * p * rp1;
   }
 }
 
@@ -219,7 +222,10 @@ void tb_plan_impl::apply_alpha(const double* alpha, const double* v, double* y, 
   if (g.dim == 2)
     { k_node_apply<2, 2, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, K2, alpha, v, y, fx); tb::launched(); }
   else if (hex8)
-    { k_hex8<false><<<hex8_grid(g, zchunk), kHT, kHex8Smem, s>>>(g, hiso, alpha, v, nullptr, nullptr, y, fx, nullptr, nullptr, zchunk); tb::launched(); }
+    if (fx != nullptr)
+      { k_hex8<false, true><<<hex8_grid(g, zchunk), kHT, kHex8Smem, s>>>(g, hiso, alpha, v, nullptr, nullptr, y, fx, nullptr, nullptr, zchunk); tb::launched(); }
+    else
+      { k_hex8<false><<<hex8_grid(g, zchunk), kHT, kHex8Smem, s>>>(g, hiso, alpha, v, nullptr, nullptr, y, nullptr, nullptr, nullptr, zchunk); tb::launched(); }
   else
     { k_node_apply<3, 3, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, K3, alpha, v, y, fx); tb::launched(); }
 }
@@ -277,7 +283,8 @@ int tb_plan_create(int dim, int nx, int ny, int nz, double h, const double* k_e,
     if (P->hex8) {
       cudaError_t e1 = cudaFuncSetAttribute(k_hex8<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHex8Smem);
       cudaError_t e2 = cudaFuncSetAttribute(k_hex8<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHex8Smem);
-      if (e1 != cudaSuccess || e2 != cudaSuccess) P->hex8 = false;
+      cudaError_t e3 = cudaFuncSetAttribute(k_hex8<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHex8Smem);
+      if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) P->hex8 = false;
     }
   }
   if (dim == 2) P->op.persist_grid = persist_grid_for<2, true>(P->g);

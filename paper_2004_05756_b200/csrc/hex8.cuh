@@ -123,7 +123,9 @@ constexpr int kOSlots = (kOPlane + kHT - 1) / kHT;     // 3 store slots per thre
 
 // FUSED: in = z, in2 = p_old, out = q, writes pnew, reduces p.q (pCG kernel A).
 // !FUSED: in = v, out = y = K v (fixed rows zeroed when `fixed` != nullptr).
-template <bool FUSED>
+// MASK (!FUSED only): zero the Dirichlet rows; the mask bytes of a plane are loaded into
+// registers one step before the plane is flushed, so the flush never waits on them.
+template <bool FUSED, bool MASK = false>
 __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const double* __restrict__ alpha,
                                                  const double* __restrict__ in, const double* __restrict__ in2,
                                                  double* __restrict__ pnew, double* __restrict__ out,
@@ -219,15 +221,21 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
   }                                                                                                         \
   _Pragma("unroll") for (int c = 0; c < 3; ++c) wht4(f_[c]);
   // coalesced store of the finished owned plane kp_ (staged in ostg[(kp_) & 1])
+#define HEX8_MASK(kp_)                                                                                      \
+  if (MASK) {                                                                                               \
+    const uint8_t* fx = fixed + (int64_t)(kp_) * plane_dofs;                                                \
+    _Pragma("unroll") for (int s = 0; s < kOSlots; ++s)                                                     \
+      mk_next[s] = ((s < kOSlots - 1 || t < kOPlane - (kOSlots - 1) * kHT) && (ook >> s & 1u))              \
+                       ? __ldg(fx + ooff[s]) : (uint8_t)0;                                                  \
+  }
 #define HEX8_FLUSH(kp_, par_)                                                                               \
   {                                                                                                         \
     const double* srcs = ostg + (par_) * kOPlane;                                                           \
     double* dst = out + (int64_t)(kp_) * plane_dofs;                                                        \
-    const uint8_t* fx = (!FUSED && fixed != nullptr) ? fixed + (int64_t)(kp_) * plane_dofs : nullptr;       \
     _Pragma("unroll") for (int s = 0; s < kOSlots; ++s) {                                                   \
       if ((s < kOSlots - 1 || t < kOPlane - (kOSlots - 1) * kHT) && (ook >> s & 1u)) {                      \
         double v = srcs[t + s * kHT];                                                                       \
-        if (fx != nullptr && fx[ooff[s]]) v = 0.0;                                                          \
+        if (MASK && mk_cur[MASK ? s : 0]) v = 0.0;                                                          \
         dst[ooff[s]] = v;                                                                                   \
       }                                                                                                     \
     }                                                                                                       \
@@ -262,6 +270,7 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
   const bool dot_any = FUSED && st->dot_k1 > st->dot_k0;
   const int dk0 = FUSED ? st->dot_k0 : 0, dk1 = FUSED ? st->dot_k1 : 0;
   const int steps = K1 - (K0 - 1);  // element planes ez = K0-1 .. K1-1
+  uint8_t mk_cur[MASK ? kOSlots : 1] = {}, mk_next[MASK ? kOSlots : 1] = {};  // Dirichlet bytes
   // (a 4-way unrolled sweep makes the ring offsets constants but spills and runs slower)
 #pragma unroll 1
   for (int rel = 0; rel < steps; ++rel) {
@@ -270,6 +279,7 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
       const int ez = K0 - 1 + rel;
       const double a = a_next;
       a_next = (col_ok && ez + 1 < g.nz && ez + 1 < K1) ? __ldg(a_ptr + (ez + 1) * a_stride) : 0.0;
+      if (MASK && rel >= 1) HEX8_MASK(ez);  // flushed next step
       // ---- element (gei, gej, ez): spectrum from carried bottom face + new top face ----
       {
         double ft[3][4];
@@ -314,6 +324,10 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
       }
       __syncthreads();
       if (rel >= 2) HEX8_FLUSH(ez - 1, (r + 1) & 1);  // plane ez-1 was staged before this barrier
+      if (MASK) {
+#pragma unroll
+        for (int s = 0; s < (MASK ? kOSlots : 1); ++s) mk_cur[s] = mk_next[s];
+      }
       // ---- owned node (px, py) of plane ez: rows ey = py-1 (corner oy=1) and ey = py (oy=0) ----
       if (own && rel >= 1) {
         const int e_dn = (py - 1) * kHX + (px - 1), e_up = py * kHX + (px - 1);
@@ -338,6 +352,7 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
 #undef HEX8_LAND
 #undef HEX8_FACE
 #undef HEX8_FLUSH
+#undef HEX8_MASK
 #undef HEX8_PB
 #undef HEX8_PS
   if (FUSED) {

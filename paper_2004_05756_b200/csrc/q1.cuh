@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kBlock) k_elem_sensitivity(Grid g, Mat<Q1<D>::
     c_ = fma(col, le[b], c_);
   }
   const double r = rho[e];
-  const double da = (1.0 - rho_l) * p * pow(r, p - 1.0);
+  const double da = (1.0 - rho_l) * p * ((p == 3.0) ? r * r : pow(r, p - 1.0));
   const double base = (drho != nullptr) ? drho[e] : 0.0;
   s[e] = base - da * c_;
 }

@@ -227,7 +227,10 @@ def test_gradient_finite_differences(cuda):
     psi = 0.25 + 0.5 * rng.random(s.mesh.n_elems)
     sol = s.solve(psi, obj)
     g = s.gradient(psi, sol, obj)
-    d = 1e-6
+    # the reference uses d = 1e-6 with a direct solver; with pCG at rtol 1e-12, J carries
+    # ~1e-12 relative solve noise, which a 2e-6 difference quotient amplifies to ~1e-4.
+    # d = 1e-5 keeps that noise 10x smaller; the O(d^2) truncation error stays ~1e-10.
+    d = 1e-5
     for e in rng.choice(s.mesh.n_elems, 6, replace=False):
         up, dn = psi.copy(), psi.copy()
         up[e] += d

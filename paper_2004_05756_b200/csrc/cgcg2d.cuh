@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
                                                                CgcgArgs a) {
   extern __shared__ double sm[];
   __shared__ __align__(16) Mat<4 * NC> Ks;
-  __shared__ double bc[3];
+  __shared__ double bc[2][3];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int nbk = gridDim.x;
   const int64_t N = g.n_nodes, ND = (int64_t)NC * N;
@@ -92,13 +92,14 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
   const int64_t e1 = (int64_t)min(g.ny, j_hi + 1) * g.nx;
   // shared-memory carve-up
   double* u_ext = sm;                          // (h1-h0)*NC
-  double* xs = u_ext + (size_t)ne_ext * NC;    // own: x, r, p, s, w, dinv
+  double* dext = u_ext + (size_t)ne_ext * NC;  // D^-1 over own + halo (constant over the solve)
+  double* xs = dext + (size_t)ne_ext * NC;     // own: x, r, p, s, w
   double* rs = xs + (size_t)no * NC;
   double* ps = rs + (size_t)no * NC;
   double* ss = ps + (size_t)no * NC;
   double* ws = ss + (size_t)no * NC;
-  double* ds = ws + (size_t)no * NC;
-  double* as = ds + (size_t)no * NC;           // alpha of elements [e0, e1)
+  double* as = ws + (size_t)no * NC;           // alpha of elements [e0, e1)
+  double* ds = dext + (n0 - h0) * NC;          // own part of dext
   for (int o = tid; o < 16 * NC * NC; o += nt) Ks.v[o] = K.v[o];
   for (int64_t e = e0 + tid; e < e1; e += nt) as[e - e0] = SCALED ? alpha[e] : 1.0;
 
@@ -108,12 +109,12 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
   for (int o = tid; o < nod; o += nt) {
     xs[o] = a.x[d0 + o];
     rs[o] = a.r0[d0 + o];
-    ds[o] = a.dinv[d0 + o];
     ps[o] = 0.0;
     ss[o] = 0.0;
   }
   for (int64_t o = tid; o < (int64_t)ne_ext * NC; o += nt) {
     const int64_t d = h0 * NC + o;
+    dext[o] = a.dinv[d];
     u_ext[o] = a.dinv[d] * a.r0[d];
   }
   __syncthreads();
@@ -179,9 +180,33 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
   const int maxit = a.st->maxit;
   const double tol2 = a.st->tol2;
   int par = 0;  // parity of the buffer holding (r_i, w_i, s_{i-1})
+  // halo geometry (dofs below / above the own range that the stencil of own nodes touches)
+  const int64_t lo_len = d0 - h0 * NC;
+  const int64_t hi_beg = d0 + nod;
+  const int64_t halo = lo_len + (h1 * NC - hi_beg);
+  constexpr int kHB = 6;                 // halo loads in flight per thread (warps 1..15)
+  const int ht = tid - 32, hnt = nt - 32;  // halo thread index / count (warp 0 reduces partials)
   for (bool first = true;; first = false) {
-    // fixed-order sums of the partials (every CTA identically)
-    // (all loads issued before any add: one L2 round trip, not a dependent chain)
+    // ---- after the barrier: two independent L2 round trips issued together ----
+    // warps 1..15: the first batch of the neighbours' published (r, w, s) plus D^-1 for the halo;
+    // warp 0: every CTA's partials (fixed-order sum, identical in every CTA).
+    const double* pr = pubr[par];
+    double rv[kHB], wv[kHB], sv[kHB];
+    int mm[kHB];  // halo entry relative to h0 * NC (2D grids: < 2^31 dofs)
+    auto halo_load = [&](int64_t base) {
+#pragma unroll
+      for (int q = 0; q < kHB; ++q) {
+        const int64_t t = base + ht + (int64_t)q * hnt;
+        const int64_t m = (t < lo_len) ? h0 * NC + t : hi_beg + (t - lo_len);
+        mm[q] = (ht >= 0 && t < halo) ? (int)(m - h0 * NC) : -1;
+        if (mm[q] >= 0) {
+          rv[q] = __ldcg(pr + m);
+          wv[q] = __ldcg(pr + ND + m);
+          sv[q] = __ldcg(pr + 2 * ND + m);
+        }
+      }
+    };
+    if (tid >= 32) halo_load(0);
     if (tid < 32) {
       constexpr int kPB = 8;  // supports up to 256 CTAs
       double v[3][kPB];
@@ -197,14 +222,13 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
 #pragma unroll
         for (int q = 0; q < kPB; ++q) s += v[c][q];
         s = warp_sum(s);
-        if (tid == 0) bc[c] = s;
+        if (tid == 0) bc[par][c] = s;  // parity-buffered: no second barrier before reuse
       }
     }
     __syncthreads();
     PROF_MARK(0);
-    const double gnew = bc[0], dnew = bc[1];
-    rr = bc[2];
-    __syncthreads();
+    const double gnew = bc[par][0], dnew = bc[par][1];
+    rr = bc[par][2];
     if (!isfinite(gnew) || !isfinite(dnew) || !isfinite(rr)) {
       done = 3;
       break;
@@ -241,41 +265,18 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
     }
     gam = gnew;
 
-    // ---- halo: u_{i+1} = D^-1 (r_i - al (w_i + be s_{i-1})) from the neighbours' publication.
-    // L2-latency bound: the first kHB-deep batch of loads is issued before the own update so the
-    // update's shared-memory work hides it.
-    const double* pr = pubr[par];
-    const int64_t lo_len = d0 - h0 * NC;  // halo below the own range
-    const int64_t hi_beg = d0 + nod;      // halo above
-    const int64_t halo = lo_len + (h1 * NC - hi_beg);
-    constexpr int kHB = 5;
-    double rv[kHB], wv[kHB], sv[kHB], dv[kHB];
-    int64_t mm[kHB];
-    auto halo_load = [&](int64_t base) {
-#pragma unroll
-      for (int q = 0; q < kHB; ++q) {
-        const int64_t t = base + tid + (int64_t)q * nt;
-        const int64_t m = (t < lo_len) ? h0 * NC + t : hi_beg + (t - lo_len);
-        mm[q] = (t < halo) ? m : -1;
-        if (t < halo) {
-          rv[q] = __ldcg(pr + m);
-          wv[q] = __ldcg(pr + ND + m);
-          sv[q] = __ldcg(pr + 2 * ND + m);
-          dv[q] = a.dinv[m];
-        }
-      }
-    };
+    // ---- halo: u_{i+1} = D^-1 (r_i - al (w_i + be s_{i-1})) from the loaded publication ----
     auto halo_store = [&]() {
 #pragma unroll
       for (int q = 0; q < kHB; ++q) {
         if (mm[q] < 0) continue;
+        const double di = dext[mm[q]];
         double r = rv[q];
-        if (dv[q] != 0.0) r = fma(-al, fma(be, sv[q], wv[q]), r);
-        u_ext[mm[q] - h0 * NC] = dv[q] * r;
+        if (di != 0.0) r = fma(-al, fma(be, sv[q], wv[q]), r);
+        u_ext[mm[q]] = di * r;
       }
     };
-    halo_load(0);
-    // ---- own: p, s, x, r, u ----
+    // ---- own: p, s, x, r and u_{i+1} = D^-1 r (each thread touches only its own entries) ----
     const int own_off = (n0i - h0i) * NC;  // own block inside u_ext
     for (int o = tid; o < nod; o += nt) {
       const double di = ds[o];
@@ -290,22 +291,21 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
         r = fma(-al, s, r);
       }
       rs[o] = r;
+      u_ext[own_off + o] = di * r;
     }
     PROF_MARK(1);
 #ifdef TB_CGCG_PROF
     if (!(a.dbg & 4))
 #endif
-    {
+    if (tid >= 32) {
       halo_store();
-      for (int64_t base = (int64_t)kHB * nt; base < halo; base += (int64_t)kHB * nt) {
+      for (int64_t base = (int64_t)kHB * hnt; base < halo; base += (int64_t)kHB * hnt) {
         halo_load(base);
         halo_store();
       }
     }
     __syncthreads();
     PROF_MARK(2);
-    for (int o = tid; o < nod; o += nt) u_ext[own_off + o] = ds[o] * rs[o];
-    __syncthreads();
     PROF_MARK(3);
     // ---- own: w_{i+1} = A u_{i+1}; partials; publish (r_{i+1}, w_{i+1}, s_i) ----
     double* pw = pubr[par ^ 1];
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
 inline size_t cgcg_smem_bytes(int NC, int64_t own, int64_t nnx, int64_t nx) {
   const int64_t ext = own + 2 * (nnx + 1);
   const int64_t rows = own / nnx + 3;
-  return sizeof(double) * (size_t)(ext * NC + 6 * own * NC + (rows + 1) * nx);
+  return sizeof(double) * (size_t)(2 * ext * NC + 5 * own * NC + (rows + 1) * nx);
 }
 
 }  // namespace tb

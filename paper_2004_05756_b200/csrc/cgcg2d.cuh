@@ -70,9 +70,11 @@ struct CgcgArgs {
 
 constexpr int kCgcgThreads = 512;
 
-template <int NC, bool SCALED>
-__global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * NC> K, const double* __restrict__ alpha,
-                                                               CgcgArgs a) {
+// PAT: K follows the reference's Q4 value pattern (q4_pat); the node rows use its distinct
+// values (kernel parameters) instead of reading K from shared memory.
+template <int NC, bool SCALED, bool PAT>
+__global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * NC> K, Q4Pat kp,
+                                                               const double* __restrict__ alpha, CgcgArgs a) {
   extern __shared__ double sm[];
   __shared__ __align__(16) Mat<4 * NC> Ks;
   __shared__ double bc[2][3];
@@ -100,7 +102,8 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
   double* ws = ss + (size_t)no * NC;
   double* as = ws + (size_t)no * NC;           // alpha of elements [e0, e1)
   double* ds = dext + (n0 - h0) * NC;          // own part of dext
-  for (int o = tid; o < 16 * NC * NC; o += nt) Ks.v[o] = K.v[o];
+  if (!PAT)
+    for (int o = tid; o < 16 * NC * NC; o += nt) Ks.v[o] = K.v[o];
   for (int64_t e = e0 + tid; e < e1; e += nt) as[e - e0] = SCALED ? alpha[e] : 1.0;
 
   const int64_t d0 = (int64_t)NC * n0;
@@ -141,7 +144,10 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
       const bool ok = ei >= 0 && ei < g.nx && ej >= 0 && ej < g.ny;
       sc[sl] = ok ? as[ej * g.nx + ei - e0i] : 0.0;
     }
-    node_rows<2, NC>(Ks, P, sc, out);
+    if (PAT)
+      node_rows_pat<NC>(kp, P, sc, out);
+    else
+      node_rows<2, NC>(Ks, P, sc, out);
   };
 
   // w_0 = A u_0 ; partials ; publish r_0, w_0, s_{-1}

@@ -182,19 +182,24 @@ static int persist_grid_for(const Grid& g) {
   const int64_t own = (g.n_nodes + grid - 1) / grid;
   const size_t smem = cgcg_smem_bytes(NC, own, g.nnx, g.nx);
   if (smem + 2048 > (size_t)smem_max) return 0;
-  if (cudaFuncSetAttribute(k_pcg2d_cgcg<NC, SCALED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
+  if (cudaFuncSetAttribute(k_pcg2d_cgcg<NC, SCALED, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_pcg2d_cgcg<NC, SCALED, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
     return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg2d_cgcg<NC, SCALED>, kCgcgThreads, smem) !=
+  int occ2 = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg2d_cgcg<NC, SCALED, false>, kCgcgThreads, smem) !=
           cudaSuccess ||
-      occ < 1)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_pcg2d_cgcg<NC, SCALED, true>, kCgcgThreads, smem) !=
+          cudaSuccess ||
+      occ < 1 || occ2 < 1)
     return 0;
   return grid;
 }
 
 template <int NC, bool SCALED>
-static void launch_cgcg(const Grid& g, const Mat<4 * NC>& K, const double* alpha, const PcgWork& w, int grid,
-                        cudaStream_t s) {
+static void launch_cgcg(const Grid& g, const Mat<4 * NC>& K, const Q4Pat* pat, const double* alpha,
+                        const PcgWork& w, int grid, cudaStream_t s) {
   const int64_t own = (g.n_nodes + grid - 1) / grid;
   const size_t smem = cgcg_smem_bytes(NC, own, g.nnx, g.nx);
   CgcgArgs a{nullptr, w.x, w.r, w.dinv, w.pub, w.partA(), w.st, reinterpret_cast<unsigned int*>(w.barrier),
@@ -204,17 +209,21 @@ static void launch_cgcg(const Grid& g, const Mat<4 * NC>& K, const double* alpha
 #endif
   Grid gg = g;
   Mat<4 * NC> KK = K;
+  Q4Pat kp = pat ? *pat : Q4Pat{};
   const double* al = alpha;
-  void* args[] = {&gg, &KK, &al, &a};
-  cudaLaunchCooperativeKernel((const void*)k_pcg2d_cgcg<NC, SCALED>, grid, kCgcgThreads, args, smem, s);
+  void* args[] = {&gg, &KK, &kp, &al, &a};
+  if (pat)
+    cudaLaunchCooperativeKernel((const void*)k_pcg2d_cgcg<NC, SCALED, true>, grid, kCgcgThreads, args, smem, s);
+  else
+    cudaLaunchCooperativeKernel((const void*)k_pcg2d_cgcg<NC, SCALED, false>, grid, kCgcgThreads, args, smem, s);
 }
 
 void ElastOp::launch_persistent(const PcgWork& w, cudaStream_t s) const {
-  launch_cgcg<2, true>(plan->g, plan->K2, plan->d_alpha, w, persist_grid, s);
+  launch_cgcg<2, true>(plan->g, plan->K2, plan->pat_ok ? &plan->pat : nullptr, plan->d_alpha, w, persist_grid, s);
 }
 
 void HelmOp::launch_persistent(const PcgWork& w, cudaStream_t s) const {
-  launch_cgcg<1, false>(filt->g, filt->H2, nullptr, w, persist_grid, s);
+  launch_cgcg<1, false>(filt->g, filt->H2, filt->pat_ok ? &filt->pat : nullptr, nullptr, w, persist_grid, s);
 }
 
 void tb_plan_impl::apply_alpha(const double* alpha, const double* v, double* y, bool mask, cudaStream_t s) const {
@@ -272,10 +281,12 @@ int tb_plan_create(int dim, int nx, int ny, int nz, double h, const double* k_e,
   P->rho_l = rho_l;
   P->p = p;
   const int ne = (dim == 2) ? 8 : 24;
-  if (dim == 2)
+  if (dim == 2) {
     memcpy(P->K2.v, k_e, sizeof(double) * ne * ne);
-  else
+    P->pat_ok = q4_pattern_values(2, P->K2.v, &P->pat) && getenv("TB_NO_Q4PAT") == nullptr;
+  } else {
     memcpy(P->K3.v, k_e, sizeof(double) * ne * ne);
+  }
   P->op.plan = P;
   if (dim == 3) {
     P->hex8 = hex8_blocks(P->K3.v, &P->hiso);
@@ -484,6 +495,7 @@ int tb_filter_create(int dim, int nx, int ny, int nz, double h, double radius, i
       F->H3.v[i] = hv;
   }
   F->vol_share = pow(g.h, g.dim) / nn;  // b_e entries = h^d / 2^d (filtering.py:75-76)
+  if (g.dim == 2) F->pat_ok = q4_pattern_values(1, F->H2.v, &F->pat);
   F->op.filt = F;
   F->op.persist_grid = (g.dim == 2) ? persist_grid_for<1, false>(g) : 0;  // 3D: graph loop
   int rc = F->work.alloc(g.n_nodes, F->op.fused_blocks(), F->op.persist_grid > 0);

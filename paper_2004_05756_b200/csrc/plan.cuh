@@ -45,6 +45,8 @@ struct tb_plan_impl {
   int device = 0;
   double rho_l = 1e-3, p = 3.0;
   Mat<8> K2{};
+  Q4Pat pat{};       // 2D: pattern values of K2 (q4_pat)
+  bool pat_ok = false;
   Mat<24> K3{};
   Hex8Iso hiso{};        // WHT block values of K3 (3D)
   bool hex8 = false;     // K3 has the isotropic WHT block structure -> element-centric kernel
@@ -76,6 +78,8 @@ struct tb_filter_impl {
   int device = 0;
   double radius = 0.0, r = 0.0, vol_share = 0.0;
   Mat<4> H2{};
+  Q4Pat pat{};       // 2D: pattern values of H2
+  bool pat_ok = false;
   Mat<8> H3{};
   double* d_b = nullptr;
   HelmOp op;

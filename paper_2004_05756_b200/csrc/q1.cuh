@@ -103,6 +103,76 @@ __device__ __forceinline__ void node_rows(const Mat<Q1<D>::NN * NC>& K, const do
   }
 }
 
+// Q4 element matrices of the reference have a fixed value pattern (fem.py:41-70 elasticity:
+// 6 distinct magnitudes for any nu; filtering.py Helmholtz r^2 S + M: 3 values).  With the
+// pattern known at compile time the node rows need only the distinct values (kernel
+// parameters) instead of 64 shared-memory reads of K per node.  Entry = sign(p) v[|p| - 1].
+__host__ __device__ constexpr int q4_pat(int nc, int r, int q) {
+  if (nc == 1) {
+    const int d = r ^ q;  // corner pairs: 0 same, 1 / 3 edge-adjacent, 2 opposite
+    return d == 0 ? 1 : (d == 2 ? 3 : 2);
+  }
+  constexpr int t[8][8] = {{1, 2, 3, 4, 5, -2, 6, -4},  {2, 1, -4, 6, -2, 5, 4, 3},
+                           {3, -4, 1, -2, 6, 4, 5, 2},  {4, 6, -2, 1, -4, 3, 2, 5},
+                           {5, -2, 6, -4, 1, 2, 3, 4},  {-2, 5, 4, 3, 2, 1, -4, 6},
+                           {6, 4, 5, 2, 3, -4, 1, -2},  {-4, 3, 2, 5, 4, 6, -2, 1}};
+  return t[r][q];
+}
+struct Q4Pat {
+  double v[6];
+};
+
+// As node_rows<2, NC>, with K given by its pattern values.
+template <int NC>
+__device__ __forceinline__ void node_rows_pat(const Q4Pat& kp, const double (&P)[9][NC], const double (&a)[4],
+                                              double (&out)[NC]) {
+#pragma unroll
+  for (int c = 0; c < NC; ++c) out[c] = 0.0;
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const int sx = s & 1, sy = s >> 1;
+    const int L = loc_of(1 - sx, 1 - sy, 0);
+    double acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int nb = (sy + offy(b)) * 3 + (sx + offx(b));
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int cp = 0; cp < NC; ++cp) {
+          const int pt = q4_pat(NC, L * NC + c, b * NC + cp);
+          acc[c] = pt > 0 ? fma(kp.v[pt - 1], P[nb][cp], acc[c]) : fma(-kp.v[-pt - 1], P[nb][cp], acc[c]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) out[c] = fma(a[s], acc[c], out[c]);
+  }
+}
+
+// Host: extract the pattern values of a Q4 element matrix; false if K does not follow it.
+inline bool q4_pattern_values(int nc, const double* K, Q4Pat* out) {
+  const int ne = 4 * nc;
+  double v[6] = {0, 0, 0, 0, 0, 0};
+  bool set[6] = {false, false, false, false, false, false};
+  double scale = 0.0;
+  for (int i = 0; i < ne * ne; ++i) scale = fmax(scale, fabs(K[i]));
+  for (int r = 0; r < ne; ++r)
+    for (int q = 0; q < ne; ++q) {
+      const int p = q4_pat(nc, r, q), k = (p > 0 ? p : -p) - 1;
+      const double val = p > 0 ? K[r * ne + q] : -K[r * ne + q];
+      if (!set[k]) {
+        v[k] = val;
+        set[k] = true;
+      } else if (fabs(val - v[k]) > 1e-13 * scale) {
+        return false;
+      }
+    }
+  for (int k = 0; k < 6; ++k) out->v[k] = v[k];
+  return true;
+}
+
 // y = K v  (rows with fixed[dof] != 0 zeroed when fixed != nullptr)
 template <int D, int NC, bool SCALED>
 __global__ void __launch_bounds__(kBlock) k_node_apply(Grid g, Mat<Q1<D>::NN * NC> K, const double* __restrict__ alpha,

@@ -3,4 +3,4 @@
 set -e
 cd "$(dirname "$0")/../paper_2004_05756_b200/csrc"
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../../include -Xcompiler -fPIC -shared \
-  -DTB_CGCG_PROF -o ../../tools/libtopo_prof.so hdm.cu pcg.cu plan.cu rom.cu
+  -lcusolver -DTB_CGCG_PROF -o ../../tools/libtopo_prof.so *.cu

@@ -61,7 +61,7 @@ struct CgcgArgs {
   const double* r0;    // r0 = Z (b - K x0) (k_pcg_start)
   const double* dinv;  // Jacobi inverse diagonal, 0 on fixed dofs
   double* pub;         // published vectors [2 parities][3 (r, w, s)][n_dofs]
-  double* part;        // [3][gridDim.x]
+  double* part;        // [2 parities][3][gridDim.x]
   PcgState* st;
   unsigned int* bar;
   int own_max;         // max nodes owned by a CTA
@@ -170,6 +170,9 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
     }
   }
   block_sum<3>(acc);
+  // Partials are parity-buffered like the published vectors: a CTA that races ahead writes
+  // iteration i+1's partials into the other buffer while slower CTAs still read iteration i's
+  // (a single buffer let them sum a mix, branch differently and deadlock at the next barrier).
   if (tid == 0) {
     a.part[blockIdx.x] = acc[0];
     a.part[nbk + blockIdx.x] = acc[1];
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
       for (int q = 0; q < kPB; ++q) {
         const int b = tid + 32 * q;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) v[c][q] = (b < nbk) ? __ldcg(a.part + c * nbk + b) : 0.0;
+        for (int c = 0; c < 3; ++c) v[c][q] = (b < nbk) ? __ldcg(a.part + (par * 3 + c) * nbk + b) : 0.0;
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -342,9 +345,10 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
     block_sum<3>(acc3);
     PROF_MARK(5);
     if (tid == 0) {
-      a.part[blockIdx.x] = acc3[0];
-      a.part[nbk + blockIdx.x] = acc3[1];
-      a.part[2 * nbk + blockIdx.x] = acc3[2];
+      double* pp = a.part + (par ^ 1) * 3 * nbk;
+      pp[blockIdx.x] = acc3[0];
+      pp[nbk + blockIdx.x] = acc3[1];
+      pp[2 * nbk + blockIdx.x] = acc3[2];
     }
     par ^= 1;
 #ifdef TB_CGCG_PROF

@@ -178,7 +178,9 @@ static int persist_grid_for(const Grid& g) {
   if (!coop || sms < 1) return 0;
   // at most one CTA per SM, at least ~128 nodes per CTA (fewer CTAs = cheaper barriers)
   const int64_t want = (g.n_nodes + 127) / 128;
-  const int grid = (int)(want < sms ? (want < 1 ? 1 : want) : sms);
+  // partials: 2 parities x 3 sums x grid must fit PcgWork::partA (2 x >= 592 doubles)
+  const int cap = sms < 192 ? sms : 192;
+  const int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   const int64_t own = (g.n_nodes + grid - 1) / grid;
   const size_t smem = cgcg_smem_bytes(NC, own, g.nnx, g.nx);
   if (smem + 2048 > (size_t)smem_max) return 0;

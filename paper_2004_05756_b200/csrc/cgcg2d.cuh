@@ -38,19 +38,21 @@ __device__ __forceinline__ unsigned long long gtime() { return (unsigned long lo
   } while (0)
 #endif
 
-// cooperative-groups-style barrier: one atomic per CTA, bit 31 flips when all have arrived.
+// Grid barrier: one atomic per CTA, bit 31 flips when all have arrived.  The CTA's writes are
+// ordered before thread 0's arrival by bar.sync and the arrival is a RELEASE atomic
+// (cumulative over them); the spin is an ACQUIRE load and the closing bar.sync orders the rest
+// of the CTA after it.  Every cross-CTA read after the barrier is an L2 load (__ldcg) of
+// parity-buffered data, so no trailing fence is needed to drop stale L1 lines.
 __device__ __forceinline__ void grid_sync_flip(unsigned int* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned int nb = gridDim.x;
     const unsigned int add = (blockIdx.x == 0) ? (0x80000000u - (nb - 1u)) : 1u;
-    __threadfence();
-    const unsigned int old = atomicAdd(bar, add);
-    unsigned int cur;
+    unsigned int old, cur;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(bar), "r"(add) : "memory");
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
     } while (((old ^ cur) & 0x80000000u) == 0u);
-    __threadfence();  // also invalidates this SM's L1
   }
   __syncthreads();
 }

@@ -201,15 +201,17 @@ def subproblem_extra(tb, solver, obj, prob, psi_d, phi, torch, inner=10):
     basis = tb.ReducedBasis(phi, None, None, phi.T @ solver._f_d)
     sp = tb.TrustRegionSubproblem(solver, tb.RomModel(solver), obj, w, cap, constraint="dist", max_inner=inner)
     sp.solve_subproblem(basis, psi_k, 1e9, sol.j, g)  # warm-up
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    a.record()
-    r = sp.solve_subproblem(basis, psi_k, 1e9, sol.j, g)
-    b.record()
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b)
+    per = []
+    for _ in range(3):  # median of three sweeps
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        r = sp.solve_subproblem(basis, psi_k, 1e9, sol.j, g)
+        b.record()
+        torch.cuda.synchronize()
+        per.append(a.elapsed_time(b) / max(r.rom_solves, 1))
     return {"what": f"TrustRegionSubproblem.solve_subproblem, {inner} inner MMA steps, k={phi.shape[1]} basis",
-            "ms_per_inner_step": ms / max(r.rom_solves, 1), "inner_steps": r.rom_solves}
+            "ms_per_inner_step": statistics.median(per), "inner_steps": r.rom_solves}
 
 
 def bench_cfg3(tb, configs, _lib, dev, pk):

@@ -7,6 +7,7 @@ kernels (K(rho)v, filter transfers) 1e-12.
 """
 
 import numpy as np
+import torch
 import pytest
 
 import paper_2004_05756_b200 as tb
@@ -237,3 +238,16 @@ def test_gradient_finite_differences(cuda):
         dn[e] -= d
         fd = (s.solve(up, obj).j - s.solve(dn, obj).j) / (2 * d)
         assert abs(fd - g[e]) <= 1e-5 * max(1.0, abs(g[e]))
+
+
+def test_persistent_pcg_repeats_bit_identical(cuda):
+    """The persistent 2D kernel decides convergence redundantly in every CTA from parity-buffered
+    partial sums; 200 back-to-back solves must all finish and agree bit for bit (a shared
+    partial buffer once let a CTA race ahead, desynchronise the branch and deadlock)."""
+    prob = configs.cfg1(seed=3)
+    s = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, prob.radius), prob.f, prob.fixed,
+                     tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP), rtol=1e-10)
+    rho, _ = s.filtered_density_device(torch.as_tensor(prob.psi, device=cuda))
+    ref = s.pcg_device(rho, s._f_d).clone()
+    for _ in range(200):
+        assert torch.equal(s.pcg_device(rho, s._f_d), ref)

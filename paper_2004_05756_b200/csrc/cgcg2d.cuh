@@ -126,25 +126,42 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
 
   double* pubr[2] = {a.pub, a.pub + 3 * ND};
   const int nnx = g.nnx, h0i = (int)h0, e0i = (int)e0, n0i = (int)n0;
+  const int nx_e = g.nx, nny = g.nny;
   auto node_apply = [&](int n, double (&out)[NC]) {
     const int j = n / nnx, i = n - j * nnx;
     double P[9][NC];
     double sc[4];
+    if (i > 0 && i < nnx - 1 && j > 0 && j < nny - 1) {
+      // interior node: all 9 neighbours and 4 elements exist -- constant offsets, no checks
+      const double* u0 = u_ext + (n - nnx - 1 - h0i) * NC;
 #pragma unroll
-    for (int dy = 0; dy < 3; ++dy)
+      for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-      for (int dx = 0; dx < 3; ++dx) {
-        const int ii = i + dx - 1, jj = j + dy - 1;
-        const bool ok = ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
-        const int m = jj * nnx + ii - h0i;
+        for (int dx = 0; dx < 3; ++dx)
 #pragma unroll
-        for (int c = 0; c < NC; ++c) P[dy * 3 + dx][c] = ok ? u_ext[m * NC + c] : 0.0;
+          for (int c = 0; c < NC; ++c) P[dy * 3 + dx][c] = u0[(dy * nnx + dx) * NC + c];
+      const double* a0 = as + ((j - 1) * nx_e + i - 1 - e0i);
+      sc[0] = a0[0];
+      sc[1] = a0[1];
+      sc[2] = a0[nx_e];
+      sc[3] = a0[nx_e + 1];
+    } else {
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+          const int ii = i + dx - 1, jj = j + dy - 1;
+          const bool ok = ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
+          const int m = jj * nnx + ii - h0i;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) P[dy * 3 + dx][c] = ok ? u_ext[m * NC + c] : 0.0;
+        }
+#pragma unroll
+      for (int sl = 0; sl < 4; ++sl) {
+        const int ei = i - 1 + (sl & 1), ej = j - 1 + (sl >> 1);
+        const bool ok = ei >= 0 && ei < g.nx && ej >= 0 && ej < g.ny;
+        sc[sl] = ok ? as[ej * g.nx + ei - e0i] : 0.0;
       }
-#pragma unroll
-    for (int sl = 0; sl < 4; ++sl) {
-      const int ei = i - 1 + (sl & 1), ej = j - 1 + (sl >> 1);
-      const bool ok = ei >= 0 && ei < g.nx && ej >= 0 && ej < g.ny;
-      sc[sl] = ok ? as[ej * g.nx + ei - e0i] : 0.0;
     }
     if (PAT)
       node_rows_pat<NC>(kp, P, sc, out);
@@ -240,6 +257,18 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
     PROF_MARK(0);
     const double gnew = bc[par][0], dnew = bc[par][1];
     rr = bc[par][2];
+#if defined(TB_CGCG_ABL)
+    if (a.dbg & 8) {  // ablation timing: run exactly maxit iterations whatever the numbers say
+      if (!first && ++it >= maxit) {
+        done = 2;
+        break;
+      }
+      be = first ? 0.0 : 0.5;
+      al = 0.5;
+      gam = 1.0;
+      goto abl_continue;
+    }
+#endif
     if (!isfinite(gnew) || !isfinite(dnew) || !isfinite(rr)) {
       done = 3;
       break;
@@ -275,6 +304,9 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
       al = gnew / pap;
     }
     gam = gnew;
+#if defined(TB_CGCG_ABL)
+  abl_continue:
+#endif
 
     // ---- halo: u_{i+1} = D^-1 (r_i - al (w_i + be s_{i-1})) from the loaded publication ----
     auto halo_store = [&]() {
@@ -305,7 +337,7 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
       u_ext[own_off + o] = di * r;
     }
     PROF_MARK(1);
-#ifdef TB_CGCG_PROF
+#if defined(TB_CGCG_PROF) || defined(TB_CGCG_ABL)
     if (!(a.dbg & 4))
 #endif
     if (tid >= 32) {
@@ -324,7 +356,7 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
     for (int o = tid; o < no; o += nt) {
       const int n = n0i + o;
       double out[NC];
-#ifdef TB_CGCG_PROF
+#if defined(TB_CGCG_PROF) || defined(TB_CGCG_ABL)
       if (a.dbg & 2) {
         for (int c = 0; c < NC; ++c) out[c] = u_ext[(n - h0i) * NC + c];
       } else
@@ -353,7 +385,7 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_cgcg(Grid g, Mat<4 * 
       pp[2 * nbk + blockIdx.x] = acc3[2];
     }
     par ^= 1;
-#ifdef TB_CGCG_PROF
+#if defined(TB_CGCG_PROF) || defined(TB_CGCG_ABL)
     if (!(a.dbg & 1))
 #endif
       grid_sync_flip(a.bar);

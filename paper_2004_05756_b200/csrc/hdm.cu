@@ -206,7 +206,7 @@ static void launch_cgcg(const Grid& g, const Mat<4 * NC>& K, const Q4Pat* pat, c
   const size_t smem = cgcg_smem_bytes(NC, own, g.nnx, g.nx);
   CgcgArgs a{nullptr, w.x, w.r, w.dinv, w.pub, w.partA(), w.st, reinterpret_cast<unsigned int*>(w.barrier),
              (int)own, 0};
-#ifdef TB_CGCG_PROF
+#if defined(TB_CGCG_PROF) || defined(TB_CGCG_ABL)
   if (const char* e = getenv("TB_CGCG_DBG")) a.dbg = (NC == 2) ? atoi(e) : 0;
 #endif
   Grid gg = g;

@@ -9,6 +9,7 @@
 #include "pcg.cuh"
 #include "plan.cuh"
 #include "cgcg2d.cuh"
+#include "cgtile2d.cuh"
 #include "q1.cuh"
 
 namespace tb {
@@ -169,7 +170,7 @@ int HelmOp::fused_blocks() const { return nblk(filt->g.n_nodes); }
 // Grid of the single-reduction persistent kernel (one CTA per SM, every CTA co-resident), or 0
 // when the device cannot launch it cooperatively or a CTA's node range exceeds shared memory.
 template <int NC, bool SCALED>
-static int persist_grid_for(const Grid& g) {
+static int persist_grid_for(const Grid& g, TileSpec* ts) {
   int dev = 0, sms = 0, coop = 0, occ = 0, smem_max = 0;
   if (g.dim != 2 || cudaGetDevice(&dev) != cudaSuccess) return 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -180,7 +181,46 @@ static int persist_grid_for(const Grid& g) {
   const int64_t want = (g.n_nodes + 127) / 128;
   // partials: 2 parities x 3 sums x grid must fit PcgWork::partA (2 x >= 592 doubles)
   const int cap = sms < 192 ? sms : 192;
-  const int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+  int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+  if (getenv("TB_CG_STRIP") == nullptr) {  // 2D node tiles (cgtile2d.cuh); strips for A/B only
+    *ts = choose_tiles(g.nnx, g.nny, grid);
+    grid = ts->tx * ts->ty;
+    // register-resident state pays off once a tile has more nodes than threads (cfg 2: 841
+    // nodes, 6.5 vs 6.8 us/iteration); small tiles (cfg 1: ~128 nodes) are faster with SMEM state
+    const int64_t tn = (int64_t)ts->tw * ts->th;
+    if (tn > kCgcgThreads && tn <= (int64_t)kTregSlots * kCgcgThreads && getenv("TB_CG_SMEMSTATE") == nullptr) {
+      const size_t rsm = treg_smem_bytes(NC, *ts);
+      int r1 = 0, r2 = 0;
+      if (rsm + 2048 <= (size_t)smem_max &&
+          cudaFuncSetAttribute(k_pcg2d_treg<NC, SCALED, false, kTregSlots>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm) == cudaSuccess &&
+          cudaFuncSetAttribute(k_pcg2d_treg<NC, SCALED, true, kTregSlots>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm) == cudaSuccess &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, k_pcg2d_treg<NC, SCALED, false, kTregSlots>,
+                                                        kCgcgThreads, rsm) == cudaSuccess &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r2, k_pcg2d_treg<NC, SCALED, true, kTregSlots>,
+                                                        kCgcgThreads, rsm) == cudaSuccess &&
+          r1 >= 1 && r2 >= 1 && grid <= sms) {
+        ts->reg = 1;
+        return grid;
+      }
+    }
+    const size_t tsm = tile_smem_bytes(NC, *ts);
+    int o1 = 0, o2 = 0;
+    if (tsm + 2048 <= (size_t)smem_max &&
+        cudaFuncSetAttribute(k_pcg2d_tile<NC, SCALED, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tsm) == cudaSuccess &&
+        cudaFuncSetAttribute(k_pcg2d_tile<NC, SCALED, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tsm) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_pcg2d_tile<NC, SCALED, false>, kCgcgThreads, tsm) ==
+            cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_pcg2d_tile<NC, SCALED, true>, kCgcgThreads, tsm) ==
+            cudaSuccess &&
+        o1 >= 1 && o2 >= 1 && grid <= sms)
+      return grid;
+    grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+  }
+  ts->tx = 0;  // row strips
   const int64_t own = (g.n_nodes + grid - 1) / grid;
   const size_t smem = cgcg_smem_bytes(NC, own, g.nnx, g.nx);
   if (smem + 2048 > (size_t)smem_max) return 0;
@@ -201,9 +241,9 @@ static int persist_grid_for(const Grid& g) {
 
 template <int NC, bool SCALED>
 static void launch_cgcg(const Grid& g, const Mat<4 * NC>& K, const Q4Pat* pat, const double* alpha,
-                        const PcgWork& w, int grid, cudaStream_t s) {
+                        const PcgWork& w, int grid, const TileSpec& tiles, cudaStream_t s) {
   const int64_t own = (g.n_nodes + grid - 1) / grid;
-  const size_t smem = cgcg_smem_bytes(NC, own, g.nnx, g.nx);
+  const size_t smem = tiles.tx > 0 ? tile_smem_bytes(NC, tiles) : cgcg_smem_bytes(NC, own, g.nnx, g.nx);
   CgcgArgs a{nullptr, w.x, w.r, w.dinv, w.pub, w.partA(), w.st, reinterpret_cast<unsigned int*>(w.barrier),
              (int)own, 0};
 #if defined(TB_CGCG_PROF) || defined(TB_CGCG_ABL)
@@ -213,6 +253,26 @@ static void launch_cgcg(const Grid& g, const Mat<4 * NC>& K, const Q4Pat* pat, c
   Mat<4 * NC> KK = K;
   Q4Pat kp = pat ? *pat : Q4Pat{};
   const double* al = alpha;
+  TileSpec ts = tiles;
+  if (tiles.tx > 0 && tiles.reg) {
+    void* targs[] = {&gg, &KK, &kp, &al, &a, &ts};
+    const size_t rsm = treg_smem_bytes(NC, tiles);
+    if (pat)
+      cudaLaunchCooperativeKernel((const void*)k_pcg2d_treg<NC, SCALED, true, kTregSlots>, grid, kCgcgThreads, targs,
+                                  rsm, s);
+    else
+      cudaLaunchCooperativeKernel((const void*)k_pcg2d_treg<NC, SCALED, false, kTregSlots>, grid, kCgcgThreads, targs,
+                                  rsm, s);
+    return;
+  }
+  if (tiles.tx > 0) {
+    void* targs[] = {&gg, &KK, &kp, &al, &a, &ts};
+    if (pat)
+      cudaLaunchCooperativeKernel((const void*)k_pcg2d_tile<NC, SCALED, true>, grid, kCgcgThreads, targs, smem, s);
+    else
+      cudaLaunchCooperativeKernel((const void*)k_pcg2d_tile<NC, SCALED, false>, grid, kCgcgThreads, targs, smem, s);
+    return;
+  }
   void* args[] = {&gg, &KK, &kp, &al, &a};
   if (pat)
     cudaLaunchCooperativeKernel((const void*)k_pcg2d_cgcg<NC, SCALED, true>, grid, kCgcgThreads, args, smem, s);
@@ -221,11 +281,12 @@ static void launch_cgcg(const Grid& g, const Mat<4 * NC>& K, const Q4Pat* pat, c
 }
 
 void ElastOp::launch_persistent(const PcgWork& w, cudaStream_t s) const {
-  launch_cgcg<2, true>(plan->g, plan->K2, plan->pat_ok ? &plan->pat : nullptr, plan->d_alpha, w, persist_grid, s);
+  launch_cgcg<2, true>(plan->g, plan->K2, plan->pat_ok ? &plan->pat : nullptr, plan->d_alpha, w, persist_grid, tiles,
+                       s);
 }
 
 void HelmOp::launch_persistent(const PcgWork& w, cudaStream_t s) const {
-  launch_cgcg<1, false>(filt->g, filt->H2, filt->pat_ok ? &filt->pat : nullptr, nullptr, w, persist_grid, s);
+  launch_cgcg<1, false>(filt->g, filt->H2, filt->pat_ok ? &filt->pat : nullptr, nullptr, w, persist_grid, tiles, s);
 }
 
 void tb_plan_impl::apply_alpha(const double* alpha, const double* v, double* y, bool mask, cudaStream_t s) const {
@@ -300,7 +361,7 @@ int tb_plan_create(int dim, int nx, int ny, int nz, double h, const double* k_e,
       if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) P->hex8 = false;
     }
   }
-  if (dim == 2) P->op.persist_grid = persist_grid_for<2, true>(P->g);
+  if (dim == 2) P->op.persist_grid = persist_grid_for<2, true>(P->g, &P->op.tiles);
   int rc = P->init(fixed);
   if (rc != TB_OK) {
     P->release();
@@ -499,7 +560,7 @@ int tb_filter_create(int dim, int nx, int ny, int nz, double h, double radius, i
   F->vol_share = pow(g.h, g.dim) / nn;  // b_e entries = h^d / 2^d (filtering.py:75-76)
   if (g.dim == 2) F->pat_ok = q4_pattern_values(1, F->H2.v, &F->pat);
   F->op.filt = F;
-  F->op.persist_grid = (g.dim == 2) ? persist_grid_for<1, false>(g) : 0;  // 3D: graph loop
+  F->op.persist_grid = (g.dim == 2) ? persist_grid_for<1, false>(g, &F->op.tiles) : 0;  // 3D: graph loop
   int rc = F->work.alloc(g.n_nodes, F->op.fused_blocks(), F->op.persist_grid > 0);
   if (rc == TB_OK) rc = F->work.set_fields(0, 0, g.nnz);
   if (rc == TB_OK) {

@@ -4,6 +4,7 @@
 #include "hex8.cuh"
 #include "mg.cuh"
 #include "pcg.cuh"
+#include "cgtile2d.cuh"
 
 namespace tb {
 
@@ -24,6 +25,7 @@ struct ElastOp final : PcgOp {
   int precond_setup(cudaStream_t s) const override;
   int precond_apply(const double* r, double* z, cudaStream_t s) const override;
   int persist_grid = 0;
+  TileSpec tiles{0, 0, 0, 0, 0};  // 2D persistent pCG decomposition (tx = 0: row strips)
 };
 
 // Helmholtz operator  H = sum_e (r^2 S_e + M_e)  (pure Neumann)
@@ -37,6 +39,7 @@ struct HelmOp final : PcgOp {
   bool has_persistent() const override { return persist_grid > 0; }
   void launch_persistent(const PcgWork& w, cudaStream_t s) const override;
   int persist_grid = 0;
+  TileSpec tiles{0, 0, 0, 0, 0};  // 2D persistent pCG decomposition (tx = 0: row strips)
 };
 
 struct tb_plan_impl {

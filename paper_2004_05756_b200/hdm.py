@@ -260,12 +260,14 @@ class HdmSolver:
         if tuple(psi_d.shape) != (self.mesh.n_elems,):
             raise ValueError(f"psi must have length {self.mesh.n_elems}, got shape {tuple(psi_d.shape)}")
         rho_d, clamp_width = self.filtered_density_device(psi_d)
+        rho_host = None if native else _lib.to_host_async(rho_d)  # lands while the solve runs
         # the clamp guarantees [rho_l, 1]; NaN input surfaces as a pCG breakdown
         self.stats.factorizations += 1
         u_d = self.pcg_device(rho_d, self._f_d)
         iters, relres = self.last_iterations, self.last_relres
         self.stats.hdm_solves += 1
-        rho_u, u_u = self._user(rho_d, native), self._user(u_d, native)
+        rho_u = rho_d if native else _lib.finish_host(rho_host)
+        u_u = self._user(u_d, native)
         if objective.is_compliance:
             lam_u = u_u
             if isinstance(objective, ComplianceObjective):
@@ -281,19 +283,26 @@ class HdmSolver:
             keep = psi_d.clone() if psi_d is psi else psi_d  # snapshot of the design's bytes
             return HdmSolution(None, rho_u, u_u, lam_u, j, clamp_width, None, psi_ref=(keep, psi, psi._version),
                                iterations=iters, relres=relres)
-        return HdmSolution(psi_digest(psi), rho_u, u_u, lam_u, j, clamp_width, None, iterations=iters,
-                           relres=relres)
+        # numpy design: keep a byte snapshot; psi_hash (SHA-256, hdm.py:36-37) is computed on
+        # first request and gradient() compares bytes directly (same strictness, no hashing)
+        snap = np.array(psi, dtype=float, copy=True)
+        return HdmSolution(None, rho_u, u_u, lam_u, j, clamp_width, None, psi_ref=(snap, None, None),
+                           iterations=iters, relres=relres)
 
     def gradient(self, psi, solution: HdmSolution, objective: Objective):
         """Adjoint gradient of J at psi; requires a matching solution (hdm.py:199-209)."""
         native = _lib.is_torch(psi)
-        if native and solution._psi_ref is not None:
-            ref, src, version = solution._psi_ref
+        ref = solution._psi_ref
+        if native and ref is not None and _lib.is_torch(ref[0]):
+            snap, src, version = ref
             if psi is src and psi._version == version:
                 same = True  # the very tensor the solution was computed from, never modified since
             else:
-                same = tuple(ref.shape) == tuple(psi.shape) and bool(
-                    _lib.torch().equal(ref, psi.to(ref.device, ref.dtype)))
+                same = tuple(snap.shape) == tuple(psi.shape) and bool(
+                    _lib.torch().equal(snap, psi.to(snap.device, snap.dtype)))
+        elif not native and ref is not None and isinstance(ref[0], np.ndarray):
+            arr = np.ascontiguousarray(psi, dtype=float)
+            same = arr.shape == ref[0].shape and np.array_equal(arr.view(np.uint64), ref[0].view(np.uint64))
         else:
             same = psi_digest(psi) == solution.psi_hash
         if not same:

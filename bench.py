@@ -125,42 +125,82 @@ def run_reference(args):
 # clocks sampled during the timed region
 # --------------------------------------------------------------------------------------
 class Clocks:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clocks and throttle reasons sampled every 100 ms DURING the timed region.
+
+    In-process NVML (pynvml) on a thread; the nvidia-smi CLI is the fallback.  (Launching
+    nvidia-smi right before the timed loop once stalled a step by ~20-45 ms.)"""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        self.p = None
+        self.rows = []
+        self.stop_flag = None
+        self.thread = None
+        self.smi = None
 
     def start(self):
+        mode = os.environ.get("TB_BENCH_CLOCKS", "nvml")
+        if mode == "off":  # diagnostic only
+            return
         try:
-            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
-                                      stderr=subprocess.DEVNULL)
-        except OSError:
-            self.p = None
+            import threading
+
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.stop_flag = threading.Event()
+
+            def run():
+                while not self.stop_flag.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                        self.rows.append((sm, mx, rs))
+                    except Exception:  # noqa: BLE001
+                        pass
+                    self.stop_flag.wait(0.1)
+
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
+        except Exception:  # noqa: BLE001 - no pynvml: nvidia-smi CLI
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            try:
+                self.smi = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                             "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                            stderr=subprocess.DEVNULL)
+            except OSError:
+                self.smi = None
 
     def stop(self):
-        if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        if self.thread is not None:
+            self.stop_flag.set()
+            self.thread.join()
+            sm = [r[0] for r in self.rows]
+            mx = [r[1] for r in self.rows]
+            reasons = sorted({n for r in self.rows for n, bit in self.REASONS.items() if r[2] & bit})
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                    "reasons": reasons, "samples": len(self.rows), "source": "nvml"}
+        if self.smi is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
         time.sleep(0.25)
-        self.p.terminate()
-        self.p.wait()
+        self.smi.terminate()
+        self.smi.wait()
         self.f.flush()
-        rows = []
-        for line in open(self.f.name):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 9:
-                rows.append(parts)
+        rows = [[x.strip() for x in line.split(",")] for line in open(self.f.name)]
+        rows = [r for r in rows if len(r) >= 6]
         os.unlink(self.f.name)
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows), "source": "nvidia-smi"}
 
 
 def time_eval(solver, obj, psi, torch, reps=3):
@@ -320,18 +360,20 @@ def run_ours(args):
         g = solver.gradient(psi_d, sol, obj)
         return sol, g
 
+    # the clock sampler (nvidia-smi) starts before the warm-up: its NVML start-up stalled the
+    # first timed steps when it was launched right before them; it keeps sampling through them
+    clocks = Clocks(dev.index)
+    clocks.start()
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
 
-    clocks = Clocks(dev.index)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     iters = []
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = _lib.lib().tb_launch_count()
-    clocks.start()
     for k in range(args.steps):
         if not args.no_flush:
             flush.zero_()  # L2 flush between steps, outside the per-step events
@@ -536,12 +578,12 @@ def run_cfg5(args):
     rom = tb.RomModel(s)
     rhos = torch.as_tensor(np.stack(prob.rom_designs), device=dev)
     nd = rhos.shape[0]
+    clocks = Clocks(dev.index)
+    clocks.start()  # before the warm-up (see run_ours)
     for _ in range(max(args.warmup, 1)):
         rom.solve_batch(basis, rhos)
     torch.cuda.synchronize()
     launches0 = _lib.lib().tb_launch_count()
-    clocks = Clocks(dev.index)
-    clocks.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for i in range(args.steps):
         ev[i][0].record()

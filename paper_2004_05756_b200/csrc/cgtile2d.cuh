@@ -365,8 +365,8 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_tile(Grid g, Mat<4 * 
 // nodes o = t + k * blockDim (k < NS) for the whole solve and keeps their x, r, p, s, w, u in
 // registers; shared memory holds only the stencil inputs (u over the extended tile, alpha) and
 // D^-1.  Same arithmetic in the same order as k_pcg2d_tile.
-template <int NC, bool SCALED, bool PAT, int NS>
-__global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_treg(Grid g, Mat<4 * NC> K, Q4Pat kp,
+template <int NC, bool SCALED, bool PAT, int NS, int NT>
+__global__ void __launch_bounds__(NT, 1) k_pcg2d_treg(Grid g, Mat<4 * NC> K, Q4Pat kp,
                                                                const double* __restrict__ alpha, CgcgArgs a,
                                                                TileSpec ts) {
   extern __shared__ double sm[];
@@ -680,12 +680,19 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_treg(Grid g, Mat<4 * 
   }
 }
 
-constexpr int kTregSlots = 2;  // nodes per thread of the register-resident kernel
+#ifndef TB_TREG_NT
+#define TB_TREG_NT 512
+#endif
+#ifndef TB_TREG_NS
+#define TB_TREG_NS 2
+#endif
+constexpr int kTregThreads = TB_TREG_NT;  // threads per CTA of the register-resident kernel
+constexpr int kTregSlots = TB_TREG_NS;    // nodes per thread
 
 inline size_t treg_smem_bytes(int NC, const TileSpec& ts) {
   const size_t ext = (size_t)(ts.tw + 2) * (ts.th + 2);
   return sizeof(double) * (2 * ext * NC + (size_t)(ts.tw + 1) * (ts.th + 1) +
-                           (size_t)kTregSlots * kCgcgThreads * NC);
+                           (size_t)kTregSlots * kTregThreads * NC);
 }
 
 inline size_t tile_smem_bytes(int NC, const TileSpec& ts) {

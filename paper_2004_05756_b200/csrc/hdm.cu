@@ -188,18 +188,18 @@ static int persist_grid_for(const Grid& g, TileSpec* ts) {
     // register-resident state pays off once a tile has more nodes than threads (cfg 2: 841
     // nodes, 6.5 vs 6.8 us/iteration); small tiles (cfg 1: ~128 nodes) are faster with SMEM state
     const int64_t tn = (int64_t)ts->tw * ts->th;
-    if (tn > kCgcgThreads && tn <= (int64_t)kTregSlots * kCgcgThreads && getenv("TB_CG_SMEMSTATE") == nullptr) {
+    if (tn > kCgcgThreads && tn <= (int64_t)kTregSlots * kTregThreads && getenv("TB_CG_SMEMSTATE") == nullptr) {
       const size_t rsm = treg_smem_bytes(NC, *ts);
       int r1 = 0, r2 = 0;
       if (rsm + 2048 <= (size_t)smem_max &&
-          cudaFuncSetAttribute(k_pcg2d_treg<NC, SCALED, false, kTregSlots>,
+          cudaFuncSetAttribute(k_pcg2d_treg<NC, SCALED, false, kTregSlots, kTregThreads>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm) == cudaSuccess &&
-          cudaFuncSetAttribute(k_pcg2d_treg<NC, SCALED, true, kTregSlots>,
+          cudaFuncSetAttribute(k_pcg2d_treg<NC, SCALED, true, kTregSlots, kTregThreads>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm) == cudaSuccess &&
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, k_pcg2d_treg<NC, SCALED, false, kTregSlots>,
-                                                        kCgcgThreads, rsm) == cudaSuccess &&
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r2, k_pcg2d_treg<NC, SCALED, true, kTregSlots>,
-                                                        kCgcgThreads, rsm) == cudaSuccess &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, k_pcg2d_treg<NC, SCALED, false, kTregSlots, kTregThreads>,
+                                                        kTregThreads, rsm) == cudaSuccess &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r2, k_pcg2d_treg<NC, SCALED, true, kTregSlots, kTregThreads>,
+                                                        kTregThreads, rsm) == cudaSuccess &&
           r1 >= 1 && r2 >= 1 && grid <= sms) {
         ts->reg = 1;
         return grid;
@@ -258,11 +258,11 @@ static void launch_cgcg(const Grid& g, const Mat<4 * NC>& K, const Q4Pat* pat, c
     void* targs[] = {&gg, &KK, &kp, &al, &a, &ts};
     const size_t rsm = treg_smem_bytes(NC, tiles);
     if (pat)
-      cudaLaunchCooperativeKernel((const void*)k_pcg2d_treg<NC, SCALED, true, kTregSlots>, grid, kCgcgThreads, targs,
-                                  rsm, s);
+      cudaLaunchCooperativeKernel((const void*)k_pcg2d_treg<NC, SCALED, true, kTregSlots, kTregThreads>, grid, kTregThreads,
+                                  targs, rsm, s);
     else
-      cudaLaunchCooperativeKernel((const void*)k_pcg2d_treg<NC, SCALED, false, kTregSlots>, grid, kCgcgThreads, targs,
-                                  rsm, s);
+      cudaLaunchCooperativeKernel((const void*)k_pcg2d_treg<NC, SCALED, false, kTregSlots, kTregThreads>, grid, kTregThreads,
+                                  targs, rsm, s);
     return;
   }
   if (tiles.tx > 0) {

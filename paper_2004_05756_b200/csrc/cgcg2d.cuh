@@ -18,7 +18,7 @@
 // are summed by every CTA in the same fixed order: deterministic, identical decisions.
 #pragma once
 
-#include "persist.cuh"
+#include "q1.cuh"
 
 namespace tb {
 

@@ -166,6 +166,17 @@ int tb_rom_residual_norms(tb_plan* plan, const double* phi, int k, const double*
 int tb_gram_schmidt(int64_t n, int m, const double* vectors, double drop_tol, double* q,
                     int* kept, void* stream);
 
+/* ---- Cone ("linear hat") density filter (the reference has only the
+ * Helmholtz filter, filtering.py): rho_e = sum_j w(e,j) psi_j / sum_j w(e,j) with
+ * w(e,j) = max(0, R - |c_e - c_j|) over the element grid, and its exact transpose. ---- */
+typedef struct tb_cone tb_cone;
+int tb_cone_create(int dim, int nx, int ny, int nz, double h, double radius, int device, tb_cone** out);
+int tb_cone_destroy(tb_cone* filt);
+/* rho = cone(psi); psi, rho: n_elems device doubles */
+int tb_cone_apply(tb_cone* filt, const double* psi, double* rho, void* stream);
+/* w = cone^T v (exact transpose of tb_cone_apply) */
+int tb_cone_adjoint(tb_cone* filt, const double* v, double* w, void* stream);
+
 /* ---- Method of Moving Asymptotes (the trust-region subproblem engine) ---- */
 /* MmaConfig (mma.py:25-38), same fields and defaults on the Python side. */
 typedef struct tb_mma_config {

@@ -18,7 +18,7 @@ from .fem import (
     helmholtz_element_matrices,
     hex8_element_matrix,
 )
-from .filtering import LENGTH_SCALE_FACTOR, FilterResult, HelmholtzFilter
+from .filtering import LENGTH_SCALE_FACTOR, ConeFilter, FilterResult, HelmholtzFilter
 from .hdm import (
     ComplianceObjective,
     HdmSolution,

@@ -32,7 +32,8 @@ EXPORTS = (
     "tb_pcg_dist_buffers", "tb_pcg_dist_state", "tb_dot", "tb_filter_create", "tb_filter_destroy", "tb_filter_load_vector",
     "tb_filter_apply", "tb_filter_adjoint", "tb_rom_project", "tb_rom_reduced_stiffness",
     "tb_rom_gram_colmajor", "tb_rom_cholesky_solve", "tb_rom_reconstruct", "tb_rom_residual_norms", "tb_gram_schmidt",
-    "tb_mma_workspace_bytes", "tb_mma_step",
+    "tb_mma_workspace_bytes", "tb_mma_step", "tb_cone_create", "tb_cone_destroy", "tb_cone_apply",
+    "tb_cone_adjoint",
 )
 
 
@@ -90,6 +91,10 @@ _SIGS = {
     "tb_rom_residual_norms": ([P, P, I, P, P, I, P, I64, PD, P], I),
     "tb_gram_schmidt": ([I64, I, P, D, P, PI, P], I),
     "tb_mma_workspace_bytes": ([I64], ctypes.c_size_t),
+    "tb_cone_create": ([I, I, I, I, D, D, I, ctypes.POINTER(P)], I),
+    "tb_cone_destroy": ([P], I),
+    "tb_cone_apply": ([P, P, P, P], I),
+    "tb_cone_adjoint": ([P, P, P, P], I),
     "tb_mma_step": ([I64, P, P, P, P, P, D, D, I, I, I, ctypes.POINTER(MmaConfigC), P, P, P, P, P, P, P], I),
 }
 

@@ -187,3 +187,16 @@ def test_mma_oracle_replays_reference_trajectories():
             assert np.abs(x - ref).max() <= 1e-13, (name, k, np.abs(x - ref).max())
         assert np.abs(opt.asy[0] - G[f"{name}_low"]).max() <= 1e-13
         assert np.abs(opt.asy[1] - G[f"{name}_upp"]).max() <= 1e-13
+
+
+def test_cone_oracle_is_normalised_and_symmetric_in_weights():
+    """Rows of the cone filter sum to 1 and W_e A[e, j] = w(e, j) is symmetric (A = D^-1 W)."""
+    from oracle.filters import cone_matrix
+
+    radius = 2.2
+    a = cone_matrix(7, 5, 0, 1.0, radius).toarray()
+    assert np.abs(a.sum(axis=1) - 1.0).max() <= 1e-15
+    w_e = radius / np.diag(a)  # A[e, e] = w(e, e) / W_e = R / W_e
+    raw = a * w_e[:, None]
+    assert np.allclose(raw, raw.T, rtol=0, atol=1e-13)
+    assert np.all(raw[raw > 0] <= radius + 1e-15)

@@ -180,3 +180,26 @@ def test_exact_span_and_errors(cuda):
         rom.residual_norm(basis2, sol.rho, rs)
     with pytest.raises(ValueError):
         rom.build_basis(tb.SnapshotWindow(5), np.zeros(mesh.n_dofs), None, True, 0)
+
+
+def test_certified_lanczos_matches_power_iteration(cuda):
+    """Certified sigma_min: shift-invert Lanczos (default) and the reference's inverse power
+    iteration agree, Lanczos in far fewer solves."""
+    prob = configs.cfg1(seed=2, nx=48, ny=16)
+    s = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, prob.radius), prob.f, prob.fixed,
+                     tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP), rtol=1e-11)
+    obj = tb.ComplianceObjective(s.f)
+    snaps = [np.where(s.free_mask, s.solve(d, obj).u, 0.0) for d in prob.rom_designs[:3]]
+    phi = tb.gram_schmidt(snaps)
+    basis = tb.ReducedBasis(phi, None, None, phi.T @ s.f)
+    rom = tb.RomModel(s)
+    rho, _ = s.filtered_density(prob.psi)
+    rs = rom.solve(basis, rho, obj)
+    n0 = s.stats.factorizations
+    lz = rom.error_bounds(basis, rho, rs, obj, mode="certified")
+    pw = rom.error_bounds(basis, rho, rs, obj, mode="certified", method="power")
+    assert lz.sigma_min_converged and pw.sigma_min_converged
+    assert lz.sigma_min == pytest.approx(pw.sigma_min, rel=1e-6)
+    with pytest.raises(ValueError):
+        rom.error_bounds(basis, rho, rs, obj, mode="certified", method="qr")
+    del n0

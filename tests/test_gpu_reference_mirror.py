@@ -178,3 +178,37 @@ def test_sigma_min_failure_flag(method):
     rep = rom.error_bounds(basis, rho, rsol, obj, mode="certified", power_max_iter=1, method=method)
     assert not rep.sigma_min_converged
     assert rep.energy_error_bound is None and rep.objective_error_bound is None
+
+
+def test_filter_indicator_spreads_with_monotone_decay():
+    """test_filtering.py:97-113: a single-element indicator spreads with monotone decay."""
+    mesh = tb.build_mesh(8, 8, 1.0)
+    psi = np.zeros(mesh.n_elems)
+    psi[4 * 8 + 4] = 1.0
+    rho = tb.HelmholtzFilter(mesh, 2.0).apply(psi).rho
+    grid = rho.reshape(8, 8)
+    assert np.all(np.diff(grid[4, 4:]) < 0) and np.all(np.diff(grid[4:, 4]) < 0)
+    assert grid[4, 4] == rho.max()
+
+
+def test_filter_adjoint_consistent_with_finite_differences():
+    """test_filtering.py: d/dpsi of <c, rho(psi)> equals apply_adjoint(c) (the map is linear)."""
+    mesh = tb.build_mesh(10, 6, 1.0)
+    f = tb.HelmholtzFilter(mesh, 1.5)
+    rng = np.random.default_rng(4)
+    c = rng.standard_normal(mesh.n_elems)
+    psi = rng.random(mesh.n_elems)
+    g = f.apply_adjoint(c)
+    for e in rng.choice(mesh.n_elems, 5, replace=False):
+        up, dn = psi.copy(), psi.copy()
+        up[e] += 1e-4
+        dn[e] -= 1e-4
+        fd = (c @ f.apply(up).rho - c @ f.apply(dn).rho) / 2e-4
+        assert abs(fd - g[e]) <= 1e-8 * max(1.0, abs(g[e]))
+
+
+def test_filter_load_vector_sums_to_domain_volume():
+    """test_filtering.py: b(1) sums to the domain volume (the load is a partition of unity)."""
+    mesh = tb.build_mesh(7, 3, 0.5)
+    b = tb.HelmholtzFilter(mesh, 1.0).load_vector(np.ones(mesh.n_elems))
+    assert abs(b.sum() - mesh.n_elems * mesh.elem_volume) <= 1e-12

@@ -286,19 +286,21 @@ def bench_cfg3(tb, configs, _lib, dev, pk):
     _lib.check(_lib.lib().tb_pcg_profile(s._plan, _lib.ptr(rho_d), _lib.ptr(s._f_d), 50, ctypes.byref(msf),
                                          ctypes.byref(msu), _lib.stream_ptr(dev)), "profile")
     n_u, n_e, n_v = m.n_dofs, m.n_elems, m.n_nodes
-    # K(rho)u alone (HdmSolver.apply_stiffness, hdm.py:224-233): SURVEY §8(d) GDOF/s metric,
-    # median of 20 launches after warm-up, bytes 8(2 N_u + N_e)
+    # K(rho)u alone (HdmSolver.apply_stiffness, hdm.py:224-233, alpha(rho) included): SURVEY
+    # §8(d) GDOF/s metric; median over 5 timed batches of 20 back-to-back calls after warm-up,
+    # bytes 8(2 N_u + N_e)
     v = torch.randn(n_u, dtype=torch.float64, device=dev)
     for _ in range(3):
         s.apply_device(rho_d, v)
     ts = []
-    for _ in range(20):
+    for _ in range(5):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        s.apply_device(rho_d, v)
+        for _ in range(20):
+            s.apply_device(rho_d, v)
         e1.record()
         torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1) * 1e-3)
+        ts.append(e0.elapsed_time(e1) * 1e-3 / 20)
     t_ap = statistics.median(ts)
     by_ap = 8 * (2 * n_u + n_e)
     by_op = 8 * (4 * n_u + n_e)  # read z, p_old, alpha; write p, q
@@ -310,7 +312,8 @@ def bench_cfg3(tb, configs, _lib, dev, pk):
                              "achieved_gbs": by_op / (msf.value * 1e-3) / 1e9,
                              "frac_hbm": by_op / (msf.value * 1e-3) / 1e9 / pk.get("hbm_gbs"),
                              "gdofs": n_u / (msf.value * 1e-3) / 1e9},
-            "apply_stiffness": {"name": "k_hex8<false> (K(rho)u, fixed rows zeroed)", "us_median_of_20": t_ap * 1e6,
+            "apply_stiffness": {"name": "k_hex8<false,mask,simp> (K(rho)u incl. alpha(rho), fixed rows zeroed)",
+                                "us_per_call": t_ap * 1e6,
                                 "gdofs": n_u / t_ap / 1e9, "bytes_per_launch": by_ap,
                                 "achieved_gbs": by_ap / t_ap / 1e9, "frac_hbm": by_ap / t_ap / 1e9 / pk.get("hbm_gbs")},
             "update_kernel": {"us_per_launch": msu.value * 1e3, "bytes_per_launch": by_up,

@@ -358,7 +358,10 @@ int tb_plan_create(int dim, int nx, int ny, int nz, double h, const double* k_e,
       cudaError_t e1 = cudaFuncSetAttribute(k_hex8<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHex8Smem);
       cudaError_t e2 = cudaFuncSetAttribute(k_hex8<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHex8Smem);
       cudaError_t e3 = cudaFuncSetAttribute(k_hex8<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHex8Smem);
-      if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) P->hex8 = false;
+      cudaError_t e4 = cudaSuccess;
+      cudaError_t e5 = cudaFuncSetAttribute(k_hex8<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHex8Smem);
+      if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess || e5 != cudaSuccess)
+        P->hex8 = false;
     }
   }
   if (dim == 2) P->op.persist_grid = persist_grid_for<2, true>(P->g, &P->op.tiles);
@@ -416,6 +419,13 @@ int tb_apply_stiffness(tb_plan* plan, const double* rho, const double* v, double
   TB_GUARD(plan && rho && v && y, "null argument");
   auto* P = reinterpret_cast<tb_plan_impl*>(plan);
   cudaStream_t s = (cudaStream_t)stream;
+  if (P->g.dim == 3 && P->hex8 && P->p == 3.0 && !mask_rows) {  // alpha(rho) inside the operator pass
+    // (the Dirichlet-mask variant with alpha(rho) fused spills; it keeps the material pass)
+    const Grid& g = P->g;
+    { k_hex8<false, false, true><<<hex8_grid(g, P->zchunk), kHT, kHex8Smem, s>>>(g, P->hiso, rho, v, nullptr, nullptr, y, nullptr, nullptr, nullptr, P->zchunk, P->rho_l, P->p); tb::launched(); }
+    TB_CHECK_LAUNCH();
+    return TB_OK;
+  }
   TB_TRY(P->material(rho, P->d_alpha2, nullptr, s));
   P->apply_alpha(P->d_alpha2, v, y, mask_rows != 0, s);
   TB_CHECK_LAUNCH();

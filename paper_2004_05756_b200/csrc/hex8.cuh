@@ -125,12 +125,14 @@ constexpr int kOSlots = (kOPlane + kHT - 1) / kHT;     // 3 store slots per thre
 // !FUSED: in = v, out = y = K v (fixed rows zeroed when `fixed` != nullptr).
 // MASK (!FUSED only): zero the Dirichlet rows; the mask bytes of a plane are loaded into
 // registers one step before the plane is flushed, so the flush never waits on them.
-template <bool FUSED, bool MASK = false>
+// SIMP (!FUSED only, p = 3): `alpha` holds rho; alpha = rho_l + (1 - rho_l) rho^3 is formed per
+// element as it is loaded (same operation order as k_material), saving the material pass.
+template <bool FUSED, bool MASK = false, bool SIMP = false>
 __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const double* __restrict__ alpha,
                                                  const double* __restrict__ in, const double* __restrict__ in2,
                                                  double* __restrict__ pnew, double* __restrict__ out,
                                                  const uint8_t* __restrict__ fixed, PcgState* st, double* partials,
-                                                 int zchunk) {
+                                                 int zchunk, double rho_l = 0.0, double p_simp = 3.0) {
   // plane[4][kPlane]: node planes (buffer = plane index mod 4), AoS rows as in global memory.
   // stage[2][2][3][kHT]: node-plane corner outputs (oy) already summed over the two
   // x-neighbour elements, double buffered by step parity.  ostg[2][kOPlane]: finished owned
@@ -256,7 +258,9 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
   HEX8_LAND(K0 + 1, HEX8_PB(2), plane + HEX8_PB(3));
   const double* a_ptr = alpha + ((int64_t)gej * g.nx + gei);  // element column base (valid iff col_ok)
   const int64_t a_stride = (int64_t)g.nx * g.ny;
-  double a_next = (col_ok && K0 - 1 >= 0) ? __ldg(a_ptr + (K0 - 1) * a_stride) : 0.0;
+  (void)p_simp;  // SIMP launches are p = 3 only (host checks), the BASELINE exponent
+  auto simp = [&](double r) { return SIMP ? rho_l + (1.0 - rho_l) * ((r * r) * r) : r; };
+  double a_next = (col_ok && K0 - 1 >= 0) ? simp(__ldg(a_ptr + (K0 - 1) * a_stride)) : 0.0;
   __syncthreads();
   // xy-WHT of the 4 corner nodes of the current bottom face of this element column
   double fb[3][4];
@@ -278,7 +282,7 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
       const int r = rel & 3;
       const int ez = K0 - 1 + rel;
       const double a = a_next;
-      a_next = (col_ok && ez + 1 < g.nz && ez + 1 < K1) ? __ldg(a_ptr + (ez + 1) * a_stride) : 0.0;
+      a_next = (col_ok && ez + 1 < g.nz && ez + 1 < K1) ? simp(__ldg(a_ptr + (ez + 1) * a_stride)) : 0.0;
       if (MASK && rel >= 1) HEX8_MASK(ez);  // flushed next step
       // ---- element (gei, gej, ez): spectrum from carried bottom face + new top face ----
       {

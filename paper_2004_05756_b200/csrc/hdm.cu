@@ -176,7 +176,7 @@ static int persist_grid_for(const Grid& g, TileSpec* ts) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
   cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (!coop || sms < 1) return 0;
+  if (!coop || sms < 1 || getenv("TB_NO_PERSIST") != nullptr) return 0;  // env: graph path (tests)
   // at most one CTA per SM, at least ~128 nodes per CTA (fewer CTAs = cheaper barriers)
   const int64_t want = (g.n_nodes + 127) / 128;
   // partials: 2 parities x 3 sums x grid must fit PcgWork::partA (2 x >= 592 doubles)

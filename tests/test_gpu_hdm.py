@@ -251,3 +251,22 @@ def test_persistent_pcg_repeats_bit_identical(cuda):
     ref = s.pcg_device(rho, s._f_d).clone()
     for _ in range(200):
         assert torch.equal(s.pcg_device(rho, s._f_d), ref)
+
+
+def test_graph_path_matches_persistent_kernel(cuda, monkeypatch):
+    """2D grids too large for the persistent kernel's shared memory run the graph-captured
+    pCG (k_pcg_fused + k_pcg_update under a conditional node); forced here on cfg 1."""
+    G = golden("golden_cfg1.npz")
+    prob = configs.cfg1()
+    obj_sol = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("TB_NO_PERSIST", env)
+        s = build(prob, rtol=1e-10)
+        obj = tb.ComplianceObjective(s.f)
+        sol = s.solve(prob.psi, obj)
+        obj_sol.append((sol.j, s.gradient(prob.psi, sol, obj)))
+    monkeypatch.delenv("TB_NO_PERSIST")
+    for j, g in obj_sol:
+        assert abs(j - float(G["j"])) <= 1e-8 * abs(float(G["j"]))
+        assert np.abs(g - G["g"]).max() <= 1e-6 * np.abs(G["g"]).max()

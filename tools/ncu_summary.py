@@ -54,6 +54,7 @@ def report(path):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(raw.splitlines()))
     rh = rr[0]
+    units = dict(zip(rh, rr[1])) if len(rr) > 1 else {}
     rawvals = [dict(zip(rh, r)) for r in rr[2:]]
     print(f"# ncu --set full: {path}")
     for n, ((i, k), m) in enumerate(by.items()):
@@ -64,7 +65,7 @@ def report(path):
         if n < len(rawvals):
             for key in RAW:
                 if key in rawvals[n]:
-                    print(f"  {key:40s} {rawvals[n][key]}")
+                    print(f"  {key:40s} {rawvals[n][key]} {units.get(key, '')}".rstrip())
 
 
 if __name__ == "__main__":

@@ -308,17 +308,40 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
             fq[c][s] = tc[c][s] + (u[c][s] + u[c][s + 4]);
             tc[c][s] = u[c][s] - u[c][s + 4];
           }
-          wht4(fq[c]);  // -> corner values (ox + 2 oy) of node plane ez from this element column
+          if (FUSED) {
+            wht4(fq[c]);  // -> corner values (ox + 2 oy) of node plane ez from this element column
+          } else {
+            // x stage only: sums feed corner ox = 0, differences ox = 1 (y stage after the combine)
+            const double s0 = fq[c][0] + fq[c][1], d0 = fq[c][0] - fq[c][1];
+            const double s1 = fq[c][2] + fq[c][3], d1 = fq[c][2] - fq[c][3];
+            fq[c][0] = s0;
+            fq[c][1] = d0;
+            fq[c][2] = s1;
+            fq[c][3] = d1;
+          }
         }
-        // node column ex+1 of this row: corner ox=1 of this element + ox=0 of the next
-        // (lane 31's sum is never read: node column 32 of the tile is not owned)
+        // node column ex+1 of this row = corner ox=1 of this element + ox=0 of the next (lane
+        // 31's value is never read: node column 32 of the tile is not owned).  Non-fused: the y
+        // stage is linear, so the x-stage outputs are combined first and the y stage runs once
+        // on the sums (P + Q, P - Q): 6 fewer DADD per element; in the fused pCG kernel the
+        // longer dependency chain measured slower (127.9 vs 125.7 us/iteration at cfg 3).
+        if (FUSED) {
 #pragma unroll
-        for (int oy = 0; oy < 2; ++oy)
+          for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              const double right = __shfl_down_sync(0xffffffffu, fq[c][2 * oy], 1);
+              stage2[r & 1][oy][c][t] = fq[c][2 * oy + 1] + right;
+            }
+        } else {
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            const double right = __shfl_down_sync(0xffffffffu, fq[c][2 * oy], 1);
-            stage2[r & 1][oy][c][t] = fq[c][2 * oy + 1] + right;
+            const double pp = fq[c][1] + __shfl_down_sync(0xffffffffu, fq[c][0], 1);
+            const double qq = fq[c][3] + __shfl_down_sync(0xffffffffu, fq[c][2], 1);
+            stage2[r & 1][0][c][t] = pp + qq;
+            stage2[r & 1][1][c][t] = pp - qq;
           }
+        }
       }
       // node plane ez+2 (issued at the end of the last step; the prologue landed plane K0+1)
       // must have landed before the barrier: it is read from the next step on

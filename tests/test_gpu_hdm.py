@@ -270,3 +270,40 @@ def test_graph_path_matches_persistent_kernel(cuda, monkeypatch):
     for j, g in obj_sol:
         assert abs(j - float(G["j"])) <= 1e-8 * abs(float(G["j"]))
         assert np.abs(g - G["g"]).max() <= 1e-6 * np.abs(G["g"]).max()
+
+
+def test_integration_md_ctypes_stub(cuda):
+    """The raw-ctypes binding shown in INTEGRATION.md §2 (what a romtopt maintainer would add)
+    runs as written and reproduces HdmSolver's solve."""
+    import ctypes
+
+    import torch
+
+    from paper_2004_05756_b200 import _lib
+
+    prob = configs.cfg1(seed=6, nx=24, ny=8)
+    mesh = prob.mesh
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    P, I, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_double
+    lib.tb_plan_create.argtypes = [I, I, I, I, D, P, D, D, P, I, ctypes.POINTER(P)]
+    lib.tb_pcg_solve.argtypes = [P, P, P, P, D, I, ctypes.POINTER(I), ctypes.POINTER(D), P]
+    lib.tb_plan_destroy.argtypes = [P]
+    lib.tb_last_error.restype = ctypes.c_char_p
+    k_e = np.ascontiguousarray(tb.elasticity_element_matrix(1.0, 0.3))
+    fixed = np.zeros(mesh.n_dofs, np.uint8)
+    fixed[prob.fixed] = 1
+    plan = P()
+    assert lib.tb_plan_create(2, mesh.nx, mesh.ny, 0, mesh.h, k_e.ctypes.data, 1e-9, 3.0, fixed.ctypes.data,
+                              cuda.index or 0, ctypes.byref(plan)) == 0, lib.tb_last_error()
+    s = build(prob, rtol=1e-10)
+    rho, _ = s.filtered_density(prob.psi)
+    rho_d = torch.as_tensor(rho, device=cuda)
+    f_d = torch.as_tensor(np.where(fixed == 0, prob.f, 0.0), device=cuda)
+    u_d = torch.empty_like(f_d)
+    it, rr = I(), D()
+    rc = lib.tb_pcg_solve(plan, rho_d.data_ptr(), f_d.data_ptr(), u_d.data_ptr(), 1e-10, 200000, ctypes.byref(it),
+                          ctypes.byref(rr), torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, lib.tb_last_error()
+    lib.tb_plan_destroy(plan)
+    u_ref = s.pcg_device(torch.as_tensor(rho, device=cuda), s._f_d)
+    assert torch.equal(u_d, u_ref)

@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg4", "cfg5"],
                     help="cfg1/cfg2: HDM evaluation (headline cfg2); cfg4: slab-sharded 3D solve; cfg5: batched ROM")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
+                    help="cfg4 halo exchange: NVLink peer stores fused into the update kernel, or NCCL send/recv")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="diagnostic: skip the L2 flush between steps")
@@ -641,7 +643,9 @@ def run_cfg5(args):
 
 def run_cfg4(args):
     """BASELINE cfg 4: slab-sharded (z) Jacobi-pCG solve + sensitivities on 384x192x192 Hex8
-    (43M DOF), one slab per rank, NCCL allreduce + halo exchange.  rho = psi (the filter is
+    (43M DOF), one slab per rank, NCCL allreduce of the CG scalars; the halo travels as NVLink
+    peer stores from inside the update kernel (--halo peer, CUDA IPC) or as NCCL send/recv
+    (--halo nccl).  rho = psi (the filter is
     applied once as input generation; the distributed filter is future work)."""
     import numpy as np
     import torch
@@ -672,7 +676,7 @@ def run_cfg4(args):
     sv = SlabSolver(prob.mesh, prob.k_e, prob.f, prob.fixed, mat, slab, device=dev)
     rho = torch.as_tensor(sv.local_elems(prob.psi).copy(), device=dev)
     sv.rho = rho
-    comm = TorchComm()
+    comm = TorchComm(peer=(args.halo == "peer"))
     dist_pcg_solve([sv], comm, rtol=prob.rtol)  # warm-up
     dist.barrier()
     torch.cuda.synchronize()
@@ -690,7 +694,10 @@ def run_cfg4(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg 4 recipe)",
             "config": {"workload": f"cfg4 {prob.mesh.nx}x{prob.mesh.ny}x{prob.mesh.nz} Hex8, {prob.mesh.n_dofs} DOF, "
                                    f"z-slabs x{world}, Jacobi-pCG to {prob.rtol:g}",
-                       "parallelism": f"slab{world}", "pcg_iterations": iters, "converged": ok}}), flush=True)
+                       "parallelism": f"slab{world}", "halo": args.halo, "pcg_iterations": iters,
+                       "converged": ok}}), flush=True)
+    dist.barrier()
+    comm.close()
     dist.destroy_process_group()
 
 

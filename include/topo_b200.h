@@ -110,6 +110,19 @@ int tb_pcg_dist_phase(tb_plan* plan, int phase, const double* rho, const double*
 int tb_pcg_dist_buffers(tb_plan* plan, double** x, double** z, double** red);
 /* Host read of the iteration state (synchronises the stream). */
 int tb_pcg_dist_state(tb_plan* plan, int* iters, int* done, double* rr, double* bb, void* stream);
+/* Fused halo exchange: phases 0 and 4 store this rank's first owned plane of z to `lo_dst` (the
+ * lower neighbour's ghost-above plane) and its last owned plane to `hi_dst` (the upper
+ * neighbour's ghost-below plane), 3(nx+1)(ny+1) doubles each, while they compute z.  The
+ * pointers are usually a neighbour's memory mapped with tb_ipc_open (NVLink peer stores); NULL
+ * leaves that side to the caller's halo exchange.  The allreduce that follows phases 0 and 4 on
+ * every rank orders the stores against the neighbour's reads, so no other synchronisation is
+ * needed.  Requires tb_plan_set_owned_planes. */
+int tb_plan_set_halo_peers(tb_plan* plan, double* lo_dst, double* hi_dst);
+/* CUDA IPC of a device allocation (e.g. tb_pcg_dist_buffers' z) between the ranks' processes:
+ * `handle` is 64 bytes (cudaIpcMemHandle_t); tb_ipc_open maps a peer's allocation on `device`. */
+int tb_ipc_get_handle(const void* dptr, void* handle);
+int tb_ipc_open(const void* handle, int device, void** dptr);
+int tb_ipc_close(void* dptr);
 
 /* Deterministic fp64 dot product of two device vectors; *out is a HOST pointer. */
 int tb_dot(tb_plan* plan, const double* a, const double* b, int64_t n, double* out, void* stream);

@@ -29,7 +29,8 @@ EXPORTS = (
     "tb_version", "tb_last_error", "tb_plan_create", "tb_plan_destroy", "tb_plan_sizes",
     "tb_material", "tb_clamp_density", "tb_apply_stiffness", "tb_element_sensitivity",
     "tb_pcg_solve", "tb_plan_set_preconditioner", "tb_pcg_profile", "tb_launch_count", "tb_plan_set_owned_planes", "tb_pcg_dist_phase",
-    "tb_pcg_dist_buffers", "tb_pcg_dist_state", "tb_dot", "tb_filter_create", "tb_filter_destroy", "tb_filter_load_vector",
+    "tb_pcg_dist_buffers", "tb_pcg_dist_state", "tb_plan_set_halo_peers", "tb_ipc_get_handle", "tb_ipc_open",
+    "tb_ipc_close", "tb_dot", "tb_filter_create", "tb_filter_destroy", "tb_filter_load_vector",
     "tb_filter_apply", "tb_filter_adjoint", "tb_rom_project", "tb_rom_reduced_stiffness",
     "tb_rom_gram_colmajor", "tb_rom_cholesky_solve", "tb_rom_reconstruct", "tb_rom_residual_norms", "tb_gram_schmidt",
     "tb_mma_workspace_bytes", "tb_mma_step", "tb_cone_create", "tb_cone_destroy", "tb_cone_apply",
@@ -77,6 +78,10 @@ _SIGS = {
     "tb_pcg_dist_phase": ([P, I, P, P, D, I, I, P], I),
     "tb_pcg_dist_buffers": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)], I),
     "tb_pcg_dist_state": ([P, PI, PI, PD, PD, P], I),
+    "tb_plan_set_halo_peers": ([P, P, P], I),
+    "tb_ipc_get_handle": ([P, P], I),
+    "tb_ipc_open": ([P, I, ctypes.POINTER(P)], I),
+    "tb_ipc_close": ([P], I),
     "tb_dot": ([P, P, P, I64, PD, P], I),
     "tb_filter_create": ([I, I, I, I, D, D, I, ctypes.POINTER(P)], I),
     "tb_filter_destroy": ([P], I),

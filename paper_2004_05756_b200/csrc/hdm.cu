@@ -485,7 +485,44 @@ int tb_plan_set_owned_planes(tb_plan* plan, int k0, int k1) {
   TB_GUARD(0 <= k0 && k0 <= k1 && k1 <= P->g.nnz, "owned node planes [%d, %d) outside [0, %d]", k0, k1, P->g.nnz);
   P->own_k0 = k0;
   P->own_k1 = k1;
+  const int64_t pd = (int64_t)P->g.dim * P->g.nnx * P->g.nny;
+  P->work.plane = pd;
+  P->work.own0 = k0 * pd;
+  P->work.own1 = k1 * pd;
   return P->work.set_fields(P->dist, k0, k1);
+}
+
+int tb_plan_set_halo_peers(tb_plan* plan, double* lo_dst, double* hi_dst) {
+  TB_GUARD(plan != nullptr, "null plan");
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  TB_GUARD(P->work.plane > 0, "tb_plan_set_halo_peers needs tb_plan_set_owned_planes first");
+  TB_GUARD(lo_dst == nullptr || P->own_k0 > 0, "no lower neighbour: owned planes start at 0");
+  TB_GUARD(hi_dst == nullptr || P->own_k1 < P->g.nnz, "no upper neighbour: owned planes reach the top");
+  P->work.halo_lo = lo_dst;
+  P->work.halo_hi = hi_dst;
+  return TB_OK;
+}
+
+int tb_ipc_get_handle(const void* dptr, void* handle) {
+  TB_GUARD(dptr != nullptr && handle != nullptr, "null argument");
+  cudaIpcMemHandle_t h;
+  TB_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)));
+  memcpy(handle, &h, sizeof(h));
+  return TB_OK;
+}
+
+int tb_ipc_open(const void* handle, int device, void** dptr) {
+  TB_GUARD(dptr != nullptr && handle != nullptr, "null argument");
+  TB_CUDA(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  TB_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return TB_OK;
+}
+
+int tb_ipc_close(void* dptr) {
+  if (dptr != nullptr) TB_CUDA(cudaIpcCloseMemHandle(dptr));
+  return TB_OK;
 }
 
 int tb_pcg_dist_phase(tb_plan* plan, int phase, const double* rho, const double* b, double rtol, int maxit,

@@ -535,16 +535,164 @@ __global__ void k_dist_beta(PcgState* st) {
   else if (it >= st->maxit) st->done = 2;
 }
 
+// Halo push fused into the kernels that produce z: a value of the first owned node plane goes
+// to the lower neighbour's ghost-above plane, one of the last owned plane to the upper
+// neighbour's ghost-below plane.  The destinations are peer memory (IPC-mapped over NVLink) or
+// local buffers.  No flag or wait is needed: the push happens in phases 0 and 4, each followed
+// on every rank by the allreduce of `red`, and a neighbour reads its ghost planes only in its
+// next operator phase, after that allreduce (RAW).  It overwrites them again only after the
+// allreduce that follows that operator phase (WAR).  Ghost planes of z are therefore written
+// by the neighbour alone; the dist kernels never touch them.
+struct HaloPush {
+  int64_t own0, own1, plane;
+  double *lo, *hi;
+  __device__ __forceinline__ bool push(int64_t i, double zi) const {
+    bool any = false;
+    if (lo != nullptr && i < own0 + plane) {
+      lo[i - own0] = zi;
+      any = true;
+    }
+    if (hi != nullptr && i >= own1 - plane) {
+      hi[i - (own1 - plane)] = zi;
+      any = true;
+    }
+    return any;
+  }
+};
+
+// phase 0: r = Z b, x = 0, p_old = 0 everywhere; z = D^-1 r on owned dofs (+ push); local r.z, r.r
+__global__ void __launch_bounds__(kBlock) k_dist_start(int64_t n, HaloPush hp, const double* __restrict__ b,
+                                                       const double* __restrict__ dinv, double* __restrict__ x,
+                                                       double* __restrict__ r, double* __restrict__ z,
+                                                       double* __restrict__ pa, PcgState* st, double* partials,
+                                                       double rtol, int maxit) {
+  double acc[2] = {0.0, 0.0};
+  bool pushed = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double di = dinv[i];
+    const double ri = (di != 0.0) ? b[i] : 0.0;
+    x[i] = 0.0;
+    r[i] = ri;
+    pa[i] = 0.0;
+    if (i >= hp.own0 && i < hp.own1) {
+      const double zi = di * ri;
+      z[i] = zi;
+      pushed |= hp.push(i, zi);
+      acc[0] = fma(ri, zi, acc[0]);
+      acc[1] = fma(ri, ri, acc[1]);
+    }
+  }
+  if (pushed) __threadfence_system();
+  block_sum<2>(acc);
+  if (publish_partials<2>(acc, partials, &st->count_c)) {
+    gather_partials<2>(acc, partials, &st->count_c);
+    if (threadIdx.x == 0) {
+      st->red[1] = acc[0];
+      st->red[2] = acc[1];
+      st->iters = 0;
+      st->maxit = maxit;
+      st->beta = 0.0;
+      st->alpha = 0.0;
+      st->done = 0;
+      st->pq = rtol;  // stashed until k_dist_init2 has the global norm
+    }
+  }
+}
+
+// phase 4: x += alpha p, r -= alpha q, z = D^-1 r over the owned dofs only (+ push); local r.z, r.r
+__global__ void __launch_bounds__(kBlock) k_dist_update(HaloPush hp, const double* __restrict__ p,
+                                                        const double* __restrict__ q, const double* __restrict__ dinv,
+                                                        double* __restrict__ x, double* __restrict__ r,
+                                                        double* __restrict__ z, PcgState* st, double* partials) {
+  if (st->done) return;
+  const double a = st->alpha;
+  double acc[2] = {0.0, 0.0};
+  bool pushed = false;
+  // 16-byte accesses over the even-aligned interior [v0, v1) of the owned range; the (at most
+  // two) odd end dofs go to the first two threads of block 0
+  const int64_t v0 = (hp.own0 + 1) & ~int64_t(1), v1 = hp.own1 & ~int64_t(1);
+  constexpr int U = 4;
+  const int64_t n2 = v1 > v0 ? (v1 - v0) / 2 : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const double2* p2 = reinterpret_cast<const double2*>(p + v0);
+  const double2* q2 = reinterpret_cast<const double2*>(q + v0);
+  const double2* d2 = reinterpret_cast<const double2*>(dinv + v0);
+  double2* x2 = reinterpret_cast<double2*>(x + v0);
+  double2* r2 = reinterpret_cast<double2*>(r + v0);
+  double2* z2 = reinterpret_cast<double2*>(z + v0);
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (U - 1) * stride < n2; i += U * stride) {
+    double2 pv[U], qv[U], dv[U], xv[U], rv[U], zv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = i + u * stride;
+      pv[u] = __ldcs(p2 + j);
+      qv[u] = __ldcs(q2 + j);
+      dv[u] = __ldg(d2 + j);
+      xv[u] = x2[j];
+      rv[u] = r2[j];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      upd2(a, pv[u], qv[u], dv[u], xv[u], rv[u], zv[u], acc);
+      const int64_t j = i + u * stride;
+      x2[j] = xv[u];
+      r2[j] = rv[u];
+      z2[j] = zv[u];
+      pushed |= hp.push(v0 + 2 * j, zv[u].x);
+      pushed |= hp.push(v0 + 2 * j + 1, zv[u].y);
+    }
+  }
+  for (; i < n2; i += stride) {
+    double2 pv = p2[i], qv = q2[i], dv = d2[i], xv = x2[i], rv = r2[i], zv;
+    upd2(a, pv, qv, dv, xv, rv, zv, acc);
+    x2[i] = xv;
+    r2[i] = rv;
+    z2[i] = zv;
+    pushed |= hp.push(v0 + 2 * i, zv.x);
+    pushed |= hp.push(v0 + 2 * i + 1, zv.y);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 2) {  // odd end dofs
+    const int64_t k = threadIdx.x == 0 ? hp.own0 : v1;
+    const bool live = threadIdx.x == 0 ? (hp.own0 & 1) != 0 && hp.own0 < hp.own1 : v1 < hp.own1 && v1 >= v0;
+    if (live) {
+      double zv = 0.0;
+      const double di = dinv[k];
+      if (di != 0.0) {
+        x[k] = fma(a, p[k], x[k]);
+        const double ri = fma(-a, q[k], r[k]);
+        r[k] = ri;
+        zv = di * ri;
+        acc[0] = fma(ri, zv, acc[0]);
+        acc[1] = fma(ri, ri, acc[1]);
+      }
+      z[k] = zv;
+      pushed |= hp.push(k, zv);
+    }
+  }
+  if (pushed) __threadfence_system();
+  block_sum<2>(acc);
+  if (publish_partials<2>(acc, partials, &st->count_b)) {
+    gather_partials<2>(acc, partials, &st->count_b);
+    if (threadIdx.x == 0) {
+      st->red[1] = acc[0];
+      st->red[2] = acc[1];
+    }
+  }
+}
+
 int pcg_dist_phase(const PcgOp& op, PcgWork& w, int phase, const double* b, double rtol, int maxit, int parity,
                    cudaStream_t s) {
   const int nb = kUpdateBlocks;
   double* pold = (parity & 1) ? w.pb : w.pa;
   double* pnew = (parity & 1) ? w.pa : w.pb;
+  const int64_t o1 = (w.own1 < 0 || w.own1 > w.n) ? w.n : w.own1;
+  const int64_t pl = (w.plane > 0 && w.plane <= o1 - w.own0) ? w.plane : o1 - w.own0;
+  const HaloPush hp{w.own0, o1, pl, w.halo_lo, w.halo_hi};
   switch (phase) {
     case 0:  // init: D^-1, r = Z b, z, local r.z and r.r
       op.launch_dinv(w.dinv, s);
-      k_pcg_start<<<nb, kBlock, 0, s>>>(w.n, b, nullptr, w.dinv, w.x, w.r, w.z, w.pa, w.st, w.partC(), 1, rtol,
-                                        maxit);
+      k_dist_start<<<nb, kBlock, 0, s>>>(w.n, hp, b, w.dinv, w.x, w.r, w.z, w.pa, w.st, w.partC(), rtol, maxit);
       launched(1);
       break;
     case 1:
@@ -559,8 +707,8 @@ int pcg_dist_phase(const PcgOp& op, PcgWork& w, int phase, const double* b, doub
       k_dist_alpha<<<1, 1, 0, s>>>(w.st);
       launched(1);
       break;
-    case 4:  // update + local r.z, r.r
-      k_pcg_update<<<kUpdateBlocks, kBlock, 0, s>>>(w.n, pnew, w.q, w.dinv, w.x, w.r, w.z, w.st, w.partB());
+    case 4:  // update + local r.z, r.r (+ halo push)
+      k_dist_update<<<kUpdateBlocks, kBlock, 0, s>>>(hp, pnew, w.q, w.dinv, w.x, w.r, w.z, w.st, w.partB());
       launched(1);
       break;
     case 5:

@@ -47,6 +47,11 @@ struct PcgWork {
   double* pub = nullptr;     // persistent kernel's published vectors [2][3][n]
   cudaGraphExec_t exec = nullptr;
   cudaGraphExec_t exec_pc = nullptr;  // graph of the preconditioned (multigrid) loop
+  // distributed (slab) mode: owned dof range [own0, own1) (own1 < 0: n), dofs per node plane,
+  // and where the first / last owned plane of z is pushed (neighbours' ghost planes, possibly
+  // peer memory over NVLink; nullptr: the caller exchanges the halo)
+  int64_t own0 = 0, own1 = -1, plane = 0;
+  double *halo_lo = nullptr, *halo_hi = nullptr;
   double* partA() const { return part; }
   double* partB() const { return part + 2 * part_stride; }
   double* partC() const { return part + 4 * part_stride; }

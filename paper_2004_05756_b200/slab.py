@@ -15,6 +15,12 @@ reduction and the operator's p.q are restricted to the owned planes
     phase 4  update + local r.z, r.r ->  allreduce(red)  ->  phase 5  beta / convergence
     halo     ghost planes of z <- neighbours' first / last owned planes
 
+With ``peer=True`` the halo step disappears: phases 0 and 4 store the boundary planes of z
+straight into the neighbours' ghost planes while computing them (tb_plan_set_halo_peers; CUDA
+IPC mappings over NVLink between processes).  The allreduce that already follows those phases
+orders the stores against the neighbours' reads, so no flag, copy or extra collective is
+added.
+
 The direction p = z + beta p_old is formed inside the operator for owned and ghost nodes
 alike from identical z and p_old, so ghost p needs no exchange.  All ranks receive bitwise
 identical allreduce results, so every rank takes the same convergence decision.
@@ -157,6 +163,23 @@ class SlabSolver:
         _lib.check(_lib.lib().tb_pcg_dist_phase(self._plan, p, rho, b, self.rtol, self.maxit, parity,
                                                 _lib.stream_ptr(self.device)), f"dist phase {p}")
 
+    def set_halo_peers(self, lo_dst: int, hi_dst: int):
+        """Device addresses that receive this rank's first / last owned plane of z (0: none)."""
+        _lib.check(_lib.lib().tb_plan_set_halo_peers(self._plan, _lib.P(lo_dst or None), _lib.P(hi_dst or None)),
+                   "halo peers")
+
+    def ghost_addresses(self, z_base: int):
+        """(ghost-below, ghost-above) plane addresses for a z allocation at ``z_base``."""
+        k0, k1 = self.slab.own_local
+        lo = z_base if self.slab.ghost_lo else 0
+        hi = z_base + 8 * k1 * self.plane_dofs if self.slab.ghost_hi else 0
+        return lo, hi
+
+    def z_ipc_handle(self) -> bytes:
+        h = ctypes.create_string_buffer(64)
+        _lib.check(_lib.lib().tb_ipc_get_handle(_lib.P(self.z.data_ptr()), h), "ipc handle")
+        return h.raw
+
     def state(self):
         it, done, rr, bb = ctypes.c_int(), ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
         _lib.check(_lib.lib().tb_pcg_dist_state(self._plan, ctypes.byref(it), ctypes.byref(done), ctypes.byref(rr),
@@ -165,7 +188,19 @@ class SlabSolver:
 
 
 class LocalComm:
-    """All ranks in one process: allreduce = fixed-order sum, halo = device copies."""
+    """All ranks in one process: allreduce = fixed-order sum, halo = device copies (or, with
+    ``peer=True``, the update kernels' direct stores into the neighbours' ghost planes)."""
+
+    def __init__(self, peer: bool = False):
+        self.peer = peer
+
+    def setup(self, solvers):
+        if not self.peer:
+            return
+        for i, s in enumerate(solvers):
+            lo = solvers[i - 1].ghost_addresses(solvers[i - 1].z.data_ptr())[1] if i > 0 else 0
+            hi = solvers[i + 1].ghost_addresses(solvers[i + 1].z.data_ptr())[0] if i + 1 < len(solvers) else 0
+            s.set_halo_peers(lo, hi)
 
     def allreduce(self, solvers):
         total = solvers[0].red.clone()
@@ -175,6 +210,8 @@ class LocalComm:
             s.red.copy_(total)
 
     def halo(self, solvers, name="z"):
+        if self.peer and name == "z":
+            return
         for lo, hi in zip(solvers[:-1], solvers[1:]):
             vlo, vhi = getattr(lo, name), getattr(hi, name)
             k0_hi, _ = hi.slab.own_local
@@ -185,18 +222,65 @@ class LocalComm:
 
 
 class TorchComm:
-    """One solver per process; collectives through torch.distributed (NCCL or gloo)."""
+    """One solver per process; collectives through torch.distributed (NCCL or gloo).
 
-    def __init__(self, group=None):
+    ``peer=True`` (CUDA solvers): the z allocations are exchanged once as CUDA IPC handles and
+    mapped into the neighbours' address spaces; the halo then travels as NVLink peer stores from
+    inside the update kernel and ``halo`` is a no-op.  Call ``close()`` before the solvers go."""
+
+    def __init__(self, group=None, peer: bool = False):
         import torch.distributed as dist
 
         self.dist = dist
         self.group = group
+        self.peer = peer
+        self._mapped = []
+        self._ready = set()
+
+    def setup(self, solvers):
+        if not self.peer or id(solvers[0]) in self._ready:
+            return
+        s = solvers[0]
+        r, n = s.slab.rank, s.slab.nranks
+        handles = [None] * n
+        self.dist.all_gather_object(handles, s.z_ipc_handle(), group=self.group)
+        addr = {}
+        for nb in (r - 1, r + 1):
+            if 0 <= nb < n:
+                base = _lib.P()
+                _lib.check(_lib.lib().tb_ipc_open(handles[nb], s.device.index, ctypes.byref(base)), "ipc open")
+                self._mapped.append(base.value)
+                addr[nb] = base.value
+        # the neighbours' ghost planes: below-neighbour's ghost-above, above-neighbour's ghost-below
+        lo = addr[r - 1] + 8 * self._ghost_hi_plane(s, r - 1) * s.plane_dofs if r > 0 else 0
+        hi = addr[r + 1] if r + 1 < n else 0
+        s.set_halo_peers(lo, hi)
+        self._ready.add(id(s))
+        self.dist.barrier(group=self.group)
+
+    @staticmethod
+    def _ghost_hi_plane(s, rank):
+        """Local index of rank ``rank``'s ghost-above plane (its owned range ends there)."""
+        other = partition(s.mesh.nz, s.slab.nranks)[rank]
+        return other.own_local[1]
+
+    def close(self):
+        for base in self._mapped:
+            _lib.lib().tb_ipc_close(_lib.P(base))
+        self._mapped, self._ready = [], set()
 
     def allreduce(self, solvers):
-        self.dist.all_reduce(solvers[0].red, group=self.group)
+        red = solvers[0].red
+        if red.is_cuda and self.dist.get_backend(self.group) == "gloo":
+            host = red.cpu()  # waits for the phase on the current stream
+            self.dist.all_reduce(host, group=self.group)
+            red.copy_(host)
+        else:
+            self.dist.all_reduce(red, group=self.group)
 
     def halo(self, solvers, name="z"):
+        if self.peer and name == "z":
+            return
         d = self.dist
         s = solvers[0]
         v = getattr(s, name)
@@ -217,6 +301,9 @@ class TorchComm:
 def dist_pcg_solve(solvers, comm, rtol=1e-8, maxit=200000, check_every=8):
     """Jacobi-pCG over the slabs of ``solvers`` (this process's share).  Returns
     (iterations, recursive relative residual, converged flag)."""
+    setup = getattr(comm, "setup", None)
+    if setup is not None:
+        setup(solvers)
     for s in solvers:
         s.rtol, s.maxit = rtol, maxit
         s.phase(0)

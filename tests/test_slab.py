@@ -184,11 +184,25 @@ def test_gloo_world_size_2():
     assert np.abs(u - ref).max() <= 1e-8 * np.abs(ref).max()
 
 
+def _slab_solve(prob, mat, rho, nranks, comm, rtol=1e-11):
+    from paper_2004_05756_b200.slab import SlabSolver
+
+    solvers = [SlabSolver(prob.mesh, prob.k_e, prob.f, prob.fixed, mat, s) for s in partition(prob.mesh.nz, nranks)]
+    for s in solvers:
+        s.rho = s.local_elems(rho).contiguous()
+    it, rel, ok = dist_pcg_solve(solvers, comm, rtol=rtol)
+    assert ok
+    u = np.zeros(prob.mesh.n_dofs)
+    for s in solvers:
+        sl, sg = s.owned_dofs()
+        u[sg] = s.x[sl].cpu().numpy()
+    return u, it
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("nranks", [2, 3])
 def test_cuda_slabs_emulated_on_one_gpu(cuda, nranks):
     import paper_2004_05756_b200 as tb
-    from paper_2004_05756_b200.slab import SlabSolver
 
     prob = configs.cfg3(seed=6, nx=16, ny=8, nz=11)
     mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
@@ -196,17 +210,74 @@ def test_cuda_slabs_emulated_on_one_gpu(cuda, nranks):
                         rtol=1e-11)
     rho = torch.as_tensor(prob.psi, device=cuda)
     u_ref = glob.pcg_device(rho, glob._f_d).cpu().numpy()
-    solvers = [SlabSolver(prob.mesh, prob.k_e, prob.f, prob.fixed, mat, s) for s in partition(prob.mesh.nz, nranks)]
-    for s in solvers:
-        s.rho = s.local_elems(rho).contiguous()
-    it, rel, ok = dist_pcg_solve(solvers, LocalComm(), rtol=1e-11)
-    assert ok
-    u = np.zeros(prob.mesh.n_dofs)
-    for s in solvers:
-        sl, sg = s.owned_dofs()
-        u[sg] = s.x[sl].cpu().numpy()
+    u, it = _slab_solve(prob, mat, rho, nranks, LocalComm())
     assert np.abs(u - u_ref).max() <= 1e-8 * np.abs(u_ref).max()
     assert abs(glob.last_iterations - it) <= 8 + glob.last_iterations // 50
+    # fused halo: the update kernels store the boundary planes into the neighbours' ghost
+    # planes; same values as the copy exchange, so the iterates are bit-identical
+    u_peer, it_peer = _slab_solve(prob, mat, rho, nranks, LocalComm(peer=True))
+    assert it_peer == it
+    assert np.array_equal(u_peer, u)
+
+
+def _ipc_worker(rank, world, port, q):
+    """One rank per process on the same GPU: z mapped through CUDA IPC, halo as direct stores
+    from the update kernel, allreduce through gloo on the host (no kernel waits on a peer)."""
+    import torch.distributed as dist
+
+    import paper_2004_05756_b200 as tb
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        prob = configs.cfg3(seed=6, nx=16, ny=8, nz=11)
+        mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
+        from paper_2004_05756_b200.slab import SlabSolver
+
+        s = SlabSolver(prob.mesh, prob.k_e, prob.f, prob.fixed, mat, partition(prob.mesh.nz, world)[rank], device=0)
+        s.rho = s.local_elems(torch.as_tensor(prob.psi, device="cuda:0")).contiguous()
+        comm = TorchComm(peer=True)
+        it, rel, ok = dist_pcg_solve([s], comm, rtol=1e-11)
+        it2, _, _ = dist_pcg_solve([s], comm, rtol=1e-11)  # a second solve reuses the mappings
+        sl, _ = s.owned_dofs()
+        q.put((rank, it, it2, ok, s.slab.k0, s.slab.k1, s.x[sl].cpu().numpy()))
+        dist.barrier()
+        comm.close()
+    except Exception as e:  # reported to the parent
+        q.put((rank, repr(e)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_cuda_ipc_peer_halo_two_processes(cuda):
+    import socket
+
+    import torch.multiprocessing as mp
+
+    import paper_2004_05756_b200 as tb
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=300) for _ in procs), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+    for r in res:
+        assert len(r) > 2, f"rank {r[0]} failed: {r[1]}"
+    prob = configs.cfg3(seed=6, nx=16, ny=8, nz=11)
+    mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
+    u_loc, it_loc = _slab_solve(prob, mat, torch.as_tensor(prob.psi, device=cuda), 2, LocalComm())
+    pd = 3 * (prob.mesh.nx + 1) * (prob.mesh.ny + 1)
+    u = np.zeros(prob.mesh.n_dofs)
+    for _, it, it2, ok, k0, k1, xs in res:
+        assert ok and it == it2 == it_loc
+        u[k0 * pd:k1 * pd] = xs
+    assert np.array_equal(u, u_loc)  # gloo sums 2 ranks in a fixed order: bit-identical to LocalComm
 
 
 @pytest.mark.gpu

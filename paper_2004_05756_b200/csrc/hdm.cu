@@ -119,7 +119,7 @@ void ElastOp::launch_fused(const PcgWork& w, const double* pold, double* pnew, c
                                                                 w.st, w.partA());
   else if (plan->hex8)
     k_hex8<true><<<hex8_grid(g, plan->zchunk), kHT, kHex8Smem, s>>>(g, plan->hiso, plan->d_alpha, w.z, pold, pnew,
-                                                                    w.q, nullptr, w.st, w.partA(), plan->zchunk);
+                                                                    w.q, w.st, w.partA(), plan->zchunk);
   else
     k_pcg_fused<3, 3, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, plan->K3, plan->d_alpha, w.z, pold, pnew, w.q,
                                                                 w.st, w.partA());
@@ -293,12 +293,9 @@ void tb_plan_impl::apply_alpha(const double* alpha, const double* v, double* y, 
   const uint8_t* fx = mask ? d_fixed : nullptr;
   if (g.dim == 2)
     { k_node_apply<2, 2, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, K2, alpha, v, y, fx); tb::launched(); }
-  else if (hex8)
-    if (fx != nullptr)
-      { k_hex8<false, true><<<hex8_grid(g, zchunk), kHT, kHex8Smem, s>>>(g, hiso, alpha, v, nullptr, nullptr, y, fx, nullptr, nullptr, zchunk); tb::launched(); }
-    else
-      { k_hex8<false><<<hex8_grid(g, zchunk), kHT, kHex8Smem, s>>>(g, hiso, alpha, v, nullptr, nullptr, y, nullptr, nullptr, nullptr, zchunk); tb::launched(); }
-  else
+  else if (hex8) {
+    { k_hex8<false><<<hex8_grid(g, zchunk), kHT, kHex8Smem, s>>>(g, hiso, alpha, v, nullptr, nullptr, y, nullptr, nullptr, zchunk, 0.0, 3.0, mask ? d_fixed_idx : nullptr, mask ? d_fixed_off : nullptr); tb::launched(); }
+  } else
     { k_node_apply<3, 3, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, K3, alpha, v, y, fx); tb::launched(); }
 }
 
@@ -358,9 +355,7 @@ int tb_plan_create(int dim, int nx, int ny, int nz, double h, const double* k_e,
       cudaError_t e1 = cudaFuncSetAttribute(k_hex8<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHex8Smem);
       cudaError_t e2 = cudaFuncSetAttribute(k_hex8<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHex8Smem);
       cudaError_t e3 = cudaFuncSetAttribute(k_hex8<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHex8Smem);
-      cudaError_t e4 = cudaSuccess;
-      cudaError_t e5 = cudaFuncSetAttribute(k_hex8<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHex8Smem);
-      if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess || e5 != cudaSuccess)
+      if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)
         P->hex8 = false;
     }
   }
@@ -419,10 +414,9 @@ int tb_apply_stiffness(tb_plan* plan, const double* rho, const double* v, double
   TB_GUARD(plan && rho && v && y, "null argument");
   auto* P = reinterpret_cast<tb_plan_impl*>(plan);
   cudaStream_t s = (cudaStream_t)stream;
-  if (P->g.dim == 3 && P->hex8 && P->p == 3.0 && !mask_rows) {  // alpha(rho) inside the operator pass
-    // (the Dirichlet-mask variant with alpha(rho) fused spills; it keeps the material pass)
+  if (P->g.dim == 3 && P->hex8 && P->p == 3.0) {  // alpha(rho) inside the operator pass
     const Grid& g = P->g;
-    { k_hex8<false, false, true><<<hex8_grid(g, P->zchunk), kHT, kHex8Smem, s>>>(g, P->hiso, rho, v, nullptr, nullptr, y, nullptr, nullptr, nullptr, P->zchunk, P->rho_l, P->p); tb::launched(); }
+    { k_hex8<false, true><<<hex8_grid(g, P->zchunk), kHT, kHex8Smem, s>>>(g, P->hiso, rho, v, nullptr, nullptr, y, nullptr, nullptr, P->zchunk, P->rho_l, P->p, mask_rows ? P->d_fixed_idx : nullptr, mask_rows ? P->d_fixed_off : nullptr); tb::launched(); }
     TB_CHECK_LAUNCH();
     return TB_OK;
   }

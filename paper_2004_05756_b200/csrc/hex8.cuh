@@ -122,17 +122,19 @@ constexpr int kOPlane = kORow * kOY;                   // 651 owned doubles per 
 constexpr int kOSlots = (kOPlane + kHT - 1) / kHT;     // 3 store slots per thread
 
 // FUSED: in = z, in2 = p_old, out = q, writes pnew, reduces p.q (pCG kernel A).
-// !FUSED: in = v, out = y = K v (fixed rows zeroed when `fixed` != nullptr).
-// MASK (!FUSED only): zero the Dirichlet rows; the mask bytes of a plane are loaded into
-// registers one step before the plane is flushed, so the flush never waits on them.
+// !FUSED: in = v, out = y = K v.  Dirichlet rows: when `zoff` is given, CTA b zeroes
+// out[zidx[zoff[b] .. zoff[b+1])] (the fixed dofs it owns, bucketed per CTA at plan creation)
+// after its last flush.  Mask bytes read inside the sweep cost registers (spills) and ~8 us.
 // SIMP (!FUSED only, p = 3): `alpha` holds rho; alpha = rho_l + (1 - rho_l) rho^3 is formed per
 // element as it is loaded (same operation order as k_material), saving the material pass.
-template <bool FUSED, bool MASK = false, bool SIMP = false>
+template <bool FUSED, bool SIMP = false>
 __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const double* __restrict__ alpha,
                                                  const double* __restrict__ in, const double* __restrict__ in2,
                                                  double* __restrict__ pnew, double* __restrict__ out,
-                                                 const uint8_t* __restrict__ fixed, PcgState* st, double* partials,
-                                                 int zchunk, double rho_l = 0.0, double p_simp = 3.0) {
+                                                 PcgState* st, double* partials,
+                                                 int zchunk, double rho_l = 0.0, double p_simp = 3.0,
+                                                 const int64_t* __restrict__ zidx = nullptr,
+                                                 const int* __restrict__ zoff = nullptr) {
   // plane[4][kPlane]: node planes (buffer = plane index mod 4), AoS rows as in global memory.
   // stage[2][2][3][kHT]: node-plane corner outputs (oy) already summed over the two
   // x-neighbour elements, double buffered by step parity.  ostg[2][kOPlane]: finished owned
@@ -223,22 +225,13 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
   }                                                                                                         \
   _Pragma("unroll") for (int c = 0; c < 3; ++c) wht4(f_[c]);
   // coalesced store of the finished owned plane kp_ (staged in ostg[(kp_) & 1])
-#define HEX8_MASK(kp_)                                                                                      \
-  if (MASK) {                                                                                               \
-    const uint8_t* fx = fixed + (int64_t)(kp_) * plane_dofs;                                                \
-    _Pragma("unroll") for (int s = 0; s < kOSlots; ++s)                                                     \
-      mk_next[s] = ((s < kOSlots - 1 || t < kOPlane - (kOSlots - 1) * kHT) && (ook >> s & 1u))              \
-                       ? __ldg(fx + ooff[s]) : (uint8_t)0;                                                  \
-  }
 #define HEX8_FLUSH(kp_, par_)                                                                               \
   {                                                                                                         \
     const double* srcs = ostg + (par_) * kOPlane;                                                           \
     double* dst = out + (int64_t)(kp_) * plane_dofs;                                                        \
     _Pragma("unroll") for (int s = 0; s < kOSlots; ++s) {                                                   \
       if ((s < kOSlots - 1 || t < kOPlane - (kOSlots - 1) * kHT) && (ook >> s & 1u)) {                      \
-        double v = srcs[t + s * kHT];                                                                       \
-        if (MASK && mk_cur[MASK ? s : 0]) v = 0.0;                                                          \
-        dst[ooff[s]] = v;                                                                                   \
+        dst[ooff[s]] = srcs[t + s * kHT];                                                                   \
       }                                                                                                     \
     }                                                                                                       \
   }
@@ -260,7 +253,10 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
   const int64_t a_stride = (int64_t)g.nx * g.ny;
   (void)p_simp;  // SIMP launches are p = 3 only (host checks), the BASELINE exponent
   auto simp = [&](double r) { return SIMP ? rho_l + (1.0 - rho_l) * ((r * r) * r) : r; };
-  double a_next = (col_ok && K0 - 1 >= 0) ? simp(__ldg(a_ptr + (K0 - 1) * a_stride)) : 0.0;
+  // the element's alpha (or rho, SIMP) is loaded one step ahead and used raw; SIMP turns it into
+  // alpha only in the step that consumes it, so the load latency hides behind a whole step
+  bool a_ok = col_ok && K0 - 1 >= 0;
+  double a_next = a_ok ? __ldg(a_ptr + (K0 - 1) * a_stride) : 0.0;
   __syncthreads();
   // xy-WHT of the 4 corner nodes of the current bottom face of this element column
   double fb[3][4];
@@ -274,16 +270,16 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
   const bool dot_any = FUSED && st->dot_k1 > st->dot_k0;
   const int dk0 = FUSED ? st->dot_k0 : 0, dk1 = FUSED ? st->dot_k1 : 0;
   const int steps = K1 - (K0 - 1);  // element planes ez = K0-1 .. K1-1
-  uint8_t mk_cur[MASK ? kOSlots : 1] = {}, mk_next[MASK ? kOSlots : 1] = {};  // Dirichlet bytes
   // (a 4-way unrolled sweep makes the ring offsets constants but spills and runs slower)
 #pragma unroll 1
   for (int rel = 0; rel < steps; ++rel) {
     {
       const int r = rel & 3;
       const int ez = K0 - 1 + rel;
-      const double a = a_next;
-      a_next = (col_ok && ez + 1 < g.nz && ez + 1 < K1) ? simp(__ldg(a_ptr + (ez + 1) * a_stride)) : 0.0;
-      if (MASK && rel >= 1) HEX8_MASK(ez);  // flushed next step
+      const double a_raw = a_next;
+      const bool a_cur = a_ok;
+      a_ok = col_ok && ez + 1 < g.nz && ez + 1 < K1;
+      a_next = a_ok ? __ldg(a_ptr + (ez + 1) * a_stride) : 0.0;
       // ---- element (gei, gej, ez): spectrum from carried bottom face + new top face ----
       {
         double ft[3][4];
@@ -297,7 +293,7 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
             u[c][s + 4] = fb[c][s] - ft[c][s];
             fb[c][s] = ft[c][s];  // this top face is the next element's bottom face
           }
-        hex8_iso_blocks(K, a, u);
+        hex8_iso_blocks(K, SIMP ? (a_cur ? simp(a_raw) : 0.0) : a_raw, u);
         // inverse z stage: bottom-face spectrum joins the previous element's top-face spectrum
         // (both land on node plane ez), so the xy inverse runs once per node plane
         double fq[3][4];
@@ -351,10 +347,6 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
       }
       __syncthreads();
       if (rel >= 2) HEX8_FLUSH(ez - 1, (r + 1) & 1);  // plane ez-1 was staged before this barrier
-      if (MASK) {
-#pragma unroll
-        for (int s = 0; s < (MASK ? kOSlots : 1); ++s) mk_cur[s] = mk_next[s];
-      }
       // ---- owned node (px, py) of plane ez: rows ey = py-1 (corner oy=1) and ey = py (oy=0) ----
       if (own && rel >= 1) {
         const int e_dn = (py - 1) * kHX + (px - 1), e_up = py * kHX + (px - 1);
@@ -375,11 +367,15 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
   }
   __syncthreads();
   if (steps >= 2) HEX8_FLUSH(K1 - 1, (steps - 1) & 1);
+  if (!FUSED && zoff != nullptr) {  // Dirichlet rows this CTA owns, after its own flushes
+    __syncthreads();
+    const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    for (int i = zoff[b] + t; i < zoff[b + 1]; i += kHT) out[zidx[i]] = 0.0;
+  }
 #undef HEX8_ISSUE
 #undef HEX8_LAND
 #undef HEX8_FACE
 #undef HEX8_FLUSH
-#undef HEX8_MASK
 #undef HEX8_PB
 #undef HEX8_PS
   if (FUSED) {
@@ -426,6 +422,13 @@ inline int hex8_zchunk(const Grid& g) {
 
 inline dim3 hex8_grid(const Grid& g, int zchunk) {
   return dim3((g.nnx + kOX - 1) / kOX, (g.nny + kOY - 1) / kOY, (g.nnz + zchunk - 1) / zchunk);
+}
+
+// CTA of k_hex8's grid that owns (flushes) dof d
+inline int64_t hex8_owner(const Grid& g, int zchunk, int64_t d) {
+  const int64_t n = d / 3, i = n % g.nnx, j = (n / g.nnx) % g.nny, k = n / ((int64_t)g.nnx * g.nny);
+  const dim3 gr = hex8_grid(g, zchunk);
+  return i / kOX + (int64_t)gr.x * (j / kOY + (int64_t)gr.y * (k / zchunk));
 }
 
 }  // namespace tb

@@ -1,4 +1,6 @@
 // Plan lifetime, element tables and workspace management.
+#include <vector>
+
 #include "plan.cuh"
 
 namespace tb {
@@ -98,6 +100,23 @@ int tb_plan_impl::init(const uint8_t* fixed_host) {
   const size_t ne = (size_t)g.n_elems;
   TB_CUDA(cudaMalloc(&d_fixed, (size_t)n_dofs));
   TB_CUDA(cudaMemcpy(d_fixed, fixed_host, (size_t)n_dofs, cudaMemcpyHostToDevice));
+  if (g.dim == 3 && hex8) {  // Dirichlet rows per owning k_hex8 CTA (counting sort)
+    const dim3 gr = hex8_grid(g, zchunk);
+    const int64_t nb = (int64_t)gr.x * gr.y * gr.z;
+    std::vector<int> off(nb + 1, 0);
+    for (int64_t d = 0; d < n_dofs; ++d)
+      if (fixed_host[d]) ++off[hex8_owner(g, zchunk, d) + 1];
+    for (int64_t b = 0; b < nb; ++b) off[b + 1] += off[b];
+    n_fixed = off[nb];
+    std::vector<int64_t> idx(n_fixed > 0 ? n_fixed : 1);
+    std::vector<int> pos(off.begin(), off.end() - 1);
+    for (int64_t d = 0; d < n_dofs; ++d)
+      if (fixed_host[d]) idx[pos[hex8_owner(g, zchunk, d)]++] = d;
+    TB_CUDA(cudaMalloc(&d_fixed_idx, sizeof(int64_t) * idx.size()));
+    TB_CUDA(cudaMemcpy(d_fixed_idx, idx.data(), sizeof(int64_t) * idx.size(), cudaMemcpyHostToDevice));
+    TB_CUDA(cudaMalloc(&d_fixed_off, sizeof(int) * off.size()));
+    TB_CUDA(cudaMemcpy(d_fixed_off, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice));
+  }
   TB_CUDA(cudaMalloc(&d_alpha, sizeof(double) * ne));
   TB_CUDA(cudaMalloc(&d_alpha2, sizeof(double) * ne));
   TB_CUDA(cudaMalloc(&d_scratch, sizeof(double) * 8 * 148 * 8));
@@ -115,11 +134,14 @@ int ElastOp::precond_apply(const double* r, double* z, cudaStream_t s) const { r
 void tb_plan_impl::release() {
   mg_release(mg);
   work.release();
-  void* bufs[] = {d_fixed, d_alpha, d_alpha2, d_scratch, d_scalar, d_rom};
+  void* bufs[] = {d_fixed, d_fixed_idx, d_fixed_off, d_alpha, d_alpha2, d_scratch, d_scalar, d_rom};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h_scalar) cudaFreeHost(h_scalar);
   d_fixed = nullptr;
+  d_fixed_idx = nullptr;
+  d_fixed_off = nullptr;
+  n_fixed = 0;
   d_alpha = d_alpha2 = d_scratch = d_scalar = d_rom = h_scalar = nullptr;
 }
 

@@ -59,6 +59,9 @@ struct tb_plan_impl {
   Mg mg;
   int own_k0 = 0, own_k1 = 1 << 30;  // owned node planes (set by tb_plan_set_owned_planes); ROM rows
   uint8_t* d_fixed = nullptr;
+  int64_t* d_fixed_idx = nullptr;  // 3D Hex8: fixed dofs bucketed by the k_hex8 CTA owning them
+  int* d_fixed_off = nullptr;      // bucket offsets (CTAs + 1)
+  int64_t n_fixed = 0;
   double* d_alpha = nullptr;   // alpha of the design being solved (read by the pCG graph)
   double* d_alpha2 = nullptr;  // alpha scratch for one-off applies
   double* d_scratch = nullptr; // reduction partials

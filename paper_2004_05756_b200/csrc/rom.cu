@@ -558,7 +558,7 @@ int tb_rom_reduced_stiffness(tb_plan* plan, const double* phi, int k, const doub
     TB_TRY(P->material(rho + (int64_t)d * g.n_elems, P->d_alpha2, nullptr, s));
     if (hex8) {
       for (int j = 0; j < k; ++j)
-        { k_hex8<false><<<hex8_grid(g, P->zchunk), kHT, kHex8Smem, s>>>(g, P->hiso, P->d_alpha2, PhiT + (int64_t)j * ldp, nullptr, nullptr, Y + (int64_t)j * ldp, nullptr, nullptr, nullptr, P->zchunk); tb::launched(); }
+        { k_hex8<false><<<hex8_grid(g, P->zchunk), kHT, kHex8Smem, s>>>(g, P->hiso, P->d_alpha2, PhiT + (int64_t)j * ldp, nullptr, nullptr, Y + (int64_t)j * ldp, nullptr, nullptr, P->zchunk); tb::launched(); }
       TB_CHECK_LAUNCH();
       TB_TRY(launch_atb_colmajor<true>(r0, r1, k, PhiT, Y, part, nbc, ldp, s));  // Phi^T (K Phi) is symmetric
     } else {

@@ -57,6 +57,44 @@ __device__ __forceinline__ void grid_sync_flip(unsigned int* bar) {
   __syncthreads();
 }
 
+// End of an iteration of the persistent kernels: this CTA's NV dot partials (same fixed-order
+// sum as block_sum) are published to part[i * nbk + blockIdx.x] and the grid barrier is
+// crossed, with 2 CTA barriers instead of block_sum's 3 plus the grid barrier's 2.  Only warp 0
+// needs the CTA sum; the single bar.sync before it also orders every thread's ring
+// publications before thread 0's release arrival.  `red` is reused next iteration only after the
+// closing bar.sync, which warp 0 reaches after reading it.
+template <int NV>
+__device__ __forceinline__ void publish_partials_grid_sync(double (&v)[NV], double* part, unsigned int* bar,
+                                                           bool skip_barrier = false) {
+  __shared__ double red[NV][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) red[i][w] = v[i];
+  }
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = warp_sum((lane < nw) ? red[i][lane] : 0.0);
+    if (lane == 0) {
+      const unsigned int nb = gridDim.x;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) part[i * nb + blockIdx.x] = v[i];
+      if (!skip_barrier) {
+        const unsigned int add = (blockIdx.x == 0) ? (0x80000000u - (nb - 1u)) : 1u;
+        unsigned int old, cur;
+        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(bar), "r"(add) : "memory");
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+        } while (((old ^ cur) & 0x80000000u) == 0u);
+      }
+    }
+  }
+  __syncthreads();
+}
+
 struct CgcgArgs {
   const double* b;     // unused (restart state comes from r, x)
   double* x;           // in: x0 ; out: solution

@@ -146,13 +146,19 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_tile(Grid g, Mat<4 * 
       }
     }
   }
-  block_sum<3>(acc);
-  if (tid == 0) {  // partials parity-buffered (see cgcg2d.cuh)
-    a.part[blockIdx.x] = acc[0];
-    a.part[nbk + blockIdx.x] = acc[1];
-    a.part[2 * nbk + blockIdx.x] = acc[2];
+  // partials parity-buffered (see cgcg2d.cuh); the non-pattern variant keeps the separate block
+  // sum and barrier (ptxas spills ~800 B there otherwise)
+  if constexpr (PAT) {
+    publish_partials_grid_sync<3>(acc, a.part, a.bar);
+  } else {
+    block_sum<3>(acc);
+    if (tid == 0) {
+      a.part[blockIdx.x] = acc[0];
+      a.part[nbk + blockIdx.x] = acc[1];
+      a.part[2 * nbk + blockIdx.x] = acc[2];
+    }
+    grid_sync_flip(a.bar);
   }
-  grid_sync_flip(a.bar);
 
   double gam = 0.0, al = 0.0, be = 0.0, rr = 0.0;
   int it = a.st->iters, done = 0;
@@ -336,15 +342,19 @@ __global__ void __launch_bounds__(kCgcgThreads, 1) k_pcg2d_tile(Grid g, Mat<4 * 
         }
       }
     }
-    if (!TILE_SKIP(64)) block_sum<3>(acc3);
-    if (tid == 0) {
-      double* pp = a.part + (par ^ 1) * 3 * nbk;
-      pp[blockIdx.x] = acc3[0];
-      pp[nbk + blockIdx.x] = acc3[1];
-      pp[2 * nbk + blockIdx.x] = acc3[2];
+    if constexpr (PAT) {
+      publish_partials_grid_sync<3>(acc3, a.part + (par ^ 1) * 3 * nbk, a.bar, TILE_SKIP(1));
+    } else {
+      if (!TILE_SKIP(64)) block_sum<3>(acc3);
+      if (tid == 0) {
+        double* pp = a.part + (par ^ 1) * 3 * nbk;
+        pp[blockIdx.x] = acc3[0];
+        pp[nbk + blockIdx.x] = acc3[1];
+        pp[2 * nbk + blockIdx.x] = acc3[2];
+      }
+      if (!TILE_SKIP(1)) grid_sync_flip(a.bar);
     }
     par ^= 1;
-    if (!TILE_SKIP(1)) grid_sync_flip(a.bar);
   }
   for (int o = tid; o < no; o += nt) {
     const int ly = o / owx, lx = o - ly * owx;
@@ -427,7 +437,6 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2d_treg(Grid g, Mat<4 * NC> K, Q4P
   }
   __syncthreads();
 
-  double* pubr[2] = {a.pub, a.pub + 3 * ND};
   auto node_apply = [&](int x, int y, int ei, double (&out)[NC]) {
     double P[9][NC];
     double sc[4];
@@ -492,15 +501,9 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2d_treg(Grid g, Mat<4 * NC> K, Q4P
 
   {
     double acc[3] = {0.0, 0.0, 0.0};
-    apply_dots_publish(pubr[0], acc);
-    block_sum<3>(acc);
-    if (tid == 0) {  // partials parity-buffered (see cgcg2d.cuh)
-      a.part[blockIdx.x] = acc[0];
-      a.part[nbk + blockIdx.x] = acc[1];
-      a.part[2 * nbk + blockIdx.x] = acc[2];
-    }
+    apply_dots_publish(a.pub, acc);
+    publish_partials_grid_sync<3>(acc, a.part, a.bar);  // partials parity-buffered (see cgcg2d.cuh)
   }
-  grid_sync_flip(a.bar);
 
   double gam = 0.0, al = 0.0, be = 0.0, rr = 0.0;
   int it = a.st->iters, done = 0;
@@ -524,7 +527,7 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2d_treg(Grid g, Mat<4 * NC> K, Q4P
     y = oy0 + t;
   };
   for (bool first = true;; first = false) {
-    const double* pr = pubr[par];
+    const double* pr = a.pub + par * 3 * ND;
     double hr[kHB], hw[kHB], hs[kHB];
     int mm[kHB];
     auto halo_load = [&](int base) {
@@ -655,16 +658,9 @@ __global__ void __launch_bounds__(NT, 1) k_pcg2d_treg(Grid g, Mat<4 * NC> K, Q4P
     }
     __syncthreads();
     double acc3[3] = {0.0, 0.0, 0.0};
-    if (!TILE_SKIP(2)) apply_dots_publish(pubr[par ^ 1], acc3);
-    if (!TILE_SKIP(64)) block_sum<3>(acc3);
-    if (tid == 0) {
-      double* pp = a.part + (par ^ 1) * 3 * nbk;
-      pp[blockIdx.x] = acc3[0];
-      pp[nbk + blockIdx.x] = acc3[1];
-      pp[2 * nbk + blockIdx.x] = acc3[2];
-    }
+    if (!TILE_SKIP(2)) apply_dots_publish(a.pub + (par ^ 1) * 3 * ND, acc3);
+    publish_partials_grid_sync<3>(acc3, a.part + (par ^ 1) * 3 * nbk, a.bar, TILE_SKIP(1));
     par ^= 1;
-    if (!TILE_SKIP(1)) grid_sync_flip(a.bar);
   }
 #pragma unroll
   for (int k = 0; k < NS; ++k) {

@@ -369,8 +369,12 @@ def run_ours(args):
     # first timed steps when it was launched right before them; it keeps sampling through them
     clocks = Clocks(dev.index)
     clocks.start()
+    # warm-up keeps each step's results alive through the next step, as the timed loop does, so
+    # the caching allocator already holds two sets of output buffers (otherwise the second timed
+    # step paid a cudaMalloc inside its events)
+    sol = g = None
     for _ in range(max(args.warmup, 3)):
-        step()
+        sol, g = step()
     torch.cuda.synchronize()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -405,9 +409,9 @@ def run_ours(args):
     psi_pin = torch.empty(mesh.n_elems, dtype=torch.float64, pin_memory=True)
     psi_pin.copy_(torch.from_numpy(prob.psi))
     psi_host = psi_pin.numpy()
-    for _ in range(2):
+    for _ in range(2):  # same result liveness as the timed loop (see the warm-up above)
         s_ = solver.solve(psi_host, obj)
-        solver.gradient(psi_host, s_, obj)
+        g_h = solver.gradient(psi_host, s_, obj)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
@@ -465,9 +469,31 @@ def run_ours(args):
             solver.apply_device(rho_d, v)
         b.record()
         torch.cuda.synchronize()
-        t_apply = a.elapsed_time(b) / 50 * 1e-3
+        t_host = a.elapsed_time(b) / 50 * 1e-3
+        # GPU time of K(rho)u: 20 back-to-back calls captured in a CUDA graph, median of 5
+        # replays (a Python loop measures the host's call rate at this size, ~20 us per call)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for _ in range(20):
+                solver.apply_device(rho_d, v)
+        graph.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            a.record()
+            graph.replay()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) / 20 * 1e-3)
+        t_apply = statistics.median(ts)
+        by_apply = 8 * (2 * n_u + prob.mesh.n_elems)
         extras["apply_gdofs"] = n_u / t_apply / 1e9
         extras["apply_us"] = t_apply * 1e6
+        extras["apply"] = {"what": "HdmSolver.apply_device (tb_apply_stiffness: alpha(rho) + K u + Dirichlet rows, one "
+                                   "launch), 20 calls in a CUDA graph", "bytes_per_launch": by_apply,
+                           "achieved_gbs": by_apply / t_apply / 1e9,
+                           "note": "4.8 MB working set stays in L2 between calls",
+                           "us_per_call_python_loop": t_host * 1e6}
         k = prob.rom_k
         phi = torch.linalg.qr(torch.randn(n_u, k, dtype=torch.float64, device=dev))[0].contiguous()
         rom = tb.RomModel(solver)
@@ -585,8 +611,8 @@ def run_cfg5(args):
     nd = rhos.shape[0]
     clocks = Clocks(dev.index)
     clocks.start()  # before the warm-up (see run_ours)
-    for _ in range(max(args.warmup, 1)):
-        rom.solve_batch(basis, rhos)
+    for _ in range(max(args.warmup, 1)):  # results kept alive as in the timed loop (allocator)
+        khat, uhat, norms = rom.solve_batch(basis, rhos)
     torch.cuda.synchronize()
     launches0 = _lib.lib().tb_launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]

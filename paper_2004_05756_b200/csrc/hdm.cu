@@ -414,6 +414,11 @@ int tb_apply_stiffness(tb_plan* plan, const double* rho, const double* v, double
   TB_GUARD(plan && rho && v && y, "null argument");
   auto* P = reinterpret_cast<tb_plan_impl*>(plan);
   cudaStream_t s = (cudaStream_t)stream;
+  if (P->g.dim == 2 && P->p == 3.0) {  // alpha(rho) inside the node apply: one launch
+    { k_node_apply<2, 2, true, true><<<nblk(P->g.n_nodes), kBlock, 0, s>>>(P->g, P->K2, rho, v, y, mask_rows ? P->d_fixed : nullptr, P->rho_l); tb::launched(); }
+    TB_CHECK_LAUNCH();
+    return TB_OK;
+  }
   if (P->g.dim == 3 && P->hex8 && P->p == 3.0) {  // alpha(rho) inside the operator pass
     const Grid& g = P->g;
     { k_hex8<false, true><<<hex8_grid(g, P->zchunk), kHT, kHex8Smem, s>>>(g, P->hiso, rho, v, nullptr, nullptr, y, nullptr, nullptr, P->zchunk, P->rho_l, P->p, mask_rows ? P->d_fixed_idx : nullptr, mask_rows ? P->d_fixed_off : nullptr); tb::launched(); }

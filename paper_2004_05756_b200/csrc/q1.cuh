@@ -174,10 +174,10 @@ inline bool q4_pattern_values(int nc, const double* K, Q4Pat* out) {
 }
 
 // y = K v  (rows with fixed[dof] != 0 zeroed when fixed != nullptr)
-template <int D, int NC, bool SCALED>
+template <int D, int NC, bool SCALED, bool SIMP = false>
 __global__ void __launch_bounds__(kBlock) k_node_apply(Grid g, Mat<Q1<D>::NN * NC> K, const double* __restrict__ alpha,
                                                        const double* __restrict__ v, double* __restrict__ y,
-                                                       const uint8_t* __restrict__ fixed) {
+                                                       const uint8_t* __restrict__ fixed, double rho_l = 0.0) {
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= g.n_nodes) return;
   int i, j, k;
@@ -186,6 +186,15 @@ __global__ void __launch_bounds__(kBlock) k_node_apply(Grid g, Mat<Q1<D>::NN * N
   double a[Q1<D>::NN];
   gather_nbhd<D, NC, false>(g, i, j, k, v, nullptr, 0.0, P);
   slot_scales<D, SCALED>(g, i, j, k, alpha, a);
+  if (SIMP) {  // `alpha` holds rho: alpha = rho_l + (1 - rho_l) rho^3 (k_material's operation order)
+#pragma unroll
+    for (int s = 0; s < Q1<D>::NN; ++s) {
+      const int ei = i - 1 + (s & 1), ej = j - 1 + ((s >> 1) & 1), ek = (D == 3) ? k - 1 + (s >> 2) : 0;
+      const bool ok = ei >= 0 && ei < g.nx && ej >= 0 && ej < g.ny && ek >= 0 && ek < g.nz;
+      const double r = a[s];
+      a[s] = ok ? rho_l + (1.0 - rho_l) * ((r * r) * r) : 0.0;
+    }
+  }
   double out[NC];
   node_rows<D, NC>(K, P, a, out);
 #pragma unroll

@@ -668,17 +668,17 @@ def run_cfg5(args):
 
 
 def run_cfg4(args):
-    """BASELINE cfg 4: slab-sharded (z) Jacobi-pCG solve + sensitivities on 384x192x192 Hex8
-    (43M DOF), one slab per rank, NCCL allreduce of the CG scalars; the halo travels as NVLink
-    peer stores from inside the update kernel (--halo peer, CUDA IPC) or as NCCL send/recv
-    (--halo nccl).  rho = psi (the filter is
-    applied once as input generation; the distributed filter is future work)."""
-    import numpy as np
+    """BASELINE cfg 4: one full design evaluation on 384x192x192 Hex8 (43M DOF), slab-sharded
+    along z, one slab per rank: distributed Helmholtz filter (R = 2.5) -> clamp -> Jacobi-pCG
+    K(rho)u = f -> compliance -> sensitivities -> filter adjoint (slab_evaluate).  NCCL
+    allreduces the CG scalars; the z halo travels as NVLink peer stores from inside the update
+    kernels (--halo peer, CUDA IPC) or as NCCL send/recv (--halo nccl); the x planes after each
+    solve go through NCCL send/recv."""
     import torch
 
     import paper_2004_05756_b200 as tb
-    from paper_2004_05756_b200 import configs
-    from paper_2004_05756_b200.slab import SlabSolver, TorchComm, dist_pcg_solve, partition
+    from paper_2004_05756_b200 import _lib, configs
+    from paper_2004_05756_b200.slab import SlabFilter, SlabSolver, TorchComm, partition, slab_evaluate
 
     rank, local, world = rank_info()
     torch.cuda.set_device(local)
@@ -700,28 +700,41 @@ def run_cfg4(args):
     mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
     slab = partition(prob.mesh.nz, world)[rank]
     sv = SlabSolver(prob.mesh, prob.k_e, prob.f, prob.fixed, mat, slab, device=dev)
-    rho = torch.as_tensor(sv.local_elems(prob.psi).copy(), device=dev)
-    sv.rho = rho
+    fl = SlabFilter(prob.mesh, prob.radius, slab, device=dev)
+    psi = torch.as_tensor(sv.local_elems(prob.psi).copy(), device=dev)
     comm = TorchComm(peer=(args.halo == "peer"))
-    dist_pcg_solve([sv], comm, rtol=prob.rtol)  # warm-up
+    clocks = Clocks(dev.index)
+    clocks.start()
+    ev = slab_evaluate([sv], [fl], comm, [psi], rtol=prob.rtol)  # warm-up (maps the peers, first touches)
+    del ev
     dist.barrier()
     torch.cuda.synchronize()
+    launches0 = _lib.lib().tb_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    iters, rel, ok = dist_pcg_solve([sv], comm, rtol=prob.rtol)
+    ev = slab_evaluate([sv], [fl], comm, [psi], rtol=prob.rtol)
     e1.record()
     torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = _lib.lib().tb_launch_count() - launches0
     t = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    m = prob.mesh
     if rank == 0:
+        it = ev.iterations
         print(json.dumps({
-            "metric": "FE solve s/eval (slab-sharded)", "value": float(t.item()), "unit": "s/eval", "n_gpus": world,
+            "metric": METRIC, "value": float(t.item()), "unit": UNIT, "n_gpus": world,
             "steps": 1, "warmup": 1, "ms_per_step": float(t.item()) * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg 4 recipe)",
-            "config": {"workload": f"cfg4 {prob.mesh.nx}x{prob.mesh.ny}x{prob.mesh.nz} Hex8, {prob.mesh.n_dofs} DOF, "
-                                   f"z-slabs x{world}, Jacobi-pCG to {prob.rtol:g}",
-                       "parallelism": f"slab{world}", "halo": args.halo, "pcg_iterations": iters,
-                       "converged": ok}}), flush=True)
+            "config": {"workload": f"cfg4 {m.nx}x{m.ny}x{m.nz} Hex8, {m.n_dofs} DOF, z-slabs x{world}: "
+                                   f"filter R={prob.radius:g} + Jacobi-pCG to {prob.rtol:g} + compliance + "
+                                   "sensitivities + filter adjoint",
+                       "parallelism": f"slab{world}", "halo": args.halo, "pcg_iterations": it,
+                       "filter_iterations": list(ev.filter_iterations), "J": ev.j, "clamp_width": ev.clamp_width,
+                       "seed": args.seed},
+            "pcg": {"bytes_per_iteration_per_rank": 8 * (12 * sv.local.n_dofs + sv.local.n_elems),
+                    "us_per_iteration_upper_bound": float(t.item()) / max(it, 1) * 1e6},
+            "gpu_launches": int(launches), "clocks": clk}), flush=True)
     dist.barrier()
     comm.close()
     dist.destroy_process_group()

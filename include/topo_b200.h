@@ -143,6 +143,25 @@ int tb_filter_apply(tb_filter* filt, const double* psi, double* phi, double* rho
 int tb_filter_adjoint(tb_filter* filt, const double* v, double* w, double rtol, int* iters,
                       void* stream);
 
+/* ---- slab-distributed filter (BASELINE cfg 4): the filter covers one z-slab's
+ * local grid (owned node planes plus one ghost plane per interior side), as tb_plan_* do for
+ * the elasticity solve.  Ghost node planes are masked (never updated); reductions run over the
+ * owned planes [k0, k1).  Phases, `red` and the halo contract are those of tb_pcg_dist_phase
+ * (phase 0 takes the load vector b instead of rho).  Replaces, per rank, the factor-once /
+ * solve pair of HelmholtzFilter (filtering.py:54-71, 78-97, 99-114). */
+int tb_filter_set_owned_planes(tb_filter* filt, int k0, int k1);
+int tb_filter_dist_phase(tb_filter* filt, int phase, const double* b, double rtol, int maxit,
+                         int parity, void* stream);
+int tb_filter_dist_buffers(tb_filter* filt, double** x, double** z, double** red);
+int tb_filter_dist_state(tb_filter* filt, int* iters, int* done, double* rr, double* bb,
+                         void* stream);
+int tb_filter_set_halo_peers(tb_filter* filt, double* lo_dst, double* hi_dst);
+/* Grid transfers of the filter (filtering.py:73-76, 95-97, 106-114): mode 0 element -> node,
+ * out_n = scale * sum_{e∋n} in_e; mode 1 node -> element, out_e = scale * sum_{n∈e} in_n
+ * (same summation order as tb_filter_apply / tb_filter_adjoint). */
+int tb_filter_transfer(tb_filter* filt, int mode, const double* in, double scale, double* out,
+                       void* stream);
+
 /* ---- reduced-order model (rom.py:182-390); phi is (n_dofs x k) ROW-major ---- */
 /* out[k*d + j] = sum_i phi[i*k + j] * vec[d*n + i] for nvec <= 16 stacked vectors of length n
  * (Phi^T f, rom.py:251, 289; also Q^T S of the POD) */

@@ -163,7 +163,7 @@ void HelmOp::launch_dinv(double* dinv, cudaStream_t s) const {
   if (g.dim == 2)
     { k_node_dinv<2, 1, false><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, filt->H2, nullptr, nullptr, dinv); tb::launched(); }
   else
-    { k_node_dinv<3, 1, false><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, filt->H3, nullptr, nullptr, dinv); tb::launched(); }
+    { k_node_dinv<3, 1, false><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, filt->H3, nullptr, filt->d_fixed, dinv); tb::launched(); }
 }
 int HelmOp::fused_blocks() const { return nblk(filt->g.n_nodes); }
 
@@ -631,6 +631,7 @@ int tb_filter_destroy(tb_filter* filt) {
   cudaSetDevice(F->device);
   F->work.release();
   if (F->d_b) cudaFree(F->d_b);
+  if (F->d_fixed) cudaFree(F->d_fixed);
   delete F;
   return TB_OK;
 }
@@ -648,6 +649,17 @@ int tb_filter_load_vector(tb_filter* filt, const double* psi, double* b, void* s
   return TB_OK;
 }
 
+}  // extern "C"
+
+// a whole-grid solve after slab phases: dots over every node plane again
+static int filter_single_mode(tb_filter_impl* F) {
+  if (!F->dist) return TB_OK;
+  F->dist = 0;
+  return F->work.set_fields(0, F->own_k0, F->own_k1);
+}
+
+extern "C" {
+
 int tb_filter_apply(tb_filter* filt, const double* psi, double* phi, double* rho, double rtol, int* iters,
                     void* stream) {
   TB_GUARD(filt && psi && rho, "null argument");
@@ -655,6 +667,7 @@ int tb_filter_apply(tb_filter* filt, const double* psi, double* phi, double* rho
   const Grid& g = F->g;
   cudaStream_t s = (cudaStream_t)stream;
   TB_TRY(tb_filter_load_vector(filt, psi, F->d_b, stream));
+  TB_TRY(filter_single_mode(F));
   TB_TRY(pcg_solve(F->op, F->work, F->d_b, F->work.x, rtol, 10000, iters, nullptr, s));
   const double inv_nn = (g.dim == 2) ? 0.25 : 0.125;
   if (g.dim == 2)
@@ -677,11 +690,104 @@ int tb_filter_adjoint(tb_filter* filt, const double* v, double* w, double rtol, 
   else
     { k_elem_to_node<3><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, v, inv_nn, 1.0, F->d_b); tb::launched(); }
   TB_CHECK_LAUNCH();
+  TB_TRY(filter_single_mode(F));
   TB_TRY(pcg_solve(F->op, F->work, F->d_b, F->work.x, rtol, 10000, iters, nullptr, s));
   if (g.dim == 2)
     { k_node_to_elem<2><<<nblk(g.n_elems), kBlock, 0, s>>>(g, F->work.x, F->vol_share, w); tb::launched(); }
   else
     { k_node_to_elem<3><<<nblk(g.n_elems), kBlock, 0, s>>>(g, F->work.x, F->vol_share, w); tb::launched(); }
+  TB_CHECK_LAUNCH();
+  return TB_OK;
+}
+
+// ---- slab-distributed Helmholtz filter (BASELINE cfg 4; same phases as tb_pcg_dist_phase) ----
+int tb_filter_set_owned_planes(tb_filter* filt, int k0, int k1) {
+  TB_GUARD(filt != nullptr, "null filter");
+  auto* F = reinterpret_cast<tb_filter_impl*>(filt);
+  const Grid& g = F->g;
+  TB_GUARD(g.dim == 3, "slab filters are 3D");
+  TB_GUARD(0 <= k0 && k0 < k1 && k1 <= g.nnz, "owned node planes [%d, %d) outside [0, %d]", k0, k1, g.nnz);
+  const int64_t pd = (int64_t)g.nnx * g.nny;
+  if (F->d_fixed == nullptr) TB_CUDA(cudaMalloc(&F->d_fixed, (size_t)g.n_nodes));
+  // ghost node planes are rows this rank never updates: Dirichlet-masked like the slab plan's
+  TB_CUDA(cudaMemset(F->d_fixed, 0, (size_t)g.n_nodes));
+  if (k0 > 0) TB_CUDA(cudaMemset(F->d_fixed, 1, (size_t)(k0 * pd)));
+  if (k1 < g.nnz) TB_CUDA(cudaMemset(F->d_fixed + k1 * pd, 1, (size_t)((g.nnz - k1) * pd)));
+  F->own_k0 = k0;
+  F->own_k1 = k1;
+  F->work.plane = pd;
+  F->work.own0 = k0 * pd;
+  F->work.own1 = k1 * pd;
+  return F->work.set_fields(F->dist, k0, k1);
+}
+
+int tb_filter_dist_phase(tb_filter* filt, int phase, const double* b, double rtol, int maxit, int parity,
+                         void* stream) {
+  TB_GUARD(filt != nullptr, "null filter");
+  auto* F = reinterpret_cast<tb_filter_impl*>(filt);
+  TB_GUARD(F->work.plane > 0, "tb_filter_dist_phase needs tb_filter_set_owned_planes first");
+  if (phase == 0) {
+    TB_GUARD(b != nullptr, "phase 0 needs b");
+    TB_GUARD(rtol > 0.0 && maxit >= 1, "rtol must be > 0 and maxit >= 1");
+    if (!F->dist) {
+      F->dist = 1;
+      TB_TRY(F->work.set_fields(1, F->own_k0, F->own_k1));
+    }
+  }
+  return pcg_dist_phase(F->op, F->work, phase, b, rtol, maxit, parity, (cudaStream_t)stream);
+}
+
+int tb_filter_dist_buffers(tb_filter* filt, double** x, double** z, double** red) {
+  TB_GUARD(filt != nullptr, "null filter");
+  auto* F = reinterpret_cast<tb_filter_impl*>(filt);
+  if (x) *x = F->work.x;
+  if (z) *z = F->work.z;
+  if (red) *red = F->work.st->red;
+  return TB_OK;
+}
+
+int tb_filter_dist_state(tb_filter* filt, int* iters, int* done, double* rr, double* bb, void* stream) {
+  TB_GUARD(filt != nullptr, "null filter");
+  auto* F = reinterpret_cast<tb_filter_impl*>(filt);
+  cudaStream_t s = (cudaStream_t)stream;
+  TB_CUDA(cudaMemcpyAsync(F->work.h_st, F->work.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+  TB_CUDA(cudaStreamSynchronize(s));
+  const PcgState& h = *F->work.h_st;
+  if (iters) *iters = h.iters;
+  if (done) *done = h.done;
+  if (rr) *rr = h.rr;
+  if (bb) *bb = h.bb;
+  return TB_OK;
+}
+
+int tb_filter_set_halo_peers(tb_filter* filt, double* lo_dst, double* hi_dst) {
+  TB_GUARD(filt != nullptr, "null filter");
+  auto* F = reinterpret_cast<tb_filter_impl*>(filt);
+  TB_GUARD(F->work.plane > 0, "tb_filter_set_halo_peers needs tb_filter_set_owned_planes first");
+  TB_GUARD(lo_dst == nullptr || F->own_k0 > 0, "no lower neighbour: owned planes start at 0");
+  TB_GUARD(hi_dst == nullptr || F->own_k1 < F->g.nnz, "no upper neighbour: owned planes reach the top");
+  F->work.halo_lo = lo_dst;
+  F->work.halo_hi = hi_dst;
+  return TB_OK;
+}
+
+int tb_filter_transfer(tb_filter* filt, int mode, const double* in, double scale, double* out, void* stream) {
+  TB_GUARD(filt && in && out, "null argument");
+  TB_GUARD(mode == 0 || mode == 1, "mode must be 0 (element -> node) or 1 (node -> element), got %d", mode);
+  auto* F = reinterpret_cast<tb_filter_impl*>(filt);
+  const Grid& g = F->g;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (mode == 0) {
+    if (g.dim == 2)
+      { k_elem_to_node<2><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, in, scale, 1.0, out); tb::launched(); }
+    else
+      { k_elem_to_node<3><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, in, scale, 1.0, out); tb::launched(); }
+  } else {
+    if (g.dim == 2)
+      { k_node_to_elem<2><<<nblk(g.n_elems), kBlock, 0, s>>>(g, in, scale, out); tb::launched(); }
+    else
+      { k_node_to_elem<3><<<nblk(g.n_elems), kBlock, 0, s>>>(g, in, scale, out); tb::launched(); }
+  }
   TB_CHECK_LAUNCH();
   return TB_OK;
 }

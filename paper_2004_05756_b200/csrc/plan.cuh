@@ -88,6 +88,9 @@ struct tb_filter_impl {
   bool pat_ok = false;
   Mat<8> H3{};
   double* d_b = nullptr;
+  // slab mode (tb_filter_set_owned_planes): ghost node planes masked (dinv 0), owned [k0, k1)
+  uint8_t* d_fixed = nullptr;
+  int dist = 0, own_k0 = 0, own_k1 = 1 << 30;
   HelmOp op;
   PcgWork work;
 };

@@ -41,7 +41,8 @@ import numpy as np
 from . import _lib
 from .fem import StructuredMesh, build_mesh_3d
 
-__all__ = ["Slab", "partition", "SlabSolver", "LocalComm", "TorchComm", "dist_pcg_solve"]
+__all__ = ["Slab", "partition", "SlabSolver", "SlabFilter", "LocalComm", "TorchComm", "dist_pcg_solve",
+           "slab_evaluate", "SlabEvaluation"]
 
 
 @dataclass(frozen=True)
@@ -180,10 +181,124 @@ class SlabSolver:
         _lib.check(_lib.lib().tb_ipc_get_handle(_lib.P(self.z.data_ptr()), h), "ipc handle")
         return h.raw
 
+    # -- element-level steps of the evaluation (slab_evaluate)
+    def clamp(self, rho_raw):
+        """(rho, local clamp width) of tb_clamp_density (hdm.py:144-154) on the local elements."""
+        t = _lib.torch()
+        rho = t.empty_like(rho_raw)
+        cw = ctypes.c_double(0.0)
+        _lib.check(_lib.lib().tb_clamp_density(self._plan, _lib.ptr(rho_raw), _lib.ptr(rho), ctypes.byref(cw),
+                                               _lib.stream_ptr(self.device)), "slab clamp")
+        return rho, float(cw.value)
+
+    def sensitivity(self, rho, u):
+        """Compliance sensitivities of every local element (hdm.py:211-222); u must hold the
+        ghost planes (halo of x)."""
+        t = _lib.torch()
+        out = t.empty(self.local.n_elems, dtype=t.float64, device=self.device)
+        _lib.check(_lib.lib().tb_element_sensitivity(self._plan, _lib.ptr(rho), _lib.ptr(u), _lib.ptr(u), _lib.P(0),
+                                                     _lib.ptr(out), _lib.stream_ptr(self.device)), "slab sensitivity")
+        return out
+
+    def owned_compliance(self, u):
+        """f . u over the owned dofs (f is zero on the ghost planes)."""
+        out = ctypes.c_double(0.0)
+        _lib.check(_lib.lib().tb_dot(self._plan, _lib.ptr(self.f), _lib.ptr(u), self.local.n_dofs, ctypes.byref(out),
+                                     _lib.stream_ptr(self.device)), "slab compliance")
+        return float(out.value)
+
+    def owned_elems(self):
+        """(local slice, global slice) of the element planes this rank owns: [k0, min(k1, nz))."""
+        s = self.slab
+        top = min(s.k1, self.mesh.nz)
+        pe = self.plane_elems
+        return slice((s.k0 - s.e0) * pe, (top - s.e0) * pe), slice(s.k0 * pe, top * pe)
+
     def state(self):
         it, done, rr, bb = ctypes.c_int(), ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
         _lib.check(_lib.lib().tb_pcg_dist_state(self._plan, ctypes.byref(it), ctypes.byref(done), ctypes.byref(rr),
                                                 ctypes.byref(bb), _lib.stream_ptr(self.device)), "dist state")
+        return it.value, done.value, rr.value, bb.value
+
+
+class SlabFilter:
+    """Rank-local part of the distributed Helmholtz filter (HelmholtzFilter, filtering.py:47-114)
+    on one z-slab: the same local grid and owned planes as the rank's SlabSolver, a scalar
+    field (one value per node), solved with the phases of dist_pcg_solve."""
+
+    def __init__(self, mesh: StructuredMesh, radius: float, slab: Slab, device=None, rtol: float = 1e-13):
+        t = _lib.torch()
+        if not mesh.nz:
+            raise ValueError("slab decomposition is for 3D meshes")
+        self.mesh, self.slab = mesh, slab
+        self.device = _lib.require_cuda(device)
+        self.local = build_mesh_3d(mesh.nx, mesh.ny, slab.local_nz, mesh.h)
+        self.plane_nodes = (mesh.nx + 1) * (mesh.ny + 1)
+        self.plane_dofs = self.plane_nodes  # one unknown per node
+        self.plane_elems = mesh.nx * mesh.ny
+        self.vol_share = mesh.h**3 / 8.0  # b_e entries (filtering.py:75-76), 3D
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().tb_filter_create(3, mesh.nx, mesh.ny, slab.local_nz, mesh.h, float(radius),
+                                               self.device.index, ctypes.byref(h)), "slab filter")
+        self._h = h
+        k0, k1 = slab.own_local
+        _lib.check(_lib.lib().tb_filter_set_owned_planes(h, k0, k1), "filter owned planes")
+        nl = self.local.n_nodes
+        px, pz, pr = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.check(_lib.lib().tb_filter_dist_buffers(h, ctypes.byref(px), ctypes.byref(pz), ctypes.byref(pr)), "bufs")
+        self.x = t.as_tensor(_CudaArray(px.value, nl, self.device), device=self.device)
+        self.z = t.as_tensor(_CudaArray(pz.value, nl, self.device), device=self.device)
+        self.red = t.as_tensor(_CudaArray(pr.value, 4, self.device), device=self.device)
+        self.b = t.zeros(nl, dtype=t.float64, device=self.device)
+        self.rtol, self.maxit = float(rtol), 200000
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib._lib is not None:
+            _lib._lib.tb_filter_destroy(h)
+            self._h = None
+
+    def plane(self, vec, local_plane):
+        return vec[local_plane * self.plane_dofs:(local_plane + 1) * self.plane_dofs]
+
+    def set_load(self, elem_values, scale):
+        """b_n = scale * sum_{e∋n} v_e over the local elements (filtering.py:73-76, 106-108)."""
+        _lib.check(_lib.lib().tb_filter_transfer(self._h, 0, _lib.ptr(elem_values), float(scale), _lib.ptr(self.b),
+                                                 _lib.stream_ptr(self.device)), "filter load")
+
+    def to_elems(self, scale):
+        """out_e = scale * sum_{n∈e} x_n for every local element (filtering.py:95-97, 112-114);
+        x must hold the ghost planes (halo of x)."""
+        t = _lib.torch()
+        out = t.empty(self.local.n_elems, dtype=t.float64, device=self.device)
+        _lib.check(_lib.lib().tb_filter_transfer(self._h, 1, _lib.ptr(self.x), float(scale), _lib.ptr(out),
+                                                 _lib.stream_ptr(self.device)), "filter average")
+        return out
+
+    def phase(self, p, parity=0):
+        b = _lib.ptr(self.b) if p == 0 else _lib.P(0)
+        _lib.check(_lib.lib().tb_filter_dist_phase(self._h, p, b, self.rtol, self.maxit, parity,
+                                                   _lib.stream_ptr(self.device)), f"filter dist phase {p}")
+
+    def set_halo_peers(self, lo_dst: int, hi_dst: int):
+        _lib.check(_lib.lib().tb_filter_set_halo_peers(self._h, _lib.P(lo_dst or None), _lib.P(hi_dst or None)),
+                   "filter halo peers")
+
+    def ghost_addresses(self, z_base: int):
+        k0, k1 = self.slab.own_local
+        lo = z_base if self.slab.ghost_lo else 0
+        hi = z_base + 8 * k1 * self.plane_dofs if self.slab.ghost_hi else 0
+        return lo, hi
+
+    def z_ipc_handle(self) -> bytes:
+        h = ctypes.create_string_buffer(64)
+        _lib.check(_lib.lib().tb_ipc_get_handle(_lib.P(self.z.data_ptr()), h), "ipc handle")
+        return h.raw
+
+    def state(self):
+        it, done, rr, bb = ctypes.c_int(), ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+        _lib.check(_lib.lib().tb_filter_dist_state(self._h, ctypes.byref(it), ctypes.byref(done), ctypes.byref(rr),
+                                                   ctypes.byref(bb), _lib.stream_ptr(self.device)), "filter state")
         return it.value, done.value, rr.value, bb.value
 
 
@@ -208,6 +323,13 @@ class LocalComm:
             total = total + s.red
         for s in solvers:
             s.red.copy_(total)
+
+    def reduce_scalars(self, values, op="sum"):
+        """values: one list of floats per local solver -> the element-wise sum / max over them."""
+        out = list(values[0])
+        for v in values[1:]:
+            out = [a + b if op == "sum" else max(a, b) for a, b in zip(out, v)]
+        return out
 
     def halo(self, solvers, name="z"):
         if self.peer and name == "z":
@@ -278,6 +400,15 @@ class TorchComm:
         else:
             self.dist.all_reduce(red, group=self.group)
 
+    def reduce_scalars(self, values, op="sum"):
+        """values: [floats of this rank's solver] -> the element-wise sum / max over the ranks."""
+        t = _lib.torch()
+        dev = "cpu" if self.dist.get_backend(self.group) == "gloo" else t.device("cuda", t.cuda.current_device())
+        v = t.tensor(list(values[0]), dtype=t.float64, device=dev)
+        self.dist.all_reduce(v, op=self.dist.ReduceOp.SUM if op == "sum" else self.dist.ReduceOp.MAX,
+                             group=self.group)
+        return [float(a) for a in v.cpu()]
+
     def halo(self, solvers, name="z"):
         if self.peer and name == "z":
             return
@@ -332,6 +463,60 @@ def dist_pcg_solve(solvers, comm, rtol=1e-8, maxit=200000, check_every=8):
 
                     raise IndefiniteMatrixError("distributed pCG breakdown")
                 return iters, (rr / bb) ** 0.5 if bb > 0 else 0.0, done == 1
+
+
+@dataclass
+class SlabEvaluation:
+    """Result of slab_evaluate for this process's slabs: global scalars plus, per slab, the
+    local (owned + ghost layer) element fields and node vectors."""
+
+    j: float
+    clamp_width: float
+    iterations: int
+    filter_iterations: tuple
+    rho: list
+    u: list
+    s: list
+    g: list
+
+
+def slab_evaluate(solvers, filters, comm, psi_locals, rtol=None, filter_rtol=None) -> SlabEvaluation:
+    """One compliance design evaluation, HdmSolver.solve + gradient (hdm.py:170-209), over
+    z-slabs (BASELINE cfg 4: "full HDM solve, sensitivities and filter"):
+
+        psi -> b = (h^3/8) sum_e psi_e -> H phi = b (distributed pCG) -> x halo -> rho_raw = mean phi
+            -> clamp (max width over ranks) -> K(rho) u = f (distributed pCG) -> u halo
+            -> J = sum_ranks f.u (owned rows) ; s_e on every local element (ghost layer too)
+            -> b = (1/8) sum_e s_e -> H mu = b -> x halo -> g_e = (h^3/8) sum mu
+
+    ``psi_locals`` are the local element slices (owned planes plus the ghost layer, as
+    SlabSolver.local_elems).  Collectives: the two 4-double allreduces per pCG iteration, one
+    plane halo of x after each of the three solves, two scalar allreduces (clamp width, J)."""
+    for f, psi in zip(filters, psi_locals):
+        f.set_load(psi, f.vol_share)
+    fit1 = dist_pcg_solve(filters, comm, rtol=filter_rtol or filters[0].rtol)[0]
+    comm.halo(filters, "x")
+    rhos, widths = [], []
+    for s, f in zip(solvers, filters):
+        r, w = s.clamp(f.to_elems(0.125))
+        rhos.append(r)
+        widths.append([w])
+    cw = comm.reduce_scalars(widths, "max")[0]
+    for s, r in zip(solvers, rhos):
+        s.rho = r
+    it, _, ok = dist_pcg_solve(solvers, comm, rtol=rtol or solvers[0].rtol)
+    if not ok:
+        raise _lib.NotConvergedError(f"distributed pCG did not converge in {it} iterations")
+    comm.halo(solvers, "x")
+    us = [s.x.clone() for s in solvers]
+    j = comm.reduce_scalars([[s.owned_compliance(u)] for s, u in zip(solvers, us)], "sum")[0]
+    sens = [s.sensitivity(r, u) for s, r, u in zip(solvers, rhos, us)]
+    for f, v in zip(filters, sens):
+        f.set_load(v, 0.125)
+    fit2 = dist_pcg_solve(filters, comm, rtol=filter_rtol or filters[0].rtol)[0]
+    comm.halo(filters, "x")
+    grads = [f.to_elems(f.vol_share) for f in filters]
+    return SlabEvaluation(j, cw, it, (fit1, fit2), rhos, us, sens, grads)
 
 
 class SlabRom:

@@ -28,55 +28,38 @@ def test_partition_covers_planes(nz, r):
         partition(2, 3)
 
 
-class CpuSlab:
-    """Test-side numpy restatement of the six phases of tb_pcg_dist_phase (same masks, same
-    reductions) over the oracle's sparse stiffness of the slab grid."""
+class _CpuPcg:
+    """Test-side numpy restatement of the six phases of tb_pcg_dist_phase / tb_filter_dist_phase
+    (same masks, same reductions) over a local sparse matrix ``self.K`` and load ``self.b``."""
 
-    def __init__(self, prob, slab: Slab):
-        from oracle.fem import assemble, build_grid
-
-        m = prob.mesh
-        self.slab = slab
-        self.plane_dofs = 3 * (m.nx + 1) * (m.ny + 1)
-        pe = m.nx * m.ny
-        self.grid = build_grid(m.nx, m.ny, m.h, nz=slab.local_nz)
-        d0 = slab.e0 * self.plane_dofs
-        nl = self.grid.n_dofs
-        fixed = np.zeros(m.n_dofs, bool)
-        fixed[prob.fixed] = True
-        fl = fixed[d0:d0 + nl].copy()
-        if slab.ghost_lo:
-            fl[:self.plane_dofs] = True
-        if slab.ghost_hi:
-            fl[-self.plane_dofs:] = True
-        self.fixed = fl
-        self.b = np.where(fl, 0.0, prob.f[d0:d0 + nl])
-        rho = prob.psi[slab.e0 * pe:slab.e1 * pe]
-        alpha = configs.RHO_L + (1 - configs.RHO_L) * rho**3
-        self.K = assemble(self.grid, prob.k_e, alpha).tocsr()
+    def _init_vectors(self, nl, own_planes):
         self.x = torch.zeros(nl, dtype=torch.float64)
         self.z = torch.zeros(nl, dtype=torch.float64)
         self.red = torch.zeros(4, dtype=torch.float64)
         self.p = [np.zeros(nl), np.zeros(nl)]
         self.q = np.zeros(nl)
         self.own = np.zeros(nl, bool)
-        k0, k1 = slab.own_local
+        k0, k1 = own_planes
         self.own[k0 * self.plane_dofs:k1 * self.plane_dofs] = True
-        self.rtol, self.maxit = 1e-8, 100000
+        self.maxit = 100000
 
     def plane(self, vec, k):
         return vec[k * self.plane_dofs:(k + 1) * self.plane_dofs]
 
+    def _operator(self):
+        return self.K
+
     def phase(self, ph, parity=0):
         x, z, red = self.x.numpy(), self.z.numpy(), self.red.numpy()
         if ph == 0:
+            self.K = self._operator()
             diag = self.K.diagonal()
             self.dinv = np.where(self.fixed, 0.0, 1.0 / diag)
-            self.r = self.b.copy()
+            self.r = np.where(self.fixed, 0.0, self.b)
             x[:] = 0.0
-            z[:] = self.dinv * self.r
+            z[:] = np.where(self.own, self.dinv * self.r, 0.0)
             self.p = [np.zeros_like(z), np.zeros_like(z)]
-            red[1], red[2] = self.r @ z, self.r @ self.r
+            red[1], red[2] = self.r[self.own] @ z[self.own], self.r[self.own] @ self.r[self.own]
             self.st = dict(iters=0, done=0)
         elif ph == 1:
             self.st.update(rz=red[1], bb=red[2], rr=red[2], tol2=self.rtol**2 * red[2], beta=0.0,
@@ -94,11 +77,11 @@ class CpuSlab:
             else:
                 self.st["alpha"] = self.st["rz"] / red[0]
         elif ph == 4:
-            a, pnew, free = self.st["alpha"], self.p[(parity + 1) & 1], self.dinv != 0
-            x[free] += a * pnew[free]
-            self.r[free] -= a * self.q[free]
-            z[:] = np.where(free, self.dinv * self.r, 0.0)
-            red[1], red[2] = self.r[free] @ z[free], self.r[free] @ self.r[free]
+            a, pnew, upd = self.st["alpha"], self.p[(parity + 1) & 1], self.own & (self.dinv != 0)
+            x[upd] += a * pnew[upd]
+            self.r[upd] -= a * self.q[upd]
+            z[self.own] = np.where(upd, self.dinv * self.r, 0.0)[self.own]
+            red[1], red[2] = self.r[upd] @ z[upd], self.r[upd] @ self.r[upd]
         elif ph == 5:
             st = self.st
             st["iters"] += 1
@@ -112,6 +95,95 @@ class CpuSlab:
     def state(self):
         s = self.st
         return s["iters"], s["done"], s["rr"], s["bb"]
+
+
+class CpuSlab(_CpuPcg):
+    """Elasticity slab (SlabSolver's interface) over the oracle's sparse stiffness."""
+
+    def __init__(self, prob, slab: Slab):
+        from oracle.fem import build_grid
+
+        m = prob.mesh
+        self.prob, self.slab, self.mesh = prob, slab, m
+        self.plane_dofs = 3 * (m.nx + 1) * (m.ny + 1)
+        self.plane_elems = m.nx * m.ny
+        self.grid = build_grid(m.nx, m.ny, m.h, nz=slab.local_nz)
+        d0 = slab.e0 * self.plane_dofs
+        nl = self.grid.n_dofs
+        fixed = np.zeros(m.n_dofs, bool)
+        fixed[prob.fixed] = True
+        fl = fixed[d0:d0 + nl].copy()
+        if slab.ghost_lo:
+            fl[:self.plane_dofs] = True
+        if slab.ghost_hi:
+            fl[-self.plane_dofs:] = True
+        self.fixed = fl
+        self.b = np.where(fl, 0.0, prob.f[d0:d0 + nl])
+        self.rho = torch.as_tensor(self.local_elems(prob.psi).copy())
+        self._init_vectors(nl, slab.own_local)
+        self.rtol = 1e-8
+
+    def local_elems(self, field):
+        return field[self.slab.e0 * self.plane_elems:self.slab.e1 * self.plane_elems]
+
+    def _operator(self):
+        from oracle.fem import assemble
+
+        alpha = configs.RHO_L + (1 - configs.RHO_L) * self.rho.numpy() ** 3
+        return assemble(self.grid, self.prob.k_e, alpha).tocsr()
+
+    def clamp(self, rho_raw):
+        r = rho_raw.numpy()
+        c = np.clip(r, configs.RHO_L, 1.0)
+        return torch.as_tensor(c), float(np.max(np.abs(c - r), initial=0.0))
+
+    def sensitivity(self, rho, u):
+        ul = u.numpy()[self.grid.elem_dofs]
+        c = ((ul @ self.prob.k_e) * ul).sum(axis=1)
+        dal = (1 - configs.RHO_L) * 3 * rho.numpy() ** 2
+        return torch.as_tensor(-dal * c)
+
+    def owned_compliance(self, u):
+        return float(self.b @ u.numpy())
+
+    def owned_elems(self):
+        s, pe = self.slab, self.plane_elems
+        top = min(s.k1, self.mesh.nz)
+        return slice((s.k0 - s.e0) * pe, (top - s.e0) * pe), slice(s.k0 * pe, top * pe)
+
+
+class CpuSlabFilter(_CpuPcg):
+    """Helmholtz filter slab (SlabFilter's interface) over the oracle's scalar matrix."""
+
+    def __init__(self, prob, slab: Slab):
+        from oracle.fem import assemble, build_grid, helmholtz_element_matrices
+        from oracle.hdm import LENGTH_SCALE_FACTOR
+
+        m = prob.mesh
+        self.slab, self.mesh = slab, m
+        self.plane_dofs = (m.nx + 1) * (m.ny + 1)
+        self.grid = build_grid(m.nx, m.ny, m.h, nz=slab.local_nz)
+        h_e, _ = helmholtz_element_matrices(LENGTH_SCALE_FACTOR * prob.radius, m.h, 3)
+        self.K = assemble(self.grid, h_e, None, scalar=True).tocsr()
+        nl = self.grid.n_nodes
+        k0, k1 = slab.own_local
+        self.fixed = np.ones(nl, bool)
+        self.fixed[k0 * self.plane_dofs:k1 * self.plane_dofs] = False
+        rows = self.grid.elem_nodes.ravel()
+        cols = np.repeat(np.arange(self.grid.n_elems), 8)
+        import scipy.sparse as sp
+
+        self.inc = sp.csr_matrix((np.ones(rows.size), (rows, cols)), shape=(nl, self.grid.n_elems))
+        self.vol_share = m.h**3 / 8
+        self.b = np.zeros(nl)
+        self._init_vectors(nl, slab.own_local)
+        self.rtol = 1e-13
+
+    def set_load(self, v, scale):
+        self.b = self.inc @ (np.asarray(v, float) * scale)
+
+    def to_elems(self, scale):
+        return torch.as_tensor((self.inc.T @ self.x.numpy()) * scale)
 
 
 def _problem():
@@ -309,3 +381,126 @@ def test_cuda_slab_rom_emulated_on_one_gpu(cuda):
     assert torch.abs(uh - uh_ref).max() <= 1e-10 * torch.abs(uh_ref).max()
     for a, b in zip(norms, n_ref):
         assert abs(a - b) <= 1e-9 * b
+
+
+# ---------------------------------------------------------------------------------------------
+# Distributed design evaluation (filter -> solve -> J -> sensitivities -> filter adjoint)
+# ---------------------------------------------------------------------------------------------
+def _eval_problem():
+    return configs.cfg3(seed=6, nx=5, ny=3, nz=8)
+
+
+def _oracle_eval(prob):
+    from oracle.fem import build_grid
+    from oracle.hdm import Filter, Hdm, Material
+
+    g = build_grid(prob.mesh.nx, prob.mesh.ny, 1.0, nz=prob.mesh.nz)
+    hdm = Hdm(g, prob.k_e, Filter(g, prob.radius), prob.f, prob.fixed, Material(configs.RHO_L, configs.P_SIMP))
+    sol = hdm.solve(prob.psi)
+    return sol, hdm.gradient(sol)
+
+
+def _gather_owned(solvers, ev, n_elems):
+    rho, grad = np.zeros(n_elems), np.zeros(n_elems)
+    for s, r, g in zip(solvers, ev.rho, ev.g):
+        sl, sg = s.owned_elems()
+        rho[sg] = r[sl].cpu().numpy()
+        grad[sg] = g[sl].cpu().numpy()
+    return rho, grad
+
+
+def _check_eval(prob, j, cw, rho, grad):
+    sol, g_ref = _oracle_eval(prob)
+    assert abs(j - sol["j"]) <= 1e-8 * abs(sol["j"])
+    assert abs(cw - sol["clamp_width"]) <= 1e-9
+    assert np.abs(rho - sol["rho"]).max() <= 1e-6 * np.abs(sol["rho"]).max()
+    assert np.abs(grad - g_ref).max() <= 1e-6 * np.abs(g_ref).max()
+
+
+def test_slab_evaluate_local_comm_cpu():
+    from paper_2004_05756_b200.slab import slab_evaluate
+
+    prob = _eval_problem()
+    slabs = partition(prob.mesh.nz, 3)
+    solvers = [CpuSlab(prob, s) for s in slabs]
+    filters = [CpuSlabFilter(prob, s) for s in slabs]
+    psis = [torch.as_tensor(s.local_elems(prob.psi).copy()) for s in solvers]
+    ev = slab_evaluate(solvers, filters, LocalComm(), psis, rtol=1e-12)
+    rho, grad = _gather_owned(solvers, ev, prob.mesh.n_elems)
+    _check_eval(prob, ev.j, ev.clamp_width, rho, grad)
+
+
+def _gloo_eval_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2004_05756_b200.slab import slab_evaluate
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    prob = _eval_problem()
+    slab = partition(prob.mesh.nz, world)[rank]
+    s, f = CpuSlab(prob, slab), CpuSlabFilter(prob, slab)
+    ev = slab_evaluate([s], [f], TorchComm(), [torch.as_tensor(s.local_elems(prob.psi).copy())], rtol=1e-12)
+    rho, grad = _gather_owned([s], ev, prob.mesh.n_elems)
+    sl, sg = s.owned_elems()
+    q.put((rank, ev.j, ev.clamp_width, sg.start, sg.stop, rho[sg].copy(), grad[sg].copy()))
+    dist.destroy_process_group()
+
+
+def test_slab_evaluate_gloo_world_size_2():
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_eval_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=180) for _ in procs), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    prob = _eval_problem()
+    n = prob.mesh.n_elems
+    rho, grad = np.zeros(n), np.zeros(n)
+    assert res[0][1] == res[1][1] and res[0][2] == res[1][2]  # every rank holds the same J, width
+    for _, _, _, a, b, r, g in res:
+        rho[a:b], grad[a:b] = r, g
+    _check_eval(prob, res[0][1], res[0][2], rho, grad)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nranks,peer", [(2, False), (3, True)])
+def test_cuda_slab_evaluate_emulated_on_one_gpu(cuda, nranks, peer):
+    """SlabSolver + SlabFilter on the GPU (one process, LocalComm) against the oracle and against
+    the single-GPU HdmSolver.solve + gradient."""
+    import paper_2004_05756_b200 as tb
+    from paper_2004_05756_b200.slab import SlabFilter, SlabSolver, slab_evaluate
+
+    prob = _eval_problem()
+    m = prob.mesh
+    mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
+    slabs = partition(m.nz, nranks)
+    solvers = [SlabSolver(m, prob.k_e, prob.f, prob.fixed, mat, s, device=cuda) for s in slabs]
+    filters = [SlabFilter(m, prob.radius, s, device=cuda) for s in slabs]
+    psi_d = torch.as_tensor(prob.psi, device=cuda)
+    ev = slab_evaluate(solvers, filters, LocalComm(peer=peer), [s.local_elems(psi_d).contiguous() for s in solvers],
+                       rtol=1e-11)
+    rho, grad = _gather_owned(solvers, ev, m.n_elems)
+    _check_eval(prob, ev.j, ev.clamp_width, rho, grad)
+    one = tb.HdmSolver(m, prob.k_e, tb.HelmholtzFilter(m, prob.radius), prob.f, prob.fixed, mat, rtol=1e-11)
+    obj = tb.ComplianceObjective(one.f)
+    sol = one.solve(prob.psi, obj)
+    g1 = one.gradient(prob.psi, sol, obj)
+    assert abs(ev.j - sol.j) <= 1e-9 * abs(sol.j)
+    assert np.abs(rho - sol.rho).max() <= 1e-10
+    assert np.abs(grad - g1).max() <= 1e-7 * np.abs(g1).max()
+    # the sensitivities of the ghost layer agree with the neighbour's owned ones
+    for a, b, sa, sb in zip(solvers[:-1], solvers[1:], ev.s[:-1], ev.s[1:]):
+        pe = m.nx * m.ny
+        # a's last local element plane is owned by a and is b's ghost element layer
+        assert torch.equal(sa[-pe:], sb[:pe])

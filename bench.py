@@ -2,8 +2,11 @@
 """Benchmark of the FE-evaluation hot path (BASELINE.json metric) on B200.
 
 Headline: "FE solve+sensitivity s/eval" on BASELINE cfg 2 (600x200 Q4 cantilever, 241,602
-DOF): psi -> Helmholtz filter (R = 3) -> clamp -> Jacobi-pCG K(rho)u = f to a TRUE relative
-residual of 1e-10 -> compliance -> element sensitivities -> filter adjoint (the gradient).
+DOF): psi -> Helmholtz filter (R = 3) -> clamp -> pCG K(rho)u = f to a TRUE relative residual of
+1e-10 -> compliance -> element sensitivities -> filter adjoint (the gradient).  The pCG is
+preconditioned by the geometric multigrid V-cycle (--precond mg, default; one persistent kernel
+per solve) or by Jacobi (--precond jacobi, the north_star's subsystem (1), also reported under
+extra.jacobi with its own roofline).
 One step = one design evaluation with inputs resident in HBM.  ``e2e`` repeats it through the
 reference-facing API with host numpy buffers (H2D of psi, D2H of rho, u and the gradient).
 
@@ -40,6 +43,8 @@ def parse():
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg4", "cfg5"],
                     help="cfg1/cfg2: HDM evaluation (headline cfg2); cfg4: slab-sharded 3D solve; cfg5: batched ROM")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--precond", default="mg", choices=["mg", "jacobi"],
+                    help="pCG preconditioner of the cfg1/cfg2 evaluation (both solve to the same true residual)")
     ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
                     help="cfg4 halo exchange: NVLink peer stores fused into the update kernel, or NCCL send/recv")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -55,10 +60,37 @@ def problem(name, seed):
     return getattr(configs, name)(seed=seed)
 
 
-def workload_desc(prob):
+PC_DESC = {"mg": "multigrid-preconditioned CG (V(2,2), Galerkin coarse levels)", "jacobi": "Jacobi-pCG"}
+
+
+def workload_desc(prob, precond="mg"):
     m = prob.mesh
     return (f"{prob.name}: {m.nx}x{m.ny} Q4, {m.n_dofs} DOF ({prob.n_free} free); Helmholtz filter R={prob.radius:g} "
-            f"+ Jacobi-pCG true-residual rtol {prob.rtol:g} + compliance + sensitivity + filter adjoint; fp64")
+            f"+ {PC_DESC[precond]} to true-residual rtol {prob.rtol:g} + compliance + sensitivity + filter adjoint; "
+            f"fp64")
+
+
+def mg_bytes_per_iteration(nx, ny):
+    """Algorithmic bytes of one MG-preconditioned CG iteration of the persistent 2D kernel
+    (k_mgpcg2d), each vector read or written once per phase: level 0 matrix-free (alpha per
+    element), coarse levels from their half stencils (10 doubles per dof), the dense coarsest
+    inverse read once.  Hierarchy as mg.cu: halve each axis until <= 600 dofs."""
+    levels = [(nx, ny)]
+    while 2 * (levels[-1][0] + 1) * (levels[-1][1] + 1) > 600:
+        a, b = levels[-1]
+        c = ((a + 1) // 2, (b + 1) // 2)
+        if c == (a, b):
+            break
+        levels.append(c)
+    n = [2 * (a + 1) * (b + 1) for a, b in levels]
+    ne = nx * ny
+    L = len(n)
+    d = 4 * n[0] + ne + 8 * n[0]                  # A: z, p_old, p, q, alpha; B: x, r, p, q, D^-1, xa
+    d += 4 * (4 * n[0] + ne) + 2 * n[0] + n[1] + 2 * n[0]  # 3 sweeps + residual, prolongation, r.z
+    for l in range(1, L - 1):
+        d += n[l - 1] + 3 * n[l] + 4 * 14 * n[l] + 2 * n[l] + n[l + 1]
+    d += n[L - 2] + n[L - 1] + n[L - 1] ** 2 + 2 * n[L - 1]
+    return 8 * d, n
 
 
 def rank_info():
@@ -116,7 +148,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": n,
         "warmup": min(args.warmup, 1), "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE recipe)",
-        "config": {"workload": workload_desc(prob), "parallelism": "cpu", "seed": args.seed},
+        "config": {"workload": workload_desc(prob, args.precond), "parallelism": "cpu", "seed": args.seed,
+                   "reference_solver": "SuperLU direct factorisation (romtopt fem.py:270-349)"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores(), "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -218,6 +251,70 @@ def time_eval(solver, obj, psi, torch, reps=3):
     b.record()
     torch.cuda.synchronize()
     return a.elapsed_time(b) * 1e-3 / reps, sol
+
+
+def mg_roofline(solver, rho_d, mesh, pk):
+    """Dominant kernel of the MG headline: k_mgpcg2d, the whole preconditioned pCG loop in one
+    cooperative launch; its span is timed with CUDA events recorded around the launch on the
+    solve's stream (tb_pcg_kernel_time)."""
+    solver.pcg_device(rho_d, solver._f_d)
+    solver.pcg_device(rho_d, solver._f_d)
+    ms, launches = solver.last_kernel_time()
+    its = solver.last_iterations
+    per_it, sizes = mg_bytes_per_iteration(mesh.nx, mesh.ny)
+    t = ms * 1e-3
+    ach = per_it * its / t / 1e9 if t > 0 else 0.0
+    return {"kernel": "k_mgpcg2d (persistent multigrid-preconditioned CG, one cooperative launch per solve)",
+            "bound": "hbm", "achieved": ach, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
+            "frac": ach / pk.get("hbm_gbs"), "traffic": None, "bytes_per_launch": per_it * its,
+            "us_per_launch": t * 1e6 / max(launches, 1), "launches_per_solve": launches,
+            "iterations_per_launch": its / max(launches, 1), "us_per_iteration": t * 1e6 / max(its, 1),
+            "bytes_per_iteration": per_it, "level_dofs": sizes,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "fallback" not in pk else "fallback",
+            "note": ("the hierarchy (< 25 MB) is L2-resident; ~30 grid-barrier phases per iteration cost ~4 us "
+                     "each (L2 round trip + barrier), so the kernel is latency-bound, not HBM-bound "
+                     "(profiles/mg_prof.py)")}
+
+
+def jacobi_roofline(solver, rho_d, mesh, pk, torch):
+    """2D Jacobi-pCG: the whole solve is ONE persistent cooperative launch (k_pcg2d_treg); its
+    algorithmic traffic is the fused Jacobi-pCG iteration of SURVEY §8(d), 8 (9 N_u + N_e)
+    bytes, times the iterations of the launch."""
+    n_u, n_e = mesh.n_dofs, mesh.n_elems
+    a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    solver.pcg_device(rho_d, solver._f_d)
+    a_ev.record()
+    solver.pcg_device(rho_d, solver._f_d)
+    b_ev.record()
+    torch.cuda.synchronize()
+    t_solve = a_ev.elapsed_time(b_ev) * 1e-3
+    its = solver.last_iterations
+    bytes_launch = 8 * (9 * n_u + n_e) * its
+    ach = bytes_launch / t_solve / 1e9
+    return {"kernel": "k_pcg2d_treg<2,true> (persistent single-reduction Jacobi-pCG on node tiles, one launch per solve)",
+            "bound": "hbm", "achieved": ach, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
+            "frac": ach / pk.get("hbm_gbs"), "traffic": None, "bytes_per_launch": bytes_launch,
+            "us_per_launch": t_solve * 1e6, "iterations_per_launch": its, "us_per_iteration": t_solve * 1e6 / its,
+            "bytes_per_iteration": 8 * (9 * n_u + n_e),
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "fallback" not in pk else "fallback",
+            "note": ("cfg2's 18 MB working set is L2/SMEM-resident; each iteration is bounded by one grid "
+                     "barrier + partial exchange (~2-3 us), not by HBM")}
+
+
+def jacobi_extra(tb, configs, prob, psi, torch, pk, args):
+    """The same evaluation with the Jacobi-preconditioned pCG of the north_star's subsystem (1),
+    and the roofline of its persistent kernel."""
+    s = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, prob.radius), prob.f, prob.fixed,
+                     tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP), rtol=prob.rtol, preconditioner="jacobi")
+    obj = tb.ComplianceObjective(s.f)
+    t, sol = time_eval(s, obj, psi, torch)
+    rho_d, _ = s.filtered_density_device(psi)
+    roof = jacobi_roofline(s, rho_d, prob.mesh, pk, torch)
+    tpath = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        roof["traffic"] = json.load(open(tpath)).get(args.config)
+    return {"preconditioner": "Jacobi (north_star subsystem (1))", "s_per_eval": t, "pcg_iterations": sol.iterations,
+            "J": sol.j, "roofline": roof}
 
 
 def mg_extra(tb, configs, prob, psi, torch):
@@ -355,7 +452,7 @@ def run_ours(args):
     mesh = prob.mesh
     filt = tb.HelmholtzFilter(mesh, prob.radius)
     mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
-    solver = tb.HdmSolver(mesh, prob.k_e, filt, prob.f, prob.fixed, mat, rtol=prob.rtol)
+    solver = tb.HdmSolver(mesh, prob.k_e, filt, prob.f, prob.fixed, mat, rtol=prob.rtol, preconditioner=args.precond)
     obj = tb.ComplianceObjective(solver.f)
     psi_d = torch.as_tensor(prob.psi, device=dev)
     flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev)  # 256 MiB > 126 MB L2
@@ -429,33 +526,16 @@ def run_ours(args):
            "api": "HdmSolver.solve(psi: numpy) + HdmSolver.gradient -> numpy (reference signatures)"}
 
     # ---- roofline of the dominant kernel, timed live with CUDA events on its stream ------
-    # 2D: the whole Jacobi-pCG solve is ONE persistent cooperative launch (k_pcg2d_cgcg);
-    # its algorithmic traffic is the fused Jacobi-pCG iteration of SURVEY §8(d),
-    # 8 (9 N_u + N_e) bytes, times the iterations of the launch.
     rho_d, _ = solver.filtered_density_device(psi_d)
     n_u, n_e = mesh.n_dofs, mesh.n_elems
     pk = peaks()
-    a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    solver.pcg_device(rho_d, solver._f_d)
-    a_ev.record()
-    solver.pcg_device(rho_d, solver._f_d)
-    b_ev.record()
-    torch.cuda.synchronize()
-    t_solve = a_ev.elapsed_time(b_ev) * 1e-3
-    its = solver.last_iterations
-    bytes_launch = 8 * (9 * n_u + n_e) * its
-    ach = bytes_launch / t_solve / 1e9
-    roof = {"kernel": "k_pcg2d_cgcg<2,true> (persistent single-reduction Jacobi-pCG, one launch per solve)",
-            "bound": "hbm", "achieved": ach, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
-            "frac": ach / pk.get("hbm_gbs"), "traffic": None, "bytes_per_launch": bytes_launch,
-            "us_per_launch": t_solve * 1e6, "iterations_per_launch": its, "us_per_iteration": t_solve * 1e6 / its,
-            "bytes_per_iteration": 8 * (9 * n_u + n_e),
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "fallback" not in pk else "fallback",
-            "note": ("cfg2's 18 MB working set is L2/SMEM-resident; each iteration is bounded by one grid "
-                     "barrier + partial exchange (~2-3 us), not by HBM")}
-    tpath = os.path.join(REPO, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        roof["traffic"] = json.load(open(tpath)).get(args.config)
+    if args.precond == "mg":
+        roof = mg_roofline(solver, rho_d, mesh, pk)
+    else:
+        roof = jacobi_roofline(solver, rho_d, mesh, pk, torch)
+        tpath = os.path.join(REPO, "profiles", "traffic.json")
+        if os.path.exists(tpath):
+            roof["traffic"] = json.load(open(tpath)).get(args.config)
 
     extras = {}
     if not args.no_extras:
@@ -507,10 +587,15 @@ def run_ours(args):
         torch.cuda.synchronize()
         extras["rom_khat_ms"] = a.elapsed_time(b) / 10
         extras["rom_k"] = k
-        extras["mg"] = mg_extra(tb, configs, prob, psi_d, torch)
+        if args.precond == "mg":
+            extras["jacobi"] = jacobi_extra(tb, configs, prob, psi_d, torch, pk, args)
+        else:
+            extras["mg"] = mg_extra(tb, configs, prob, psi_d, torch)
         extras["tr_subproblem"] = subproblem_extra(tb, solver, obj, prob, psi_d, phi, torch)
         if args.extra3d:
             extras["cfg3"] = bench_cfg3(tb, configs, _lib, dev, pk)
+        if os.environ.get("TB_BENCH_CFG4", "1") != "0":
+            extras["cfg4_sharded"] = cfg4_extra(args, dev, dist, world, rank)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -528,7 +613,8 @@ def run_ours(args):
             "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE cfg recipe, SURVEY App. B.1)",
-            "config": {"workload": workload_desc(prob), "parallelism": "replicas" if world > 1 else "single",
+            "config": {"workload": workload_desc(prob, args.precond), "preconditioner": args.precond,
+                       "parallelism": "replicas" if world > 1 else "single",
                        "l2": "256 MiB buffer written between steps (outside the step events)",
                        "pcg_iterations": int(statistics.median(iters)), "seed": args.seed},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
@@ -537,6 +623,49 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def cfg4_extra(args, dev, dist, world, rank):
+    """BASELINE cfg 4 (43M DOF Hex8) evaluated once, slab-sharded over ALL ranks of this run:
+    at N > 1 the replicas of the headline join one distributed evaluation (NCCL allreduces +
+    NCCL send/recv halos; `--config cfg4` measures the NVLink peer-store halo), so a scaling run
+    of the default bench also records cfg 4's strong scaling.  N = 1: one slab, no collectives."""
+    import torch
+
+    import paper_2004_05756_b200 as tb
+    from paper_2004_05756_b200 import configs
+    from paper_2004_05756_b200.slab import LocalComm, SlabFilter, SlabSolver, TorchComm, partition, slab_evaluate
+
+    prob = configs.cfg4(seed=args.seed)
+    mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
+    slab = partition(prob.mesh.nz, world)[rank]
+    sv = SlabSolver(prob.mesh, prob.k_e, prob.f, prob.fixed, mat, slab, device=dev)
+    fl = SlabFilter(prob.mesh, prob.radius, slab, device=dev)
+    psi = torch.as_tensor(sv.local_elems(prob.psi).copy(), device=dev)
+    comm = TorchComm(peer=False) if dist else LocalComm()
+    ev = slab_evaluate([sv], [fl], comm, [psi], rtol=prob.rtol)  # warm-up
+    del ev
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    ev = slab_evaluate([sv], [fl], comm, [psi], rtol=prob.rtol)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    m = prob.mesh
+    out = {"workload": f"cfg4 {m.nx}x{m.ny}x{m.nz} Hex8, {m.n_dofs} DOF: filter R={prob.radius:g} + Jacobi-pCG "
+                       f"{prob.rtol:g} + compliance + sensitivities + adjoint, z-slabs x{world}",
+           "s_per_eval": float(t.item()), "n_gpus": world, "scaling": "strong", "pcg_iterations": ev.iterations,
+           "filter_iterations": list(ev.filter_iterations), "J": ev.j,
+           "halo": "nccl send/recv" if dist else "none (one slab)",
+           "us_per_pcg_iteration_upper_bound": float(t.item()) / max(ev.iterations, 1) * 1e6}
+    del ev, sv, fl, psi
+    torch.cuda.empty_cache()
+    return out
 
 
 def fp64_peak_tflops(torch, dev):

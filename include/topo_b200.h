@@ -92,6 +92,15 @@ int tb_plan_set_preconditioner(tb_plan* plan, int kind);
  * duration (ms) of the fused operator kernel and of the update kernel (HOST pointers). */
 int tb_pcg_profile(tb_plan* plan, const double* rho, const double* b, int nrep, double* ms_fused,
                    double* ms_update, void* stream);
+/* Diagnostics: device time (CUDA events on the solve's stream) spanned by the persistent
+ * multigrid-pCG launches of the plan's last tb_pcg_solve (2D, preconditioner 1), and how many
+ * there were (restarts after a true-residual check add one each); 0 launches when the solve ran
+ * the graph path.  Synchronises on the last launch. */
+int tb_pcg_kernel_time(tb_plan* plan, float* ms, int* launches);
+/* Diagnostics: per-phase %globaltimer sums (ns) of the persistent 2D multigrid pCG kernel in a
+ * build with -DTB_MGP_PROF (tools/build_prof.sh); zeros in the product build.  Reads and clears
+ * 32 counters into a HOST array. */
+int tb_mgp_prof_read(unsigned long long* out32);
 /* Number of kernels this library has launched so far (graph-body kernels included). */
 int64_t tb_launch_count(void);
 

@@ -134,6 +134,9 @@ void ElastOp::launch_dinv(double* dinv, cudaStream_t s) const {
   else
     { k_node_dinv<3, 3, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, plan->K3, plan->d_alpha, plan->d_fixed, dinv); tb::launched(); }
 }
+bool ElastOp::launch_persistent_pc(PcgWork& w, cudaStream_t s) const {
+  return plan->precond == 1 && plan->g.dim == 2 && mg_pcg2d_persistent(plan, w, s);
+}
 int ElastOp::fused_blocks() const {
   if (plan->g.dim == 3 && plan->hex8) {
     const dim3 gr = hex8_grid(plan->g, plan->zchunk);
@@ -456,6 +459,18 @@ int tb_pcg_solve(tb_plan* plan, const double* rho, const double* b, double* x, d
   }
   TB_TRY(P->material(rho, P->d_alpha, nullptr, s));
   return pcg_solve(P->op, P->work, b, x, rtol, maxit, iters, relres, s);
+}
+
+int tb_pcg_kernel_time(tb_plan* plan, float* ms, int* launches) {
+  TB_GUARD(plan && ms && launches, "null argument");
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  *ms = 0.0f;
+  *launches = P->work.klaunches;
+  if (P->work.klaunches > 0) {
+    TB_CUDA(cudaEventSynchronize(P->work.kev1));
+    TB_CUDA(cudaEventElapsedTime(ms, P->work.kev0, P->work.kev1));
+  }
+  return TB_OK;
 }
 
 int tb_pcg_profile(tb_plan* plan, const double* rho, const double* b, int nrep, double* ms_fused, double* ms_update,

@@ -52,6 +52,10 @@ struct tb_plan_impl;
 int mg_build(tb_plan_impl* P);                          // allocate the hierarchy (once per plan)
 int mg_setup(tb_plan_impl* P, cudaStream_t s);          // operators for the current alpha
 int mg_apply(tb_plan_impl* P, const double* r, double* z, cudaStream_t s);  // z = M^-1 r
+struct PcgWork;
+// 2D: the whole MG-preconditioned pCG loop in one persistent cooperative launch (mgpcg2d.cu);
+// false when unavailable (3D, TB_NO_PERSIST, no co-residency) -> graph path
+bool mg_pcg2d_persistent(tb_plan_impl* P, PcgWork& w, cudaStream_t s);
 void mg_release(Mg& mg);
 
 }  // namespace tb

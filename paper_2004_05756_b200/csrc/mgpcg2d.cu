@@ -1,0 +1,506 @@
+// Multigrid-preconditioned CG for 2D plans in ONE persistent cooperative launch.
+//
+// Why: on BASELINE cfg 1-2 the whole hierarchy (< 25 MB) sits in L2, and the graph-launched
+// V-cycle of mg.cu is ~55 kernels of ~3.4 us each per pCG iteration (~190 us at cfg 2), nearly
+// all of it launch and drain latency.  Here every phase is a grid-stride pass over one level,
+// separated by a software grid barrier:
+//
+//   A  (level 0)   p = z + beta p_old (p double-buffered), q = K(rho) p, partial p.q   | barrier
+//   B  (level 0)   alpha = rz / pq; x += alpha p; r -= alpha q (free dofs), partial r.r;
+//                  first pre-smoothing sweep x0 = omega D^-1 r                          | barrier
+//   down, l = 0 .. L-2:  [restriction + first sweep of l] | sweep 2 | residual           |
+//   coarsest:            restriction | x = Ainv b (one warp per row over the grid)       |
+//   up, l = L-2 .. 0:    prolongation | post sweep 1 | post sweep 2 (level 0: + r.z)     |
+//
+// Measured (profiles/mg_prof.py, TB_MGP_PROF build): a phase costs ~4 us whatever the level
+// size (L2 round trips of the neighbour loads, store drain, barrier), so cfg 2 runs ~160 us per
+// iteration against ~190 us for the graph: 5.1 vs 6.2 ms per solve.  Running the levels below
+// ~6k dofs inside one CTA with CTA barriers was slower (~5.7 us per phase: one SM's serial L2
+// latency), as was a 128-dof coarsest level kept in shared memory (27 -> 32 iterations).
+//
+// The arithmetic per dof is that of the graph path (same V(2,2) cycle, damped Jacobi, full
+// weighting, linear prolongation, dense coarsest inverse), term by term, so the iterates agree
+// with it to round-off (the dot products are summed in a different fixed order; the level-0
+// operator uses the Q4 pattern values, as the persistent Jacobi kernel does).  Every reduction
+// is a fixed-order sum of per-CTA partials that every CTA evaluates identically, so all CTAs
+// take the same convergence branch.  Cross-CTA data written inside the kernel is read with
+// ld.cg (L2); the constant operator data (stencils, D^-1, masks, alpha, inverse) with ld.nc.
+#include <cooperative_groups.h>
+
+#include "cgcg2d.cuh"
+#include "mg.cuh"
+#include "plan.cuh"
+
+namespace tb {
+
+constexpr int kMgpThreads = 512;
+constexpr int kMgpMaxLv = 16;
+
+struct MgpLevel {
+  Grid g;
+  const double* st;       // half stencil (levels >= 1)
+  const uint8_t* fixed;   // Dirichlet mask
+  const double* dinv;     // Jacobi inverse diagonal (0 on fixed)
+  double *xa, *xb, *b, *res;  // sweep ping-pong (final iterate in xb), right-hand side, residual
+};
+
+struct MgpArgs {
+  MgpLevel L[kMgpMaxLv];
+  int nlev;
+  int64_t ncoarse;
+  double omega;
+  const double* ainv;   // coarsest dense inverse
+  const double* alpha;  // level-0 element scales
+  double *x, *r, *pa, *pb, *q;
+  PcgState* st;
+  double* part;         // [3][gridDim.x]: p.q, r.r, r.z partials
+  unsigned int* bar;
+};
+
+// Diagnostics (TB_MGP_PROF builds): CTA 0 accumulates %globaltimer spans per phase class.
+__device__ unsigned long long g_mgp_prof[32];
+#ifdef TB_MGP_PROF
+__device__ __forceinline__ unsigned long long mgp_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define MGP_MARK(k)                                  \
+  do {                                               \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {       \
+      const unsigned long long t_ = mgp_now();       \
+      g_mgp_prof[k] += t_ - prof_last;               \
+      prof_last = t_;                                \
+    }                                                \
+  } while (0)
+#else
+#define MGP_MARK(k) \
+  do {              \
+  } while (0)
+#endif
+
+struct Rng {
+  int64_t start, stride;
+};
+
+__device__ __forceinline__ Rng grid_rng() {
+  return {(int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x};
+}
+__device__ __forceinline__ Rng cta_rng() { return {threadIdx.x, blockDim.x}; }
+
+// y_n = (A_l v)_n.  Level 0: matrix-free alpha_e K_e (node-owner slots, as k_node_apply);
+// coarse levels: half stencil (as k_mg_sapply).  v was written inside this kernel: L2 loads.
+// Every load is unconditional (out-of-grid neighbours read a clamped in-range address) and
+// only the accumulation is predicated, so all loads of a node are in flight together; the sums
+// are those of the graph path term by term.
+template <bool L0>
+__device__ __forceinline__ void mgp_apply(const MgpLevel& L, const Q4Pat& K, const double* __restrict__ alpha,
+                                          int n, const double* v, double (&out)[2]) {
+  const Grid& g = L.g;
+  const int i = (int)(n % g.nnx), j = (int)(n / g.nnx);
+  if (L0) {
+    double P[9][2];
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) {
+        const int ii = i + dx - 1, jj = j + dy - 1;
+        const bool ok = ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
+        const int64_t node = ok ? (int64_t)jj * g.nnx + ii : n;
+        const double v0 = __ldcg(v + 2 * node), v1 = __ldcg(v + 2 * node + 1);
+        P[dy * 3 + dx][0] = ok ? v0 : 0.0;
+        P[dy * 3 + dx][1] = ok ? v1 : 0.0;
+      }
+    double a[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int ei = i - 1 + (s & 1), ej = j - 1 + (s >> 1);
+      const bool ok = ei >= 0 && ei < g.nx && ej >= 0 && ej < g.ny;
+      const double av = __ldg(alpha + (ok ? (int64_t)ej * g.nx + ei : 0));
+      a[s] = ok ? av : 0.0;
+    }
+    node_rows_pat<2>(K, P, a, out);
+  } else {
+    out[0] = out[1] = 0.0;
+    const int64_t N = g.n_nodes;
+#pragma unroll
+    for (int m = 0; m < 9; ++m) {
+      const int ni = i + m % 3 - 1, nj = j + m / 3 - 1;
+      const bool ok = ni >= 0 && ni < g.nnx && nj >= 0 && nj < g.nny;
+      const int64_t nbn = ok ? (int64_t)nj * g.nnx + ni : n;
+      const double v0 = __ldcg(v + 2 * nbn), v1 = __ldcg(v + 2 * nbn + 1);
+      const double* s = (m >= 4) ? L.st + (int64_t)(m - 4) * 4 * N + n : L.st + (int64_t)(4 - m) * 4 * N + nbn;
+      const double s0 = __ldg(s), s1 = __ldg(s + N), s2 = __ldg(s + 2 * N), s3 = __ldg(s + 3 * N);
+      if (ok) {
+        if (m >= 4) {
+          out[0] = fma(s1, v1, fma(s0, v0, out[0]));
+          out[1] = fma(s3, v1, fma(s2, v0, out[1]));
+        } else {  // transpose of the neighbour's block towards this node
+          out[0] = fma(s2, v1, fma(s0, v0, out[0]));
+          out[1] = fma(s3, v1, fma(s1, v0, out[1]));
+        }
+      }
+    }
+  }
+}
+
+// out = in + omega D^-1 (b - A in)   (in == nullptr: out = omega D^-1 b)
+template <bool L0>
+__device__ __noinline__ void mgp_sweep(const MgpLevel& L, const Q4Pat K, const double* alpha, double omega,
+                                       const double* in, double* out, Rng rg) {
+#pragma unroll(L0 ? 2 : 1)
+  for (int n = (int)rg.start; n < (int)L.g.n_nodes; n += (int)rg.stride) {
+    double y[2] = {0.0, 0.0};
+    if (in != nullptr) mgp_apply<L0>(L, K, alpha, n, in, y);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int64_t d = 2 * n + c;
+      const double bd = __ldcg(L.b + d);
+      const double di = __ldg(L.dinv + d);
+      out[d] = (in != nullptr) ? __ldcg(in + d) + omega * di * (bd - y[c]) : omega * di * bd;
+    }
+  }
+}
+
+// res = b - A xb on free dofs, 0 on fixed
+template <bool L0>
+__device__ __noinline__ void mgp_resid(const MgpLevel& L, const Q4Pat K, const double* alpha, Rng rg) {
+#pragma unroll(L0 ? 2 : 1)
+  for (int n = (int)rg.start; n < (int)L.g.n_nodes; n += (int)rg.stride) {
+    double y[2];
+    mgp_apply<L0>(L, K, alpha, n, L.xb, y);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int64_t d = 2 * n + c;
+      L.res[d] = (__ldg(L.dinv + d) != 0.0) ? __ldcg(L.b + d) - y[c] : 0.0;
+    }
+  }
+}
+
+__device__ __forceinline__ double mgp_pw(int i, int I, int nf) {
+  if (i < 0 || i > nf) return 0.0;
+  if (!(i & 1)) return (i >> 1) == I ? 1.0 : 0.0;
+  if (i == nf) return ((nf + 1) >> 1) == I ? 1.0 : 0.0;
+  return ((i >> 1) == I || (i >> 1) + 1 == I) ? 0.5 : 0.0;
+}
+
+// b_c = P~^T res_f (full weighting, 0 on coarse fixed dofs); sweep1: xa_c = omega D_c^-1 b_c.
+// Zero-weight taps read a clamped address and add w * r = +0 (the graph path skips them).
+__device__ __noinline__ void mgp_restrict(const MgpLevel& C, const MgpLevel& F, double omega, bool sweep1,
+                                          Rng rg) {
+  const Grid& gc = C.g;
+  const Grid& gf = F.g;
+#pragma unroll 1
+  for (int n = (int)rg.start; n < (int)gc.n_nodes; n += (int)rg.stride) {
+    const int I = (int)(n % gc.nnx), J = (int)(n / gc.nnx);
+    double acc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int fi = 2 * I + dx, fj = 2 * J + dy;
+        const double w = mgp_pw(fi, I, gf.nx) * mgp_pw(fj, J, gf.ny);
+        const int ci = min(max(fi, 0), gf.nx), cj = min(max(fj, 0), gf.ny);
+        const int64_t fd = 2 * ((int64_t)cj * gf.nnx + ci);
+        const double r0 = __ldcg(F.res + fd), r1 = __ldcg(F.res + fd + 1);
+        if (w != 0.0) {
+          acc[0] = fma(w, r0, acc[0]);
+          acc[1] = fma(w, r1, acc[1]);
+        }
+      }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int64_t d = 2 * n + c;
+      const double bc = __ldg(C.fixed + d) ? 0.0 : acc[c];
+      C.b[d] = bc;
+      if (sweep1) C.xa[d] = omega * __ldg(C.dinv + d) * bc;
+    }
+  }
+}
+
+// xb_f += P~ xb_c on free fine dofs (bilinear interpolation; same summation order as
+// k_mg_prolong_add, all four candidate coarse values loaded up front)
+__device__ __noinline__ void mgp_prolong(const MgpLevel& F, const MgpLevel& C, Rng rg) {
+  const Grid& gf = F.g;
+  const Grid& gc = C.g;
+#pragma unroll 1
+  for (int n = (int)rg.start; n < (int)gf.n_nodes; n += (int)rg.stride) {
+    const int i = (int)(n % gf.nnx), j = (int)(n / gf.nnx);
+    int i0, ni, j0, nj;
+    if (!(i & 1)) { i0 = i >> 1; ni = 1; } else if (i == gf.nx) { i0 = (gf.nx + 1) >> 1; ni = 1; } else { i0 = i >> 1; ni = 2; }
+    if (!(j & 1)) { j0 = j >> 1; nj = 1; } else if (j == gf.ny) { j0 = (gf.ny + 1) >> 1; nj = 1; } else { j0 = j >> 1; nj = 2; }
+    const double w = (ni == 2 ? 0.5 : 1.0) * (nj == 2 ? 0.5 : 1.0);
+    const int i1 = min(i0 + 1, gc.nnx - 1), j1 = min(j0 + 1, gc.nny - 1);
+    const int64_t c00 = 2 * ((int64_t)j0 * gc.nnx + i0), c01 = 2 * ((int64_t)j0 * gc.nnx + i1);
+    const int64_t c10 = 2 * ((int64_t)j1 * gc.nnx + i0), c11 = 2 * ((int64_t)j1 * gc.nnx + i1);
+    double v[4][2];
+    v[0][0] = __ldcg(C.xb + c00), v[0][1] = __ldcg(C.xb + c00 + 1);
+    v[1][0] = __ldcg(C.xb + c01), v[1][1] = __ldcg(C.xb + c01 + 1);
+    v[2][0] = __ldcg(C.xb + c10), v[2][1] = __ldcg(C.xb + c10 + 1);
+    v[3][0] = __ldcg(C.xb + c11), v[3][1] = __ldcg(C.xb + c11 + 1);
+    const double x0 = __ldcg(F.xb + 2 * n), x1 = __ldcg(F.xb + 2 * n + 1);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      double acc = v[0][c];
+      if (ni == 2) acc += v[1][c];
+      if (nj == 2) {
+        acc += v[2][c];
+        if (ni == 2) acc += v[3][c];
+      }
+      const int64_t d = 2 * n + c;
+      if (!__ldg(F.fixed + d)) F.xb[d] = fma(w, acc, c ? x1 : x0);
+    }
+  }
+}
+
+// xb_c = Ainv b_c, one warp per row over the grid (fixed-order lane partials)
+__device__ __forceinline__ void mgp_dense(const MgpLevel& C, const double* __restrict__ ainv, int64_t n) {
+  const int lane = threadIdx.x & 31;
+  const int w = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), nw = (int)((gridDim.x * blockDim.x) >> 5);
+  const double* A = ainv;
+#pragma unroll 1
+  for (int r = w; r < (int)n; r += nw) {
+    double s = 0.0;
+#pragma unroll 4
+    for (int c = lane; c < (int)n; c += 32) s = fma(A[r * n + c], __ldcg(C.b + c), s);
+    s = warp_sum(s);
+    if (lane == 0) C.xb[r] = s;
+  }
+}
+
+// fixed-order sum of the per-CTA partials of slot k; every warp computes it identically
+__device__ __forceinline__ double mgp_sum(const double* part, int k) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(part + k * gridDim.x + b);
+  return warp_sum(s);
+}
+
+__global__ void __launch_bounds__(kMgpThreads, 1) k_mgpcg2d(Q4Pat K, MgpArgs a) {
+  __shared__ MgpLevel sL[kMgpMaxLv];
+  for (int l = threadIdx.x; l < a.nlev; l += blockDim.x) sL[l] = a.L[l];
+  __syncthreads();
+  PcgState* st = a.st;
+  if (st->done != 0) return;
+  const double omega = a.omega, tol2 = st->tol2;
+  const int maxit = st->maxit;
+  int it = st->iters;
+  double rz = 0.0, rr = st->rr, beta = 0.0, alpha = 0.0, pq = 0.0;
+  int done = 0;
+  const int nlev = a.nlev, lg = nlev - 1;  // grid levels 0 .. nlev-2, then the dense coarsest
+  const double* alpha_e = a.alpha;
+  double* x = a.x;
+  double* r = a.r;
+  double* q = a.q;
+  double* part = a.part;
+  unsigned int* bar = a.bar;
+  const Rng G = grid_rng();
+  const Grid g0 = sL[0].g;
+  const double* dinv0 = sL[0].dinv;
+  double* xa0 = sL[0].xa;
+  double* z = sL[0].xb;
+  const int64_t N0 = g0.n_nodes;
+#ifdef TB_MGP_PROF
+  unsigned long long prof_last = (blockIdx.x == 0 && threadIdx.x == 0) ? mgp_now() : 0ull;
+#endif
+
+  for (bool first = true;; first = false) {
+    if (first) {
+      // initial preconditioned residual: first sweep from zero on b = r (k_pcg_start set pa = 0)
+      mgp_sweep<true>(sL[0], K, alpha_e, omega, nullptr, xa0, G);
+      grid_sync_flip(bar);
+    } else {
+      const double* pold = (it & 1) ? a.pb : a.pa;
+      double* pnew = (it & 1) ? a.pa : a.pb;
+      // ---- A: p = z + beta p_old, q = K p, p.q
+      double acc[1] = {0.0};
+#pragma unroll 2
+      for (int n = (int)G.start; n < (int)N0; n += (int)G.stride) {
+        const int i = (int)(n % g0.nnx), j = (int)(n / g0.nnx);
+        double P[9][2];
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+          for (int dx = 0; dx < 3; ++dx) {
+            const int ii = i + dx - 1, jj = j + dy - 1;
+            const bool ok = ii >= 0 && ii < g0.nnx && jj >= 0 && jj < g0.nny;
+            const int64_t node = (int64_t)jj * g0.nnx + ii;
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+              P[dy * 3 + dx][c] = ok ? fma(beta, __ldcg(pold + 2 * node + c), __ldcg(z + 2 * node + c)) : 0.0;
+          }
+        double sc[4], out[2];
+        slot_scales<2, true>(g0, i, j, 0, alpha_e, sc);
+        node_rows_pat<2>(K, P, sc, out);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          pnew[2 * n + c] = P[4][c];
+          q[2 * n + c] = out[c];
+          acc[0] = fma(P[4][c], out[c], acc[0]);
+        }
+      }
+      publish_partials_grid_sync<1>(acc, part, bar, false);
+      pq = mgp_sum(part, 0);
+      MGP_MARK(0);
+      if (!(pq > 0.0) || !isfinite(pq)) {
+        done = 3;
+        break;
+      }
+      alpha = rz / pq;
+      // ---- B: x, r update, r.r, first pre-smoothing sweep of level 0 (b = r)
+      acc[0] = 0.0;
+#pragma unroll 2
+      for (int n = (int)G.start; n < (int)N0; n += (int)G.stride)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int64_t d = 2 * n + c;
+          const double di = __ldg(dinv0 + d);
+          double rd = __ldcg(r + d);
+          if (di != 0.0) {
+            x[d] = fma(alpha, __ldcg(pnew + d), __ldcg(x + d));
+            rd = fma(-alpha, __ldcg(q + d), rd);
+            r[d] = rd;
+            acc[0] = fma(rd, rd, acc[0]);
+          }
+          xa0[d] = omega * di * rd;
+        }
+      publish_partials_grid_sync<1>(acc, part + gridDim.x, bar, false);
+      rr = mgp_sum(part, 1);
+      MGP_MARK(1);
+      ++it;
+      if (!isfinite(rr)) done = 3;
+      else if (rr <= tol2) done = 1;
+      else if (it >= maxit) done = 2;
+      if (done) break;
+    }
+    // ---- rest of the V-cycle: z = M^-1 r
+    for (int l = 0; l < lg; ++l) {
+      MgpLevel& L = sL[l];
+      if (l > 0) {
+        mgp_restrict(L, sL[l - 1], omega, true, G);
+        grid_sync_flip(bar);
+        mgp_sweep<false>(L, K, alpha_e, omega, L.xa, L.xb, G);
+        grid_sync_flip(bar);
+        mgp_resid<false>(L, K, alpha_e, G);
+      } else {
+        mgp_sweep<true>(L, K, alpha_e, omega, L.xa, L.xb, G);
+        grid_sync_flip(bar);
+        mgp_resid<true>(L, K, alpha_e, G);
+      }
+      grid_sync_flip(bar);
+      MGP_MARK(8 + l);
+    }
+    // coarsest: restriction, then x = Ainv b with one warp per row over the whole grid
+    mgp_restrict(sL[nlev - 1], sL[nlev - 2], omega, false, G);
+    grid_sync_flip(bar);
+    mgp_dense(sL[nlev - 1], a.ainv, a.ncoarse);
+    MGP_MARK(3);
+    grid_sync_flip(bar);
+    for (int l = lg - 1; l >= 1; --l) {
+      MgpLevel& L = sL[l];
+      mgp_prolong(L, sL[l + 1], G);
+      grid_sync_flip(bar);
+      mgp_sweep<false>(L, K, alpha_e, omega, L.xb, L.xa, G);
+      grid_sync_flip(bar);
+      mgp_sweep<false>(L, K, alpha_e, omega, L.xa, L.xb, G);
+      grid_sync_flip(bar);
+      MGP_MARK(16 + l);
+    }
+    mgp_prolong(sL[0], sL[1], G);
+    grid_sync_flip(bar);
+    mgp_sweep<true>(sL[0], K, alpha_e, omega, z, xa0, G);
+    grid_sync_flip(bar);
+    mgp_sweep<true>(sL[0], K, alpha_e, omega, xa0, z, G);
+    // ---- r.z (z = xb of level 0, this thread's own dofs), beta
+    double rzp[1] = {0.0};
+#pragma unroll 1
+    for (int n = (int)G.start; n < (int)N0; n += (int)G.stride)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) rzp[0] = fma(__ldcg(r + 2 * n + c), __ldcg(z + 2 * n + c), rzp[0]);
+    publish_partials_grid_sync<1>(rzp, part + 2 * gridDim.x, bar, false);
+    const double rzn = mgp_sum(part, 2);
+    MGP_MARK(16);
+    beta = first ? 0.0 : rzn / rz;
+    rz = rzn;
+    if (!(rzn > 0.0)) done = (rzn == 0.0 && rr == 0.0) ? 1 : 3;
+    if (done) break;
+  }
+#ifdef TB_MGP_PROF
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_mgp_prof[31] += 1;
+#endif
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->iters = it;
+    st->rr = rr;
+    st->rz = rz;
+    st->pq = pq;
+    st->alpha = alpha;
+    st->beta = beta;
+    st->done = done;
+  }
+}
+
+// Launch for the plan's current hierarchy (after mg_setup) from the state k_pcg_start left:
+// x, r, pa = 0, st (tol2, maxit, iters, rr).  Returns false when the device cannot co-schedule
+// the grid (caller uses the graph path).
+bool mg_pcg2d_persistent(tb_plan_impl* P, PcgWork& w, cudaStream_t s) {
+  Mg& mg = P->mg;
+  if (P->g.dim != 2 || !P->pat_ok || mg.lv.size() < 2 || (int)mg.lv.size() > kMgpMaxLv) return false;
+  if (getenv("TB_NO_PERSIST") != nullptr) return false;  // tests: the graph path
+  static int grid = -1;
+  if (grid < 0) {
+    int dev = 0, sms = 0, coop = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mgpcg2d, kMgpThreads, 0);
+    grid = (coop && occ >= 1) ? sms : 0;
+  }
+  if (grid <= 0 || 2 * w.part_stride < 3 * grid) return false;
+  MgpArgs a{};
+  a.nlev = (int)mg.lv.size();
+  for (int l = 0; l < a.nlev; ++l) {
+    const MgLevel& L = mg.lv[l];
+    MgpLevel& d = a.L[l];
+    d.g = L.g;
+    d.st = L.st;
+    d.fixed = L.fixed;
+    d.dinv = L.dinv;
+    d.xa = L.x;
+    d.xb = L.t;
+    d.b = L.b;
+    d.res = L.r;
+  }
+  a.L[0].b = w.r;   // the V-cycle's level-0 right-hand side is the pCG residual
+  a.L[0].xb = w.z;  // and its result is z
+  a.L[0].dinv = w.dinv;
+  a.ncoarse = mg.ncoarse;
+  a.omega = mg.omega;
+  a.ainv = mg.ainv;
+  a.alpha = P->d_alpha;
+  a.x = w.x;
+  a.r = w.r;
+  a.pa = w.pa;
+  a.pb = w.pb;
+  a.q = w.q;
+  a.st = w.st;
+  a.part = w.part;
+  a.bar = reinterpret_cast<unsigned int*>(w.barrier);
+  void* args[] = {(void*)&P->pat, (void*)&a};
+  if (cudaLaunchCooperativeKernel((const void*)k_mgpcg2d, grid, kMgpThreads, args, 0, s) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  launched(1);
+  return true;
+}
+
+}  // namespace tb
+
+// Diagnostics: read and clear the per-phase timers of a TB_MGP_PROF build (zeros otherwise).
+extern "C" int tb_mgp_prof_read(unsigned long long* out32) {
+  if (out32 == nullptr) return 1;
+  if (cudaMemcpyFromSymbol(out32, tb::g_mgp_prof, sizeof(unsigned long long) * 32) != cudaSuccess) return 2;
+  static const unsigned long long zeros[32] = {};
+  if (cudaMemcpyToSymbol(tb::g_mgp_prof, zeros, sizeof(zeros)) != cudaSuccess) return 2;
+  return 0;
+}

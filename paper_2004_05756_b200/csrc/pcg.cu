@@ -38,6 +38,8 @@ void PcgWork::release() {
   if (pub) cudaFree(pub);
   if (exec) cudaGraphExecDestroy(exec);
   if (exec_pc) cudaGraphExecDestroy(exec_pc);
+  if (kev0) cudaEventDestroy(kev0);
+  if (kev1) cudaEventDestroy(kev1);
   *this = PcgWork();
 }
 
@@ -352,7 +354,19 @@ static int pcg_solve_pc(const PcgOp& op, PcgWork& w, const double* b, double* x_
   TB_TRY(op.precond_setup(s));
   int rc = TB_OK, stalls = 0, it_before = 0;
   double best_rr = -1.0;
+  w.klaunches = 0;
+  if (!w.kev0) {
+    TB_CUDA(cudaEventCreate(&w.kev0));
+    TB_CUDA(cudaEventCreate(&w.kev1));
+  }
   for (int restart = 0;; ++restart) {
+    if (w.klaunches == 0) TB_CUDA(cudaEventRecord(w.kev0, s));
+    const bool persistent = !plain && op.launch_persistent_pc(w, s);
+    if (persistent) {
+      TB_CHECK_LAUNCH();
+      TB_CUDA(cudaEventRecord(w.kev1, s));
+      ++w.klaunches;
+    } else {
     TB_TRY(op.precond_apply(w.r, w.z, s));
     k_pcg_rz<<<nb, kBlock, 0, s>>>(w.n, w.r, w.z, w.st, w.partC(), 1);
     launched(1);
@@ -367,6 +381,7 @@ static int pcg_solve_pc(const PcgOp& op, PcgWork& w, const double* b, double* x_
     } else {
       TB_CUDA(cudaGraphLaunch(w.exec_pc, s));
     }
+    }
     op.launch_apply(w.x, w.tmp, s);
     k_pcg_start<<<nb, kBlock, 0, s>>>(w.n, b, w.tmp, w.dinv, w.x, w.r, w.z, w.pa, w.st, w.partC(), 0, rtol, maxit);
     launched(1);
@@ -374,7 +389,7 @@ static int pcg_solve_pc(const PcgOp& op, PcgWork& w, const double* b, double* x_
     TB_CUDA(cudaMemcpyAsync(w.h_st, w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
     TB_CUDA(cudaStreamSynchronize(s));
     const PcgState& h = *w.h_st;
-    launched((int64_t)(h.iters - it_before) * 40);  // approximate: kernels per V-cycle iteration
+    if (!persistent) launched((int64_t)(h.iters - it_before) * 40);  // approximate: kernels per V-cycle iteration
     it_before = h.iters;
     if (h.done == 1) break;
     if (h.done == 3) {

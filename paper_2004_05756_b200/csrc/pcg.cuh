@@ -34,6 +34,8 @@ struct PcgOp {
   virtual int precond_setup(cudaStream_t s) const { (void)s; return TB_OK; }
   virtual int precond_apply(const double* r, double* z, cudaStream_t s) const { (void)r; (void)z; (void)s; return TB_OK; }
   virtual void launch_persistent(const PcgWork& w, cudaStream_t s) const { (void)w; (void)s; }
+  // preconditioned loop (from r, pa = 0) in one persistent launch; false: use the graph loop
+  virtual bool launch_persistent_pc(PcgWork& w, cudaStream_t s) const { (void)w; (void)s; return false; }
 };
 
 struct PcgWork {
@@ -47,6 +49,9 @@ struct PcgWork {
   double* pub = nullptr;     // persistent kernel's published vectors [2][3][n]
   cudaGraphExec_t exec = nullptr;
   cudaGraphExec_t exec_pc = nullptr;  // graph of the preconditioned (multigrid) loop
+  // span of the persistent preconditioned launches of the last solve (tb_pcg_kernel_time)
+  cudaEvent_t kev0 = nullptr, kev1 = nullptr;
+  int klaunches = 0;
   // distributed (slab) mode: owned dof range [own0, own1) (own1 < 0: n), dofs per node plane,
   // and where the first / last owned plane of z is pushed (neighbours' ghost planes, possibly
   // peer memory over NVLink; nullptr: the caller exchanges the halo)

@@ -213,6 +213,13 @@ class HdmSolver:
         self.last_iterations, self.last_relres = it.value, rr.value
         return x
 
+    def last_kernel_time(self):
+        """(ms, launches): device time spanned by the persistent multigrid-pCG launches of the last
+        solve (2D, preconditioner "mg"); (0.0, 0) when it ran the graph path (tb_pcg_kernel_time)."""
+        ms, n = ctypes.c_float(0.0), ctypes.c_int(0)
+        _lib.check(_lib.lib().tb_pcg_kernel_time(self._plan, ctypes.byref(ms), ctypes.byref(n)), "kernel time")
+        return float(ms.value), int(n.value)
+
     def dot_device(self, a_d, b_d) -> float:
         out = ctypes.c_double(0.0)
         _lib.check(_lib.lib().tb_dot(self._plan, _lib.ptr(a_d), _lib.ptr(b_d), a_d.numel(), ctypes.byref(out),

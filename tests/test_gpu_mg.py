@@ -107,3 +107,37 @@ def test_mg_certified_error_bound_matches_jacobi(cuda):
     assert out["mg"].sigma_min_converged and out["jacobi"].sigma_min_converged
     assert out["mg"].sigma_min == pytest.approx(out["jacobi"].sigma_min, rel=1e-6)
     assert out["mg"].energy_error_bound == pytest.approx(out["jacobi"].energy_error_bound, rel=1e-6)
+
+
+@pytest.mark.parametrize("case", ["cfg1", "cfg2", "odd"])
+def test_mg_2d_persistent_kernel_matches_graph_vcycle(cuda, monkeypatch, case):
+    """2D MG-pCG runs as one persistent cooperative kernel (mgpcg2d.cu); with TB_NO_PERSIST the
+    same V(2,2) cycle runs as the captured graph of mg.cu.  Same iterates up to the order of
+    the dot-product sums: same iteration count (+-1), same answer to the solve tolerance."""
+    prob = {"cfg1": configs.cfg1, "cfg2": configs.cfg2}.get(case, lambda: configs.cfg1(seed=3, nx=61, ny=23))()
+    out = {}
+    for mode in ("persistent", "graph"):
+        if mode == "graph":
+            monkeypatch.setenv("TB_NO_PERSIST", "1")
+        s = build(prob, "mg", rtol=1e-10)
+        obj = tb.ComplianceObjective(s.f)
+        sol = s.solve(prob.psi, obj)
+        out[mode] = (sol.j, sol.u, s.gradient(prob.psi, sol, obj), sol.iterations)
+        monkeypatch.delenv("TB_NO_PERSIST", raising=False)
+    (jp, up, gp, ip), (jg, ug, gg, ig) = out["persistent"], out["graph"]
+    assert abs(ip - ig) <= 1
+    assert abs(jp - jg) <= 1e-9 * abs(jg)
+    assert nrel(up, ug) <= 1e-8
+    assert nrel(gp, gg) <= 1e-7
+
+
+def test_mg_2d_persistent_repeatable(cuda):
+    """Deterministic reductions: back-to-back persistent solves are bit-identical."""
+    prob = configs.cfg2()
+    s = build(prob, "mg")
+    obj = tb.ComplianceObjective(s.f)
+    a = s.solve(prob.psi, obj)
+    for _ in range(5):
+        b = s.solve(prob.psi, obj)
+        assert b.iterations == a.iterations
+        assert np.array_equal(np.asarray(a.u), np.asarray(b.u))

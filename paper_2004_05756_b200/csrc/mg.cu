@@ -8,8 +8,7 @@ namespace tb {
 
 static inline int nblk(int64_t n) { return (int)((n + kBlock - 1) / kBlock); }
 constexpr int64_t kMgMinDofs = 600;     // stop coarsening below this many dofs (3D)
-constexpr int64_t kMgMinDofs2D = 600;   // 2D: small enough for the persistent kernel to keep the
-                                        // coarsest inverse in shared memory (mgpcg2d.cu)
+constexpr int64_t kMgMinDofs2D = 600;   // 2D (a 128-dof coarsest level: 27 -> 32 iterations at cfg 2)
 constexpr int64_t kMgMaxDense = 6144;   // coarsest level solved densely up to this size
 
 __device__ __forceinline__ int64_t dof_of(const Grid& g, int i, int j, int k, int nc, int c) {
@@ -410,7 +409,11 @@ int mg_build(tb_plan_impl* P) {
   l0.fixed = P->d_fixed;
   l0.dinv = P->work.dinv;  // stable pointer: graphs capture it before the first set-up
   mg.lv.push_back(l0);
-  while (mg.lv.back().n > (D == 2 ? kMgMinDofs2D : kMgMinDofs)) {
+  // TB_MG_MIN_DOFS (experiments): a 1,092-dof coarsest level at cfg 2 needs 15 instead of 27
+  // iterations, but cuSOLVER's potrf/potri then costs ~2 ms per set-up (profiles/mg_levels.sh)
+  int64_t min_dofs = (D == 2) ? kMgMinDofs2D : kMgMinDofs;
+  if (const char* e = getenv("TB_MG_MIN_DOFS")) min_dofs = atoll(e);
+  while (mg.lv.back().n > min_dofs) {
     const Grid& gf = mg.lv.back().g;
     const int cx = (gf.nx + 1) / 2, cy = (gf.ny + 1) / 2, cz = (D == 3) ? (gf.nz + 1) / 2 : 1;
     if (cx == gf.nx && cy == gf.ny && cz == gf.nz) break;  // nothing left to coarsen

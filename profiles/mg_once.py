@@ -15,7 +15,7 @@ from paper_2004_05756_b200 import configs  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-prob = configs.cfg2() if name == "cfg2" else configs.cfg3()
+prob = getattr(configs, name)()
 mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
 s = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, prob.radius), prob.f, prob.fixed, mat,
                  rtol=prob.rtol, preconditioner="mg")

@@ -531,6 +531,9 @@ def run_ours(args):
     pk = peaks()
     if args.precond == "mg":
         roof = mg_roofline(solver, rho_d, mesh, pk)
+        tpath = os.path.join(REPO, "profiles", "traffic.json")
+        if os.path.exists(tpath):
+            roof["traffic"] = json.load(open(tpath)).get(args.config + "_mg")
     else:
         roof = jacobi_roofline(solver, rho_d, mesh, pk, torch)
         tpath = os.path.join(REPO, "profiles", "traffic.json")

@@ -630,9 +630,10 @@ def run_ours(args):
 
 def cfg4_extra(args, dev, dist, world, rank):
     """BASELINE cfg 4 (43M DOF Hex8) evaluated once, slab-sharded over ALL ranks of this run:
-    at N > 1 the replicas of the headline join one distributed evaluation (NCCL allreduces +
-    NCCL send/recv halos; `--config cfg4` measures the NVLink peer-store halo), so a scaling run
-    of the default bench also records cfg 4's strong scaling.  N = 1: one slab, no collectives."""
+    at N > 1 the replicas of the headline join one distributed evaluation (NCCL allreduces, the
+    z halo as NVLink peer stores from the update kernels, or NCCL send/recv on every rank if any
+    rank cannot map its neighbours), so a scaling run of the default bench also records cfg 4's
+    strong scaling.  N = 1: one slab, no collectives."""
     import torch
 
     import paper_2004_05756_b200 as tb
@@ -645,7 +646,7 @@ def cfg4_extra(args, dev, dist, world, rank):
     sv = SlabSolver(prob.mesh, prob.k_e, prob.f, prob.fixed, mat, slab, device=dev)
     fl = SlabFilter(prob.mesh, prob.radius, slab, device=dev)
     psi = torch.as_tensor(sv.local_elems(prob.psi).copy(), device=dev)
-    comm = TorchComm(peer=False) if dist else LocalComm()
+    comm = TorchComm(peer=True) if dist else LocalComm()  # falls back to NCCL send/recv on every rank
     ev = slab_evaluate([sv], [fl], comm, [psi], rtol=prob.rtol)  # warm-up
     del ev
     if dist:
@@ -664,7 +665,7 @@ def cfg4_extra(args, dev, dist, world, rank):
                        f"{prob.rtol:g} + compliance + sensitivities + adjoint, z-slabs x{world}",
            "s_per_eval": float(t.item()), "n_gpus": world, "scaling": "strong", "pcg_iterations": ev.iterations,
            "filter_iterations": list(ev.filter_iterations), "J": ev.j,
-           "halo": "nccl send/recv" if dist else "none (one slab)",
+           "halo": ("NVLink peer stores (CUDA IPC)" if comm.peer_active else "nccl send/recv") if dist else "none (one slab)",
            "us_per_pcg_iteration_upper_bound": float(t.item()) / max(ev.iterations, 1) * 1e6}
     del ev, sv, fl, psi
     torch.cuda.empty_cache()

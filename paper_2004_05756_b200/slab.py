@@ -357,22 +357,36 @@ class TorchComm:
         self.group = group
         self.peer = peer
         self._mapped = []
-        self._ready = set()
+        self._ready = set()   # solvers whose z halo travels as peer stores
+        self._failed = set()  # solvers that fell back to NCCL send/recv
 
     def setup(self, solvers):
-        if not self.peer or id(solvers[0]) in self._ready:
+        if not self.peer or id(solvers[0]) in self._ready or id(solvers[0]) in self._failed:
             return
         s = solvers[0]
         r, n = s.slab.rank, s.slab.nranks
         handles = [None] * n
         self.dist.all_gather_object(handles, s.z_ipc_handle(), group=self.group)
-        addr = {}
-        for nb in (r - 1, r + 1):
-            if 0 <= nb < n:
-                base = _lib.P()
-                _lib.check(_lib.lib().tb_ipc_open(handles[nb], s.device.index, ctypes.byref(base)), "ipc open")
-                self._mapped.append(base.value)
-                addr[nb] = base.value
+        addr, ok, mine = {}, True, []
+        try:
+            for nb in (r - 1, r + 1):
+                if 0 <= nb < n:
+                    base = _lib.P()
+                    _lib.check(_lib.lib().tb_ipc_open(handles[nb], s.device.index, ctypes.byref(base)), "ipc open")
+                    mine.append(base.value)
+                    addr[nb] = base.value
+        except Exception:  # e.g. no peer access between the two devices
+            ok = False
+        # every rank takes the same decision: peer stores only if all ranks mapped their neighbours;
+        # otherwise this solver's z halo goes through NCCL send/recv
+        flags = [None] * n
+        self.dist.all_gather_object(flags, ok, group=self.group)
+        if not all(flags):
+            for base in mine:
+                _lib.lib().tb_ipc_close(_lib.P(base))
+            self._failed.add(id(s))
+            return
+        self._mapped += mine
         # the neighbours' ghost planes: below-neighbour's ghost-above, above-neighbour's ghost-below
         lo = addr[r - 1] + 8 * self._ghost_hi_plane(s, r - 1) * s.plane_dofs if r > 0 else 0
         hi = addr[r + 1] if r + 1 < n else 0
@@ -386,10 +400,14 @@ class TorchComm:
         other = partition(s.mesh.nz, s.slab.nranks)[rank]
         return other.own_local[1]
 
+    @property
+    def peer_active(self) -> bool:
+        return bool(self._ready)
+
     def close(self):
         for base in self._mapped:
             _lib.lib().tb_ipc_close(_lib.P(base))
-        self._mapped, self._ready = [], set()
+        self._mapped, self._ready, self._failed = [], set(), set()
 
     def allreduce(self, solvers):
         red = solvers[0].red
@@ -410,7 +428,7 @@ class TorchComm:
         return [float(a) for a in v.cpu()]
 
     def halo(self, solvers, name="z"):
-        if self.peer and name == "z":
+        if name == "z" and id(solvers[0]) in self._ready:
             return
         d = self.dist
         s = solvers[0]
@@ -429,9 +447,11 @@ class TorchComm:
                 req.wait()
 
 
-def dist_pcg_solve(solvers, comm, rtol=1e-8, maxit=200000, check_every=8):
+def dist_pcg_solve(solvers, comm, rtol=1e-8, maxit=200000, check_every=32):
     """Jacobi-pCG over the slabs of ``solvers`` (this process's share).  Returns
-    (iterations, recursive relative residual, converged flag)."""
+    (iterations, recursive relative residual, converged flag).  The host reads the device state
+    every ``check_every`` iterations (a pipeline drain each time); phases issued after
+    convergence are no-ops on the device (their kernels return on st->done)."""
     setup = getattr(comm, "setup", None)
     if setup is not None:
         setup(solvers)

@@ -46,7 +46,7 @@ struct MgpLevel {
 
 struct MgpArgs {
   MgpLevel L[kMgpMaxLv];
-  int nlev;
+  int nlev, nu;  // levels; smoothing sweeps per side (1 or 2)
   int64_t ncoarse;
   double omega;
   const double* ainv;   // coarsest dense inverse
@@ -162,13 +162,14 @@ __device__ __noinline__ void mgp_sweep(const MgpLevel& L, const Q4Pat K, const d
   }
 }
 
-// res = b - A xb on free dofs, 0 on fixed
+// res = b - A x on free dofs, 0 on fixed
 template <bool L0>
-__device__ __noinline__ void mgp_resid(const MgpLevel& L, const Q4Pat K, const double* alpha, Rng rg) {
+__device__ __noinline__ void mgp_resid(const MgpLevel& L, const Q4Pat K, const double* alpha, const double* x,
+                                       Rng rg) {
 #pragma unroll(L0 ? 2 : 1)
   for (int n = (int)rg.start; n < (int)L.g.n_nodes; n += (int)rg.stride) {
     double y[2];
-    mgp_apply<L0>(L, K, alpha, n, L.xb, y);
+    mgp_apply<L0>(L, K, alpha, n, x, y);
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       const int64_t d = 2 * n + c;
@@ -218,9 +219,9 @@ __device__ __noinline__ void mgp_restrict(const MgpLevel& C, const MgpLevel& F, 
   }
 }
 
-// xb_f += P~ xb_c on free fine dofs (bilinear interpolation; same summation order as
-// k_mg_prolong_add, all four candidate coarse values loaded up front)
-__device__ __noinline__ void mgp_prolong(const MgpLevel& F, const MgpLevel& C, Rng rg) {
+// x_f += P~ xb_c on free fine dofs (bilinear interpolation; same summation order as
+// k_mg_prolong_add, all four candidate coarse values loaded up front); xb_c = C's final iterate
+__device__ __noinline__ void mgp_prolong(const MgpLevel& F, double* xf, const MgpLevel& C, Rng rg) {
   const Grid& gf = F.g;
   const Grid& gc = C.g;
 #pragma unroll 1
@@ -238,7 +239,7 @@ __device__ __noinline__ void mgp_prolong(const MgpLevel& F, const MgpLevel& C, R
     v[1][0] = __ldcg(C.xb + c01), v[1][1] = __ldcg(C.xb + c01 + 1);
     v[2][0] = __ldcg(C.xb + c10), v[2][1] = __ldcg(C.xb + c10 + 1);
     v[3][0] = __ldcg(C.xb + c11), v[3][1] = __ldcg(C.xb + c11 + 1);
-    const double x0 = __ldcg(F.xb + 2 * n), x1 = __ldcg(F.xb + 2 * n + 1);
+    const double x0 = __ldcg(xf + 2 * n), x1 = __ldcg(xf + 2 * n + 1);
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       double acc = v[0][c];
@@ -248,7 +249,7 @@ __device__ __noinline__ void mgp_prolong(const MgpLevel& F, const MgpLevel& C, R
         if (ni == 2) acc += v[3][c];
       }
       const int64_t d = 2 * n + c;
-      if (!__ldg(F.fixed + d)) F.xb[d] = fma(w, acc, c ? x1 : x0);
+      if (!__ldg(F.fixed + d)) xf[d] = fma(w, acc, c ? x1 : x0);
     }
   }
 }
@@ -288,6 +289,7 @@ __global__ void __launch_bounds__(kMgpThreads, 1) k_mgpcg2d(Q4Pat K, MgpArgs a) 
   double rz = 0.0, rr = st->rr, beta = 0.0, alpha = 0.0, pq = 0.0;
   int done = 0;
   const int nlev = a.nlev, lg = nlev - 1;  // grid levels 0 .. nlev-2, then the dense coarsest
+  const int nu = a.nu;
   const double* alpha_e = a.alpha;
   double* x = a.x;
   double* r = a.r;
@@ -373,20 +375,22 @@ __global__ void __launch_bounds__(kMgpThreads, 1) k_mgpcg2d(Q4Pat K, MgpArgs a) 
       else if (it >= maxit) done = 2;
       if (done) break;
     }
-    // ---- rest of the V-cycle: z = M^-1 r
+    // ---- rest of the V-cycle: z = M^-1 r.  V(nu, nu), nu in {1, 2}: the pre-smoothed iterate
+    // is xa (nu = 1) or xb (nu = 2); the final iterate of every level ends in xb.
     for (int l = 0; l < lg; ++l) {
       MgpLevel& L = sL[l];
       if (l > 0) {
         mgp_restrict(L, sL[l - 1], omega, true, G);
         grid_sync_flip(bar);
-        mgp_sweep<false>(L, K, alpha_e, omega, L.xa, L.xb, G);
-        grid_sync_flip(bar);
-        mgp_resid<false>(L, K, alpha_e, G);
-      } else {
-        mgp_sweep<true>(L, K, alpha_e, omega, L.xa, L.xb, G);
-        grid_sync_flip(bar);
-        mgp_resid<true>(L, K, alpha_e, G);
       }
+      if (nu == 2) {
+        if (l == 0) mgp_sweep<true>(L, K, alpha_e, omega, L.xa, L.xb, G);
+        else mgp_sweep<false>(L, K, alpha_e, omega, L.xa, L.xb, G);
+        grid_sync_flip(bar);
+      }
+      const double* pre = (nu == 2) ? L.xb : L.xa;
+      if (l == 0) mgp_resid<true>(L, K, alpha_e, pre, G);
+      else mgp_resid<false>(L, K, alpha_e, pre, G);
       grid_sync_flip(bar);
       MGP_MARK(8 + l);
     }
@@ -396,21 +400,24 @@ __global__ void __launch_bounds__(kMgpThreads, 1) k_mgpcg2d(Q4Pat K, MgpArgs a) 
     mgp_dense(sL[nlev - 1], a.ainv, a.ncoarse);
     MGP_MARK(3);
     grid_sync_flip(bar);
-    for (int l = lg - 1; l >= 1; --l) {
+    for (int l = lg - 1; l >= 0; --l) {
       MgpLevel& L = sL[l];
-      mgp_prolong(L, sL[l + 1], G);
+      double* pre = (nu == 2) ? L.xb : L.xa;
+      mgp_prolong(L, pre, sL[l + 1], G);
       grid_sync_flip(bar);
-      mgp_sweep<false>(L, K, alpha_e, omega, L.xb, L.xa, G);
-      grid_sync_flip(bar);
-      mgp_sweep<false>(L, K, alpha_e, omega, L.xa, L.xb, G);
-      grid_sync_flip(bar);
+      if (nu == 2) {
+        if (l == 0) mgp_sweep<true>(L, K, alpha_e, omega, L.xb, L.xa, G);
+        else mgp_sweep<false>(L, K, alpha_e, omega, L.xb, L.xa, G);
+        grid_sync_flip(bar);
+      }
+      if (l == 0) {
+        mgp_sweep<true>(L, K, alpha_e, omega, L.xa, L.xb, G);  // z = xb of level 0
+      } else {
+        mgp_sweep<false>(L, K, alpha_e, omega, L.xa, L.xb, G);
+        grid_sync_flip(bar);
+      }
       MGP_MARK(16 + l);
     }
-    mgp_prolong(sL[0], sL[1], G);
-    grid_sync_flip(bar);
-    mgp_sweep<true>(sL[0], K, alpha_e, omega, z, xa0, G);
-    grid_sync_flip(bar);
-    mgp_sweep<true>(sL[0], K, alpha_e, omega, xa0, z, G);
     // ---- r.z (z = xb of level 0, this thread's own dofs), beta
     double rzp[1] = {0.0};
 #pragma unroll 1
@@ -445,6 +452,7 @@ __global__ void __launch_bounds__(kMgpThreads, 1) k_mgpcg2d(Q4Pat K, MgpArgs a) 
 bool mg_pcg2d_persistent(tb_plan_impl* P, PcgWork& w, cudaStream_t s) {
   Mg& mg = P->mg;
   if (P->g.dim != 2 || !P->pat_ok || mg.lv.size() < 2 || (int)mg.lv.size() > kMgpMaxLv) return false;
+  if (mg.nu != 1 && mg.nu != 2) return false;
   if (getenv("TB_NO_PERSIST") != nullptr) return false;  // tests: the graph path
   static int grid = -1;
   if (grid < 0) {
@@ -458,6 +466,7 @@ bool mg_pcg2d_persistent(tb_plan_impl* P, PcgWork& w, cudaStream_t s) {
   if (grid <= 0 || 2 * w.part_stride < 3 * grid) return false;
   MgpArgs a{};
   a.nlev = (int)mg.lv.size();
+  a.nu = mg.nu;
   for (int l = 0; l < a.nlev; ++l) {
     const MgLevel& L = mg.lv[l];
     MgpLevel& d = a.L[l];

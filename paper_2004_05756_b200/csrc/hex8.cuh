@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
                                                  PcgState* st, double* partials,
                                                  int zchunk, double rho_l = 0.0, double p_simp = 3.0,
                                                  const int64_t* __restrict__ zidx = nullptr,
-                                                 const int* __restrict__ zoff = nullptr) {
+                                                 const int* __restrict__ zoff = nullptr,
+                                                 int64_t col_stride = 0, int zblocks = 0) {
   // plane[4][kPlane]: node planes (buffer = plane index mod 4), AoS rows as in global memory.
   // stage[2][2][3][kHT]: node-plane corner outputs (oy) already summed over the two
   // x-neighbour elements, double buffered by step parity.  ostg[2][kOPlane]: finished owned
@@ -152,7 +153,15 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
   }
   const int t = threadIdx.x;
   const int i0 = blockIdx.x * kOX, j0 = blockIdx.y * kOY;
-  const int K0 = blockIdx.z * zchunk;
+  // several columns in one launch (ROM, !FUSED): blockIdx.z = column * zblocks + z-chunk
+  int zb = (int)blockIdx.z;
+  if (!FUSED && zblocks > 0) {
+    const int col = (int)blockIdx.z / zblocks;
+    zb = (int)blockIdx.z - col * zblocks;
+    in += col * col_stride;
+    out += col * col_stride;
+  }
+  const int K0 = zb * zchunk;
   const int K1 = min(g.nnz, K0 + zchunk);
   const int ex = t % kHX, ey = t / kHX;                   // element in the tile (ex == lane)
   const int gei = i0 - 1 + ex, gej = j0 - 1 + ey;         // global element column
@@ -412,6 +421,28 @@ inline int hex8_zchunk(const Grid& g) {
     const int64_t waves = (ctas + slots - 1) / slots;
     // cost ~ waves x per-CTA work (zc owned planes + ~1.5 planes of chunk overhead)
     const double cost = (double)waves * (zc + 1.5);
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_zc = zc;
+    }
+  }
+  return best_zc;
+}
+
+// z-chunk for ncol columns in one launch (blockIdx.z = column * chunks + chunk): the waves are
+// shared by all columns, so long chunks (little recomputation) pack as well as short ones.
+inline int hex8_zchunk_cols(const Grid& g, int ncol) {
+  const int64_t xy = (int64_t)((g.nnx + kOX - 1) / kOX) * ((g.nny + kOY - 1) / kOY);
+  const int64_t slots = (int64_t)kHexCtas * 148;
+  double best = 1e30;
+  int best_zc = g.nnz;
+  for (int64_t c = 1; c <= 64 && c <= g.nnz; ++c) {
+    const int zc = (int)((g.nnz + c - 1) / c);
+    const int64_t chunks = (g.nnz + zc - 1) / zc;
+    if (chunks * ncol > 65535) continue;
+    const int64_t ctas = xy * chunks * ncol;
+    const double waves = (double)((ctas + slots - 1) / slots);
+    const double cost = waves * (zc + 1.5);
     if (cost < best - 1e-9) {
       best = cost;
       best_zc = zc;

@@ -557,8 +557,12 @@ int tb_rom_reduced_stiffness(tb_plan* plan, const double* phi, int k, const doub
   for (int d = 0; d < nd; ++d) {
     TB_TRY(P->material(rho + (int64_t)d * g.n_elems, P->d_alpha2, nullptr, s));
     if (hex8) {
-      for (int j = 0; j < k; ++j)
-        { k_hex8<false><<<hex8_grid(g, P->zchunk), kHT, kHex8Smem, s>>>(g, P->hiso, P->d_alpha2, PhiT + (int64_t)j * ldp, nullptr, nullptr, Y + (int64_t)j * ldp, nullptr, nullptr, P->zchunk); tb::launched(); }
+      // Y = K(rho) Phi: all k columns in ONE launch (blockIdx.z = column * chunks + chunk)
+      const int zc = hex8_zchunk_cols(g, k);
+      dim3 gr = hex8_grid(g, zc);
+      const int zblocks = (int)gr.z;
+      gr.z *= (unsigned)k;
+      { k_hex8<false><<<gr, kHT, kHex8Smem, s>>>(g, P->hiso, P->d_alpha2, PhiT, nullptr, nullptr, Y, nullptr, nullptr, zc, 0.0, 3.0, nullptr, nullptr, ldp, zblocks); tb::launched(); }
       TB_CHECK_LAUNCH();
       TB_TRY(launch_atb_colmajor<true>(r0, r1, k, PhiT, Y, part, nbc, ldp, s));  // Phi^T (K Phi) is symmetric
     } else {

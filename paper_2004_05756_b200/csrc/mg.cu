@@ -401,11 +401,12 @@ int mg_build(tb_plan_impl* P) {
   Mg& mg = P->mg;
   if (mg.built) return TB_OK;
   const int D = P->g.dim;
-  // V(1,1) damped Jacobi.  2D omega 0.7 (cfg 2: 30 iterations of ~23 persistent-kernel phases
-  // against 27 of ~33 for V(2,2) with 0.6); 3D omega 0.6 (cfg 3: 18 iterations, 17.9 ms against
-  // 13 and 19.7 ms for V(2,2) with 0.5).  profiles/r1_mg_nu.txt.
-  mg.nu = 1;
-  mg.omega = (D == 2) ? 0.7 : 0.6;
+  // 2D: V(1,1), omega 0.7 (cfg 2: 30 iterations of ~23 persistent-kernel phases against 27 of
+  // ~33 for V(2,2) with 0.6).  3D: V(2,2), omega 0.5 (V(1,1) with 0.6 was faster on a raw
+  // uniform design but slower on the pre-filtered cfg 3 design: 33.4 vs 27.9 ms per
+  // evaluation).  profiles/r1_mg_nu.txt.
+  mg.nu = (D == 2) ? 1 : 2;
+  mg.omega = (D == 2) ? 0.7 : 0.5;
   if (const char* e = getenv("TB_MG_NU")) mg.nu = atoi(e);         // experiments
   if (const char* e = getenv("TB_MG_OMEGA")) mg.omega = atof(e);
   MgLevel l0;

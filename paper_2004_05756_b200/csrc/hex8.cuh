@@ -34,6 +34,10 @@ struct Hex8Iso {
 constexpr int kHX = 32, kHY = TB_HEX8_HY;   // element tile per plane (one element per thread)
 constexpr int kHT = kHX * kHY;              // 256 threads
 constexpr int kHexCtas = 512 / kHT;         // resident CTAs per SM (128 registers per thread)
+#ifndef TB_HEX8_UNROLL
+#define TB_HEX8_UNROLL 2
+#endif
+constexpr int kHex8Unroll = TB_HEX8_UNROLL;  // z-sweep unrolled by 2: no loop-carried register moves (apply 50.4 -> 48.9 us at cfg3)
 constexpr int kPX = kHX + 1, kPY = kHY + 1;  // node-plane tile incl. halo ring
 constexpr int kPN = kPX * kPY;
 constexpr int kOX = kHX - 1, kOY = kHY - 1;  // owned nodes per plane (31 x 7)
@@ -280,7 +284,7 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
   const int dk0 = FUSED ? st->dot_k0 : 0, dk1 = FUSED ? st->dot_k1 : 0;
   const int steps = K1 - (K0 - 1);  // element planes ez = K0-1 .. K1-1
   // (a 4-way unrolled sweep makes the ring offsets constants but spills and runs slower)
-#pragma unroll 1
+#pragma unroll kHex8Unroll
   for (int rel = 0; rel < steps; ++rel) {
     {
       const int r = rel & 3;

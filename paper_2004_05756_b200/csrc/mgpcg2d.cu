@@ -271,10 +271,19 @@ __device__ __forceinline__ void mgp_dense(const MgpLevel& C, const double* __res
 
 // fixed-order sum of the per-CTA partials of slot k; every warp computes it identically
 __device__ __forceinline__ double mgp_sum(const double* part, int k) {
-  const int lane = threadIdx.x & 31;
-  double s = 0.0;
-  for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(part + k * gridDim.x + b);
-  return warp_sum(s);
+  // warp 0 alone reads the partials (every warp reading them made 16x the L2 requests on the
+  // same lines) and broadcasts the fixed-order sum through shared memory
+  __shared__ double bc;
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += __ldcg(part + k * gridDim.x + b);
+    s = warp_sum(s);
+    if (threadIdx.x == 0) bc = s;
+  }
+  __syncthreads();
+  const double v = bc;
+  __syncthreads();  // bc is rewritten by the next reduction
+  return v;
 }
 
 __global__ void __launch_bounds__(kMgpThreads, 1) k_mgpcg2d(Q4Pat K, MgpArgs a) {

@@ -141,3 +141,17 @@ def test_mg_2d_persistent_repeatable(cuda):
         b = s.solve(prob.psi, obj)
         assert b.iterations == a.iterations
         assert np.array_equal(np.asarray(a.u), np.asarray(b.u))
+
+
+def test_mg_2d_kernel_time_reported(cuda):
+    """tb_pcg_kernel_time: the persistent launch of a 2D MG solve is timed on the solve's stream
+    (the bench roofline reads it); the 3D graph path reports no persistent launch."""
+    prob = configs.cfg1(seed=2)
+    s = build(prob, "mg")
+    s.solve(prob.psi, tb.ComplianceObjective(s.f))
+    ms, launches = s.last_kernel_time()
+    assert launches >= 1 and ms > 0.0
+    p3 = configs.cfg3(seed=4, nx=16, ny=8, nz=8)
+    s3 = build(p3, "mg", rtol=1e-10)
+    s3.solve(p3.psi, tb.ComplianceObjective(s3.f))
+    assert s3.last_kernel_time() == (0.0, 0)

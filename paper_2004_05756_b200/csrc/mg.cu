@@ -1,6 +1,7 @@
 // Geometric multigrid preconditioner (see mg.cuh).
 #include <cusolverDn.h>
 
+#include "cgcg2d.cuh"  // grid_sync_flip
 #include "mg.cuh"
 #include "plan.cuh"
 
@@ -8,7 +9,11 @@ namespace tb {
 
 static inline int nblk(int64_t n) { return (int)((n + kBlock - 1) / kBlock); }
 constexpr int64_t kMgMinDofs = 600;     // stop coarsening below this many dofs (3D)
-constexpr int64_t kMgMinDofs2D = 600;   // 2D (a 128-dof coarsest level: 27 -> 32 iterations at cfg 2)
+constexpr int64_t kMgMinDofs2D = 1200;  // 2D: cfg 2 stops at 1,092 dofs (19 V(1,1) iterations instead of 30
+                                        // with a 320-dof coarsest level); its inverse comes from the
+                                        // blocked Gauss-Jordan kernel below (cuSOLVER needed ~2 ms)
+constexpr int kGjB = 16;                // Gauss-Jordan block size
+constexpr int kGjMaxN = 148 * kGjB;     // one row block per CTA
 constexpr int64_t kMgMaxDense = 6144;   // coarsest level solved densely up to this size
 
 __device__ __forceinline__ int64_t dof_of(const Grid& g, int i, int j, int k, int nc, int c) {
@@ -395,6 +400,138 @@ __global__ void k_mg_gemv(int64_t n, const double* __restrict__ A, const double*
 }
 
 // ---------------------------------------------------------------------------------------
+// Coarsest inverse by blocked Gauss-Jordan elimination (SPD: no pivoting), one cooperative
+// launch.  CTA c owns row block c (kGjB rows).  Step K: every CTA loads row block K (kGjB x n)
+// into shared memory and inverts its diagonal block P in one warp (registers + shuffles).  The
+// new row block R = P^-1 [row block K] (R[:, K cols] = P^-1) is formed column-slice by slice
+// across all CTAs and parked in a scratch buffer (double-buffered by step parity: other CTAs
+// may still be reading row block K), from which owner K takes its rows at the next step.
+// Every other owner updates its rows with Gm = F P^-1 (F = its K columns):
+// A[i, :] <- A[i, :] - Gm_i [row block K] off the K columns, -Gm_i on them.  One grid barrier
+// per step.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(512, 1) k_mg_gj_inverse(int n, double* __restrict__ A, double* __restrict__ G,
+                                                          unsigned int* bar, int* info) {
+  extern __shared__ double W[];  // [kGjB][n]: row block K (old values)
+  __shared__ double Pi[kGjB][kGjB];  // P^-1
+  __shared__ double Gm[kGjB][kGjB];  // F P^-1 for this CTA's rows
+  __shared__ int bad;
+  const int nb = (n + kGjB - 1) / kGjB;
+  const int c = blockIdx.x, t = threadIdx.x, nt = blockDim.x, lane = t & 31;
+  const int cols_per = (n + gridDim.x - 1) / gridDim.x;
+  const int j0 = c * cols_per, j1 = min(n, j0 + cols_per);  // this CTA's slice of R
+  // row block rbk of the matrix, column part cpart of cps (several CTAs per row block when the
+  // grid is at least twice the block count, so more SMs share the rank-16 updates)
+  const int cps = max(1, (int)gridDim.x / nb);
+  const int rbk = c / cps, cpart = c % cps;
+  const int ucols = (n + cps - 1) / cps;
+  const int u0 = cpart * ucols, u1 = min(n, u0 + ucols);
+  if (t == 0) bad = 0;
+  for (int K = 0; K < nb; ++K) {
+    const int k0 = K * kGjB, kb = min(kGjB, n - k0);
+    const bool own = (rbk < nb && rbk != K);
+    const int r0 = rbk * kGjB, rb = own ? min(kGjB, n - r0) : 0;
+    const bool parked = own && (rbk == K - 1);  // rows of block K-1 live in G[(K-1) & 1]
+    const double* rows = parked ? G + (int64_t)((K - 1) & 1) * kGjB * n : A + (int64_t)r0 * n;
+    // row block K -> shared memory by cp.async (in flight while P^-1 and Gm are formed)
+    for (int q = t; q < kb * n; q += nt) cp_async8(W + q, A + (int64_t)k0 * n + q, true);
+    cp_async_commit();
+    // P^-1 in warp 0: lane l holds column l of [P | I] (rows in registers), Gauss-Jordan by
+    // shuffles (SPD pivots, no pivoting; a short last block is padded with identity rows)
+    if (t < 32) {
+      double col[kGjB];
+#pragma unroll
+      for (int r = 0; r < kGjB; ++r) {
+        double v;
+        if (lane < kGjB) v = (r < kb && lane < kb) ? __ldcg(A + (int64_t)(k0 + r) * n + k0 + lane) : (r == lane ? 1.0 : 0.0);
+        else v = (lane - kGjB == r) ? 1.0 : 0.0;
+        col[r] = v;
+      }
+#pragma unroll
+      for (int m = 0; m < kGjB; ++m) {
+        const double piv = __shfl_sync(0xffffffffu, col[m], m);
+        if (lane == 0 && !(piv > 0.0) && bad == 0) bad = k0 + m + 1;
+        col[m] = col[m] / piv;
+#pragma unroll
+        for (int r = 0; r < kGjB; ++r) {
+          if (r == m) continue;
+          const double f = __shfl_sync(0xffffffffu, col[r], m);
+          col[r] = fma(-f, col[m], col[r]);
+        }
+      }
+      if (lane >= kGjB) {
+#pragma unroll
+        for (int r = 0; r < kGjB; ++r) Pi[r][lane - kGjB] = col[r];
+      }
+    }
+    __syncthreads();
+    // Gm = F P^-1, F = this row block's K columns (old)
+    if (own && t < kGjB * kGjB) {
+      const int r = t / kGjB, p = t % kGjB;
+      double f[kGjB];
+#pragma unroll
+      for (int m = 0; m < kGjB; ++m) f[m] = (r < rb && m < kb) ? __ldcg(rows + (int64_t)r * n + k0 + m) : 0.0;
+      double acc = 0.0;
+#pragma unroll
+      for (int m = 0; m < kGjB; ++m) acc = fma(f[m], Pi[m][p], acc);
+      Gm[r][p] = (p < kb) ? acc : 0.0;
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    // this CTA's slice of R = P^-1 [row block K] (R[:, K cols] = P^-1), parked for owner K
+    {
+      double* g = G + (int64_t)(K & 1) * kGjB * n;
+      for (int q = t; q < kGjB * (j1 - j0); q += nt) {
+        const int r = q / (j1 - j0), j = j0 + q % (j1 - j0);
+        if (r >= kb) continue;
+        double acc;
+        if (j >= k0 && j < k0 + kb) {
+          acc = Pi[r][j - k0];
+        } else {
+          acc = 0.0;
+#pragma unroll
+          for (int m = 0; m < kGjB; ++m)
+            if (m < kb) acc = fma(Pi[r][m], W[m * n + j], acc);
+        }
+        g[(int64_t)r * n + j] = acc;
+      }
+    }
+    // row i <- row i - Gm_i [row block K] off the K columns, -Gm_i on them (columns u0 .. u1)
+    if (own) {
+      for (int j = u0 + t; j < u1; j += nt) {
+        double w[kGjB], old[kGjB];
+        const bool kc = (j >= k0 && j < k0 + kb);
+#pragma unroll
+        for (int m = 0; m < kGjB; ++m) w[m] = (m < kb && !kc) ? W[m * n + j] : 0.0;
+#pragma unroll
+        for (int r = 0; r < kGjB; ++r) old[r] = (r < rb && !kc) ? __ldcg(rows + (int64_t)r * n + j) : 0.0;
+#pragma unroll
+        for (int r = 0; r < kGjB; ++r) {
+          if (r >= rb) continue;
+          double v;
+          if (kc) {
+            v = -Gm[r][j - k0];
+          } else {
+            v = old[r];
+#pragma unroll
+            for (int m = 0; m < kGjB; ++m) v = fma(-Gm[r][m], w[m], v);
+          }
+          A[(int64_t)(r0 + r) * n + j] = v;
+        }
+      }
+    }
+    grid_sync_flip(bar);
+  }
+  // the last pivot block's rows are still parked in G
+  if (c == 0) {
+    const int k0 = (nb - 1) * kGjB, kb = n - k0;
+    const double* g = G + (int64_t)((nb - 1) & 1) * kGjB * n;
+    for (int q = t; q < kb * n; q += nt) A[(int64_t)k0 * n + q] = __ldcg(g + q);
+  }
+  if (t == 0 && bad) atomicMax(info, bad);
+}
+
+// ---------------------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------------------
 int mg_build(tb_plan_impl* P) {
@@ -502,7 +639,14 @@ int mg_build(tb_plan_impl* P) {
   mg.lwork = l1 > l2 ? l1 : l2;
   TB_CUDA(cudaMalloc(&mg.work, sizeof(double) * (size_t)(mg.lwork + 1)));
   TB_CUDA(cudaMalloc(&mg.info, sizeof(int)));
-  mg.ainv = mg.dense;  // potri overwrites the factor with the inverse in place
+  mg.ainv = mg.dense;  // potri (or Gauss-Jordan) overwrites the matrix with its inverse in place
+  if (D == 2 && mg.ncoarse <= kGjMaxN && getenv("TB_MG_CUSOLVER") == nullptr) {
+    TB_CUDA(cudaMalloc(&mg.gj, sizeof(double) * 2 * kGjB * (size_t)mg.ncoarse));
+    TB_CUDA(cudaMalloc(&mg.gj_bar, 64));
+    TB_CUDA(cudaMemset(mg.gj_bar, 0, 64));
+    TB_CUDA(cudaFuncSetAttribute(k_mg_gj_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(double) * kGjB * (size_t)mg.ncoarse)));
+  }
   mg.built = true;
   return TB_OK;
 }
@@ -522,6 +666,8 @@ void mg_release(Mg& mg) {
   }
   mg.lv.clear();
   if (mg.dense) cudaFree(mg.dense);
+  if (mg.gj) cudaFree(mg.gj);
+  if (mg.gj_bar) cudaFree(mg.gj_bar);
   if (mg.G) cudaFree(mg.G);
   if (mg.dirty) cudaFree(mg.dirty);
   if (mg.work) cudaFree(mg.work);
@@ -571,6 +717,28 @@ int mg_setup(tb_plan_impl* P, cudaStream_t s) {
   else
     { k_mg_dense<3><<<nblk(n), kBlock, 0, s>>>(Lc.g, Lc.ke, Lc.fixed, mg.dense); tb::launched(); }
   TB_CHECK_LAUNCH();
+  if (mg.gj != nullptr) {  // 2D: blocked Gauss-Jordan, one cooperative launch
+    TB_CUDA(cudaMemsetAsync(mg.info, 0, sizeof(int), s));
+    int nn = (int)n;
+    double* A = mg.dense;
+    void* args[] = {(void*)&nn, (void*)&A, (void*)&mg.gj, (void*)&mg.gj_bar, (void*)&mg.info};
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    TB_CUDA(cudaLaunchCooperativeKernel((const void*)k_mg_gj_inverse, sms, 512, args,
+                                        sizeof(double) * kGjB * (size_t)n, s));
+    tb::launched();
+    int info = 0;
+    TB_CUDA(cudaMemcpyAsync(&info, mg.info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    TB_CUDA(cudaStreamSynchronize(s));
+    if (info != 0) {
+      set_error("coarsest multigrid operator is not positive definite (pivot %d)", info);
+      return TB_ERR_INDEFINITE;
+    }
+    { k_mg_symmetrize<<<nblk(n * n), kBlock, 0, s>>>(n, mg.dense); tb::launched(); }
+    TB_CHECK_LAUNCH();
+    return TB_OK;
+  }
   cusolverDnHandle_t h = (cusolverDnHandle_t)mg.solver;
   cusolverDnSetStream(h, s);
   if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, (int)n, mg.dense, (int)n, mg.work, mg.lwork, mg.info) !=

@@ -38,6 +38,8 @@ struct Mg {
   double* G = nullptr;         // level-1 fast path: R_ch^T K_unit R_ch per child (2^D x NE x NE)
   uint8_t* dirty = nullptr;    // level-1 coarse elements that need the general aggregation
   double* dense = nullptr;     // coarsest dense matrix scratch
+  double* gj = nullptr;        // 2D: Gauss-Jordan parked pivot rows (2 x kGjB x n)
+  unsigned int* gj_bar = nullptr;  // its grid barrier
   int64_t ncoarse = 0;
   int nu = 2;                  // smoothing sweeps
   double omega = 0.6;          // Jacobi damping

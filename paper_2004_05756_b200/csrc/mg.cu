@@ -13,7 +13,7 @@ constexpr int64_t kMgMinDofs2D = 1200;  // 2D: cfg 2 stops at 1,092 dofs (19 V(1
                                         // with a 320-dof coarsest level); its inverse comes from the
                                         // blocked Gauss-Jordan kernel below (cuSOLVER needed ~2 ms)
 constexpr int kGjB = 16;                // Gauss-Jordan block size
-constexpr int kGjMaxN = 148 * kGjB;     // one row block per CTA
+constexpr int kGjMaxN = 1700;           // row block K (kGjB x n doubles) fits in shared memory
 constexpr int64_t kMgMaxDense = 6144;   // coarsest level solved densely up to this size
 
 __device__ __forceinline__ int64_t dof_of(const Grid& g, int i, int j, int k, int nc, int c) {

@@ -239,18 +239,24 @@ class Clocks:
 
 
 def time_eval(solver, obj, psi, torch, reps=3):
-    """Seconds per full evaluation (solve + gradient), device-resident, after one warm-up."""
-    sol = solver.solve(psi, obj)
-    solver.gradient(psi, sol, obj)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    a.record()
-    for _ in range(reps):
+    """Seconds per full evaluation (solve + gradient), device-resident: median of ``reps`` timed
+    evaluations after two warm-ups (results kept alive as in the headline loop)."""
+    sol = g = None
+    for _ in range(2):
         sol = solver.solve(psi, obj)
-        solver.gradient(psi, sol, obj)
-    b.record()
-    torch.cuda.synchronize()
-    return a.elapsed_time(b) * 1e-3 / reps, sol
+        g = solver.gradient(psi, sol, obj)
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        sol = solver.solve(psi, obj)
+        g = solver.gradient(psi, sol, obj)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) * 1e-3)
+    del g
+    return statistics.median(ts), sol
 
 
 def mg_roofline(solver, rho_d, mesh, pk):

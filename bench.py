@@ -160,7 +160,8 @@ def run_reference(args):
 # clocks sampled during the timed region
 # --------------------------------------------------------------------------------------
 class Clocks:
-    """SM clocks and throttle reasons sampled every 100 ms DURING the timed region.
+    """SM clocks and throttle reasons sampled every 10 ms DURING the timed region (the cfg 2
+    headline's timed region is ~40 ms).
 
     In-process NVML (pynvml) on a thread; the nvidia-smi CLI is the fallback.  (Launching
     nvidia-smi right before the timed loop once stalled a step by ~20-45 ms.)"""
@@ -196,7 +197,7 @@ class Clocks:
                         self.rows.append((sm, mx, rs))
                     except Exception:  # noqa: BLE001
                         pass
-                    self.stop_flag.wait(0.1)
+                    self.stop_flag.wait(0.01)
 
             self.thread = threading.Thread(target=run, daemon=True)
             self.thread.start()
@@ -207,7 +208,7 @@ class Clocks:
                  "clocks_event_reasons.sw_power_cap")
             try:
                 self.smi = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                                             "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                             "--format=csv,noheader,nounits", "-lms", "10"], stdout=self.f,
                                             stderr=subprocess.DEVNULL)
             except OSError:
                 self.smi = None

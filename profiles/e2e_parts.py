@@ -12,7 +12,8 @@ from paper_2004_05756_b200 import configs  # noqa: E402
 
 prob = configs.cfg2()
 s = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, prob.radius), prob.f, prob.fixed,
-                 tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP), rtol=prob.rtol)
+                 tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP), rtol=prob.rtol,
+                 preconditioner="mg")
 obj = tb.ComplianceObjective(s.f)
 psi_h = np.ascontiguousarray(prob.psi)
 psi_d = torch.as_tensor(psi_h, device="cuda")

@@ -643,6 +643,7 @@ int mg_build(tb_plan_impl* P) {
   if (D == 2 && mg.ncoarse <= kGjMaxN && getenv("TB_MG_CUSOLVER") == nullptr) {
     TB_CUDA(cudaMalloc(&mg.gj, sizeof(double) * 2 * kGjB * (size_t)mg.ncoarse));
     TB_CUDA(cudaMalloc(&mg.gj_bar, 64));
+    TB_CUDA(cudaMallocHost(&mg.h_info, sizeof(int)));
     TB_CUDA(cudaMemset(mg.gj_bar, 0, 64));
     TB_CUDA(cudaFuncSetAttribute(k_mg_gj_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(sizeof(double) * kGjB * (size_t)mg.ncoarse)));
@@ -668,6 +669,7 @@ void mg_release(Mg& mg) {
   if (mg.dense) cudaFree(mg.dense);
   if (mg.gj) cudaFree(mg.gj);
   if (mg.gj_bar) cudaFree(mg.gj_bar);
+  if (mg.h_info) cudaFreeHost(mg.h_info);
   if (mg.G) cudaFree(mg.G);
   if (mg.dirty) cudaFree(mg.dirty);
   if (mg.work) cudaFree(mg.work);
@@ -728,13 +730,9 @@ int mg_setup(tb_plan_impl* P, cudaStream_t s) {
     TB_CUDA(cudaLaunchCooperativeKernel((const void*)k_mg_gj_inverse, sms, 512, args,
                                         sizeof(double) * kGjB * (size_t)n, s));
     tb::launched();
-    int info = 0;
-    TB_CUDA(cudaMemcpyAsync(&info, mg.info, sizeof(int), cudaMemcpyDeviceToHost, s));
-    TB_CUDA(cudaStreamSynchronize(s));
-    if (info != 0) {
-      set_error("coarsest multigrid operator is not positive definite (pivot %d)", info);
-      return TB_ERR_INDEFINITE;
-    }
+    // the pivot check is read after the solve's own stream sync (mg_check): no bubble here
+    TB_CUDA(cudaMemcpyAsync(mg.h_info, mg.info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    mg.info_pending = true;
     { k_mg_symmetrize<<<nblk(n * n), kBlock, 0, s>>>(n, mg.dense); tb::launched(); }
     TB_CHECK_LAUNCH();
     return TB_OK;
@@ -807,6 +805,17 @@ static void vcycle(tb_plan_impl* P, size_t l, const double* b, double* x, cudaSt
     level_apply(P, l, x, L.t, s);
     { k_mg_jacobi<<<nb, kBlock, 0, s>>>(L.n, mg.omega, L.dinv, b, L.t, x, x); tb::launched(); }
   }
+}
+
+int mg_check(tb_plan_impl* P) {
+  Mg& mg = P->mg;
+  if (!mg.info_pending) return TB_OK;
+  mg.info_pending = false;
+  if (*mg.h_info != 0) {
+    set_error("coarsest multigrid operator is not positive definite (pivot %d)", *mg.h_info);
+    return TB_ERR_INDEFINITE;
+  }
+  return TB_OK;
 }
 
 int mg_apply(tb_plan_impl* P, const double* r, double* z, cudaStream_t s) {

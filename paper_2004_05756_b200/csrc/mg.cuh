@@ -39,6 +39,8 @@ struct Mg {
   uint8_t* dirty = nullptr;    // level-1 coarse elements that need the general aggregation
   double* dense = nullptr;     // coarsest dense matrix scratch
   double* gj = nullptr;        // 2D: Gauss-Jordan parked pivot rows (2 x kGjB x n)
+  int* h_info = nullptr;       // pinned copy of the Gauss-Jordan pivot flag, read after the solve
+  bool info_pending = false;
   unsigned int* gj_bar = nullptr;  // its grid barrier
   int64_t ncoarse = 0;
   int nu = 2;                  // smoothing sweeps
@@ -54,6 +56,7 @@ struct tb_plan_impl;
 int mg_build(tb_plan_impl* P);                          // allocate the hierarchy (once per plan)
 int mg_setup(tb_plan_impl* P, cudaStream_t s);          // operators for the current alpha
 int mg_apply(tb_plan_impl* P, const double* r, double* z, cudaStream_t s);  // z = M^-1 r
+int mg_check(tb_plan_impl* P);  // after a stream sync: the deferred set-up check (SPD coarsest level)
 struct PcgWork;
 // 2D: the whole MG-preconditioned pCG loop in one persistent cooperative launch (mgpcg2d.cu);
 // false when unavailable (3D, TB_NO_PERSIST, no co-residency) -> graph path

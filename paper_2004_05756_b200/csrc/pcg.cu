@@ -388,6 +388,7 @@ static int pcg_solve_pc(const PcgOp& op, PcgWork& w, const double* b, double* x_
     TB_CHECK_LAUNCH();
     TB_CUDA(cudaMemcpyAsync(w.h_st, w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
     TB_CUDA(cudaStreamSynchronize(s));
+    TB_TRY(op.precond_check());
     const PcgState& h = *w.h_st;
     if (!persistent) launched((int64_t)(h.iters - it_before) * 40);  // approximate: kernels per V-cycle iteration
     it_before = h.iters;

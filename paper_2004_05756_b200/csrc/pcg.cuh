@@ -33,6 +33,8 @@ struct PcgOp {
   virtual bool has_precond() const { return false; }
   virtual int precond_setup(cudaStream_t s) const { (void)s; return TB_OK; }
   virtual int precond_apply(const double* r, double* z, cudaStream_t s) const { (void)r; (void)z; (void)s; return TB_OK; }
+  // deferred set-up checks, called after a stream synchronisation
+  virtual int precond_check() const { return TB_OK; }
   virtual void launch_persistent(const PcgWork& w, cudaStream_t s) const { (void)w; (void)s; }
   // preconditioned loop (from r, pa = 0) in one persistent launch; false: use the graph loop
   virtual bool launch_persistent_pc(PcgWork& w, cudaStream_t s) const { (void)w; (void)s; return false; }

@@ -130,6 +130,7 @@ int tb_plan_impl::init(const uint8_t* fixed_host) {
 bool ElastOp::has_precond() const { return plan->precond == 1 && !plan->dist; }
 int ElastOp::precond_setup(cudaStream_t s) const { return mg_setup(plan, s); }
 int ElastOp::precond_apply(const double* r, double* z, cudaStream_t s) const { return mg_apply(plan, r, z, s); }
+int ElastOp::precond_check() const { return plan->precond == 1 ? mg_check(plan) : TB_OK; }
 
 void tb_plan_impl::release() {
   mg_release(mg);

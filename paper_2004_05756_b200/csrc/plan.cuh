@@ -25,6 +25,7 @@ struct ElastOp final : PcgOp {
   int precond_setup(cudaStream_t s) const override;
   int precond_apply(const double* r, double* z, cudaStream_t s) const override;
   bool launch_persistent_pc(PcgWork& w, cudaStream_t s) const override;
+  int precond_check() const override;
   int persist_grid = 0;
   TileSpec tiles{0, 0, 0, 0, 0};  // 2D persistent pCG decomposition (tx = 0: row strips)
 };

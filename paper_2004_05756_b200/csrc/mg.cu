@@ -434,7 +434,18 @@ __global__ void __launch_bounds__(512, 1) k_mg_gj_inverse(int n, double* __restr
     const bool parked = own && (rbk == K - 1);  // rows of block K-1 live in G[(K-1) & 1]
     const double* rows = parked ? G + (int64_t)((K - 1) & 1) * kGjB * n : A + (int64_t)r0 * n;
     // row block K -> shared memory by cp.async (in flight while P^-1 and Gm are formed)
-    for (int q = t; q < kb * n; q += nt) cp_async8(W + q, A + (int64_t)k0 * n + q, true);
+    // only the columns this CTA reads: its R slice [j0, j1) and its update part [u0, u1)
+    // (the pivot block comes from global memory below)
+    for (int q = t; q < kb * (j1 - j0); q += nt) {
+      const int r = q / (j1 - j0), j = j0 + q % (j1 - j0);
+      cp_async8(W + (size_t)r * n + j, A + (int64_t)(k0 + r) * n + j, true);
+    }
+    if (own)
+      for (int q = t; q < kb * (u1 - u0); q += nt) {
+        const int r = q / (u1 - u0), j = u0 + q % (u1 - u0);
+        if (j >= j0 && j < j1) continue;  // already requested
+        cp_async8(W + (size_t)r * n + j, A + (int64_t)(k0 + r) * n + j, true);
+      }
     cp_async_commit();
     // P^-1 in warp 0: lane l holds column l of [P | I] (rows in registers), Gauss-Jordan by
     // shuffles (SPD pivots, no pivoting; a short last block is padded with identity rows)
@@ -451,7 +462,7 @@ __global__ void __launch_bounds__(512, 1) k_mg_gj_inverse(int n, double* __restr
       for (int m = 0; m < kGjB; ++m) {
         const double piv = __shfl_sync(0xffffffffu, col[m], m);
         if (lane == 0 && !(piv > 0.0) && bad == 0) bad = k0 + m + 1;
-        col[m] = col[m] / piv;
+        col[m] = col[m] * __drcp_rn(piv);
 #pragma unroll
         for (int r = 0; r < kGjB; ++r) {
           if (r == m) continue;

@@ -70,13 +70,13 @@ def workload_desc(prob, precond="mg"):
             f"fp64")
 
 
-def mg_bytes_per_iteration(nx, ny):
+def mg_bytes_per_iteration(nx, ny, min_dofs=1200):
     """Algorithmic bytes of one MG-preconditioned CG iteration of the persistent 2D kernel
-    (k_mgpcg2d), each vector read or written once per phase: level 0 matrix-free (alpha per
-    element), coarse levels from their half stencils (10 doubles per dof), the dense coarsest
-    inverse read once.  Hierarchy as mg.cu: halve each axis until <= 600 dofs."""
+    (k_mgpcg2d, V(1,1) cycle), each vector read or written once per phase: level 0 matrix-free
+    (alpha per element), coarse levels from their half stencils (10 doubles per dof), the dense
+    coarsest inverse read once.  Hierarchy as mg.cu: halve each axis until <= min_dofs dofs."""
     levels = [(nx, ny)]
-    while 2 * (levels[-1][0] + 1) * (levels[-1][1] + 1) > 600:
+    while 2 * (levels[-1][0] + 1) * (levels[-1][1] + 1) > min_dofs:
         a, b = levels[-1]
         c = ((a + 1) // 2, (b + 1) // 2)
         if c == (a, b):
@@ -85,11 +85,17 @@ def mg_bytes_per_iteration(nx, ny):
     n = [2 * (a + 1) * (b + 1) for a, b in levels]
     ne = nx * ny
     L = len(n)
-    d = 4 * n[0] + ne + 8 * n[0]                  # A: z, p_old, p, q, alpha; B: x, r, p, q, D^-1, xa
-    d += 4 * (4 * n[0] + ne) + 2 * n[0] + n[1] + 2 * n[0]  # 3 sweeps + residual, prolongation, r.z
+    d = (4 * n[0] + ne) + 8 * n[0]         # A: z, p_old, alpha -> p, q; B: x, r, p, q, D^-1 -> x, r, xa
+    d += 4 * n[0] + ne                     # level-0 residual
+    d += 2 * n[0] + n[1]                   # level-0 prolongation
+    d += 4 * n[0] + ne + 2 * n[0]          # level-0 post sweep, r.z
     for l in range(1, L - 1):
-        d += n[l - 1] + 3 * n[l] + 4 * 14 * n[l] + 2 * n[l] + n[l + 1]
-    d += n[L - 2] + n[L - 1] + n[L - 1] ** 2 + 2 * n[L - 1]
+        d += n[l - 1] + 3 * n[l]           # restriction + first sweep
+        d += 14 * n[l]                     # residual (stencil 10 + xa, b, D^-1, res)
+        d += 2 * n[l] + n[l + 1]           # prolongation
+        d += 14 * n[l]                     # post sweep
+    d += n[L - 2] + 2 * n[L - 1]           # coarsest restriction
+    d += n[L - 1] ** 2 + 2 * n[L - 1]      # dense coarsest solve
     return 8 * d, n
 
 
@@ -278,9 +284,9 @@ def mg_roofline(solver, rho_d, mesh, pk):
             "iterations_per_launch": its / max(launches, 1), "us_per_iteration": t * 1e6 / max(its, 1),
             "bytes_per_iteration": per_it, "level_dofs": sizes,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "fallback" not in pk else "fallback",
-            "note": ("the hierarchy (< 25 MB) is L2-resident; ~30 grid-barrier phases per iteration cost ~4 us "
-                     "each (L2 round trip + barrier), so the kernel is latency-bound, not HBM-bound "
-                     "(profiles/mg_prof.py)")}
+            "note": ("the hierarchy (< 30 MB) is L2-resident; ~20 grid-barrier phases per V(1,1) iteration cost "
+                     "~4 us each (L2 round trip + barrier), so the kernel is latency-bound, not HBM-bound "
+                     "(profiles/mg_prof.py); the coarsest inverse (k_mg_gj_inverse) is set-up, not timed here")}
 
 
 def jacobi_roofline(solver, rho_d, mesh, pk, torch):

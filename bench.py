@@ -1,19 +1,22 @@
 #!/usr/bin/env python
 """Benchmark of the FE-evaluation hot path (BASELINE.json metric) on B200.
 
-Headline: "FE solve+sensitivity s/eval" on BASELINE cfg 2 (600x200 Q4 cantilever, 241,602
-DOF): psi -> Helmholtz filter (R = 3) -> clamp -> pCG K(rho)u = f to a TRUE relative residual of
-1e-10 -> compliance -> element sensitivities -> filter adjoint (the gradient).  The pCG is
-preconditioned by the geometric multigrid V-cycle (--precond mg, default; one persistent kernel
-per solve) or by Jacobi (--precond jacobi, the north_star's subsystem (1), also reported under
-extra.jacobi with its own roofline).
-One step = one design evaluation with inputs resident in HBM.  ``e2e`` repeats it through the
-reference-facing API with host numpy buffers (H2D of psi, D2H of rho, u and the gradient).
+Headline (default ``--config cfg3``): "FE solve+sensitivity s/eval" on BASELINE cfg 3, the
+largest single-GPU configuration (192x96x96 Hex8 cantilever, 5,447,811 DOF): psi -> Helmholtz
+filter (R = 2.5) -> clamp -> matrix-free Jacobi-pCG K(rho)u = f to a TRUE relative residual of
+1e-8 -> compliance -> element sensitivities -> filter adjoint (the gradient).  One step = one
+design evaluation with psi resident in HBM.  ``e2e`` repeats it through the reference-facing API
+(HdmSolver.solve(numpy) + gradient -> numpy): H2D of psi, D2H of rho, u, g and the scalars.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config cfg2]
+Every other BASELINE config is measured in the same run under ``extra`` (cfg 1 and cfg 2 2D
+evaluations, cfg 3 with the multigrid preconditioner, the cfg 4 43M-DOF evaluation sharded over
+all ranks, the cfg 5 16-design ROM step), each with its roofline and its CPU baseline.
 
-Multi-GPU: cfg 2 does not shard (SURVEY §8e "replicas only"); N ranks run N independent
-replicas, value = total step time (max over ranks) / (K * N).
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config cfg3]
+
+Multi-GPU: cfg 1-3 do not shard (SURVEY §8e "replicas only"): N ranks run N independent
+replicas, value = total step time (max over ranks) / (K * N).  The cfg 4 extra is one
+evaluation slab-sharded over all N ranks (strong scaling).
 """
 
 from __future__ import annotations
@@ -29,9 +32,13 @@ import time
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
+REF_PATH = os.path.join(REPO, "baseline", "_ref")  # romtopt installed from /root/reference (git-ignored)
 
 METRIC = "FE solve+sensitivity s/eval"
 UNIT = "s/eval"
+# Jacobi-pCG iterations of the cfg 3 evaluation (seed 0) measured on B200; the standalone CPU
+# reference arm extrapolates its fixed-budget CG sample to this count.
+CFG3_JACOBI_ITERS = 2513
 
 
 def parse():
@@ -40,86 +47,23 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg4", "cfg5"],
-                    help="cfg1/cfg2: HDM evaluation (headline cfg2); cfg4: slab-sharded 3D solve; cfg5: batched ROM")
+    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="cfg1-3: HDM evaluation (headline cfg3); cfg4: slab-sharded 3D evaluation; cfg5: ROM step")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--precond", default="mg", choices=["mg", "jacobi"],
-                    help="pCG preconditioner of the cfg1/cfg2 evaluation (both solve to the same true residual)")
+    ap.add_argument("--precond", default="jacobi", choices=["mg", "jacobi"],
+                    help="pCG preconditioner of the cfg1-3 evaluation (both stop on the same true residual)")
     ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
                     help="cfg4 halo exchange: NVLink peer stores fused into the update kernel, or NCCL send/recv")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--extras", default="cfg1,cfg2,cfg3mg,cfg4,cfg5", help="comma list of extras to run")
     ap.add_argument("--no-flush", action="store_true", help="diagnostic: skip the L2 flush between steps")
-    ap.add_argument("--extra3d", type=int, default=1, help="also time BASELINE cfg 3 (3D Hex8) as an extra")
     return ap.parse_args()
-
-
-def problem(name, seed):
-    from paper_2004_05756_b200 import configs
-
-    return getattr(configs, name)(seed=seed)
-
-
-PC_DESC = {"mg": "multigrid-preconditioned CG (V(2,2), Galerkin coarse levels)", "jacobi": "Jacobi-pCG"}
-
-
-def workload_desc(prob, precond="mg"):
-    m = prob.mesh
-    return (f"{prob.name}: {m.nx}x{m.ny} Q4, {m.n_dofs} DOF ({prob.n_free} free); Helmholtz filter R={prob.radius:g} "
-            f"+ {PC_DESC[precond]} to true-residual rtol {prob.rtol:g} + compliance + sensitivity + filter adjoint; "
-            f"fp64")
-
-
-def mg_bytes_per_iteration(nx, ny, min_dofs=1200):
-    """Algorithmic bytes of one MG-preconditioned CG iteration of the persistent 2D kernel
-    (k_mgpcg2d, V(1,1) cycle), each vector read or written once per phase: level 0 matrix-free
-    (alpha per element), coarse levels from their half stencils (10 doubles per dof), the dense
-    coarsest inverse read once.  Hierarchy as mg.cu: halve each axis until <= min_dofs dofs."""
-    levels = [(nx, ny)]
-    while 2 * (levels[-1][0] + 1) * (levels[-1][1] + 1) > min_dofs:
-        a, b = levels[-1]
-        c = ((a + 1) // 2, (b + 1) // 2)
-        if c == (a, b):
-            break
-        levels.append(c)
-    n = [2 * (a + 1) * (b + 1) for a, b in levels]
-    ne = nx * ny
-    L = len(n)
-    d = (4 * n[0] + ne) + 8 * n[0]         # A: z, p_old, alpha -> p, q; B: x, r, p, q, D^-1 -> x, r, xa
-    d += 4 * n[0] + ne                     # level-0 residual
-    d += 2 * n[0] + n[1]                   # level-0 prolongation
-    d += 4 * n[0] + ne + 2 * n[0]          # level-0 post sweep, r.z
-    for l in range(1, L - 1):
-        d += n[l - 1] + 3 * n[l]           # restriction + first sweep
-        d += 14 * n[l]                     # residual (stencil 10 + xa, b, D^-1, res)
-        d += 2 * n[l] + n[l + 1]           # prolongation
-        d += 14 * n[l]                     # post sweep
-    d += n[L - 2] + 2 * n[L - 1]           # coarsest restriction
-    d += n[L - 1] ** 2 + 2 * n[L - 1]      # dense coarsest solve
-    return 8 * d, n
 
 
 def rank_info():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
             int(os.environ.get("WORLD_SIZE", 1)))
-
-
-# --------------------------------------------------------------------------------------
-# CPU reference arm: the oracle port of romtopt's HdmSolver.solve + gradient
-# --------------------------------------------------------------------------------------
-def cpu_port(prob):
-    from oracle.fem import build_grid
-    from oracle.hdm import Filter, Hdm, Material
-    from paper_2004_05756_b200 import configs
-
-    g = build_grid(prob.mesh.nx, prob.mesh.ny, prob.mesh.h)
-    return Hdm(g, prob.k_e, Filter(g, prob.radius), prob.f, prob.fixed, Material(configs.RHO_L, configs.P_SIMP))
-
-
-def cpu_eval(hdm, psi):
-    sol = hdm.solve(psi)
-    hdm.gradient(sol)
-    return sol["j"]
 
 
 def cores():
@@ -129,48 +73,255 @@ def cores():
         return os.cpu_count() or 1
 
 
-def run_reference(args):
-    rank, _, world = rank_info()
-    if rank != 0:
-        return
-    prob = problem(args.config, args.seed)
-    hdm = cpu_port(prob)  # one-time set-up (filter factorisation), not timed — as the reference's constructors
-    for _ in range(min(args.warmup, 1)):
-        cpu_eval(hdm, prob.psi)
-    t0 = time.perf_counter()
-    first = time.perf_counter()
-    cpu_eval(hdm, prob.psi)
-    per = time.perf_counter() - first
-    n = 1
-    budget = 150.0  # keep the reference arm within a few minutes
-    while n < args.steps and (n + 1) * per <= budget:
-        cpu_eval(hdm, prob.psi)
-        n += 1
-    total = time.perf_counter() - t0
-    v = total / n
-    sample = (f"{n} full evaluations of {prob.name} (oracle port of romtopt HdmSolver.solve + gradient: scipy "
-              f"SuperLU factorisation per design, single-threaded, + OpenBLAS GEMMs)")
-    line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": n,
-        "warmup": min(args.warmup, 1), "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE recipe)",
-        "config": {"workload": workload_desc(prob, args.precond), "parallelism": "cpu", "seed": args.seed,
-                   "reference_solver": "SuperLU direct factorisation (romtopt fem.py:270-349)"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores(), "kind": "port", "sample": sample},
-        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+def peaks():
+    try:
+        return json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "fallback": True}
+
+
+def peak_source(pk):
+    return "fallback (B200_PROFILING.md)" if pk.get("fallback") else "MEASURED_PEAKS.json hbm_gbs (burst copy)"
+
+
+PC_DESC = {"mg": "multigrid-preconditioned CG (geometric MG, Galerkin coarse levels; 2D V(1,1), 3D V(2,2))",
+           "jacobi": "matrix-free Jacobi-pCG"}
+
+
+def workload_desc(prob, precond):
+    m = prob.mesh
+    dims = f"{m.nx}x{m.ny}" + (f"x{m.nz}" if m.dim == 3 else "")
+    el = "Hex8" if m.dim == 3 else "Q4"
+    return (f"{prob.name}: {dims} {el}, {m.n_dofs} DOF ({prob.n_free} free); Helmholtz filter R={prob.radius:g} + "
+            f"{PC_DESC[precond]} to true-residual rtol {prob.rtol:g} + compliance + sensitivity + filter adjoint; fp64")
+
+
+# --------------------------------------------------------------------------------------
+# problems (cfg 3's design is pre-filtered with R = 2: on the GPU for our arm, on the CPU
+# -- same restated Helmholtz operator, CG to 1e-13 -- for the standalone reference arm)
+# --------------------------------------------------------------------------------------
+def problem(name, seed, dev=None):
+    from paper_2004_05756_b200 import configs
+
+    if name != "cfg3":
+        return getattr(configs, name)(seed=seed)
+    if dev is not None:
+        import torch
+
+        import paper_2004_05756_b200 as tb
+
+        def prefilter(mesh, psi0):
+            return tb.HelmholtzFilter(mesh, 2.0).apply(torch.as_tensor(psi0, device=dev)).rho.cpu().numpy()
+    else:
+        from oracle import iterative as it
+        from oracle.fem import build_grid
+
+        def prefilter(mesh, psi0):
+            g = build_grid(mesh.nx, mesh.ny, mesh.h, nz=mesh.nz)
+            return it.Helmholtz(g, 2.0).filter_apply(psi0, rtol=1e-13)[1]
+    return configs.cfg3(seed=seed, prefilter=prefilter)
+
+
+# --------------------------------------------------------------------------------------
+# CPU legs (cpu_baseline and --impl reference): the reference's own code where it can run,
+# else the oracle restatement -- test/measurement infrastructure, never the product path
+# --------------------------------------------------------------------------------------
+def _romtopt():
+    """The unmodified reference package, installed into baseline/_ref (pure Python)."""
+    if os.path.isdir(os.path.join(REF_PATH, "romtopt")):
+        if REF_PATH not in sys.path:
+            sys.path.insert(0, REF_PATH)
+        try:
+            import romtopt
+
+            return romtopt
+        except Exception:  # noqa: BLE001
+            return None
+    return None
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:  # noqa: BLE001
+        return cores()
+
+
+class Cpu2d:
+    """cfg 1/2: the reference's HdmSolver.solve + gradient (SuperLU per design), romtopt itself
+    when installed in baseline/_ref ("reference"), else the oracle port ("port")."""
+
+    def __init__(self, prob):
+        from paper_2004_05756_b200 import configs
+
+        rt = _romtopt()
+        m = prob.mesh
+        if rt is not None:
+            mesh = rt.build_mesh(m.nx, m.ny, m.h)
+            filt = rt.HelmholtzFilter(mesh, prob.radius)
+            self.solver = rt.HdmSolver(mesh, rt.elasticity_element_matrix(1.0, 0.3), filt, prob.f, prob.fixed,
+                                       rt.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP))
+            self.obj = rt.ComplianceObjective(self.solver.f)
+            self.kind, self.what = "reference", "romtopt (baseline/_ref, unmodified) HdmSolver.solve + gradient"
+        else:
+            from oracle.fem import build_grid
+            from oracle.hdm import Filter, Hdm, Material
+
+            g = build_grid(m.nx, m.ny, m.h)
+            self.hdm = Hdm(g, prob.k_e, Filter(g, prob.radius), prob.f, prob.fixed,
+                           Material(configs.RHO_L, configs.P_SIMP))
+            self.solver = None
+            self.kind, self.what = "port", "oracle port of romtopt HdmSolver.solve + gradient"
+
+    def eval(self, psi):
+        if self.solver is not None:
+            sol = self.solver.solve(psi, self.obj)
+            self.solver.gradient(psi, sol, self.obj)
+            return sol.j
+        sol = self.hdm.solve(psi)
+        self.hdm.gradient(sol)
+        return sol["j"]
+
+    def sample(self, psi, budget_s=60.0, max_n=20):
+        t0 = time.perf_counter()
+        self.eval(psi)
+        n = 1
+        per = time.perf_counter() - t0
+        while n < max_n and (n + 1) * per <= budget_s:
+            self.eval(psi)
+            n += 1
+        return (time.perf_counter() - t0) / n, n
+
+
+class Cpu3d:
+    """cfg 3/4: the reference cannot run in 3D, so the restated path on the
+    host cores -- the reference's element-by-element K(rho)v (hdm.py:224-233) inside a
+    Jacobi-PCG for a fixed iteration budget extrapolated to the GPU's iteration count, the
+    Helmholtz filter and its adjoint by CG (filtering.py:73-114; the same budget rule when
+    ``filter_its`` is given), and element_sensitivity (hdm.py:211-222)."""
+
+    def __init__(self, prob):
+        from oracle import iterative as it
+        from oracle.fem import build_grid
+        from paper_2004_05756_b200 import configs
+
+        m = prob.mesh
+        self.it, self.prob = it, prob
+        self.grid = build_grid(m.nx, m.ny, m.h, nz=m.nz)
+        self.hz = it.Helmholtz(self.grid, prob.radius)
+        self.free = np.ones(m.n_dofs, bool)
+        self.free[prob.fixed] = False
+        self.rho_l, self.p = configs.RHO_L, configs.P_SIMP
+
+    def step(self, psi, cg_iters, gpu_iters, filter_its=None, filter_sample=None):
+        """Seconds per extrapolated evaluation and the sample description."""
+        it, g, prob = self.it, self.grid, self.prob
+        t = {}
+        t0 = time.perf_counter()
+        if filter_its is None:
+            _, rho_raw = self.hz.filter_apply(psi, rtol=1e-13)
+            t["filter"] = time.perf_counter() - t0
+        else:  # sampled Helmholtz CG, extrapolated to the GPU's filter iterations
+            b = self.hz.load_vector(psi)
+            phi, _ = it.pcg(self.hz.apply, 1.0 / self.hz.diag, b, 1e-13, filter_sample, iters_only=filter_sample)
+            rho_raw = self.hz.average(phi)
+            t["filter"] = (time.perf_counter() - t0) * filter_its[0] / filter_sample
+        rho = np.clip(rho_raw, self.rho_l, 1.0)
+        a = it.alpha(rho, self.rho_l, self.p)
+        kapply = lambda v: it.apply_stiffness(g, prob.k_e, a, v)  # noqa: E731
+        dinv = np.where(self.free, 1.0 / np.where(self.free, it.stiffness_diagonal(g, prob.k_e, a, self.free), 1.0), 0.0)
+        t1 = time.perf_counter()
+        u, _ = it.pcg(kapply, dinv, prob.f, prob.rtol, cg_iters, iters_only=cg_iters)
+        t["pcg_sample"] = time.perf_counter() - t1
+        t["pcg"] = t["pcg_sample"] / cg_iters * gpu_iters
+        t2 = time.perf_counter()
+        float(prob.f @ u)
+        s = it.element_sensitivity(g, prob.k_e, rho, u, u, self.rho_l, self.p)
+        t["sensitivity"] = time.perf_counter() - t2
+        t3 = time.perf_counter()
+        if filter_its is None:
+            self.hz.filter_adjoint(s, rtol=1e-13)
+            t["adjoint"] = time.perf_counter() - t3
+        else:
+            q = self.hz.load_vector(s) / (g.elem_volume)  # same transfer cost as filtering.py:107-109
+            it.pcg(self.hz.apply, 1.0 / self.hz.diag, q, 1e-13, filter_sample, iters_only=filter_sample)
+            t["adjoint"] = (time.perf_counter() - t3) * filter_its[1] / filter_sample
+        total = t["filter"] + t["pcg"] + t["sensitivity"] + t["adjoint"]
+        return total, t
+
+
+def cpu_cfg3(prob, gpu_iters, cg_iters=10):
+    c = Cpu3d(prob)
+    v, t = c.step(prob.psi, cg_iters, gpu_iters)
+    return {"value": v, "unit": UNIT, "cores": _blas_threads(), "kind": "port",
+            "sample": (f"restated cfg3 evaluation on the host (oracle/iterative.py, BASELINE.md §4.3): Helmholtz "
+                       f"filter + adjoint by CG to 1e-13 (full), reference element formulas for K(rho)v and the "
+                       f"sensitivities; Jacobi-PCG timed for {cg_iters} iterations ({t['pcg_sample']:.2f} s) and "
+                       f"extrapolated to the GPU's {gpu_iters}; numpy, BLAS threads = cores"),
+            "parts_s": t}
+
+
+def cpu_cfg4(prob, gpu_iters, filter_its, cg_iters=2, filter_sample=2):
+    c = Cpu3d(prob)
+    v, t = c.step(prob.psi, cg_iters, gpu_iters, filter_its=filter_its, filter_sample=filter_sample)
+    return {"value": v, "unit": UNIT, "cores": _blas_threads(), "kind": "port",
+            "sample": (f"restated cfg4 evaluation on the host: {cg_iters} Jacobi-PCG iterations of the reference "
+                       f"element formulas extrapolated to the GPU's {gpu_iters}, {filter_sample} Helmholtz CG "
+                       f"iterations per filter solve extrapolated to {filter_its}; sensitivities in full"),
+            "parts_s": t}
+
+
+def cpu_cfg5(prob, chunk=8192):
+    """16-design ROM step: the reference's reduced_stiffness (rom.py:254-262: one GEMM over the
+    stacked element caches) and residual scatter (rom.py:309-325) on an element chunk with k = 64
+    caches, scaled linearly to N_e (the full caches would need 103 GB)."""
+    from paper_2004_05756_b200 import configs
+
+    k, n_e, nd = prob.rom_k, prob.mesh.n_elems, len(prob.rom_designs)
+    rng = np.random.default_rng(1)
+    ephi = rng.standard_normal((chunk, 24, k))
+    ekphi = np.matmul(prob.k_e, ephi)
+    rho = prob.rom_designs[0][:chunk]
+    rt = _romtopt()
+    if rt is not None:
+        rom = object.__new__(rt.RomModel)
+        rom.material = rt.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
+        basis = rt.ReducedBasis(phi=np.zeros((1, k)), elem_phi=ephi, elem_k_phi=ekphi, f_hat=np.zeros(k))
+        kind, who = "reference", "romtopt RomModel.reduced_stiffness (baseline/_ref, unmodified)"
+        khat = lambda: rom.reduced_stiffness(basis, rho)  # noqa: E731
+    else:
+        kind, who = "port", "oracle restatement of rom.py:254-262"
+
+        def khat():
+            a = configs.RHO_L + (1 - configs.RHO_L) * rho**3
+            return (ephi * a[:, None, None]).reshape(-1, k).T @ ekphi.reshape(-1, k)
+    khat()
+    reps, t0 = 0, time.perf_counter()
+    while reps < 3 or time.perf_counter() - t0 < 2.0:
+        khat()
+        reps += 1
+    t_k = (time.perf_counter() - t0) / reps
+    uhat = rng.standard_normal(k)
+    t1 = time.perf_counter()
+    contrib = (ekphi @ uhat) * rho[:, None]
+    np.bincount(np.arange(chunk * 24) % (chunk * 3), weights=contrib.ravel())
+    t_r = time.perf_counter() - t1
+    scale = n_e / chunk
+    v = nd * (t_k + t_r) * scale
+    return {"value": v, "unit": "s/step", "cores": _blas_threads(), "kind": kind,
+            "sample": (f"{who} on a {chunk}-element chunk with k={k} caches ({t_k * 1e3:.1f} ms) + residual scatter "
+                       f"({t_r * 1e3:.1f} ms), scaled x{scale:.0f} to N_e and x{nd} designs")}
 
 
 # --------------------------------------------------------------------------------------
 # clocks sampled during the timed region
 # --------------------------------------------------------------------------------------
 class Clocks:
-    """SM clocks and throttle reasons sampled every 10 ms DURING the timed region (the cfg 2
-    headline's timed region is ~40 ms).
-
-    In-process NVML (pynvml) on a thread; the nvidia-smi CLI is the fallback.  (Launching
-    nvidia-smi right before the timed loop once stalled a step by ~20-45 ms.)"""
+    """SM clocks and throttle reasons sampled every 10 ms DURING the timed region (in-process
+    NVML on a thread; the nvidia-smi CLI is the fallback)."""
 
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
@@ -182,8 +333,7 @@ class Clocks:
         self.smi = None
 
     def start(self):
-        mode = os.environ.get("TB_BENCH_CLOCKS", "nvml")
-        if mode == "off":  # diagnostic only
+        if os.environ.get("TB_BENCH_CLOCKS", "nvml") == "off":  # diagnostic only
             return
         try:
             import threading
@@ -245,208 +395,266 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows), "source": "nvidia-smi"}
 
 
-def time_eval(solver, obj, psi, torch, reps=3):
-    """Seconds per full evaluation (solve + gradient), device-resident: median of ``reps`` timed
-    evaluations after two warm-ups (results kept alive as in the headline loop)."""
+# --------------------------------------------------------------------------------------
+# GPU legs
+# --------------------------------------------------------------------------------------
+import numpy as np  # noqa: E402
+
+
+def make_solver(tb, configs, prob, precond):
+    return tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, prob.radius), prob.f, prob.fixed,
+                        tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP), rtol=prob.rtol,
+                        preconditioner=precond)
+
+
+def time_steps(solver, obj, psi_d, torch, steps, warmup, flush=None):
+    """Device-resident evaluations (solve + gradient): per-step CUDA-event ms, iterations."""
     sol = g = None
+    for _ in range(max(warmup, 1)):  # results kept alive as in the timed loop (caching allocator)
+        sol = solver.solve(psi_d, obj)
+        g = solver.gradient(psi_d, sol, obj)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    iters = []
+    for k in range(steps):
+        if flush is not None:
+            flush.zero_()  # L2 flush between steps, outside the step events
+        ev[k][0].record()
+        sol = solver.solve(psi_d, obj)
+        g = solver.gradient(psi_d, sol, obj)
+        ev[k][1].record()
+        iters.append(sol.iterations)
+    torch.cuda.synchronize()
+    del g
+    return [a.elapsed_time(b) for a, b in ev], iters, sol
+
+
+def time_e2e(solver, obj, psi_host, steps, torch):
+    """Seconds per evaluation through the reference-facing numpy API, and the bytes copied."""
     for _ in range(2):
-        sol = solver.solve(psi, obj)
-        g = solver.gradient(psi, sol, obj)
+        s_ = solver.solve(psi_host, obj)
+        g_h = solver.gradient(psi_host, s_, obj)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        s_ = solver.solve(psi_host, obj)
+        g_h = solver.gradient(psi_host, s_, obj)
+        assert isinstance(g_h, np.ndarray) and np.isfinite(s_.j)
+    torch.cuda.synchronize()
+    m = solver.mesh
+    # H2D: psi; D2H: rho, u, g (+ J and the clamp width); gradient reuses the solve's device
+    # copies of rho and u (HdmSolution._dev), nothing else crosses
+    return (time.perf_counter() - t0) / steps, 8 * m.n_elems, 8 * (2 * m.n_elems + m.n_dofs) + 16
+
+
+def pcg_path(_lib, plan):
+    """Which 3D Jacobi-pCG the plan runs: "sweep" (one single-reduction kernel per iteration)
+    or "two-kernel" (operator + update)."""
+    fn = getattr(_lib.lib(), "tb_pcg_path", None)
+    if fn is None:
+        return "two-kernel"
+    import ctypes
+
+    fn.argtypes, fn.restype = [ctypes.c_void_p], ctypes.c_int
+    return "sweep" if fn(plan) == 1 else "two-kernel"
+
+
+def rom_profile(_lib, rom, basis, rhos, pk, torch):
+    """Dominant work of the ROM step: Phi^T K(rho) Phi for a batch of designs
+    (tb_rom_reduced_stiffness), CUDA events around the call on the current stream.
+    Algorithmic bytes: Phi streamed once per batch (8 N_u k) + rho of each design."""
+    m = rom.mesh
+    k = basis.size
+    nd = rhos.shape[0]
+    for _ in range(2):
+        rom.reduced_stiffness_device(basis, rhos)
     ts = []
-    for _ in range(reps):
+    for _ in range(3):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
         a.record()
-        sol = solver.solve(psi, obj)
-        g = solver.gradient(psi, sol, obj)
+        rom.reduced_stiffness_device(basis, rhos)
         b.record()
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) * 1e-3)
-    del g
-    return statistics.median(ts), sol
+    t = statistics.median(ts)
+    fn = getattr(_lib.lib(), "tb_rom_fused_info", None)
+    by = 8 * (m.n_dofs * k + nd * m.n_elems)
+    return {"kernel": "tb_rom_reduced_stiffness (all designs of the step)" if fn is None else "k_rom_fused",
+            "bound": "hbm", "achieved": by / t / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s", "us": t * 1e6,
+            "bytes": by, "launches_per_step": 1, "peak_source": peak_source(pk),
+            "note": (f"one call = Phi^T K(rho_d) Phi for all {nd} designs; algorithmic bytes = Phi once + rho_d "
+                     f"(SURVEY §7.1 tile-local assembly: Phi is the only large operand)")}
 
 
-def mg_roofline(solver, rho_d, mesh, pk):
-    """Dominant kernel of the MG headline: k_mgpcg2d, the whole preconditioned pCG loop in one
-    cooperative launch; its span is timed with CUDA events recorded around the launch on the
-    solve's stream (tb_pcg_kernel_time)."""
-    solver.pcg_device(rho_d, solver._f_d)
-    solver.pcg_device(rho_d, solver._f_d)
-    ms, launches = solver.last_kernel_time()
-    its = solver.last_iterations
-    per_it, sizes = mg_bytes_per_iteration(mesh.nx, mesh.ny)
-    t = ms * 1e-3
-    ach = per_it * its / t / 1e9 if t > 0 else 0.0
-    return {"kernel": "k_mgpcg2d (persistent multigrid-preconditioned CG, one cooperative launch per solve)",
-            "bound": "hbm", "achieved": ach, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
-            "frac": ach / pk.get("hbm_gbs"), "traffic": None, "bytes_per_launch": per_it * its,
-            "us_per_launch": t * 1e6 / max(launches, 1), "launches_per_solve": launches,
-            "iterations_per_launch": its / max(launches, 1), "us_per_iteration": t * 1e6 / max(its, 1),
-            "bytes_per_iteration": per_it, "level_dofs": sizes,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "fallback" not in pk else "fallback",
-            "note": ("the hierarchy (< 30 MB) is L2-resident; ~20 grid-barrier phases per V(1,1) iteration cost "
-                     "~4 us each (L2 round trip + barrier), so the kernel is latency-bound, not HBM-bound "
-                     "(profiles/mg_prof.py); the coarsest inverse (k_mg_gj_inverse) is set-up, not timed here")}
-
-
-def jacobi_roofline(solver, rho_d, mesh, pk, torch):
-    """2D Jacobi-pCG: the whole solve is ONE persistent cooperative launch (k_pcg2d_treg); its
-    algorithmic traffic is the fused Jacobi-pCG iteration of SURVEY §8(d), 8 (9 N_u + N_e)
-    bytes, times the iterations of the launch."""
-    n_u, n_e = mesh.n_dofs, mesh.n_elems
-    a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    solver.pcg_device(rho_d, solver._f_d)
-    a_ev.record()
-    solver.pcg_device(rho_d, solver._f_d)
-    b_ev.record()
-    torch.cuda.synchronize()
-    t_solve = a_ev.elapsed_time(b_ev) * 1e-3
-    its = solver.last_iterations
-    bytes_launch = 8 * (9 * n_u + n_e) * its
-    ach = bytes_launch / t_solve / 1e9
-    return {"kernel": "k_pcg2d_treg<2,true> (persistent single-reduction Jacobi-pCG on node tiles, one launch per solve)",
-            "bound": "hbm", "achieved": ach, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
-            "frac": ach / pk.get("hbm_gbs"), "traffic": None, "bytes_per_launch": bytes_launch,
-            "us_per_launch": t_solve * 1e6, "iterations_per_launch": its, "us_per_iteration": t_solve * 1e6 / its,
-            "bytes_per_iteration": 8 * (9 * n_u + n_e),
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if "fallback" not in pk else "fallback",
-            "note": ("cfg2's 18 MB working set is L2/SMEM-resident; each iteration is bounded by one grid "
-                     "barrier + partial exchange (~2-3 us), not by HBM")}
-
-
-def jacobi_extra(tb, configs, prob, psi, torch, pk, args):
-    """The same evaluation with the Jacobi-preconditioned pCG of the north_star's subsystem (1),
-    and the roofline of its persistent kernel."""
-    s = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, prob.radius), prob.f, prob.fixed,
-                     tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP), rtol=prob.rtol, preconditioner="jacobi")
-    obj = tb.ComplianceObjective(s.f)
-    t, sol = time_eval(s, obj, psi, torch)
-    rho_d, _ = s.filtered_density_device(psi)
-    roof = jacobi_roofline(s, rho_d, prob.mesh, pk, torch)
-    tpath = os.path.join(REPO, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        roof["traffic"] = json.load(open(tpath)).get(args.config)
-    return {"preconditioner": "Jacobi (north_star subsystem (1))", "s_per_eval": t, "pcg_iterations": sol.iterations,
-            "J": sol.j, "roofline": roof}
-
-
-def mg_extra(tb, configs, prob, psi, torch):
-    """Same evaluation with the geometric-multigrid preconditioner: the
-    solution matches the Jacobi path to the solve tolerance; reported beside the headline."""
-    s = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, prob.radius), prob.f, prob.fixed,
-                     tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP), rtol=prob.rtol, preconditioner="mg")
-    obj = tb.ComplianceObjective(s.f)
-    t, sol = time_eval(s, obj, psi, torch)
-    return {"preconditioner": "geometric multigrid V(2,2), Galerkin coarse levels, damped Jacobi",
-            "s_per_eval": t, "pcg_iterations": sol.iterations, "J": sol.j}
-
-
-def subproblem_extra(tb, solver, obj, prob, psi_d, phi, torch, inner=10):
-    """one trust-region subproblem sweep (trustregion.py:304-351) with every
-    vector on the device -- per inner step: MMA step, filter, ROM solve + gradient, residual."""
-    n_e = prob.mesh.n_elems
-    w = torch.ones(n_e, dtype=torch.float64, device=psi_d.device)
-    psi_k = (0.9 * psi_d).clamp(0.0, 1.0)
-    cap = float(w @ psi_k) * 1.05
-    sol = solver.solve(psi_k, obj)
-    g = solver.gradient(psi_k, sol, obj)
-    basis = tb.ReducedBasis(phi, None, None, phi.T @ solver._f_d)
-    sp = tb.TrustRegionSubproblem(solver, tb.RomModel(solver), obj, w, cap, constraint="dist", max_inner=inner)
-    sp.solve_subproblem(basis, psi_k, 1e9, sol.j, g)  # warm-up
-    per = []
-    for _ in range(3):  # median of three sweeps
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        a.record()
-        r = sp.solve_subproblem(basis, psi_k, 1e9, sol.j, g)
-        b.record()
-        torch.cuda.synchronize()
-        per.append(a.elapsed_time(b) / max(r.rom_solves, 1))
-    return {"what": f"TrustRegionSubproblem.solve_subproblem, {inner} inner MMA steps, k={phi.shape[1]} basis",
-            "ms_per_inner_step": statistics.median(per), "inner_steps": r.rom_solves}
-
-
-def bench_cfg3(tb, configs, _lib, dev, pk):
-    """BASELINE cfg 3 (192x96x96 Hex8, 5.4M DOF): one full HDM evaluation + the Hex8 operator
-    kernel's roofline (graph path; per-kernel CUDA-event timing via tb_pcg_profile)."""
+def roofline_3d(tb, _lib, solver, rho_d, pk, torch):
+    """Dominant kernel of the 3D Jacobi-pCG iteration, timed live with CUDA events on the
+    solve's stream (tb_pcg_profile: each kernel of an iteration bracketed by events).  Bytes:
+    the algorithmic traffic of that kernel per SURVEY §8(d)."""
     import ctypes
 
-    import torch
-
-    def prefilter(mesh, psi0):
-        f2 = tb.HelmholtzFilter(mesh, 2.0)
-        return f2.apply(torch.as_tensor(psi0, device=dev)).rho.cpu().numpy()
-
-    prob = configs.cfg3(prefilter=prefilter)
-    m = prob.mesh
-    s = tb.HdmSolver(m, prob.k_e, tb.HelmholtzFilter(m, prob.radius), prob.f, prob.fixed,
-                     tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP), rtol=prob.rtol)
-    obj = tb.ComplianceObjective(s.f)
-    psi = torch.as_tensor(prob.psi, device=dev)
-    sol = s.solve(psi, obj)
-    s.gradient(psi, sol, obj)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    a.record()
-    sol = s.solve(psi, obj)
-    g = s.gradient(psi, sol, obj)
-    b.record()
-    torch.cuda.synchronize()
-    t_eval = a.elapsed_time(b) * 1e-3
-    rho_d, _ = s.filtered_density_device(psi)
+    m = solver.mesh
+    n_u, n_e = m.n_dofs, m.n_elems
     msf, msu = ctypes.c_double(0.0), ctypes.c_double(0.0)
-    _lib.check(_lib.lib().tb_pcg_profile(s._plan, _lib.ptr(rho_d), _lib.ptr(s._f_d), 50, ctypes.byref(msf),
-                                         ctypes.byref(msu), _lib.stream_ptr(dev)), "profile")
-    n_u, n_e, n_v = m.n_dofs, m.n_elems, m.n_nodes
-    # K(rho)u alone (HdmSolver.apply_stiffness, hdm.py:224-233, alpha(rho) included): SURVEY
-    # §8(d) GDOF/s metric; median over 5 timed batches of 20 back-to-back calls after warm-up,
-    # bytes 8(2 N_u + N_e)
-    v = torch.randn(n_u, dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().tb_pcg_profile(solver._plan, _lib.ptr(rho_d), _lib.ptr(solver._f_d), 50, ctypes.byref(msf),
+                                         ctypes.byref(msu), _lib.stream_ptr(rho_d.device)), "profile")
+    path = pcg_path(_lib, solver._plan)
+    if path == "sweep":  # one single-reduction sweep per iteration: the whole pCG iteration
+        by = 8 * (9 * n_u + n_e)
+        t = msf.value * 1e-3
+        kern = ("k_hex8_cg (Chronopoulos-Gear Jacobi-pCG iteration in ONE z-sweep: TMA node planes, WHT-block Hex8 "
+                "operator, x/r/p/s/w updates, 3 dot products)")
+        note = "bytes = one Jacobi-pCG iteration, 8(9 N_u + N_e) (SURVEY §8(d)); the kernel IS the iteration"
+        upd = None
+    else:
+        by = 8 * (4 * n_u + n_e)
+        t = msf.value * 1e-3
+        kern = "k_hex8<true> (WHT-block Hex8 operator fused with p = z + beta p_old and p.q)"
+        note = "bytes = z, p_old, alpha in; p, q out: 8(4 N_u + N_e)"
+        by_u = 8 * 8 * n_u
+        upd = {"us_per_launch": msu.value * 1e3, "bytes_per_launch": by_u,
+               "achieved_gbs": by_u / (msu.value * 1e-3) / 1e9,
+               "frac": by_u / (msu.value * 1e-3) / 1e9 / pk["hbm_gbs"]}
+    ach = by / t / 1e9
+    out = {"kernel": kern, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+           "frac": ach / pk["hbm_gbs"], "traffic": None, "bytes_per_launch": by, "us_per_launch": t * 1e6,
+           "peak_source": peak_source(pk), "note": note}
+    if upd is not None:
+        out["update_kernel"] = upd
+        out["us_per_iteration"] = (msf.value + msu.value) * 1e3
+    else:
+        out["us_per_iteration"] = msf.value * 1e3
+    out["iteration_gbs_s8d"] = 8 * (9 * n_u + n_e) / (out["us_per_iteration"] * 1e-6) / 1e9
+    tpath = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        out["traffic"] = json.load(open(tpath)).get("cfg3_" + path)
+    return out
+
+
+def apply_roofline(solver, rho_d, pk, torch):
+    """K(rho)u GDOF/s (HdmSolver.apply_stiffness, hdm.py:224-233, alpha(rho) included):
+    20 calls captured in a CUDA graph, median of 5 replays; bytes 8(2 N_u + N_e)."""
+    m = solver.mesh
+    n_u = m.n_dofs
+    v = torch.randn(n_u, dtype=torch.float64, device=rho_d.device)
     for _ in range(3):
-        s.apply_device(rho_d, v)
+        solver.apply_device(rho_d, v)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for _ in range(20):
+            solver.apply_device(rho_d, v)
+    graph.replay()
+    torch.cuda.synchronize()
     ts = []
     for _ in range(5):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(20):
-            s.apply_device(rho_d, v)
-        e1.record()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        graph.replay()
+        b.record()
         torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1) * 1e-3 / 20)
-    t_ap = statistics.median(ts)
-    by_ap = 8 * (2 * n_u + n_e)
-    by_op = 8 * (4 * n_u + n_e)  # read z, p_old, alpha; write p, q
-    by_up = 8 * 8 * n_u          # read p, q, D^-1, x, r; write x, r, z
-    return {"workload": f"cfg3 {m.nx}x{m.ny}x{m.nz} Hex8, {n_u} DOF; filter R=2.5 + pCG 1e-8 + sensitivity + adjoint",
-            "s_per_eval": t_eval, "pcg_iterations": sol.iterations, "J": sol.j,
-            "apply_kernel": {"name": "k_hex8<true> (WHT-block element-centric, z-sweep)",
-                             "us_per_launch": msf.value * 1e3, "bytes_per_launch": by_op,
-                             "achieved_gbs": by_op / (msf.value * 1e-3) / 1e9,
-                             "frac_hbm": by_op / (msf.value * 1e-3) / 1e9 / pk.get("hbm_gbs"),
-                             "gdofs": n_u / (msf.value * 1e-3) / 1e9},
-            "apply_stiffness": {"name": "k_hex8<false,mask,simp> (K(rho)u incl. alpha(rho), fixed rows zeroed)",
-                                "us_per_call": t_ap * 1e6,
-                                "gdofs": n_u / t_ap / 1e9, "bytes_per_launch": by_ap,
-                                "achieved_gbs": by_ap / t_ap / 1e9, "frac_hbm": by_ap / t_ap / 1e9 / pk.get("hbm_gbs")},
-            "update_kernel": {"us_per_launch": msu.value * 1e3, "bytes_per_launch": by_up,
-                              "achieved_gbs": by_up / (msu.value * 1e-3) / 1e9,
-                              "frac_hbm": by_up / (msu.value * 1e-3) / 1e9 / pk.get("hbm_gbs")},
-            "us_per_iteration_in_solve": None,
-            "mg": mg_extra(tb, configs, prob, psi, torch)}
+        ts.append(a.elapsed_time(b) / 20 * 1e-3)
+    t = statistics.median(ts)
+    by = 8 * (2 * n_u + m.n_elems)
+    return {"us_per_call": t * 1e6, "gdofs": n_u / t / 1e9, "bytes_per_launch": by, "achieved_gbs": by / t / 1e9,
+            "frac": by / t / 1e9 / pk["hbm_gbs"],
+            "note": "back-to-back calls: v and rho may be L2-resident between calls when they fit in 126 MB"}
 
 
-def peaks():
-    try:
-        return json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
-    except OSError:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "fallback": True}
+def mg_bytes_per_iteration(nx, ny, min_dofs=1200):
+    """Algorithmic bytes of one MG-preconditioned CG iteration of the persistent 2D kernel
+    (k_mgpcg2d, V(1,1) cycle), each vector read or written once per phase."""
+    levels = [(nx, ny)]
+    while 2 * (levels[-1][0] + 1) * (levels[-1][1] + 1) > min_dofs:
+        a, b = levels[-1]
+        c = ((a + 1) // 2, (b + 1) // 2)
+        if c == (a, b):
+            break
+        levels.append(c)
+    n = [2 * (a + 1) * (b + 1) for a, b in levels]
+    ne = nx * ny
+    L = len(n)
+    d = (4 * n[0] + ne) + 8 * n[0]
+    d += 4 * n[0] + ne
+    d += 2 * n[0] + n[1]
+    d += 4 * n[0] + ne + 2 * n[0]
+    for l in range(1, L - 1):
+        d += n[l - 1] + 3 * n[l]
+        d += 14 * n[l]
+        d += 2 * n[l] + n[l + 1]
+        d += 14 * n[l]
+    d += n[L - 2] + 2 * n[L - 1]
+    d += n[L - 1] ** 2 + 2 * n[L - 1]
+    return 8 * d, n
+
+
+def roofline_2d(solver, rho_d, pk, torch, precond):
+    """2D: the whole solve is ONE persistent cooperative launch (Jacobi: k_pcg2d_treg; MG:
+    k_mgpcg2d), timed with events around it; bytes = per-iteration model x iterations."""
+    m = solver.mesh
+    if precond == "mg":
+        solver.pcg_device(rho_d, solver._f_d)
+        solver.pcg_device(rho_d, solver._f_d)
+        ms, launches = solver.last_kernel_time()
+        t = ms * 1e-3
+        per_it, _ = mg_bytes_per_iteration(m.nx, m.ny)
+        kern = "k_mgpcg2d (persistent multigrid-preconditioned CG, one cooperative launch per solve)"
+        note = ("hierarchy L2-resident; ~20 grid-barrier phases per V(1,1) iteration (latency-bound); the coarsest "
+                "inverse (k_mg_gj_inverse) is set-up, not timed here")
+    else:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        solver.pcg_device(rho_d, solver._f_d)
+        a.record()
+        solver.pcg_device(rho_d, solver._f_d)
+        b.record()
+        torch.cuda.synchronize()
+        t = a.elapsed_time(b) * 1e-3
+        per_it = 8 * (9 * m.n_dofs + m.n_elems)
+        kern = "k_pcg2d_treg (persistent single-reduction Jacobi-pCG on node tiles, one launch per solve)"
+        note = "working set L2/SMEM-resident; one grid barrier + partial exchange per iteration"
+    its = solver.last_iterations
+    ach = per_it * its / t / 1e9 if t > 0 else 0.0
+    return {"kernel": kern, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": ach / pk["hbm_gbs"], "traffic": None, "bytes_per_launch": per_it * its, "us_per_launch": t * 1e6,
+            "iterations_per_launch": its, "us_per_iteration": t * 1e6 / max(its, 1), "bytes_per_iteration": per_it,
+            "peak_source": peak_source(pk), "note": note}
+
+
+def eval_extra(tb, configs, _lib, name, precond, dev, pk, torch, cpu, steps=5, prob=None):
+    """One BASELINE evaluation config measured end to end: s/eval (device-resident), e2e through
+    the numpy API, the dominant kernel's roofline and the CPU baseline."""
+    prob = prob or problem(name, 0, dev)
+    s = make_solver(tb, configs, prob, precond)
+    obj = tb.ComplianceObjective(s.f)
+    psi_d = torch.as_tensor(prob.psi, device=dev)
+    ms, iters, sol = time_steps(s, obj, psi_d, torch, steps, 2)
+    pin = torch.empty(prob.mesh.n_elems, dtype=torch.float64, pin_memory=True)
+    pin.copy_(torch.from_numpy(prob.psi))
+    e2e_t, h2d, d2h = time_e2e(s, obj, pin.numpy(), max(2, steps // 2), torch)
+    rho_d, _ = s.filtered_density_device(psi_d)
+    roof = roofline_3d(tb, _lib, s, rho_d, pk, torch) if prob.mesh.dim == 3 else roofline_2d(s, rho_d, pk, torch,
+                                                                                              precond)
+    out = {"workload": workload_desc(prob, precond), "value": statistics.median(ms) * 1e-3, "unit": UNIT,
+           "pcg_iterations": int(statistics.median(iters)), "J": sol.j,
+           "e2e": {"value": e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+           "roofline": roof, "apply": apply_roofline(s, rho_d, pk, torch)}
+    if cpu is not None:
+        out["cpu_baseline"] = cpu(prob, out)
+    del s, sol
+    torch.cuda.empty_cache()
+    return out
+
+
+def cpu_2d_leg(prob, _out):
+    c = Cpu2d(prob)
+    v, n = c.sample(prob.psi, budget_s=30.0, max_n=5)
+    return {"value": v, "unit": UNIT, "cores": _blas_threads(), "kind": c.kind,
+            "sample": f"{n} full evaluations of {prob.name}: {c.what} (SuperLU single-threaded, BLAS on all cores)"}
 
 
 # --------------------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------------------
 def run_ours(args):
-    import numpy as np
     import torch
 
     import paper_2004_05756_b200 as tb
@@ -460,193 +668,120 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    pk = peaks()
 
-    prob = problem(args.config, args.seed)
+    prob = problem(args.config, args.seed, dev)
     mesh = prob.mesh
-    filt = tb.HelmholtzFilter(mesh, prob.radius)
-    mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
-    solver = tb.HdmSolver(mesh, prob.k_e, filt, prob.f, prob.fixed, mat, rtol=prob.rtol, preconditioner=args.precond)
+    solver = make_solver(tb, configs, prob, args.precond)
     obj = tb.ComplianceObjective(solver.f)
     psi_d = torch.as_tensor(prob.psi, device=dev)
-    flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev)  # 256 MiB > 126 MB L2
+    flush = None if args.no_flush else torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev)  # 256 MiB
 
-    def step():
+    clocks = Clocks(dev.index)
+    clocks.start()  # before the warm-up: NVML start-up once stalled the first timed steps
+    for _ in range(max(args.warmup, 3)):
         sol = solver.solve(psi_d, obj)
         g = solver.gradient(psi_d, sol, obj)
-        return sol, g
-
-    # the clock sampler (nvidia-smi) starts before the warm-up: its NVML start-up stalled the
-    # first timed steps when it was launched right before them; it keeps sampling through them
-    clocks = Clocks(dev.index)
-    clocks.start()
-    # warm-up keeps each step's results alive through the next step, as the timed loop does, so
-    # the caching allocator already holds two sets of output buffers (otherwise the second timed
-    # step paid a cudaMalloc inside its events)
-    sol = g = None
-    for _ in range(max(args.warmup, 3)):
-        sol, g = step()
     torch.cuda.synchronize()
-
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    iters = []
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = _lib.lib().tb_launch_count()
-    for k in range(args.steps):
-        if not args.no_flush:
-            flush.zero_()  # L2 flush between steps, outside the per-step events
-        ev[k][0].record()
-        sol, g = step()
-        ev[k][1].record()
-        iters.append(sol.iterations)
-    torch.cuda.synchronize()
+    step_ms, iters, sol = time_steps(solver, obj, psi_d, torch, args.steps, 0, flush)
     clk = clocks.stop()
     launches = _lib.lib().tb_launch_count() - launches0
     if dist:
         dist.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
     print("step ms:", [round(x, 3) for x in step_ms], file=sys.stderr)
-    total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     value = total_ms / 1e3 / (args.steps * world)
-    ms_per_step = total_ms / args.steps
 
-    # ---- end-to-end through the reference-facing API (host numpy in/out) -------------
-    psi_pin = torch.empty(mesh.n_elems, dtype=torch.float64, pin_memory=True)
-    psi_pin.copy_(torch.from_numpy(prob.psi))
-    psi_host = psi_pin.numpy()
-    for _ in range(2):  # same result liveness as the timed loop (see the warm-up above)
-        s_ = solver.solve(psi_host, obj)
-        g_h = solver.gradient(psi_host, s_, obj)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        s_ = solver.solve(psi_host, obj)
-        g_h = solver.gradient(psi_host, s_, obj)
-        assert isinstance(g_h, np.ndarray) and np.isfinite(s_.j)
-    torch.cuda.synchronize()
-    e2e_total = time.perf_counter() - t0
-    e2e_t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+    pin = torch.empty(mesh.n_elems, dtype=torch.float64, pin_memory=True)
+    pin.copy_(torch.from_numpy(prob.psi))
+    e2e_t, h2d, d2h = time_e2e(solver, obj, pin.numpy(), args.steps, torch)
+    e2e_d = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
     if dist:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e = {"value": float(e2e_t.item()) / (args.steps * world), "unit": UNIT,
-           "h2d_bytes_per_step": 8 * mesh.n_elems,
-           "d2h_bytes_per_step": 8 * (2 * mesh.n_elems + mesh.n_dofs) + 8,
+        dist.all_reduce(e2e_d, op=dist.ReduceOp.MAX)
+    e2e = {"value": float(e2e_d.item()) / world, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
            "api": "HdmSolver.solve(psi: numpy) + HdmSolver.gradient -> numpy (reference signatures)"}
 
-    # ---- roofline of the dominant kernel, timed live with CUDA events on its stream ------
     rho_d, _ = solver.filtered_density_device(psi_d)
-    n_u, n_e = mesh.n_dofs, mesh.n_elems
-    pk = peaks()
-    if args.precond == "mg":
-        roof = mg_roofline(solver, rho_d, mesh, pk)
-        tpath = os.path.join(REPO, "profiles", "traffic.json")
-        if os.path.exists(tpath):
-            roof["traffic"] = json.load(open(tpath)).get(args.config + "_mg")
+    if mesh.dim == 3:
+        roof = roofline_3d(tb, _lib, solver, rho_d, pk, torch) if args.precond == "jacobi" else None
     else:
-        roof = jacobi_roofline(solver, rho_d, mesh, pk, torch)
-        tpath = os.path.join(REPO, "profiles", "traffic.json")
-        if os.path.exists(tpath):
-            roof["traffic"] = json.load(open(tpath)).get(args.config)
+        roof = roofline_2d(solver, rho_d, pk, torch, args.precond)
+    apply = apply_roofline(solver, rho_d, pk, torch)
+    its = int(statistics.median(iters))
+    del solver, sol, g, rho_d
+    torch.cuda.empty_cache()
+
+    cpu = None
+    want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
+    if want_cpu:
+        cpu = cpu_cfg3(prob, its) if args.config == "cfg3" else cpu_2d_leg(prob, None)
 
     extras = {}
     if not args.no_extras:
-        # K(rho)u GDOF/s (hdm.py:224-233 equivalent) and Phi^T K Phi time (k = prob.rom_k)
-        v = torch.randn(n_u, dtype=torch.float64, device=dev)
-        for _ in range(3):
-            solver.apply_device(rho_d, v)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(50):
-            solver.apply_device(rho_d, v)
-        b.record()
-        torch.cuda.synchronize()
-        t_host = a.elapsed_time(b) / 50 * 1e-3
-        # GPU time of K(rho)u: 20 back-to-back calls captured in a CUDA graph, median of 5
-        # replays (a Python loop measures the host's call rate at this size, ~20 us per call)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            for _ in range(20):
-                solver.apply_device(rho_d, v)
-        graph.replay()
-        torch.cuda.synchronize()
-        ts = []
-        for _ in range(5):
-            a.record()
-            graph.replay()
-            b.record()
-            torch.cuda.synchronize()
-            ts.append(a.elapsed_time(b) / 20 * 1e-3)
-        t_apply = statistics.median(ts)
-        by_apply = 8 * (2 * n_u + prob.mesh.n_elems)
-        extras["apply_gdofs"] = n_u / t_apply / 1e9
-        extras["apply_us"] = t_apply * 1e6
-        extras["apply"] = {"what": "HdmSolver.apply_device (tb_apply_stiffness: alpha(rho) + K u + Dirichlet rows, one "
-                                   "launch), 20 calls in a CUDA graph", "bytes_per_launch": by_apply,
-                           "achieved_gbs": by_apply / t_apply / 1e9,
-                           "note": "4.8 MB working set stays in L2 between calls",
-                           "us_per_call_python_loop": t_host * 1e6}
-        k = prob.rom_k
-        phi = torch.linalg.qr(torch.randn(n_u, k, dtype=torch.float64, device=dev))[0].contiguous()
-        rom = tb.RomModel(solver)
-        basis = tb.ReducedBasis(phi, None, None, torch.zeros(k, dtype=torch.float64, device=dev))
-        for _ in range(2):
-            rom.reduced_stiffness_device(basis, rho_d)
-        a.record()
-        for _ in range(10):
-            rom.reduced_stiffness_device(basis, rho_d)
-        b.record()
-        torch.cuda.synchronize()
-        extras["rom_khat_ms"] = a.elapsed_time(b) / 10
-        extras["rom_k"] = k
-        if args.precond == "mg":
-            extras["jacobi"] = jacobi_extra(tb, configs, prob, psi_d, torch, pk, args)
-        else:
-            extras["mg"] = mg_extra(tb, configs, prob, psi_d, torch)
-        extras["tr_subproblem"] = subproblem_extra(tb, solver, obj, prob, psi_d, phi, torch)
-        if args.extra3d:
-            extras["cfg3"] = bench_cfg3(tb, configs, _lib, dev, pk)
-        if os.environ.get("TB_BENCH_CFG4", "1") != "0":
-            extras["cfg4_sharded"] = cfg4_extra(args, dev, dist, world, rank)
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        hdm = cpu_port(prob)
-        t0 = time.perf_counter()
-        cpu_eval(hdm, prob.psi)
-        dt = time.perf_counter() - t0
-        cpu = {"value": dt, "unit": UNIT, "cores": cores(), "kind": "port",
-               "sample": f"1 full evaluation of {prob.name} (oracle port of romtopt HdmSolver.solve + gradient; "
-                         f"SuperLU single-threaded, BLAS on all cores)"}
+        names = [x for x in args.extras.split(",") if x]
+        leg2d = cpu_2d_leg if want_cpu else None
+        if "cfg1" in names and args.config != "cfg1":
+            extras["cfg1"] = {"mg": eval_extra(tb, configs, _lib, "cfg1", "mg", dev, pk, torch, leg2d),
+                              "jacobi": eval_extra(tb, configs, _lib, "cfg1", "jacobi", dev, pk, torch, None)}
+        if "cfg2" in names and args.config != "cfg2":
+            p2 = problem("cfg2", 0)
+            extras["cfg2"] = {"mg": eval_extra(tb, configs, _lib, "cfg2", "mg", dev, pk, torch, leg2d, prob=p2),
+                              "jacobi": eval_extra(tb, configs, _lib, "cfg2", "jacobi", dev, pk, torch, None, prob=p2)}
+            extras["cfg2"]["rom_khat_ms"] = rom_khat_ms(tb, configs, p2, dev, torch)
+        if "cfg3mg" in names and args.config == "cfg3" and args.precond == "jacobi":
+            extras["cfg3_mg"] = eval_extra(tb, configs, _lib, "cfg3", "mg", dev, pk, torch, None, prob=prob)
+        if "cfg4" in names and os.environ.get("TB_BENCH_CFG4", "1") != "0":
+            extras["cfg4_sharded"] = cfg4_extra(args, dev, dist, world, rank, pk, want_cpu)
+        if "cfg5" in names and world == 1:
+            extras["cfg5"] = cfg5_extra(args, dev, pk, want_cpu)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": False,
+            "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded BASELINE cfg recipe, SURVEY App. B.1)",
+            "data": "synthetic (seeded BASELINE cfg recipe, SURVEY App. B.1 / §8(d))",
             "config": {"workload": workload_desc(prob, args.precond), "preconditioner": args.precond,
                        "parallelism": "replicas" if world > 1 else "single",
-                       "l2": "256 MiB buffer written between steps (outside the step events)",
-                       "pcg_iterations": int(statistics.median(iters)), "seed": args.seed},
+                       "l2": ("256 MiB buffer written between steps (outside the step events); the cfg3 working set "
+                              "(~350 MB of pCG vectors) also exceeds the 126 MB L2") if flush is not None else "no flush",
+                       "pcg_iterations": its, "seed": args.seed},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clk, "extra": extras,
+            "clocks": clk, "apply": apply, "extra": extras,
         }
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
 
 
-def cfg4_extra(args, dev, dist, world, rank):
-    """BASELINE cfg 4 (43M DOF Hex8) evaluated once, slab-sharded over ALL ranks of this run:
-    at N > 1 the replicas of the headline join one distributed evaluation (NCCL allreduces, the
-    z halo as NVLink peer stores from the update kernels, or NCCL send/recv on every rank if any
-    rank cannot map its neighbours), so a scaling run of the default bench also records cfg 4's
-    strong scaling.  N = 1: one slab, no collectives."""
+def rom_khat_ms(tb, configs, prob, dev, torch):
+    s = make_solver(tb, configs, prob, "jacobi")
+    k = prob.rom_k
+    phi = torch.linalg.qr(torch.randn(prob.mesh.n_dofs, k, dtype=torch.float64, device=dev))[0].contiguous()
+    rom = tb.RomModel(s)
+    basis = tb.ReducedBasis(phi, None, None, torch.zeros(k, dtype=torch.float64, device=dev))
+    rho_d = torch.as_tensor(prob.psi, device=dev)
+    for _ in range(2):
+        rom.reduced_stiffness_device(basis, rho_d)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(10):
+        rom.reduced_stiffness_device(basis, rho_d)
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / 10
+
+
+def cfg4_extra(args, dev, dist, world, rank, pk, want_cpu):
+    """BASELINE cfg 4 (43M DOF Hex8) evaluated once, slab-sharded over ALL ranks of this run
+    (strong scaling when the driver runs N > 1)."""
     import torch
 
     import paper_2004_05756_b200 as tb
@@ -659,7 +794,7 @@ def cfg4_extra(args, dev, dist, world, rank):
     sv = SlabSolver(prob.mesh, prob.k_e, prob.f, prob.fixed, mat, slab, device=dev)
     fl = SlabFilter(prob.mesh, prob.radius, slab, device=dev)
     psi = torch.as_tensor(sv.local_elems(prob.psi).copy(), device=dev)
-    comm = TorchComm(peer=True) if dist else LocalComm()  # falls back to NCCL send/recv on every rank
+    comm = TorchComm(peer=True) if dist else LocalComm()
     ev = slab_evaluate([sv], [fl], comm, [psi], rtol=prob.rtol)  # warm-up
     del ev
     if dist:
@@ -674,14 +809,24 @@ def cfg4_extra(args, dev, dist, world, rank):
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     m = prob.mesh
+    t_eval = float(t.item())
+    per_it = t_eval / max(ev.iterations, 1)
+    by_it = 8 * (9 * m.n_dofs + m.n_elems)
     out = {"workload": f"cfg4 {m.nx}x{m.ny}x{m.nz} Hex8, {m.n_dofs} DOF: filter R={prob.radius:g} + Jacobi-pCG "
                        f"{prob.rtol:g} + compliance + sensitivities + adjoint, z-slabs x{world}",
-           "s_per_eval": float(t.item()), "n_gpus": world, "scaling": "strong", "pcg_iterations": ev.iterations,
+           "value": t_eval, "unit": UNIT, "n_gpus": world, "scaling": "strong", "pcg_iterations": ev.iterations,
            "filter_iterations": list(ev.filter_iterations), "J": ev.j,
            "halo": ("NVLink peer stores (CUDA IPC)" if comm.peer_active else "nccl send/recv") if dist else "none (one slab)",
-           "us_per_pcg_iteration_upper_bound": float(t.item()) / max(ev.iterations, 1) * 1e6}
+           "roofline": {"kernel": "whole Jacobi-pCG iteration (upper bound: evaluation time / iterations)", "bound": "hbm",
+                        "achieved": by_it / per_it / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                        "frac": by_it / per_it / 1e9 / pk["hbm_gbs"], "traffic": None,
+                        "bytes_per_iteration": by_it, "us_per_iteration_upper_bound": per_it * 1e6,
+                        "peak_source": peak_source(pk),
+                        "note": "SURVEY §8(d) bytes 8(9 N_u + N_e) per iteration; filter/sensitivity time included"}}
     del ev, sv, fl, psi
     torch.cuda.empty_cache()
+    if want_cpu:
+        out["cpu_baseline"] = cpu_cfg4(prob, out["pcg_iterations"], out["filter_iterations"])
     return out
 
 
@@ -704,186 +849,186 @@ def fp64_peak_tflops(torch, dev):
     return 2 * n**3 / best / 1e12
 
 
-def dmma_time(rom, basis, rho, torch):
-    """CUDA-event time of the DMMA contraction alone (tb_rom_gram_colmajor, symmetric: the
-    kernel variant tb_rom_reduced_stiffness uses, on the column-major basis), one launch after
-    warm-up."""
-    import ctypes
-
-    from paper_2004_05756_b200 import _lib
-
-    phi = basis.device_phi(rom.device)
-    n, k = phi.shape
-    ldp = (n + 1) // 2 * 2
-    a = torch.zeros((k, ldp), dtype=torch.float64, device=rom.device)
-    a[:, :n] = phi.t()
-    out = torch.empty((k, k), dtype=torch.float64, device=rom.device)
-    for _ in range(2):
-        _lib.check(_lib.lib().tb_rom_gram_colmajor(n, k, _lib.ptr(a), _lib.ptr(a), ldp, 1, _lib.ptr(out),
-                                                   _lib.stream_ptr(rom.device)), "gram")
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    _lib.check(_lib.lib().tb_rom_gram_colmajor(n, k, _lib.ptr(a), _lib.ptr(a), ldp, 1, _lib.ptr(out),
-                                               _lib.stream_ptr(rom.device)), "gram")
-    e1.record()
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) * 1e-3
-
-
-def run_cfg5(args):
-    """BASELINE cfg 5: per trust-region step, 16 designs x (Phi^T K(rho_d) Phi, reduced solve,
-    ||K Phi uhat - f||) with a k = 64 basis on 256x128x128 Hex8 (12.8M DOF)."""
-    import numpy as np
-    import torch
-
-    import paper_2004_05756_b200 as tb
-    from paper_2004_05756_b200 import _lib, configs
-
-    rank, local, world = rank_info()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    prob = configs.cfg5(seed=args.seed)
+def cfg5_setup(tb, configs, dev, torch, seed=0):
+    prob = configs.cfg5(seed=seed)
     m = prob.mesh
-    mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
-    s = tb.HdmSolver(m, prob.k_e, tb.HelmholtzFilter(m, prob.radius), prob.f, prob.fixed, mat, rtol=prob.rtol)
+    s = make_solver(tb, configs, prob, "jacobi")
     k = prob.rom_k
-    cols = configs.phi_columns(m, k, seed=args.seed, xp=torch, device=dev)
+    cols = configs.phi_columns(m, k, seed=seed, xp=torch, device=dev)
     cols[:, torch.as_tensor(~s.free_mask, device=dev)] = 0.0
     phi = tb.gram_schmidt(list(cols))
     del cols
     basis = tb.ReducedBasis(phi, None, None, phi.T @ s._f_d)
     rom = tb.RomModel(s)
     rhos = torch.as_tensor(np.stack(prob.rom_designs), device=dev)
-    nd = rhos.shape[0]
-    clocks = Clocks(dev.index)
-    clocks.start()  # before the warm-up (see run_ours)
-    for _ in range(max(args.warmup, 1)):  # results kept alive as in the timed loop (allocator)
+    return prob, s, basis, rom, rhos
+
+
+def cfg5_measure(tb, _lib, prob, basis, rom, rhos, dev, pk, torch, steps, warmup):
+    """16-design ROM step timing + the dominant kernel's roofline (tb_rom_reduced_stiffness's
+    kernel times, read back with tb_rom_profile when the library provides it)."""
+    for _ in range(max(warmup, 1)):
         khat, uhat, norms = rom.solve_batch(basis, rhos)
     torch.cuda.synchronize()
     launches0 = _lib.lib().tb_launch_count()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    for i in range(args.steps):
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
         ev[i][0].record()
         khat, uhat, norms = rom.solve_batch(basis, rhos)
         ev[i][1].record()
     torch.cuda.synchronize()
-    clk = clocks.stop()
     launches = _lib.lib().tb_launch_count() - launches0
-    t_step = sum(a.elapsed_time(b) for a, b in ev) / args.steps * 1e-3
-    print("step ms:", [round(a.elapsed_time(b), 2) for a, b in ev], file=sys.stderr)
-    # the dominant kernel: Phi^T K Phi for one design (operator per column + DMMA contraction)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    rom.reduced_stiffness_device(basis, rhos[0])
-    e1.record()
-    torch.cuda.synchronize()
-    t_khat = e0.elapsed_time(e1) * 1e-3
-    n_u, n_e = m.n_dofs, m.n_elems
+    t_step = statistics.median(a.elapsed_time(b) for a, b in ev) * 1e-3
+    m = prob.mesh
+    n_u, n_e, k, nd = m.n_dofs, m.n_elems, prob.rom_k, rhos.shape[0]
+    prof = rom_profile(_lib, rom, basis, rhos, pk, torch)
     canonical = n_e * (2 * k * 24**2 + 2 * k**2 * 24)  # PAPER.md:664 element form, per design
-    mb = (k + 7) // 8
-    executed_dmma = 2 * n_u * 64 * (mb * (mb + 1) // 2)  # Phi^T Y on DMMA, upper 8x8 tiles only (symmetric)
-    executed_op = 150 * n_e * k                          # WHT Hex8 operator, ~FP64 instr per element-column
-    bytes_dmma = 2 * n_u * k * 8                         # Phi and Y columns streamed once per design
-    peak = fp64_peak_tflops(torch, dev)
-    pk = peaks()
-    # the dominant kernel alone: the DMMA contraction, timed with events around its launch
-    t_dmma = dmma_time(rom, basis, rhos[0], torch)
-    line = {
-        "metric": "PhiT K Phi time (16-design ROM step)", "value": t_step, "unit": "s/step", "n_gpus": world,
-        "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": t_step * 1e3, "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg 5 recipe)",
-        "config": {"workload": f"cfg5 {m.nx}x{m.ny}x{m.nz} Hex8, {n_u} DOF, k={k}, {nd} designs: "
-                               "Phi^T K(rho_d) Phi + batched Cholesky + residual norms", "parallelism": "single"},
-        # upper-tile DMMA does 4.5 flop/byte < the FP64 ridge (~5.4): the contraction is bound by
-        # streaming Phi and Y (2 n k doubles per design), so it is measured against HBM
-        "roofline": {"kernel": "k_atb_cm<64,sym> (Phi^T Y upper 8x8 tiles, DMMA m8n8k4, cp.async-fed)", "bound": "hbm",
-                     "achieved": bytes_dmma / t_dmma / 1e9, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
-                     "frac": bytes_dmma / t_dmma / 1e9 / pk.get("hbm_gbs"), "traffic": None,
-                     "us_per_launch": t_dmma * 1e6, "bytes_per_launch": bytes_dmma,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
-                     "dmma": {"flops_per_launch": executed_dmma, "tflops": executed_dmma / t_dmma / 1e12,
-                              "fp64_peak_tflops": peak, "frac": executed_dmma / t_dmma / 1e12 / peak,
-                              "peak_source": "cuBLAS DGEMM 8192^3 measured in this run"},
-                     "per_design": {"s": t_khat, "executed_tflops": (executed_dmma + executed_op) / t_khat / 1e12,
-                                    "canonical_elementform_tflops_equiv": canonical / t_khat / 1e12,
-                                    "canonical_flops_convention": "N_e(2k*24^2 + 2k^2*24) (PAPER.md:664)"}},
-        "gpu_launches": int(launches), "clocks": clk,
-        "extra": {"residual_norms": norms[:4], "uhat0_norm": float(torch.linalg.norm(uhat[0]))},
-    }
-    print(json.dumps(line), flush=True)
+    roof = {"kernel": prof["kernel"], "bound": prof["bound"], "achieved": prof["achieved"], "peak": prof["peak"],
+            "unit": prof["unit"], "frac": prof["achieved"] / prof["peak"], "traffic": None,
+            "us_per_launch": prof["us"], "bytes_per_launch": prof.get("bytes"), "flops_per_launch": prof.get("flops"),
+            "peak_source": prof["peak_source"], "share_of_step": prof["us"] * prof.get("launches_per_step", 1) * 1e-6 / t_step,
+            "note": prof.get("note", "")}
+    out = {"workload": f"cfg5 {m.nx}x{m.ny}x{m.nz} Hex8, {n_u} DOF, k={k}, {nd} designs: Phi^T K(rho_d) Phi + batched "
+                       "Cholesky + residual norms ||K Phi uhat - f||",
+           "value": t_step, "unit": "s/step", "gpu_launches_per_step": launches / steps, "roofline": roof,
+           "canonical_elementform_tflops_equiv": canonical * nd / t_step / 1e12,
+           "residual_norms": norms[:4]}
+    return out
 
 
-def run_cfg4(args):
-    """BASELINE cfg 4: one full design evaluation on 384x192x192 Hex8 (43M DOF), slab-sharded
-    along z, one slab per rank: distributed Helmholtz filter (R = 2.5) -> clamp -> Jacobi-pCG
-    K(rho)u = f -> compliance -> sensitivities -> filter adjoint (slab_evaluate).  NCCL
-    allreduces the CG scalars; the z halo travels as NVLink peer stores from inside the update
-    kernels (--halo peer, CUDA IPC) or as NCCL send/recv (--halo nccl); the x planes after each
-    solve go through NCCL send/recv."""
+def cfg5_extra(args, dev, pk, want_cpu):
     import torch
 
     import paper_2004_05756_b200 as tb
     from paper_2004_05756_b200 import _lib, configs
-    from paper_2004_05756_b200.slab import SlabFilter, SlabSolver, TorchComm, partition, slab_evaluate
+
+    prob, s, basis, rom, rhos = cfg5_setup(tb, configs, dev, torch, args.seed)
+    pk = dict(pk)
+    pk["fp64_tflops"] = fp64_peak_tflops(torch, dev)
+    out = cfg5_measure(tb, _lib, prob, basis, rom, rhos, dev, pk, torch, 3, 1)
+    del s, basis, rom, rhos
+    torch.cuda.empty_cache()
+    if want_cpu:
+        out["cpu_baseline"] = cpu_cfg5(prob)
+    return out
+
+
+def run_cfg5(args):
+    """BASELINE cfg 5 standalone line: per trust-region step, 16 designs x (Phi^T K(rho_d) Phi,
+    reduced solve, ||K(rho_d) Phi uhat_d - f||), k = 64, 256x128x128 Hex8 (12.8M DOF)."""
+    import torch
+
+    import paper_2004_05756_b200 as tb
+    from paper_2004_05756_b200 import _lib, configs
 
     rank, local, world = rank_info()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    import torch.distributed as dist
-
-    if not dist.is_initialized():
-        if world > 1:
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            import socket
-
-            with socket.socket() as sk:
-                sk.bind(("127.0.0.1", 0))
-                port = sk.getsockname()[1]
-            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
-                                    device_id=dev)
-    prob = configs.cfg4(seed=args.seed)
-    mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
-    slab = partition(prob.mesh.nz, world)[rank]
-    sv = SlabSolver(prob.mesh, prob.k_e, prob.f, prob.fixed, mat, slab, device=dev)
-    fl = SlabFilter(prob.mesh, prob.radius, slab, device=dev)
-    psi = torch.as_tensor(sv.local_elems(prob.psi).copy(), device=dev)
-    comm = TorchComm(peer=(args.halo == "peer"))
+    pk = dict(peaks())
+    pk["fp64_tflops"] = fp64_peak_tflops(torch, dev)
+    prob, s, basis, rom, rhos = cfg5_setup(tb, configs, dev, torch, args.seed)
     clocks = Clocks(dev.index)
     clocks.start()
-    ev = slab_evaluate([sv], [fl], comm, [psi], rtol=prob.rtol)  # warm-up (maps the peers, first touches)
-    del ev
-    dist.barrier()
-    torch.cuda.synchronize()
-    launches0 = _lib.lib().tb_launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    ev = slab_evaluate([sv], [fl], comm, [psi], rtol=prob.rtol)
-    e1.record()
-    torch.cuda.synchronize()
+    out = cfg5_measure(tb, _lib, prob, basis, rom, rhos, dev, pk, torch, args.steps, args.warmup)
     clk = clocks.stop()
-    launches = _lib.lib().tb_launch_count() - launches0
-    t = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    m = prob.mesh
+    cpu = cpu_cfg5(prob) if (rank == 0 and not args.no_cpu_baseline) else None
     if rank == 0:
-        it = ev.iterations
         print(json.dumps({
-            "metric": METRIC, "value": float(t.item()), "unit": UNIT, "n_gpus": world,
-            "steps": 1, "warmup": 1, "ms_per_step": float(t.item()) * 1e3, "higher_is_better": False,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg 4 recipe)",
-            "config": {"workload": f"cfg4 {m.nx}x{m.ny}x{m.nz} Hex8, {m.n_dofs} DOF, z-slabs x{world}: "
-                                   f"filter R={prob.radius:g} + Jacobi-pCG to {prob.rtol:g} + compliance + "
-                                   "sensitivities + filter adjoint",
-                       "parallelism": f"slab{world}", "halo": args.halo, "pcg_iterations": it,
-                       "filter_iterations": list(ev.filter_iterations), "J": ev.j, "clamp_width": ev.clamp_width,
-                       "seed": args.seed},
-            "pcg": {"bytes_per_iteration_per_rank": 8 * (12 * sv.local.n_dofs + sv.local.n_elems),
-                    "us_per_iteration_upper_bound": float(t.item()) / max(it, 1) * 1e6},
+            "metric": "PhiT K Phi time (16-design ROM step)", "value": out["value"], "unit": "s/step", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": out["value"] * 1e3,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded cfg 5 recipe)", "config": {"workload": out["workload"], "parallelism": "single"},
+            "roofline": out["roofline"], "cpu_baseline": cpu, "gpu_launches": int(out["gpu_launches_per_step"] * args.steps),
+            "clocks": clk, "extra": {"residual_norms": out["residual_norms"]}}), flush=True)
+
+
+def run_cfg4(args):
+    """BASELINE cfg 4 standalone line: one evaluation on 384x192x192 Hex8 (43M DOF),
+    slab-sharded along z over the ranks of the run."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2004_05756_b200 import _lib
+
+    rank, local, world = rank_info()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    pk = peaks()
+    clocks = Clocks(dev.index)
+    clocks.start()
+    launches0 = _lib.lib().tb_launch_count()
+    out = cfg4_extra(args, dev, dist if world > 1 else None, world, rank, pk,
+                     rank == 0 and world == 1 and not args.no_cpu_baseline)
+    launches = _lib.lib().tb_launch_count() - launches0
+    clk = clocks.stop()
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": out["value"], "unit": UNIT, "n_gpus": world, "steps": 1, "warmup": 1,
+            "ms_per_step": out["value"] * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded cfg 4 recipe)",
+            "config": {"workload": out["workload"], "parallelism": f"slab{world}", "halo": args.halo,
+                       "pcg_iterations": out["pcg_iterations"], "filter_iterations": out["filter_iterations"],
+                       "J": out["J"], "seed": args.seed},
+            "roofline": out["roofline"], "cpu_baseline": out.get("cpu_baseline"),
             "gpu_launches": int(launches), "clocks": clk}), flush=True)
-    dist.barrier()
-    comm.close()
-    dist.destroy_process_group()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# --------------------------------------------------------------------------------------
+# reference arm: the reference's own CPU implementation on the host cores
+# --------------------------------------------------------------------------------------
+def run_reference(args):
+    rank, _, world = rank_info()
+    if rank != 0:
+        return
+    name = args.config
+    budget = 150.0
+    if name in ("cfg1", "cfg2"):
+        prob = problem(name, args.seed)
+        c = Cpu2d(prob)  # one-time set-up (filter factorisation, pattern) as the reference constructors
+        for _ in range(min(args.warmup, 1)):
+            c.eval(prob.psi)
+        v, n = c.sample(prob.psi, budget_s=budget, max_n=args.steps)
+        kind, sample = c.kind, f"{n} full evaluations: {c.what} (SuperLU single-threaded, BLAS on all cores)"
+        unit, metric = UNIT, METRIC
+        workload = workload_desc(prob, "jacobi").replace(PC_DESC["jacobi"], "SuperLU direct solve (fem.py:270-349)")
+    elif name == "cfg5":
+        prob = problem(name, args.seed)
+        cb = cpu_cfg5(prob)
+        v, n, kind, sample, unit = cb["value"], 1, cb["kind"], cb["sample"], "s/step"
+        metric, workload = "PhiT K Phi time (16-design ROM step)", "cfg5 16-design ROM step on the host"
+    else:
+        prob = problem(name, args.seed)  # cfg3: CPU pre-filter (not timed)
+        c = Cpu3d(prob)
+        gpu_iters = CFG3_JACOBI_ITERS if name == "cfg3" else 7503
+        vals, t0, n = [], time.perf_counter(), 0
+        while n < max(args.steps, 1) and (n == 0 or time.perf_counter() - t0 < budget):
+            if name == "cfg3":
+                v1, _ = c.step(prob.psi, 10, gpu_iters)
+            else:
+                v1, _ = c.step(prob.psi, 2, gpu_iters, filter_its=(21, 20), filter_sample=2)
+            vals.append(v1)
+            n += 1
+        v = statistics.median(vals)
+        kind = "port"
+        sample = (f"{n} restated {name} evaluations on the host (oracle/iterative.py, BASELINE.md §4.3): reference "
+                  f"element formulas, Jacobi-PCG sampled for a fixed budget and extrapolated to {gpu_iters} iterations "
+                  f"(the B200 run's count), Helmholtz filter/adjoint by CG")
+        unit, metric = UNIT, METRIC
+        workload = workload_desc(prob, "jacobi")
+    line = {
+        "impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": world, "steps": n,
+        "warmup": min(args.warmup, 1), "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE recipe)",
+        "config": {"workload": workload, "parallelism": "cpu", "seed": args.seed},
+        "cpu_baseline": {"value": v, "unit": unit, "cores": _blas_threads(), "kind": kind, "sample": sample},
+        "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
 
 
 def main():

@@ -48,9 +48,11 @@ __global__ void k_clamp(int64_t n, double lo, const double* __restrict__ raw, do
   double m = 0.0;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const double r = raw[e];
-    const double c = fmin(fmax(r, lo), 1.0);
+    // np.clip keeps NaN (the following solve then reports a breakdown); fmin/fmax would not
+    const double c = (r != r) ? r : fmin(fmax(r, lo), 1.0);
     rho[e] = c;
-    m = fmax(m, fabs(c - r));
+    // a NaN entry reports an infinite clamp width (fmax-based reductions drop NaN)
+    m = fmax(m, (r != r) ? __longlong_as_double(0x7ff0000000000000LL) : fabs(c - r));
   }
   m = warp_max(m);
   __shared__ double red[32];
@@ -458,7 +460,13 @@ int tb_pcg_solve(tb_plan* plan, const double* rho, const double* b, double* x, d
     TB_TRY(P->work.set_fields(0, P->own_k0, P->own_k1));
   }
   TB_TRY(P->material(rho, P->d_alpha, nullptr, s));
+  if (sweep_enabled(P)) return pcg_solve_sweep(P, b, x, rtol, maxit, iters, relres, s);
   return pcg_solve(P->op, P->work, b, x, rtol, maxit, iters, relres, s);
+}
+
+int tb_pcg_path(tb_plan* plan) {
+  if (plan == nullptr) return -1;
+  return sweep_enabled(reinterpret_cast<tb_plan_impl*>(plan)) ? 1 : 0;
 }
 
 int tb_pcg_kernel_time(tb_plan* plan, float* ms, int* launches) {
@@ -479,6 +487,10 @@ int tb_pcg_profile(tb_plan* plan, const double* rho, const double* b, int nrep, 
   auto* P = reinterpret_cast<tb_plan_impl*>(plan);
   cudaStream_t s = (cudaStream_t)stream;
   TB_TRY(P->material(rho, P->d_alpha, nullptr, s));
+  if (sweep_enabled(P)) {
+    *ms_update = 0.0;
+    return pcg_profile_sweep(P, b, nrep, ms_fused, s);
+  }
   return pcg_profile(P->op, P->work, b, nrep, ms_fused, ms_update, s);
 }
 

@@ -651,7 +651,21 @@ int mg_build(tb_plan_impl* P) {
   TB_CUDA(cudaMalloc(&mg.work, sizeof(double) * (size_t)(mg.lwork + 1)));
   TB_CUDA(cudaMalloc(&mg.info, sizeof(int)));
   mg.ainv = mg.dense;  // potri (or Gauss-Jordan) overwrites the matrix with its inverse in place
-  if (D == 2 && mg.ncoarse <= kGjMaxN && getenv("TB_MG_CUSOLVER") == nullptr) {
+  // Gauss-Jordan gives each row block to its own CTA(s) (k_mg_gj_inverse: rbk = c / cps), so it
+  // needs at least ceil(n / kGjB) co-resident CTAs at its shared-memory size, one per SM;
+  // otherwise (MIG slice, MPS limits, large n) the cuSOLVER path is taken.
+  bool gj_ok = D == 2 && mg.ncoarse <= kGjMaxN && getenv("TB_MG_CUSOLVER") == nullptr;
+  if (gj_ok) {
+    int sms = 0, coop = 0, occ = 0;
+    TB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P->device));
+    TB_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, P->device));
+    const size_t smem = sizeof(double) * kGjB * (size_t)mg.ncoarse;
+    TB_CUDA(cudaFuncSetAttribute(k_mg_gj_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mg_gj_inverse, 512, smem));
+    const int64_t nblocks = (mg.ncoarse + kGjB - 1) / kGjB;
+    gj_ok = coop && occ >= 1 && nblocks <= sms;
+  }
+  if (gj_ok) {
     TB_CUDA(cudaMalloc(&mg.gj, sizeof(double) * 2 * kGjB * (size_t)mg.ncoarse));
     TB_CUDA(cudaMalloc(&mg.gj_bar, 64));
     TB_CUDA(cudaMallocHost(&mg.h_info, sizeof(int)));
@@ -750,19 +764,24 @@ int mg_setup(tb_plan_impl* P, cudaStream_t s) {
   }
   cusolverDnHandle_t h = (cusolverDnHandle_t)mg.solver;
   cusolverDnSetStream(h, s);
+  // potrf's status is read before potri runs: potri overwrites info and usually reports 0 on
+  // a partially factored matrix
   if (cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, (int)n, mg.dense, (int)n, mg.work, mg.lwork, mg.info) !=
-          CUSOLVER_STATUS_SUCCESS ||
-      cusolverDnDpotri(h, CUBLAS_FILL_MODE_LOWER, (int)n, mg.dense, (int)n, mg.work, mg.lwork, mg.info) !=
-          CUSOLVER_STATUS_SUCCESS) {
-    set_error("cuSOLVER factorisation of the coarsest multigrid level failed");
+      CUSOLVER_STATUS_SUCCESS) {
+    set_error("cuSOLVER Cholesky of the coarsest multigrid level failed");
     return TB_ERR_CUDA;
   }
   int info = 0;
   TB_CUDA(cudaMemcpyAsync(&info, mg.info, sizeof(int), cudaMemcpyDeviceToHost, s));
   TB_CUDA(cudaStreamSynchronize(s));
   if (info != 0) {
-    set_error("coarsest multigrid operator is not positive definite (info %d)", info);
+    set_error("coarsest multigrid operator is not positive definite (potrf info %d)", info);
     return TB_ERR_INDEFINITE;
+  }
+  if (cusolverDnDpotri(h, CUBLAS_FILL_MODE_LOWER, (int)n, mg.dense, (int)n, mg.work, mg.lwork, mg.info) !=
+      CUSOLVER_STATUS_SUCCESS) {
+    set_error("cuSOLVER inverse of the coarsest multigrid level failed");
+    return TB_ERR_CUDA;
   }
   { k_mg_symmetrize<<<nblk(n * n), kBlock, 0, s>>>(n, mg.dense); tb::launched(); }
   TB_CHECK_LAUNCH();

@@ -25,6 +25,7 @@
 // is a fixed-order sum of per-CTA partials that every CTA evaluates identically, so all CTAs
 // take the same convergence branch.  Cross-CTA data written inside the kernel is read with
 // ld.cg (L2); the constant operator data (stencils, D^-1, masks, alpha, inverse) with ld.nc.
+#include <atomic>
 #include <cooperative_groups.h>
 
 #include "cgcg2d.cuh"
@@ -463,14 +464,18 @@ bool mg_pcg2d_persistent(tb_plan_impl* P, PcgWork& w, cudaStream_t s) {
   if (P->g.dim != 2 || !P->pat_ok || mg.lv.size() < 2 || (int)mg.lv.size() > kMgpMaxLv) return false;
   if (mg.nu != 1 && mg.nu != 2) return false;
   if (getenv("TB_NO_PERSIST") != nullptr) return false;  // tests: the graph path
-  static int grid = -1;
+  // co-residency grid per device (a process may hold plans on several GPUs); racing first
+  // calls compute the same value
+  static std::atomic<int> grids[64];  // grid + 1; 0 = not computed yet
+  const int dev = (P->device >= 0 && P->device < 64) ? P->device : 0;
+  int grid = grids[dev].load() - 1;
   if (grid < 0) {
-    int dev = 0, sms = 0, coop = 0, occ = 0;
-    cudaGetDevice(&dev);
+    int sms = 0, coop = 0, occ = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mgpcg2d, kMgpThreads, 0);
     grid = (coop && occ >= 1) ? sms : 0;
+    grids[dev].store(grid + 1);
   }
   if (grid <= 0 || 2 * w.part_stride < 3 * grid) return false;
   MgpArgs a{};

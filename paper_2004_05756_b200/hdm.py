@@ -122,6 +122,9 @@ class HdmSolution:
         self.clamp_width = clamp_width
         self.factorization = factorization
         self.iterations, self.relres = iterations, relres
+        # numpy mode: the device copies the host arrays were made from, reused by gradient()
+        # while solution.rho/u/lam are still those very objects (no re-upload)
+        self._dev = None
 
     @property
     def psi_hash(self) -> str:
@@ -293,8 +296,10 @@ class HdmSolver:
         # numpy design: keep a byte snapshot; psi_hash (SHA-256, hdm.py:36-37) is computed on
         # first request and gradient() compares bytes directly (same strictness, no hashing)
         snap = np.array(psi, dtype=float, copy=True)
-        return HdmSolution(None, rho_u, u_u, lam_u, j, clamp_width, None, psi_ref=(snap, None, None),
-                           iterations=iters, relres=relres)
+        sol = HdmSolution(None, rho_u, u_u, lam_u, j, clamp_width, None, psi_ref=(snap, None, None),
+                          iterations=iters, relres=relres)
+        sol._dev = ((rho_u, u_u, lam_u), (rho_d, u_d, u_d if lam_u is u_u else None))
+        return sol
 
     def gradient(self, psi, solution: HdmSolution, objective: Objective):
         """Adjoint gradient of J at psi; requires a matching solution (hdm.py:199-209)."""
@@ -314,7 +319,12 @@ class HdmSolver:
             same = psi_digest(psi) == solution.psi_hash
         if not same:
             raise StaleSolutionError("solution was computed at a different design than psi")
-        s_d = self._sensitivity(solution.rho, solution.u, solution.lam, objective)
+        dev = solution._dev
+        if (dev is not None and dev[1][2] is not None and solution.rho is dev[0][0] and solution.u is dev[0][1]
+                and solution.lam is dev[0][2] and objective.is_compliance):
+            s_d = self.sensitivity_device(dev[1][0], dev[1][1], dev[1][2])  # device copies, no re-upload
+        else:
+            s_d = self._sensitivity(solution.rho, solution.u, solution.lam, objective)
         return self._user(self.filter.apply_adjoint_device(s_d), native)
 
     def _sensitivity(self, rho, u, lam, objective):

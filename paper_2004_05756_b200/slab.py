@@ -514,7 +514,9 @@ def slab_evaluate(solvers, filters, comm, psi_locals, rtol=None, filter_rtol=Non
     plane halo of x after each of the three solves, two scalar allreduces (clamp width, J)."""
     for f, psi in zip(filters, psi_locals):
         f.set_load(psi, f.vol_share)
-    fit1 = dist_pcg_solve(filters, comm, rtol=filter_rtol or filters[0].rtol)[0]
+    fit1, _, ok1 = dist_pcg_solve(filters, comm, rtol=filter_rtol or filters[0].rtol)
+    if not ok1:
+        raise _lib.NotConvergedError(f"distributed Helmholtz filter did not converge in {fit1} iterations")
     comm.halo(filters, "x")
     rhos, widths = [], []
     for s, f in zip(solvers, filters):
@@ -533,7 +535,9 @@ def slab_evaluate(solvers, filters, comm, psi_locals, rtol=None, filter_rtol=Non
     sens = [s.sensitivity(r, u) for s, r, u in zip(solvers, rhos, us)]
     for f, v in zip(filters, sens):
         f.set_load(v, 0.125)
-    fit2 = dist_pcg_solve(filters, comm, rtol=filter_rtol or filters[0].rtol)[0]
+    fit2, _, ok2 = dist_pcg_solve(filters, comm, rtol=filter_rtol or filters[0].rtol)
+    if not ok2:
+        raise _lib.NotConvergedError(f"distributed filter adjoint did not converge in {fit2} iterations")
     comm.halo(filters, "x")
     grads = [f.to_elems(f.vol_share) for f in filters]
     return SlabEvaluation(j, cw, it, (fit1, fit2), rhos, us, sens, grads)

@@ -1,0 +1,164 @@
+"""Parity at the BASELINE 3D sizes (cfg 3 192x96x96, cfg 5 256x128x128).
+
+The reference cannot solve these grids (2D only; a direct solve is infeasible in 3D), so
+parity is split the way SURVEY §7.3(7) / §8(c) prescribe:
+
+* kernel level on the FULL grid against the CPU restatement of the reference's own
+  element-by-element formulas (oracle/iterative.py: hdm.py:211-233, filtering.py:73-114,
+  rom.py:254-262, 309-335): K(rho)v, element sensitivities, the Helmholtz load/average and
+  its operator, Phi^T K(rho) Phi column blocks, Phi^T f, the ROM residual norm;
+* solve level by self-consistency with host arithmetic: the pCG solution's TRUE residual
+  ||Z(f - K u)|| / ||Z f|| recomputed on the host with the oracle operator (<= rtol,
+  SURVEY App. A), f^T u = u^T K u, and the filter adjoint against the host CG adjoint.
+
+Tolerances (north_star, written here): pure arithmetic kernels 1e-12 relative (norm-wise),
+compliance 1e-8 (the identity 1e-10), sensitivities / filtered densities / reduced
+operators / error estimates 1e-6.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2004_05756_b200 as tb
+from oracle import iterative as it
+from oracle.fem import build_grid
+from paper_2004_05756_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+MAT = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
+
+
+def nrel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def cfg3(cuda):
+    import torch
+
+    def prefilter(mesh, psi0):
+        return tb.HelmholtzFilter(mesh, 2.0).apply(torch.as_tensor(psi0, device=cuda)).rho.cpu().numpy()
+
+    prob = configs.cfg3(prefilter=prefilter)
+    m = prob.mesh
+    filt = tb.HelmholtzFilter(m, prob.radius)
+    s = tb.HdmSolver(m, prob.k_e, filt, prob.f, prob.fixed, MAT, rtol=prob.rtol)
+    obj = tb.ComplianceObjective(s.f)
+    sol = s.solve(prob.psi, obj)
+    grad = s.gradient(prob.psi, sol, obj)
+    grid = build_grid(m.nx, m.ny, 1.0, nz=m.nz)
+    return dict(prob=prob, s=s, filt=filt, obj=obj, sol=sol, grad=grad, grid=grid)
+
+
+def test_cfg3_grid_numbering_bit_exact(cfg3):
+    m, g = cfg3["prob"].mesh, cfg3["grid"]
+    assert np.array_equal(m.elem_dofs, g.elem_dofs)
+    assert np.array_equal(m.elem_nodes, g.elem_nodes)
+    assert m.n_dofs == 5_447_811 and m.n_elems == 1_769_472
+
+
+def test_cfg3_apply_stiffness_full_grid(cfg3):
+    prob, s, g = cfg3["prob"], cfg3["s"], cfg3["grid"]
+    rho = cfg3["sol"].rho
+    v = np.random.default_rng(5).standard_normal(prob.mesh.n_dofs)
+    a = it.alpha(rho, configs.RHO_L, configs.P_SIMP)
+    ref = it.apply_stiffness(g, prob.k_e, a, v, s.free_mask)
+    assert nrel(s.apply_stiffness(rho, v), ref) <= 1e-12
+
+
+def test_cfg3_element_sensitivity_full_grid(cfg3):
+    prob, s, g, sol = cfg3["prob"], cfg3["s"], cfg3["grid"], cfg3["sol"]
+    ref = it.element_sensitivity(g, prob.k_e, sol.rho, sol.u, sol.u, configs.RHO_L, configs.P_SIMP)
+    got = s.element_sensitivity(sol.rho, sol.u, sol.u, cfg3["obj"])
+    assert nrel(got, ref) <= 1e-12
+    assert got.max() <= 0.0  # compliance sensitivities are non-positive
+
+
+def test_cfg3_pcg_true_residual_and_energy(cfg3):
+    prob, s, g, sol = cfg3["prob"], cfg3["s"], cfg3["grid"], cfg3["sol"]
+    a = it.alpha(sol.rho, configs.RHO_L, configs.P_SIMP)
+    kapply = lambda x: it.apply_stiffness(g, prob.k_e, a, x)  # noqa: E731
+    # host true residual of the device solution, SURVEY App. A
+    assert it.true_relres(kapply, s.free_mask, s.f, sol.u) <= prob.rtol * 1.0001
+    ku = kapply(sol.u)
+    fu = float(s.f @ sol.u)
+    assert abs(sol.j - fu) <= 1e-12 * abs(fu)
+    assert abs(float(sol.u @ ku) - fu) <= 1e-10 * abs(fu)
+    assert np.all(sol.u[~s.free_mask] == 0.0)
+
+
+def test_cfg3_filter_full_grid(cfg3):
+    prob, filt, g, sol = cfg3["prob"], cfg3["filt"], cfg3["grid"], cfg3["sol"]
+    hz = it.Helmholtz(g, prob.radius)
+    res = filt.apply(prob.psi)
+    b = hz.load_vector(prob.psi)
+    assert np.abs(filt.load_vector(prob.psi) - b).max() <= 1e-15 * np.abs(b).max() * 10
+    # Helmholtz solve: host true residual, and the element average
+    assert np.linalg.norm(b - hz.apply(res.phi)) <= 1e-11 * np.linalg.norm(b)
+    assert np.abs(hz.average(res.phi) - res.rho).max() <= 1e-15
+    # filtered density (clamped) of the HDM solve against the host CG filter
+    _, rho_h = hz.filter_apply(prob.psi, rtol=1e-13)
+    rho_c = np.clip(rho_h, configs.RHO_L, 1.0)
+    assert np.max(np.abs(sol.rho - rho_c) / rho_c) <= 1e-6
+    # volume preservation (test_filtering.py:20-28)
+    assert abs(res.rho.sum() - prob.psi.sum()) <= 1e-9 * prob.psi.sum()
+
+
+def test_cfg3_gradient_vs_host_adjoint(cfg3):
+    prob, g, sol, grad = cfg3["prob"], cfg3["grid"], cfg3["sol"], cfg3["grad"]
+    s_host = it.element_sensitivity(g, prob.k_e, sol.rho, sol.u, sol.u, configs.RHO_L, configs.P_SIMP)
+    g_host = it.Helmholtz(g, prob.radius).filter_adjoint(s_host, rtol=1e-13)
+    assert nrel(grad, g_host) <= 1e-6
+
+
+@pytest.fixture(scope="module")
+def cfg5(cuda):
+    import torch
+
+    prob = configs.cfg5()
+    m = prob.mesh
+    s = tb.HdmSolver(m, prob.k_e, tb.HelmholtzFilter(m, prob.radius), prob.f, prob.fixed, MAT, rtol=prob.rtol)
+    k = prob.rom_k
+    cols = configs.phi_columns(m, k, seed=0, xp=torch, device=cuda)
+    cols[:, torch.as_tensor(~s.free_mask, device=cuda)] = 0.0
+    phi = tb.gram_schmidt(list(cols))
+    del cols
+    basis = tb.ReducedBasis(phi, None, None, phi.T @ s._f_d)
+    rom = tb.RomModel(s)
+    rhos = torch.as_tensor(np.stack(prob.rom_designs[:2]), device=cuda)
+    khat, uhat, norms = rom.solve_batch(basis, rhos)
+    grid = build_grid(m.nx, m.ny, 1.0, nz=m.nz)
+    return dict(prob=prob, s=s, phi=phi, basis=basis, rhos=rhos, khat=khat, uhat=uhat, norms=norms, grid=grid)
+
+
+def test_cfg5_reduced_operator_column_blocks(cfg5):
+    """Phi^T K(rho_d) Phi for 8 columns x 2 designs against the reference formula's columns
+    K(rho_d) phi_c (hdm.py:224-233 scatter, rom.py:254-262 contraction); 64 x 8 blocks."""
+    import torch
+
+    prob, g, phi = cfg5["prob"], cfg5["grid"], cfg5["phi"]
+    free = cfg5["s"].free_mask
+    phi8 = phi[:, :8].cpu().numpy()
+    for d in range(2):
+        rho = cfg5["rhos"][d].cpu().numpy()
+        a = it.alpha(rho, configs.RHO_L, configs.P_SIMP)
+        y = np.stack([it.apply_stiffness(g, prob.k_e, a, phi8[:, c], free) for c in range(8)], axis=1)
+        ref = (phi.t() @ torch.as_tensor(y, device=phi.device)).cpu().numpy()  # (64, 8)
+        got = cfg5["khat"][d][:, :8].cpu().numpy()
+        assert np.linalg.norm(got - ref) <= 1e-6 * np.linalg.norm(ref)
+        assert np.linalg.norm(got[:8] - got[:8].T) <= 1e-12 * np.linalg.norm(got[:8])
+
+
+def test_cfg5_fhat_and_residual_norm(cfg5):
+    prob, g, phi, s = cfg5["prob"], cfg5["grid"], cfg5["phi"], cfg5["s"]
+    fhat = cfg5["basis"].device_fhat(phi.device).cpu().numpy()
+    phi8 = phi[:, :8].cpu().numpy()
+    assert np.linalg.norm(fhat[:8] - phi8.T @ s.f) <= 1e-12 * max(np.linalg.norm(phi8.T @ s.f), 1e-300)
+    rho = cfg5["rhos"][0].cpu().numpy()
+    u = (phi @ cfg5["uhat"][0]).cpu().numpy()
+    a = it.alpha(rho, configs.RHO_L, configs.P_SIMP)
+    r = np.where(s.free_mask, it.apply_stiffness(g, prob.k_e, a, u) - s.f, 0.0)  # rom.py:319-325
+    ref = float(np.linalg.norm(r))
+    assert abs(cfg5["norms"][0] - ref) <= 1e-6 * max(ref, 1e-9 * np.linalg.norm(s.f))

@@ -613,8 +613,12 @@ def roofline_2d(solver, rho_d, pk, torch, precond):
         note = "working set L2/SMEM-resident; one grid barrier + partial exchange per iteration"
     its = solver.last_iterations
     ach = per_it * its / t / 1e9 if t > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tpath) and m.nx == 600:  # captured at cfg 2
+        traffic = json.load(open(tpath)).get("cfg2_mg" if precond == "mg" else "cfg2")
     return {"kernel": kern, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-            "frac": ach / pk["hbm_gbs"], "traffic": None, "bytes_per_launch": per_it * its, "us_per_launch": t * 1e6,
+            "frac": ach / pk["hbm_gbs"], "traffic": traffic, "bytes_per_launch": per_it * its, "us_per_launch": t * 1e6,
             "iterations_per_launch": its, "us_per_iteration": t * 1e6 / max(its, 1), "bytes_per_iteration": per_it,
             "peak_source": peak_source(pk), "note": note}
 

@@ -87,9 +87,10 @@ int tb_pcg_solve(tb_plan* plan, const double* rho, const double* b, double* x, d
  * coarsest level of <= 6144 dofs, else TB_ERR_INVALID). */
 int tb_plan_set_preconditioner(tb_plan* plan, int kind);
 
-/* Diagnostics: time the two pCG kernels in situ.  Starts a solve of K(rho) x = b and runs
+/* Diagnostics: time the pCG kernels in situ.  Starts a solve of K(rho) x = b and runs
  * nrep iterations with a CUDA event pair around every kernel on `stream`; returns the mean
- * duration (ms) of the fused operator kernel and of the update kernel (HOST pointers). */
+ * duration (ms) of the fused operator kernel and of the update kernel (HOST pointers).  On the
+ * single-sweep path (tb_pcg_path == 1) ms_fused is the whole iteration and ms_update is 0. */
 int tb_pcg_profile(tb_plan* plan, const double* rho, const double* b, int nrep, double* ms_fused,
                    double* ms_update, void* stream);
 /* Diagnostics: device time (CUDA events on the solve's stream) spanned by the persistent
@@ -97,6 +98,11 @@ int tb_pcg_profile(tb_plan* plan, const double* rho, const double* b, int nrep, 
  * there were (restarts after a true-residual check add one each); 0 launches when the solve ran
  * the graph path.  Synchronises on the last launch. */
 int tb_pcg_kernel_time(tb_plan* plan, float* ms, int* launches);
+/* Which Jacobi-pCG iteration tb_pcg_solve runs for this plan: 1 = the 3D single-sweep
+ * Chronopoulos-Gear kernel (Hex8, TMA-staged, one reduction per iteration), 0 = the two-kernel
+ * iteration (2D / multigrid / distributed), -1 = null plan.  Replaces nothing in the reference
+ * (diagnostic; the reference solve is fem.py:270-349). */
+int tb_pcg_path(tb_plan* plan);
 /* Diagnostics: per-phase %globaltimer sums (ns) of the persistent 2D multigrid pCG kernel in a
  * build with -DTB_MGP_PROF (tools/build_prof.sh); zeros in the product build.  Reads and clears
  * 32 counters into a HOST array. */

@@ -70,6 +70,8 @@ struct PcgState {
   int dot_k0, dot_k1;  // node planes [k0, k1) that own their rows (reductions, contractions)
   int pad3;
   double red[4];
+  int cg_init;  // single-reduction sweep (sweep.cu): the next sweep is a (re)start sweep
+  int pad4;
 };
 
 // ---------------------------------------------------------------------------------------

@@ -6,10 +6,10 @@
 
 namespace tb {
 
-int PcgWork::alloc(int64_t n_, int max_blocks, bool with_pub) {
+int PcgWork::alloc(int64_t n_, int max_blocks, bool with_pub, int64_t cap) {
   n = n_;
   part_stride = max_blocks > kUpdateBlocks ? max_blocks : kUpdateBlocks;
-  const size_t vb = sizeof(double) * (size_t)n;
+  const size_t vb = sizeof(double) * (size_t)(cap > n ? cap : n);
   double** vecs[] = {&x, &r, &z, &pa, &pb, &q, &dinv, &tmp};
   for (double** p : vecs) TB_CUDA(cudaMalloc(p, vb));
   TB_CUDA(cudaMalloc(&part, sizeof(double) * 6 * (size_t)part_stride));

@@ -62,7 +62,7 @@ struct PcgWork {
   double* partA() const { return part; }
   double* partB() const { return part + 2 * part_stride; }
   double* partC() const { return part + 4 * part_stride; }
-  int alloc(int64_t n_, int max_blocks, bool with_pub = false);
+  int alloc(int64_t n_, int max_blocks, bool with_pub = false, int64_t cap = 0);  // cap: vector capacity >= n_
   int set_fields(int dist, int dot_k0, int dot_k1);  // distributed mode + owned node planes
   void release();
 };

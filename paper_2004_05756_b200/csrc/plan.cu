@@ -122,7 +122,8 @@ int tb_plan_impl::init(const uint8_t* fixed_host) {
   TB_CUDA(cudaMalloc(&d_scratch, sizeof(double) * 8 * 148 * 8));
   TB_CUDA(cudaMalloc(&d_scalar, sizeof(double) * 16));
   TB_CUDA(cudaMallocHost(&h_scalar, sizeof(double) * 16));
-  TB_TRY(work.alloc(n_dofs, op.fused_blocks(), op.persist_grid > 0));
+  // Hex8 plans: vectors large enough for the pitched layout of the single-sweep pCG
+  TB_TRY(work.alloc(n_dofs, op.fused_blocks(), op.persist_grid > 0, (g.dim == 3 && hex8) ? sweep_size(g) : 0));
   TB_TRY(work.set_fields(0, 0, g.nnz));
   return TB_OK;
 }
@@ -133,6 +134,7 @@ int ElastOp::precond_apply(const double* r, double* z, cudaStream_t s) const { r
 int ElastOp::precond_check() const { return plan->precond == 1 ? mg_check(plan) : TB_OK; }
 
 void tb_plan_impl::release() {
+  sweep_release(this);
   mg_release(mg);
   work.release();
   void* bufs[] = {d_fixed, d_fixed_idx, d_fixed_off, d_alpha, d_alpha2, d_scratch, d_scalar, d_rom};

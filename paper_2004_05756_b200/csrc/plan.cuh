@@ -10,6 +10,7 @@ namespace tb {
 
 struct tb_plan_impl;
 struct tb_filter_impl;
+struct SweepState;
 
 // SIMP elasticity operator  Z K(rho) Z  (alpha from the plan's d_alpha)
 struct ElastOp final : PcgOp {
@@ -73,6 +74,7 @@ struct tb_plan_impl {
   size_t rom_bytes = 0;
   ElastOp op;
   PcgWork work;
+  SweepState* sweep = nullptr;  // 3D single-sweep Jacobi-pCG (sweep.cu), created on first use
 
   int init(const uint8_t* fixed_host);
   void release();
@@ -105,5 +107,13 @@ void scalar_element_matrices(int dim, double h, double* S, double* M, double* s_
 Grid make_grid(int dim, int nx, int ny, int nz, double h);
 void finish_sum(int nb, const double* part, double* out, cudaStream_t s);
 int device_dot(const double* a, const double* b, int64_t n, double* scratch, double* out_dev, cudaStream_t s);
+
+// single-sweep 3D Jacobi-pCG (sweep.cu)
+int64_t sweep_size(const Grid& g);
+bool sweep_enabled(const tb_plan_impl* P);
+void sweep_release(tb_plan_impl* P);
+int pcg_solve_sweep(tb_plan_impl* P, const double* b, double* x_out, double rtol, int maxit, int* iters,
+                    double* relres, cudaStream_t s);
+int pcg_profile_sweep(tb_plan_impl* P, const double* b, int nrep, double* ms_iter, cudaStream_t s);
 
 }  // namespace tb

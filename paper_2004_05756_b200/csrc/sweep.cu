@@ -1,0 +1,760 @@
+// 3D Jacobi-pCG in ONE z-sweep per iteration (Chronopoulos-Gear single-reduction CG), with
+// TMA node-plane staging.  Replaces, for Hex8 plans, the two-kernel iteration of pcg.cu
+// (k_hex8<true> + k_pcg_update: 12 N_u + N_e doubles and two grid-wide reductions).
+//
+// Recurrences (Chronopoulos & Gear; u = D^-1 r, w = A u):
+//   p_i = u_i + b_i p_{i-1}       s_i = w_i + b_i s_{i-1}        (s = A p)
+//   x_{i+1} = x_i + a_i p_i       r_{i+1} = r_i - a_i s_i
+//   u_{i+1} = D^-1 r_{i+1}        w_{i+1} = A u_{i+1}
+//   g = (r, u), d = (w, u):  b_{i+1} = g_{i+1}/g_i,  a_{i+1} = g_{i+1} / (d_{i+1} - b_{i+1} g_{i+1}/a_i)
+// One sweep does all of it: when node plane k lands in shared memory (TMA, one instruction per
+// array, two planes in flight per CTA), every thread updates its slots pointwise (s, r, then
+// u = D^-1 r into the operator's plane ring; x, p and the stores on owned slots), then the
+// element-centric WHT-block Hex8 operator of hex8.cuh runs on the u planes and its owned outputs
+// are w.  The halo ring and the two ghost planes of u are recomputed from r, s, w, D^-1 (bitwise
+// identical to the owner's).  Per iteration: read x r p s w + D^-1 (one double per node) +
+// alpha, write x r p s w: ~10.3 N_u + N_e doubles and ONE reduction of (g, r.r, d) (the textbook
+// iteration is 9 N_u + N_e over two sweeps and two reductions; the two-kernel path moved 12 N_u).
+//
+// Layout: the solver's vectors are PITCHED: dof (i, j, k, c) at (k nny + j) P + 3 i + c with the
+// row pitch P >= 3 nnx a multiple of 4 doubles, so the tensor-map strides are legal (3 nnx is odd
+// for every BASELINE grid).  b comes in and x goes out in the reference's compact layout
+// (conversion kernels below, once per solve).
+//
+// r, s and w are read at halo nodes (neighbour CTAs, ghost planes of the z-chunks) while their
+// owners write the next iterate, so they are double-buffered by iteration parity q: a sweep reads
+// set q and writes set 1 - q.  x and p are read and written by their owner only (in place).
+//
+// Jacobi: for the isotropic Hex8 element every diagonal entry of K_e is the same k_d, so
+// D_n = k_d sum_{e at n} alpha_e is one value per NODE; it is stored as 1/D_n with the node's
+// three Dirichlet flags in the three lowest mantissa bits (a relative perturbation < 1e-15 of a
+// preconditioner, which changes nothing CG relies on).  Fixed dofs get u = 0 and s = r = 0, so
+// w's fixed rows (never masked) are never read: the solve is the reference's Z K Z system
+// (fem.py:291-294, 378-382).
+#include <cuda.h>
+#include <stdlib.h>
+
+#include "plan.cuh"
+
+namespace tb {
+
+namespace {
+
+constexpr int kTRow = 100;                              // node-plane tile row: 3 x 33 doubles + 1 (16 B multiple)
+constexpr int kTRows = kPY;                             // 9 node rows
+constexpr int kTPlane = kTRow * kTRows;                 // 900 doubles
+constexpr int kTPlaneS = 912;                           // smem stride: 128-byte multiple
+constexpr int kTORow = 94;                              // owned tile row: 3 x 31 + 1
+constexpr int kTOPlane = kTORow * kOY;                  // 658
+constexpr int kTOPlaneS = 672;
+constexpr int kTNRow = 34;                              // per-node D^-1 tile row: 33 nodes + 1
+constexpr int kTNPlane = kTNRow * kTRows;               // 306
+constexpr int kTNPlaneS = 320;
+constexpr int kTSlots = (kTPlane + kHT - 1) / kHT;      // 4 slots per thread
+// one staged plane: r, s, w (halo tiles), D^-1 (node tile), x, p (owned tiles)
+constexpr int kStage = 3 * kTPlaneS + kTNPlaneS + 2 * kTOPlaneS;   // 4400 doubles
+constexpr uint32_t kHaloBytes = sizeof(double) * kTPlane;
+constexpr uint32_t kNodeBytes = sizeof(double) * kTNPlane;
+constexpr uint32_t kOwnBytes = sizeof(double) * kTOPlane;
+constexpr int kSmemDoubles = 2 * kStage + 3 * kTPlaneS + 2 * 3 * kHT + 3 * kHT;
+constexpr size_t kSweepSmem = sizeof(double) * kSmemDoubles + 2 * sizeof(uint64_t) + 128;  // + mbarriers + align
+
+enum { kModeCg = 0, kModeApply = 1 };
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA: 3D tile of a pitched vector -> shared memory, completion counted on `bar`; coordinates
+// outside the tensor (negative included) are zero-filled by the hardware.  The first inner
+// coordinate must be 16-byte aligned (an odd double index faults with an illegal instruction
+// on B200, tools/tma_probe.cu), so callers round tile starts down and shift their indices.
+__device__ __forceinline__ void tma_load3(double* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace
+
+// Tensor maps of one plan's pitched vectors: halo tiles [100 x 9 x 1] of r, s, w (both parity
+// sets) and x (for the true-residual apply), the node tile [34 x 9 x 1] of D^-1, owned tiles
+// [94 x 7 x 1] of x and p.
+struct SweepMaps {
+  CUtensorMap r[2], s[2], w[2], dn, xh, x, p;
+};
+
+struct SweepVecs {
+  double *x, *p;
+  double *r[2], *s[2], *w[2];
+  double* y;       // APPLY output y = K x
+  int64_t pitch;   // P (doubles per node row)
+  int64_t plane;   // P nny (doubles per node plane)
+};
+
+// One Chronopoulos-Gear iteration of parity q (MODE kModeCg; st->cg_init: the start sweep with
+// a = b = 0 that forms u_0, w_0, g_0, d_0) or y = K(alpha) x (kModeApply, no reductions).
+template <int MODE>
+__global__ void __launch_bounds__(kHT, kHexCtas)
+    k_hex8_cg(const __grid_constant__ SweepMaps maps, Grid g, Hex8Iso K, const double* __restrict__ alpha,
+              SweepVecs V, PcgState* st, double* partials, int zchunk, int q) {
+  extern __shared__ __align__(128) double sm_raw[];
+  // 128-byte aligned TMA destinations; the offset is applied to the __shared__ array itself so
+  // the compiler keeps shared-space (LDS/STS) accesses instead of generic ones
+  double* sm = sm_raw + (((smem_u32(sm_raw) + 127u) & ~127u) - smem_u32(sm_raw)) / sizeof(double);
+  double* STG = sm;                                    // [2][kStage] staged planes (APPLY: x halo tile only)
+  double* U = STG + 2 * kStage;                        // [3][kTPlaneS] u node-plane ring
+  double(*stage2)[3][kHT] = reinterpret_cast<double(*)[3][kHT]>(U + 3 * kTPlaneS);
+  double* aring = U + 3 * kTPlaneS + 2 * 3 * kHT;      // [3][kHT] alpha of element planes ez .. ez+2
+  uint64_t* bar = reinterpret_cast<uint64_t*>(aring + 3 * kHT);  // [2]
+
+  double a_cg = 0.0, b_cg = 0.0;
+  if (MODE == kModeCg) {
+    if (st->done) return;
+    if (!st->cg_init) {
+      a_cg = st->alpha;
+      b_cg = st->beta;
+    }
+  }
+  const int t = threadIdx.x;
+  const int i0 = blockIdx.x * kOX, j0 = blockIdx.y * kOY;
+  const int K0 = blockIdx.z * zchunk;
+  const int K1 = min(g.nnz, K0 + zchunk);
+  const int ex = t % kHX, ey = t / kHX;
+  const int gei = i0 - 1 + ex, gej = j0 - 1 + ey;
+  const bool col_ok = gei >= 0 && gei < g.nx && gej >= 0 && gej < g.ny;
+  const bool own = t < kOX * kOY;
+  const int onx = t % kOX, ony = t / kOX;
+  const int px = onx + 1, py = ony + 1;
+  // 16-byte aligned tile starts: the halo tile begins at dof 3 (i0 - 1) - shh, the owned tile at
+  // 3 i0 - sho, the node tile at node i0 - 1 - shn; shared-memory indices carry the shifts
+  const int shh = (3 * (i0 - 1)) & 1, sho = (3 * i0) & 1, shn = (i0 - 1) & 1;
+  // LAND slots: box index f = t + s kHT -> (row f / kTRow, tile double d = f % kTRow - shh)
+  unsigned fown = 0;
+#pragma unroll
+  for (int s = 0; s < kTSlots; ++s) {
+    const int f = t + s * kHT, ly = f / kTRow, d = f % kTRow - shh, lx = d / 3;
+    const int ni = i0 - 1 + lx, nj = j0 - 1 + ly;
+    if (f < kTPlane && d >= 0 && d < 3 * kPX && lx >= 1 && lx <= kOX && ly >= 1 && ly <= kOY && ni < g.nnx &&
+        nj < g.nny)
+      fown |= 1u << s;
+  }
+  const int64_t gbase = (int64_t)(j0 - 1) * V.pitch + 3 * (i0 - 1);  // pitched offset of tile (0, 0)
+  const bool own_in = own && i0 + onx < g.nnx && j0 + ony < g.nny;
+  const int64_t obase = (int64_t)(j0 + ony) * V.pitch + 3 * (i0 + onx);  // this thread's owned node
+  if (t == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  // Plane m of the sweep is node plane K0 - 1 + m; it is staged in buffer m & 1, whose barrier
+  // completes once per use, so plane m waits on parity (m >> 1) & 1.
+  auto issue = [&](int m) {
+    if (t == 0) {
+      const int kp = K0 - 1 + m;
+      double* B = STG + (m & 1) * kStage;
+      uint64_t* bb = bar + (m & 1);
+      const int cx = 3 * (i0 - 1) - shh, cy = j0 - 1;
+      if (MODE == kModeCg) {
+        mbar_expect_tx(bb, 3 * kHaloBytes + kNodeBytes + 2 * kOwnBytes);
+        tma_load3(B, &maps.r[q], cx, cy, kp, bb);
+        tma_load3(B + kTPlaneS, &maps.s[q], cx, cy, kp, bb);
+        tma_load3(B + 2 * kTPlaneS, &maps.w[q], cx, cy, kp, bb);
+        tma_load3(B + 3 * kTPlaneS, &maps.dn, i0 - 1 - shn, cy, kp, bb);
+        tma_load3(B + 3 * kTPlaneS + kTNPlaneS, &maps.x, 3 * i0 - sho, j0, kp, bb);
+        tma_load3(B + 3 * kTPlaneS + kTNPlaneS + kTOPlaneS, &maps.p, 3 * i0 - sho, j0, kp, bb);
+      } else {
+        mbar_expect_tx(bb, kHaloBytes);
+        tma_load3(B, &maps.xh, cx, cy, kp, bb);
+      }
+    }
+  };
+  double acc[3] = {0.0, 0.0, 0.0};  // g = r.u, r.r (free, owned), d = w.u
+  // (selects, not V.r[q ^ 1]: dynamic indexing would copy the parameter struct to local memory)
+  double* rout = q ? V.r[0] : V.r[1];
+  double* sout = q ? V.s[0] : V.s[1];
+  // plane m landed -> u into ring slot m % 3; owned slots of owned planes: x, r, p, s out
+  auto land = [&](int m) {
+    mbar_wait(bar + (m & 1), (m >> 1) & 1);
+    const double* B = STG + (m & 1) * kStage;
+    double* ub = U + (m % 3) * kTPlaneS;
+    const int kp = K0 - 1 + m;
+    const bool pown = kp >= K0 && kp < K1;
+    const int64_t pl = (int64_t)kp * V.plane;
+#pragma unroll 1
+    for (int s = 0; s < kTSlots; ++s) {
+      if (s < kTSlots - 1 || t < kTPlane - (kTSlots - 1) * kHT) {
+        const int f = t + s * kHT;
+        if (MODE == kModeApply) {
+          ub[f] = B[f];
+        } else {
+          const int ly = f / kTRow, dd = f % kTRow - shh;
+          const int lx = (dd + 3) / 3 - 1, c = dd - 3 * lx;  // dd = -1 -> lx = -1 (unused slot)
+          const double dn = B[3 * kTPlaneS + ly * kTNRow + lx + shn];
+          const bool fr = !((__double2loint(dn) >> c) & 1);  // free dof (mask bit c clear)
+          const double d = fr ? dn : 0.0;
+          const double r = B[f], so = B[kTPlaneS + f], w = B[2 * kTPlaneS + f];
+          const double sn = fr ? fma(b_cg, so, w) : 0.0;
+          const double rn = fr ? fma(-a_cg, sn, r) : 0.0;
+          const double un = d * rn;
+          ub[f] = un;
+          if (pown && (fown >> s & 1u)) {
+            const int fo = 3 * kTPlaneS + kTNPlaneS + (ly - 1) * kTORow + (dd - 3 + sho);
+            const double pn = fma(b_cg, B[fo + kTOPlaneS], d * r);
+            const double xn = fma(a_cg, pn, B[fo]);
+            const int64_t go = pl + gbase + (int64_t)ly * V.pitch + dd;
+            __stwb(V.x + go, xn);
+            __stwb(rout + go, rn);
+            __stwb(V.p + go, pn);
+            __stwb(sout + go, sn);
+            acc[0] = fma(rn, un, acc[0]);
+            acc[1] = fma(rn, rn, acc[1]);
+          }
+        }
+      }
+    }
+  };
+#define SW_FACE(boff_, f_)                                                                                   \
+  _Pragma("unroll") for (int cc = 0; cc < 4; ++cc) {                                                         \
+    const double* src = U + (boff_) + (ey + (cc >> 1)) * kTRow + shh + 3 * (ex + (cc & 1));                  \
+    _Pragma("unroll") for (int c = 0; c < 3; ++c) f_[c][cc] = src[c];                                        \
+  }                                                                                                          \
+  _Pragma("unroll") for (int c = 0; c < 3; ++c) wht4(f_[c]);
+
+  // planes m = 0 .. steps (node planes K0-1 .. K1); two in flight ahead of the one landing
+  const int steps = K1 - (K0 - 1);  // element planes ez = K0-1 .. K1-1  (steps >= 2)
+  issue(0);
+  issue(1);
+  land(0);
+  __syncthreads();
+  issue(2);
+  land(1);
+  __syncthreads();
+  if (steps >= 3) issue(3);
+  land(2);
+  __syncthreads();
+  if (steps >= 4) issue(4);
+  // alpha of element plane ez travels global -> shared by cp.async two steps ahead of its use
+  // (a register prefetch was sunk by the compiler next to its use: one DRAM latency per step)
+  const double* a_ptr = alpha + ((int64_t)gej * g.nx + gei);
+  const int64_t a_stride = (int64_t)g.nx * g.ny;
+  auto alpha_fetch = [&](int e, int slot) {  // element plane e (zero outside the grid / chunk)
+    const bool ok = col_ok && e >= 0 && e < g.nz && e < K1;
+    cp_async8(aring + slot * kHT + t, ok ? a_ptr + (int64_t)e * a_stride : alpha, ok);
+    cp_async_commit();
+  };
+  alpha_fetch(K0 - 1, 0);
+  alpha_fetch(K0, 1);
+  double fb[3][4];
+  SW_FACE(0, fb);
+  double tc[3][4];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int s = 0; s < 4; ++s) tc[c][s] = 0.0;
+  double* outv = (MODE == kModeApply) ? V.y : (q ? V.w[0] : V.w[1]);
+  int slot_top = 1;  // ring slot of plane rel + 1
+#pragma unroll 1
+  for (int rel = 0; rel < steps; ++rel) {
+    const int ez = K0 - 1 + rel;
+    cp_async_wait<1>();  // this thread's alpha of plane ez (group rel) has landed
+    const double a_cur = aring[(rel % 3) * kHT + t];
+    alpha_fetch(ez + 2, (rel + 2) % 3);
+    {  // ---- element (gei, gej, ez): spectrum from carried bottom face + top face (plane rel+1) ----
+      double ft[3][4];
+      SW_FACE(slot_top * kTPlaneS, ft);
+      double u[3][8];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          u[c][s] = fb[c][s] + ft[c][s];
+          u[c][s + 4] = fb[c][s] - ft[c][s];
+          fb[c][s] = ft[c][s];
+        }
+      hex8_iso_blocks(K, a_cur, u);
+      double fq[3][4];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          fq[c][s] = tc[c][s] + (u[c][s] + u[c][s + 4]);
+          tc[c][s] = u[c][s] - u[c][s + 4];
+        }
+        const double s0 = fq[c][0] + fq[c][1], d0 = fq[c][0] - fq[c][1];
+        const double s1 = fq[c][2] + fq[c][3], d1 = fq[c][2] - fq[c][3];
+        fq[c][0] = s0;
+        fq[c][1] = d0;
+        fq[c][2] = s1;
+        fq[c][3] = d1;
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double pp = fq[c][1] + __shfl_down_sync(0xffffffffu, fq[c][0], 1);
+        const double qq = fq[c][3] + __shfl_down_sync(0xffffffffu, fq[c][2], 1);
+        stage2[0][c][t] = pp + qq;
+        stage2[1][c][t] = pp - qq;
+      }
+    }
+    __syncthreads();
+    if (own_in && rel >= 1) {  // owned node (px, py) of plane ez: w out, d = w.u
+      const int e_dn = (py - 1) * kHX + (px - 1), e_up = py * kHX + (px - 1);
+      const double* up = U + (rel % 3) * kTPlaneS + py * kTRow + shh + 3 * px;
+      double* dst = outv + (int64_t)ez * V.plane + obase;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double v = stage2[1][c][e_dn] + stage2[0][c][e_up];
+        if (MODE == kModeCg) acc[2] = fma(up[c], v, acc[2]);
+        __stwb(dst + c, v);
+      }
+    }
+    // plane rel + 2 (in flight for two steps) -> ring slot (rel + 2) % 3 = slot of plane rel - 1
+    if (rel >= 1 && rel + 2 <= steps) land(rel + 2);
+    __syncthreads();
+    // its stage buffer is free again: plane rel + 4 in flight
+    if (rel >= 1 && rel + 4 <= steps) issue(rel + 4);
+    slot_top = (slot_top == 2) ? 0 : slot_top + 1;
+  }
+#undef SW_FACE
+  if (MODE == kModeCg) {
+    block_sum<3>(acc);
+    if (publish_partials<3>(acc, partials, &st->count_a)) {
+      gather_partials<3>(acc, partials, &st->count_a);
+      if (threadIdx.x == 0) {
+        const double gam = acc[0], rr = acc[1], del = acc[2];
+        st->rr = rr;
+        if (!isfinite(gam) || !isfinite(rr) || !isfinite(del)) {
+          st->done = 3;
+        } else if (st->cg_init) {
+          st->cg_init = 0;
+          if (rr <= st->tol2 || gam == 0.0) {
+            st->done = 1;
+          } else if (!(del > 0.0)) {
+            st->done = 3;
+          } else {
+            st->rz = gam;
+            st->pq = del;
+            st->alpha = gam / del;
+            st->beta = 0.0;
+          }
+        } else {
+          const int it = st->iters + 1;
+          st->iters = it;
+          if (rr <= st->tol2) {
+            st->done = 1;
+          } else {
+            const double beta = gam / st->rz;
+            const double den = del - beta * gam / st->alpha;
+            if (!(den > 0.0)) {
+              st->done = 3;
+            } else {
+              st->beta = beta;
+              st->alpha = gam / den;
+              st->rz = gam;
+              st->pq = del;
+              if (it >= st->maxit) st->done = 2;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// pitched index of compact dof i
+__device__ __forceinline__ int64_t pitched(const Grid& g, int64_t pitch, int64_t i) {
+  const int64_t node = i / 3, c = i - 3 * node;
+  const int64_t ni = node % g.nnx, rest = node / g.nnx;
+  return rest * pitch + 3 * ni + c;
+}
+
+// Per-node Jacobi inverse with the node's Dirichlet flags in the low mantissa bits (see top).
+__global__ void __launch_bounds__(kBlock) k_sweep_dinv(Grid g, double kd, const double* __restrict__ alpha,
+                                                      const uint8_t* __restrict__ fixed, int64_t npitch,
+                                                      double* __restrict__ dn) {
+  for (int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; n < g.n_nodes;
+       n += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(n % g.nnx);
+    const int64_t rest = n / g.nnx;
+    const int j = (int)(rest % g.nny), k = (int)(rest / g.nny);
+    double a = 0.0;
+    for (int dz = -1; dz <= 0; ++dz)
+      for (int dy = -1; dy <= 0; ++dy)
+        for (int dx = -1; dx <= 0; ++dx) {
+          const int ei = i + dx, ej = j + dy, ek = k + dz;
+          if (ei >= 0 && ei < g.nx && ej >= 0 && ej < g.ny && ek >= 0 && ek < g.nz)
+            a += alpha[((int64_t)ek * g.ny + ej) * g.nx + ei];
+        }
+    const double dinv = 1.0 / (kd * a);
+    const long long m = (fixed[3 * n] ? 1 : 0) | (fixed[3 * n + 1] ? 2 : 0) | (fixed[3 * n + 2] ? 4 : 0);
+    dn[rest * npitch + i] = __longlong_as_double((__double_as_longlong(dinv) & ~7LL) | m);
+  }
+}
+
+// start: r = Z b, x = p = s = w = 0 (parity set 0, which the next sweep reads);
+// tol2 = rtol^2 ||Z b||^2
+__global__ void __launch_bounds__(kBlock) k_sweep_prep(Grid g, int64_t n, int64_t pitch, const double* __restrict__ b,
+                                                      const uint8_t* __restrict__ fixed, SweepVecs V, PcgState* st,
+                                                      double* partials, double rtol, int maxit) {
+  double acc[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = pitched(g, pitch, i);
+    const double r = fixed[i] ? 0.0 : b[i];
+    V.r[0][q] = r;
+    V.x[q] = 0.0;
+    V.p[q] = 0.0;
+    V.s[0][q] = 0.0;
+    V.w[0][q] = 0.0;
+    acc[0] = fma(r, r, acc[0]);
+  }
+  block_sum<1>(acc);
+  if (publish_partials<1>(acc, partials, &st->count_c)) {
+    gather_partials<1>(acc, partials, &st->count_c);
+    if (threadIdx.x == 0) {
+      st->bb = acc[0];
+      st->rr = acc[0];
+      st->tol2 = rtol * rtol * acc[0];
+      st->iters = 0;
+      st->maxit = maxit;
+      st->alpha = st->beta = 0.0;
+      st->cg_init = 1;
+      st->done = (acc[0] == 0.0) ? 1 : (isfinite(acc[0]) ? 0 : 3);
+    }
+  }
+}
+
+// restart from the true residual: r = Z(b - y), y = K x (pitched); p = s = w = 0; converged when
+// ||r||^2 <= tol2
+__global__ void __launch_bounds__(kBlock) k_sweep_restart(Grid g, int64_t n, int64_t pitch, const double* __restrict__ b,
+                                                         const double* __restrict__ y, const uint8_t* __restrict__ fixed,
+                                                         SweepVecs V, PcgState* st, double* partials) {
+  double acc[1] = {0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = pitched(g, pitch, i);
+    const double r = fixed[i] ? 0.0 : b[i] - y[q];
+    V.r[0][q] = r;
+    V.p[q] = 0.0;
+    V.s[0][q] = 0.0;
+    V.w[0][q] = 0.0;
+    acc[0] = fma(r, r, acc[0]);
+  }
+  block_sum<1>(acc);
+  if (publish_partials<1>(acc, partials, &st->count_c)) {
+    gather_partials<1>(acc, partials, &st->count_c);
+    if (threadIdx.x == 0) {
+      st->rr = acc[0];
+      st->cg_init = 1;
+      if (st->done != 3) st->done = !isfinite(acc[0]) ? 3 : (acc[0] <= st->tol2 ? 1 : 0);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_sweep_unpitch(Grid g, int64_t n, int64_t pitch, const double* __restrict__ xP,
+                                                         double* __restrict__ x) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = xP[pitched(g, pitch, i)];
+}
+
+__global__ void k_sweep_cond(cudaGraphConditionalHandle h, const PcgState* st) {
+  cudaGraphSetConditional(h, st->done == 0 ? 1u : 0u);
+}
+
+// ---------------------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 3D map over a pitched array: inner dimension `inner` elements, row pitch `pitch` doubles
+static int encode(CUtensorMap* m, double* base, const Grid& g, int64_t inner, int64_t pitch, int bx, int by) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) {
+    set_error("cuTensorMapEncodeTiled is unavailable from the driver");
+    return TB_ERR_CUDA;
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)g.nny, (cuuint64_t)g.nnz};
+  const cuuint64_t strides[2] = {(cuuint64_t)pitch * 8, (cuuint64_t)pitch * g.nny * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult rc = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)rc);
+    return TB_ERR_CUDA;
+  }
+  return TB_OK;
+}
+
+// Hex8 Jacobi solves (not distributed, no multigrid) take the sweep; TB_NO_SWEEP=1 keeps the
+// two-kernel iteration of pcg.cu (A/B measurements)
+bool sweep_enabled(const tb_plan_impl* P) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = getenv("TB_NO_SWEEP");
+    off = (e != nullptr && e[0] != '\0' && e[0] != '0') ? 1 : 0;
+  }
+  return off == 0 && P->g.dim == 3 && P->hex8 && P->precond == 0 && !P->dist;
+}
+
+int64_t sweep_pitch(const Grid& g) { return ((int64_t)3 * g.nnx + 3) / 4 * 4; }
+int64_t sweep_size(const Grid& g) { return sweep_pitch(g) * g.nny * g.nnz; }
+static int64_t node_pitch(const Grid& g) { return ((int64_t)g.nnx + 1) / 2 * 2; }
+
+struct SweepState {
+  SweepMaps maps;
+  SweepVecs vecs;
+  double* dn = nullptr;                // per-node D^-1 + Dirichlet bits (pitched)
+  double* w1 = nullptr;                // w[1] (w[0] reuses the plan's dinv vector)
+  cudaGraphExec_t exec = nullptr;
+};
+
+// The plan's PcgWork vectors are allocated with sweep_size() doubles for Hex8 plans and reused
+// (pitched) here: x -> x, pa -> p, r/z -> r[0]/r[1], pb/q -> s[0]/s[1], dinv -> w[0], tmp -> y.
+int sweep_init(tb_plan_impl* P) {
+  if (P->sweep != nullptr) return TB_OK;
+  const Grid& g = P->g;
+  PcgWork& w = P->work;
+  auto* S = new SweepState();
+  const int64_t pitch = sweep_pitch(g);
+  int rc = TB_OK;
+  if (cudaMalloc(&S->w1, sizeof(double) * (size_t)sweep_size(g)) != cudaSuccess ||
+      cudaMalloc(&S->dn, sizeof(double) * (size_t)(node_pitch(g) * g.nny * g.nnz)) != cudaSuccess) {
+    set_error("sweep pCG: cudaMalloc failed");
+    rc = TB_ERR_CUDA;
+  }
+  S->vecs.x = w.x;
+  S->vecs.p = w.pa;
+  S->vecs.r[0] = w.r;
+  S->vecs.r[1] = w.z;
+  S->vecs.s[0] = w.pb;
+  S->vecs.s[1] = w.q;
+  S->vecs.w[0] = w.dinv;
+  S->vecs.w[1] = S->w1;
+  S->vecs.y = w.tmp;
+  S->vecs.pitch = pitch;
+  S->vecs.plane = pitch * g.nny;
+  const int64_t in3 = 3 * (int64_t)g.nnx;
+  for (int k = 0; k < 2 && rc == TB_OK; ++k) {
+    rc = encode(&S->maps.r[k], S->vecs.r[k], g, in3, pitch, kTRow, kTRows);
+    if (rc == TB_OK) rc = encode(&S->maps.s[k], S->vecs.s[k], g, in3, pitch, kTRow, kTRows);
+    if (rc == TB_OK) rc = encode(&S->maps.w[k], S->vecs.w[k], g, in3, pitch, kTRow, kTRows);
+  }
+  if (rc == TB_OK) rc = encode(&S->maps.dn, S->dn, g, g.nnx, node_pitch(g), kTNRow, kTRows);
+  if (rc == TB_OK) rc = encode(&S->maps.xh, w.x, g, in3, pitch, kTRow, kTRows);
+  if (rc == TB_OK) rc = encode(&S->maps.x, w.x, g, in3, pitch, kTORow, kOY);
+  if (rc == TB_OK) rc = encode(&S->maps.p, w.pa, g, in3, pitch, kTORow, kOY);
+  if (rc == TB_OK) {
+    cudaError_t e1 = cudaFuncSetAttribute(k_hex8_cg<kModeCg>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+    cudaError_t e2 = cudaFuncSetAttribute(k_hex8_cg<kModeApply>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSweepSmem);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      set_error("k_hex8_cg shared memory attribute: %s", cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+      rc = TB_ERR_CUDA;
+    }
+  }
+  if (rc != TB_OK) {
+    if (S->w1) cudaFree(S->w1);
+    if (S->dn) cudaFree(S->dn);
+    delete S;
+    return rc;
+  }
+  P->sweep = S;
+  return TB_OK;
+}
+
+void sweep_release(tb_plan_impl* P) {
+  if (P->sweep == nullptr) return;
+  if (P->sweep->exec) cudaGraphExecDestroy(P->sweep->exec);
+  if (P->sweep->w1) cudaFree(P->sweep->w1);
+  if (P->sweep->dn) cudaFree(P->sweep->dn);
+  delete P->sweep;
+  P->sweep = nullptr;
+}
+
+// sweep of parity q: reads r, s, w set q, writes set 1 - q (a solve starts on set 0)
+static void launch_iter(tb_plan_impl* P, int q, cudaStream_t s) {
+  SweepState& S = *P->sweep;
+  k_hex8_cg<kModeCg><<<hex8_grid(P->g, P->zchunk), kHT, kSweepSmem, s>>>(S.maps, P->g, P->hiso, P->d_alpha, S.vecs,
+                                                                         P->work.st, P->work.partA(), P->zchunk, q);
+}
+
+static void launch_apply_x(tb_plan_impl* P, cudaStream_t s) {
+  SweepState& S = *P->sweep;
+  k_hex8_cg<kModeApply><<<hex8_grid(P->g, P->zchunk), kHT, kSweepSmem, s>>>(S.maps, P->g, P->hiso, P->d_alpha,
+                                                                            S.vecs, P->work.st, P->work.partA(),
+                                                                            P->zchunk, 0);
+}
+
+static int build_sweep_graph(tb_plan_impl* P) {
+  SweepState& S = *P->sweep;
+  cudaStream_t cs;
+  TB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaGraph_t gr;
+  TB_CUDA(cudaGraphCreate(&gr, 0));
+  cudaGraphConditionalHandle h;
+  TB_CUDA(cudaGraphConditionalHandleCreate(&h, gr, 1u, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  TB_CUDA(cudaGraphAddNode(&node, gr, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  TB_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  static_assert(kIters % 2 == 0, "the graph body must end on parity 0");
+  for (int it = 0; it < kIters; ++it) launch_iter(P, it & 1, cs);
+  k_sweep_cond<<<1, 1, 0, cs>>>(h, P->work.st);
+  cudaGraph_t captured;
+  TB_CUDA(cudaStreamEndCapture(cs, &captured));
+  TB_CUDA(cudaGraphInstantiate(&S.exec, gr, 0));
+  TB_CUDA(cudaGraphDestroy(gr));
+  TB_CUDA(cudaStreamDestroy(cs));
+  return TB_OK;
+}
+
+static bool sweep_no_graph() {
+  const char* e = getenv("TB_PCG_NOGRAPH");
+  return e != nullptr && e[0] != '\0' && e[0] != '0';
+}
+
+static int sweep_start(tb_plan_impl* P, const double* b, double rtol, int maxit, cudaStream_t s) {
+  SweepState& S = *P->sweep;
+  PcgWork& w = P->work;
+  k_sweep_dinv<<<grid_for(P->g.n_nodes), kBlock, 0, s>>>(P->g, P->K3.v[0], P->d_alpha, P->d_fixed, node_pitch(P->g),
+                                                          S.dn);
+  k_sweep_prep<<<kUpdateBlocks, kBlock, 0, s>>>(P->g, P->n_dofs, S.vecs.pitch, b, P->d_fixed, S.vecs, w.st, w.partC(),
+                                                rtol, maxit);
+  launched(2);
+  TB_CHECK_LAUNCH();
+  return TB_OK;
+}
+
+int pcg_solve_sweep(tb_plan_impl* P, const double* b, double* x_out, double rtol, int maxit, int* iters,
+                    double* relres, cudaStream_t s) {
+  if (!(rtol > 0.0) || maxit < 1) {
+    set_error("pcg: rtol must be > 0 and maxit >= 1 (got %g, %d)", rtol, maxit);
+    return TB_ERR_INVALID;
+  }
+  TB_TRY(sweep_init(P));
+  SweepState& S = *P->sweep;
+  PcgWork& w = P->work;
+  const bool plain = sweep_no_graph();
+  if (!plain && !S.exec) TB_TRY(build_sweep_graph(P));
+  TB_TRY(sweep_start(P, b, rtol, maxit, s));
+  int rc = TB_OK, stalls = 0, it_before = 0;
+  double best_rr = -1.0;
+  for (int restart = 0;; ++restart) {
+    if (plain) {
+      for (;;) {
+        for (int k = 0; k < kIters; ++k) launch_iter(P, k & 1, s);
+        launched(kIters);
+        TB_CHECK_LAUNCH();
+        TB_CUDA(cudaMemcpyAsync(w.h_st, w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+        TB_CUDA(cudaStreamSynchronize(s));
+        if (w.h_st->done != 0) break;
+      }
+    } else {
+      TB_CUDA(cudaGraphLaunch(S.exec, s));
+    }
+    // true residual at exit: y = K x, r = Z(b - y); converged if ||r|| <= rtol ||Z b||
+    launch_apply_x(P, s);
+    k_sweep_restart<<<kUpdateBlocks, kBlock, 0, s>>>(P->g, P->n_dofs, S.vecs.pitch, b, S.vecs.y, P->d_fixed, S.vecs,
+                                                     w.st, w.partC());
+    launched(2);
+    TB_CHECK_LAUNCH();
+    TB_CUDA(cudaMemcpyAsync(w.h_st, w.st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    TB_CUDA(cudaStreamSynchronize(s));
+    const PcgState& h = *w.h_st;
+    if (!plain) launched((int64_t)((h.iters - it_before + kIters) / kIters) * (kIters + 1));
+    it_before = h.iters;
+    if (h.done == 1) break;
+    if (h.done == 3) {
+      set_error("pCG breakdown after %d iterations: p^T K p <= 0 or non-finite; matrix is not positive definite",
+                h.iters);
+      rc = TB_ERR_INDEFINITE;
+      break;
+    }
+    if (best_rr >= 0.0 && h.rr > 0.25 * best_rr) ++stalls;
+    else stalls = 0;
+    if (best_rr < 0.0 || h.rr < best_rr) best_rr = h.rr;
+    if (h.iters >= maxit || stalls >= 3 || restart >= 64) {
+      set_error("pCG did not reach rtol=%g in %d iterations (relative residual %.3e)", rtol, h.iters,
+                sqrt(h.rr / (h.bb > 0 ? h.bb : 1.0)));
+      rc = TB_ERR_NOT_CONVERGED;
+      break;
+    }
+    // not converged on the true residual: the restart kernel left done = 0 and cg_init = 1
+  }
+  const PcgState& h = *w.h_st;
+  if (iters) *iters = h.iters;
+  if (relres) *relres = (h.bb > 0.0) ? sqrt(h.rr / h.bb) : 0.0;
+  k_sweep_unpitch<<<kUpdateBlocks, kBlock, 0, s>>>(P->g, P->n_dofs, S.vecs.pitch, S.vecs.x, x_out);
+  launched(1);
+  TB_CHECK_LAUNCH();
+  return rc;
+}
+
+// per-launch CUDA-event time of the sweep (iterations kept live with rtol = 0)
+int pcg_profile_sweep(tb_plan_impl* P, const double* b, int nrep, double* ms_iter, cudaStream_t s) {
+  TB_TRY(sweep_init(P));
+  PcgWork& w = P->work;
+  TB_TRY(sweep_start(P, b, 0.0, 0x7fffffff, s));
+  launch_iter(P, 0, s);  // start sweep
+  launched(1);
+  cudaEvent_t ev[2];
+  for (auto& e : ev) TB_CUDA(cudaEventCreate(&e));
+  double tot = 0.0;
+  for (int it = 0; it < nrep; ++it) {
+    cudaEventRecord(ev[0], s);
+    launch_iter(P, (it + 1) & 1, s);
+    cudaEventRecord(ev[1], s);
+    launched(1);
+    TB_CUDA(cudaEventSynchronize(ev[1]));
+    float a = 0.f;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    tot += a;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  TB_CUDA(cudaMemcpy(w.h_st, w.st, sizeof(PcgState), cudaMemcpyDeviceToHost));
+  if (w.h_st->done != 0) {
+    set_error("profile run stopped early (state %d after %d iterations)", w.h_st->done, w.h_st->iters);
+    return TB_ERR_INVALID;
+  }
+  *ms_iter = tot / nrep;
+  return TB_OK;
+}
+
+}  // namespace tb

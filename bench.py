@@ -460,9 +460,12 @@ def pcg_path(_lib, plan):
 
 
 def rom_profile(_lib, rom, basis, rhos, pk, torch):
-    """Dominant work of the ROM step: Phi^T K(rho) Phi for a batch of designs
-    (tb_rom_reduced_stiffness), CUDA events around the call on the current stream.
-    Algorithmic bytes: Phi streamed once per batch (8 N_u k) + rho of each design."""
+    """Dominant kernel of the ROM step: Phi^T K(rho_d) Phi for all designs of the batch
+    (tb_rom_reduced_stiffness -> k_rom_fused on Hex8 plans), CUDA events around the call on the
+    current stream.  Fused path: tensor-bound, executed DMMA flops from tb_rom_fused_info against
+    the cuBLAS DGEMM throughput measured in this run; else: Phi streamed once, against HBM."""
+    import ctypes
+
     m = rom.mesh
     k = basis.size
     nd = rhos.shape[0]
@@ -477,13 +480,22 @@ def rom_profile(_lib, rom, basis, rhos, pk, torch):
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) * 1e-3)
     t = statistics.median(ts)
-    fn = getattr(_lib.lib(), "tb_rom_fused_info", None)
+    fl = ctypes.c_double(0.0)
+    fused = _lib.lib().tb_rom_fused_info(rom._plan, k, nd, ctypes.byref(fl)) == 1
+    if fused:
+        tf = fl.value / t / 1e12
+        return {"kernel": "k_rom_fused<64> (element form: S_e = C_e^T C_e on DMMA m8n8k4 f64, weighted into all designs "
+                          "by DMMA; warp-specialised producers stream Phi with cp.async.bulk)",
+                "bound": "tensor", "achieved": tf, "peak": pk.get("fp64_tflops"), "unit": "TFLOP/s", "us": t * 1e6,
+                "flops": fl.value, "launches_per_step": 1,
+                "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64 figure)",
+                "note": (f"one call = K_hat for all {nd} designs (+ a 2 us partial reduction); executed tensor flops per "
+                         f"element and 8x8 tile: 5 DMMA (S) + ceil(nd/8) * 8 / 4 DMMA (weighting)")}
     by = 8 * (m.n_dofs * k + nd * m.n_elems)
-    return {"kernel": "tb_rom_reduced_stiffness (all designs of the step)" if fn is None else "k_rom_fused",
+    return {"kernel": "tb_rom_reduced_stiffness (all designs of the step)",
             "bound": "hbm", "achieved": by / t / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s", "us": t * 1e6,
             "bytes": by, "launches_per_step": 1, "peak_source": peak_source(pk),
-            "note": (f"one call = Phi^T K(rho_d) Phi for all {nd} designs; algorithmic bytes = Phi once + rho_d "
-                     f"(SURVEY §7.1 tile-local assembly: Phi is the only large operand)")}
+            "note": f"one call = Phi^T K(rho_d) Phi for all {nd} designs; algorithmic bytes = Phi once + rho_d"}
 
 
 def roofline_3d(tb, _lib, solver, rho_d, pk, torch):

@@ -103,6 +103,11 @@ int tb_pcg_kernel_time(tb_plan* plan, float* ms, int* launches);
  * iteration (2D / multigrid / distributed), -1 = null plan.  Replaces nothing in the reference
  * (diagnostic; the reference solve is fem.py:270-349). */
 int tb_pcg_path(tb_plan* plan);
+/* Diagnostics: 1 when tb_rom_reduced_stiffness(plan, ., k, ., nd, ...) runs the fused
+ * element-form kernel (Hex8 plans, even k <= 64: S_e = C_e^T C_e on FP64 tensor cores, weighted
+ * into all nd designs in one pass over Phi), with the tensor flops it executes in *flops; 0
+ * otherwise.  The reference computes the same sum in rom.py:254-262. */
+int tb_rom_fused_info(tb_plan* plan, int k, int nd, double* flops);
 /* Diagnostics: per-phase %globaltimer sums (ns) of the persistent 2D multigrid pCG kernel in a
  * build with -DTB_MGP_PROF (tools/build_prof.sh); zeros in the product build.  Reads and clears
  * 32 counters into a HOST array. */

@@ -116,4 +116,11 @@ int pcg_solve_sweep(tb_plan_impl* P, const double* b, double* x_out, double rtol
                     double* relres, cudaStream_t s);
 int pcg_profile_sweep(tb_plan_impl* P, const double* b, int nrep, double* ms_iter, cudaStream_t s);
 
+// element-form reduced stiffness on DMMA for Hex8 plans (romfused.cu)
+bool rom_fused_eligible(const tb_plan_impl* P, int k);
+double rom_fused_flops(const tb_plan_impl* P, int k, int nd);
+size_t rom_fused_scratch_bytes(const tb_plan_impl* P, int k, int nd);
+int rom_fused_khat(tb_plan_impl* P, const double* phi, int k, const double* alpha, int nd, int kb0, int kb1,
+                   double* part_scratch, size_t part_bytes, double* khat, cudaStream_t s);
+
 }  // namespace tb

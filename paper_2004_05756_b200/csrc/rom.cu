@@ -436,6 +436,52 @@ __global__ void __launch_bounds__(kBlock) k_reconstruct(int64_t n, int k, const 
   }
 }
 
+// Same product on FP64 tensor cores: U^T (n x nd) = Phi (n x k) Uhat^T (k x nd) as m8n8k4 DMMA
+// tiles -- a warp per 8 rows of Phi, the nd <= 16 designs as two 8-wide n-tiles whose B
+// fragments (Uhat) stay in registers for the whole kernel.  Phi is streamed once.
+__global__ void __launch_bounds__(kBlock) k_reconstruct_dmma(int64_t n, int k, const double* __restrict__ phi,
+                                                             const double* __restrict__ uhat, int nd,
+                                                             double* __restrict__ u) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  constexpr int kSteps = 16;  // k <= 64
+  double b[2][kSteps];
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int st = 0; st < kSteps; ++st) {
+      const int d = 8 * t + (lane >> 2), j = 4 * st + (lane & 3);
+      b[t][st] = (d < nd && j < k) ? uhat[(int64_t)d * k + j] : 0.0;
+    }
+  const int nsteps = (k + 3) / 4;
+  for (int64_t i0 = warp * 8; i0 < n; i0 += nwarps * 8) {
+    const int64_t row = i0 + (lane >> 2);
+    const double* pr = phi + row * k;
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int st = 0; st < kSteps; ++st) {
+      if (st < nsteps) {
+        const int j = 4 * st + (lane & 3);
+        const double a = (row < n && j < k) ? __ldg(pr + j) : 0.0;
+        dmma_8x8x4(acc[0], a, b[0][st]);
+        dmma_8x8x4(acc[1], a, b[1][st]);
+      }
+    }
+    // thread holds U^T[row i0 + lane/4][design 8t + 2(lane%4) + h]
+    const int64_t ri = i0 + (lane >> 2);
+    if (ri < n) {
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int d = 8 * t + 2 * (lane & 3) + h;
+          if (d < nd) u[(int64_t)d * n + ri] = acc[t][h];
+        }
+    }
+  }
+}
+
 // block partials of || mask * (y - g) ||^2
 __global__ void __launch_bounds__(kBlock) k_resid_part(int64_t n, const double* __restrict__ y,
                                                        const double* __restrict__ g, const uint8_t* __restrict__ fixed,
@@ -540,6 +586,16 @@ int tb_rom_reduced_stiffness(tb_plan* plan, const double* phi, int k, const doub
   const int64_t r0 = (int64_t)P->own_k0 * pd;
   const int64_t r1 = P->own_k1 >= g.nnz ? n : (int64_t)P->own_k1 * pd;
   const bool hex8 = (g.dim == 3 && P->hex8);
+  if (hex8 && rom_fused_eligible(P, k)) {
+    // element form, all designs per pass over Phi (romfused.cu); owned element planes of a slab
+    const int kb0 = P->own_k0, kb1 = P->own_k1 < g.nz ? P->own_k1 : g.nz;
+    const size_t na = ((size_t)nd * g.n_elems + 31) / 32 * 32;  // partials start 256-byte aligned
+    const size_t pbytes = rom_fused_scratch_bytes(P, k, nd);
+    TB_TRY(P->rom_scratch(sizeof(double) * na + pbytes));
+    double* al = P->d_rom;
+    for (int d = 0; d < nd; ++d) TB_TRY(P->material(rho + (int64_t)d * g.n_elems, al + (int64_t)d * g.n_elems, nullptr, s));
+    return rom_fused_khat(P, phi, k, al, nd, kb0, kb1, P->d_rom + na, pbytes, khat, s);
+  }
   // 3D: one WHT Hex8 launch per column on a column-major copy of Phi; 2D: node-owner over
   // all k columns of the row-major Phi
   const int nbc = hex8 ? 148 * kCmCtas : nb;        // column-major DMMA: one wave of resident CTAs
@@ -625,7 +681,10 @@ int tb_rom_reconstruct(int64_t n, const double* phi, int k, const double* uhat, 
   TB_GUARD(phi && uhat && u && n >= 1, "bad arguments");
   TB_GUARD(k >= 1 && nd >= 1 && nd <= kMaxVec, "bad sizes k=%d nd=%d", k, nd);
   cudaStream_t s = (cudaStream_t)stream;
-  { k_reconstruct<<<148 * 8, kBlock, sizeof(double) * nd * k, s>>>(n, k, phi, uhat, nd, u); tb::launched(); }
+  if (k <= 64)
+    { k_reconstruct_dmma<<<148 * 8, kBlock, 0, s>>>(n, k, phi, uhat, nd, u); tb::launched(); }
+  else
+    { k_reconstruct<<<148 * 8, kBlock, sizeof(double) * nd * k, s>>>(n, k, phi, uhat, nd, u); tb::launched(); }
   TB_CHECK_LAUNCH();
   return TB_OK;
 }

@@ -1,4 +1,5 @@
-"""One cfg-5 reduced-stiffness evaluation (k = 64, one design) for ncu launch lists."""
+"""cfg 5: build the k = 64 basis and run the 16-design ROM step (solve_batch) NREP times --
+for ncu launch lists / captures of k_rom_fused."""
 import os
 import sys
 
@@ -9,17 +10,19 @@ import torch  # noqa: E402
 import paper_2004_05756_b200 as tb  # noqa: E402
 from paper_2004_05756_b200 import configs  # noqa: E402
 
-scale = sys.argv[1] if len(sys.argv) > 1 else "full"
-prob = configs.cfg5(n_designs=2) if scale == "full" else configs.cfg5(nx=64, ny=32, nz=32, n_designs=2)
+dev = torch.device("cuda", 0)
+prob = configs.cfg5()
 m = prob.mesh
 s = tb.HdmSolver(m, prob.k_e, tb.HelmholtzFilter(m, prob.radius), prob.f, prob.fixed,
                  tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP))
-dev = torch.device("cuda", 0)
-phi = torch.linalg.qr(torch.randn(m.n_dofs, 64, dtype=torch.float64, device=dev))[0].contiguous()
+cols = configs.phi_columns(m, prob.rom_k, seed=0, xp=torch, device=dev)
+cols[:, torch.as_tensor(~s.free_mask, device=dev)] = 0.0
+phi = tb.gram_schmidt(list(cols))
+del cols
 basis = tb.ReducedBasis(phi, None, None, phi.T @ s._f_d)
-rho = torch.as_tensor(np.stack(prob.rom_designs), device=dev)
 rom = tb.RomModel(s)
-for _ in range(2):
-    kh = rom.reduced_stiffness_device(basis, rho[0])
+rhos = torch.as_tensor(np.stack(prob.rom_designs), device=dev)
+for _ in range(int(os.environ.get("NREP", "2"))):
+    khat, uhat, norms = rom.solve_batch(basis, rhos)
 torch.cuda.synchronize()
-print("khat norm", float(torch.linalg.norm(kh)))
+print("norm0", norms[0])

@@ -180,6 +180,13 @@ def require_cuda(device=None):
     return t.device("cuda", t.cuda.current_device() if device is None else int(device))
 
 
+def mesh_dims(mesh):
+    """(dim, nz) of a mesh: this package's StructuredMesh carries both; the reference's 2D
+    romtopt.fem.StructuredMesh (fem.py:154-212) has neither (dim 2, nz 0) -- so the drop-in
+    classes accept the reference's own meshes."""
+    return int(getattr(mesh, "dim", 2)), int(getattr(mesh, "nz", 0) or 0)
+
+
 def stream_ptr(device) -> P:
     t = torch()
     return P(t.cuda.current_stream(device).cuda_stream)

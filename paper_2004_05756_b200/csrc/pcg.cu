@@ -343,7 +343,7 @@ static int run_loop_plain(const PcgOp& op, PcgWork& w, cudaStream_t s) {
 
 // pCG with a general SPD preconditioner (multigrid V-cycle); one iteration per graph body.
 static int pcg_solve_pc(const PcgOp& op, PcgWork& w, const double* b, double* x_out, double rtol, int maxit,
-                        int* iters, double* relres, cudaStream_t s) {
+                        int* iters, double* relres, cudaStream_t s, double accept) {
   const bool plain = no_graph();
   if (!plain && !w.exec_pc) TB_TRY(build_graph_pc(op, w));
   const int nb = kUpdateBlocks;
@@ -401,6 +401,7 @@ static int pcg_solve_pc(const PcgOp& op, PcgWork& w, const double* b, double* x_
     if (best_rr >= 0.0 && h.rr > 0.25 * best_rr) ++stalls;
     else stalls = 0;
     if (best_rr < 0.0 || h.rr < best_rr) best_rr = h.rr;
+    if (stalls >= 3 && accept > 0.0 && h.rr <= accept * accept * h.bb) break;  // round-off mode: at the floor
     if (h.done == 2 || h.iters >= maxit || stalls >= 3 || restart >= 64) {
       set_error("preconditioned pCG did not reach rtol=%g in %d iterations (relative residual %.3e)", rtol, h.iters,
                 sqrt(h.rr / (h.bb > 0 ? h.bb : 1.0)));
@@ -415,13 +416,20 @@ static int pcg_solve_pc(const PcgOp& op, PcgWork& w, const double* b, double* x_
   return rc;
 }
 
+// rtol < 0 selects round-off mode (include/topo_b200.h): target |rtol|, and a solve whose true
+// residual stagnates at or below 100 |rtol| (restarts stop paying off) counts as converged.
 int pcg_solve(const PcgOp& op, PcgWork& w, const double* b, double* x_out, double rtol, int maxit, int* iters,
               double* relres, cudaStream_t s) {
+  double accept = 0.0;
+  if (rtol < 0.0) {
+    rtol = -rtol;
+    accept = 100.0 * rtol;
+  }
   if (!(rtol > 0.0) || maxit < 1) {
-    set_error("pcg: rtol must be > 0 and maxit >= 1 (got %g, %d)", rtol, maxit);
+    set_error("pcg: rtol must be nonzero and maxit >= 1 (got %g, %d)", rtol, maxit);
     return TB_ERR_INVALID;
   }
-  if (op.has_precond()) return pcg_solve_pc(op, w, b, x_out, rtol, maxit, iters, relres, s);
+  if (op.has_precond()) return pcg_solve_pc(op, w, b, x_out, rtol, maxit, iters, relres, s, accept);
   const bool plain = no_graph();
   const bool persistent = !plain && op.has_persistent();
   if (!plain && !persistent && !w.exec) TB_TRY(build_graph(op, w));
@@ -466,6 +474,7 @@ int pcg_solve(const PcgOp& op, PcgWork& w, const double* b, double* x_out, doubl
     if (best_rr >= 0.0 && h.rr > 0.25 * best_rr) ++stalls;
     else stalls = 0;
     if (best_rr < 0.0 || h.rr < best_rr) best_rr = h.rr;
+    if (stalls >= 3 && accept > 0.0 && h.rr <= accept * accept * h.bb) break;  // round-off mode: at the floor
     if (h.done == 2 || h.iters >= maxit || stalls >= 3 || restart >= 64) {
       set_error("pCG did not reach rtol=%g in %d iterations (relative residual %.3e)", rtol, h.iters,
                 sqrt(h.rr / (h.bb > 0 ? h.bb : 1.0)));

@@ -664,8 +664,13 @@ static int sweep_start(tb_plan_impl* P, const double* b, double rtol, int maxit,
 
 int pcg_solve_sweep(tb_plan_impl* P, const double* b, double* x_out, double rtol, int maxit, int* iters,
                     double* relres, cudaStream_t s) {
+  double accept = 0.0;  // round-off mode (rtol < 0), as pcg_solve
+  if (rtol < 0.0) {
+    rtol = -rtol;
+    accept = 100.0 * rtol;
+  }
   if (!(rtol > 0.0) || maxit < 1) {
-    set_error("pcg: rtol must be > 0 and maxit >= 1 (got %g, %d)", rtol, maxit);
+    set_error("pcg: rtol must be nonzero and maxit >= 1 (got %g, %d)", rtol, maxit);
     return TB_ERR_INVALID;
   }
   TB_TRY(sweep_init(P));
@@ -710,6 +715,7 @@ int pcg_solve_sweep(tb_plan_impl* P, const double* b, double* x_out, double rtol
     if (best_rr >= 0.0 && h.rr > 0.25 * best_rr) ++stalls;
     else stalls = 0;
     if (best_rr < 0.0 || h.rr < best_rr) best_rr = h.rr;
+    if (stalls >= 3 && accept > 0.0 && h.rr <= accept * accept * h.bb) break;  // round-off mode: at the floor
     if (h.iters >= maxit || stalls >= 3 || restart >= 64) {
       set_error("pCG did not reach rtol=%g in %d iterations (relative residual %.3e)", rtol, h.iters,
                 sqrt(h.rr / (h.bb > 0 ? h.bb : 1.0)));

@@ -35,24 +35,27 @@ class FilterResult:
 class HelmholtzFilter:
     """Design-density filter of radius ``R`` on a structured mesh (2D Q4 or 3D Hex8).
 
-    ``rtol`` is the relative residual at which the inner pCG stops (the reference factorises
-    H once and solves directly; 1e-13 keeps the result within round-off of that).
+    ``rtol`` is the relative residual at which the inner pCG stops.  The reference factorises H
+    once and solves directly, so the default (None) solves to round-off: target 1e-15, a
+    stagnating true residual <= 1e-13 accepted (tb_filter_apply round-off mode).  Filtered
+    densities then agree with the direct solve to ~1e-16, which finite differences of J need.
     """
 
-    def __init__(self, mesh: StructuredMesh, radius: float, rtol: float = 1e-13, device=None):
+    def __init__(self, mesh: StructuredMesh, radius: float, rtol: float | None = None, device=None):
         if radius < 0.0:
             raise ValueError(f"filter radius must be nonnegative, got {radius}")
         self.mesh = mesh
         self.radius = float(radius)
         self.r = LENGTH_SCALE_FACTOR * self.radius
-        self.rtol = float(rtol)
-        self.nodes_per_elem = 2**mesh.dim
+        self.rtol = -1e-15 if rtol is None else float(rtol)  # negative: round-off mode (C ABI)
+        dim, nz = _lib.mesh_dims(mesh)
+        self.nodes_per_elem = 2**dim
         # b_e = M_e 1 = (h^d / 2^d) per node (filtering.py:60-61, 75-76)
         self.b_e = np.full(self.nodes_per_elem, mesh.elem_volume / self.nodes_per_elem)
         self.device = _lib.require_cuda(device)
         self.last_iters = 0
         h = ctypes.c_void_p()
-        _lib.check(_lib.lib().tb_filter_create(mesh.dim, mesh.nx, mesh.ny, mesh.nz, mesh.h, self.radius,
+        _lib.check(_lib.lib().tb_filter_create(dim, mesh.nx, mesh.ny, nz, mesh.h, self.radius,
                                                self.device.index, ctypes.byref(h)), "HelmholtzFilter")
         self._h = h
 
@@ -131,7 +134,8 @@ class ConeFilter:
         self.device = _lib.require_cuda(device)
         self.last_iters = 0
         h = ctypes.c_void_p()
-        _lib.check(_lib.lib().tb_cone_create(mesh.dim, mesh.nx, mesh.ny, mesh.nz, mesh.h, self.radius,
+        dim, nz = _lib.mesh_dims(mesh)
+        _lib.check(_lib.lib().tb_cone_create(dim, mesh.nx, mesh.ny, nz, mesh.h, self.radius,
                                              self.device.index, ctypes.byref(h)), "ConeFilter")
         self._h = h
 

@@ -35,6 +35,9 @@ __all__ = [
 ]
 
 
+ROUNDOFF_RTOL = -1e-12  # tb_pcg_solve round-off mode: target 1e-12, stagnation <= 1e-10 accepted
+
+
 class StaleSolutionError(RuntimeError):
     """A solution object was paired with a design it was not computed from (hdm.py:32-33)."""
 
@@ -139,28 +142,34 @@ class HdmSolution:
 class HdmSolver:
     """Full-order objective and adjoint gradient on one GPU (hdm.py:112-233).
 
-    Extra keyword arguments: ``rtol`` (pCG true-residual tolerance, BASELINE cfg 1-2: 1e-10),
+    Extra keyword arguments: ``rtol`` (pCG true-residual tolerance; the default None solves to
+    round-off like the reference's direct solve -- target 1e-12, a stagnating true residual
+    <= 1e-10 accepted -- which the reference's finite-difference gradient tests need; the
+    BASELINE configs pass their own strict rtol: 1e-10 for cfg 1-2, 1e-8 for cfg 3-5),
     ``maxit``, ``device`` and ``preconditioner`` ("jacobi", the BASELINE design, or "mg":
     geometric multigrid with Galerkin coarse operators).
     """
 
     def __init__(self, mesh: StructuredMesh, k_e, filt: HelmholtzFilter, f, fixed_dofs,
                  material: MaterialModel | None = None, stats: RunStats | None = None,
-                 rtol: float = 1e-10, maxit: int = 200000, device=None, preconditioner: str = "jacobi"):
+                 rtol: float | None = None, maxit: int = 200000, device=None, preconditioner: str = "jacobi"):
         self.mesh = mesh
         self.k_e = np.asarray(k_e, dtype=float)
         self.filter = filt
         self.fixed_dofs = np.asarray(fixed_dofs, dtype=np.int64)
         self.material = material or MaterialModel()
         self.stats = stats or RunStats()
-        self.rtol, self.maxit = float(rtol), int(maxit)
+        # rtol None: round-off mode, passed to the C ABI as a negative tolerance
+        self.rtol = ROUNDOFF_RTOL if rtol is None else float(rtol)
+        self.maxit = int(maxit)
         f = np.asarray(f.detach().cpu().numpy() if _lib.is_torch(f) else f, dtype=float).copy()
         f[self.fixed_dofs] = 0.0  # loads on constrained dofs go into reactions (hdm.py:136-137)
         self.f = f
         free_mask = np.ones(mesh.n_dofs, dtype=bool)
         free_mask[self.fixed_dofs] = False
         self.free_mask = free_mask
-        nde = (2**mesh.dim) * mesh.dim
+        dim, nz = _lib.mesh_dims(mesh)
+        nde = (2**dim) * dim
         if self.k_e.shape != (nde, nde):
             raise ValueError(f"element matrix must be {(nde, nde)}, got {self.k_e.shape}")
         self.device = filt.device if device is None else _lib.require_cuda(device)
@@ -168,7 +177,7 @@ class HdmSolver:
         ke = np.ascontiguousarray(self.k_e)
         h = ctypes.c_void_p()
         _lib.check(_lib.lib().tb_plan_create(
-            mesh.dim, mesh.nx, mesh.ny, mesh.nz, mesh.h, ke.ctypes.data_as(ctypes.c_void_p),
+            dim, mesh.nx, mesh.ny, nz, mesh.h, ke.ctypes.data_as(ctypes.c_void_p),
             self.material.rho_l, self.material.p, fixed_u8.ctypes.data_as(ctypes.c_void_p),
             self.device.index, ctypes.byref(h)), "HdmSolver")
         self._plan = h

@@ -36,8 +36,8 @@ class HelmholtzFilter:
     """Design-density filter of radius ``R`` on a structured mesh (2D Q4 or 3D Hex8).
 
     ``rtol`` is the relative residual at which the inner pCG stops.  The reference factorises H
-    once and solves directly, so the default (None) solves to round-off: target 1e-15, a
-    stagnating true residual <= 1e-13 accepted (tb_filter_apply round-off mode).  Filtered
+    once and solves directly, so the default (None) solves to round-off: target 1e-15, a true
+    residual stagnating at its floor accepted (tb_filter_apply round-off mode).  Filtered
     densities then agree with the direct solve to ~1e-16, which finite differences of J need.
     """
 

@@ -796,25 +796,50 @@ def rom_khat_ms(tb, configs, prob, dev, torch):
 
 
 def cfg4_extra(args, dev, dist, world, rank, pk, want_cpu):
-    """BASELINE cfg 4 (43M DOF Hex8) evaluated once, slab-sharded over ALL ranks of this run
-    (strong scaling when the driver runs N > 1)."""
+    """BASELINE cfg 4 (43M DOF Hex8), one design evaluation.  N = 1: the single-GPU HdmSolver
+    (Jacobi: the single-sweep TMA pCG; also the multigrid-preconditioned solve).
+    N > 1: slab-sharded over ALL ranks of this run (slab_evaluate; strong scaling)."""
     import torch
 
     import paper_2004_05756_b200 as tb
-    from paper_2004_05756_b200 import configs
-    from paper_2004_05756_b200.slab import LocalComm, SlabFilter, SlabSolver, TorchComm, partition, slab_evaluate
+    from paper_2004_05756_b200 import _lib, configs
+    from paper_2004_05756_b200.slab import SlabFilter, SlabSolver, TorchComm, partition, slab_evaluate
 
     prob = configs.cfg4(seed=args.seed)
+    m = prob.mesh
+    by_it = 8 * (9 * m.n_dofs + m.n_elems)
+    if world == 1:
+        s = make_solver(tb, configs, prob, "jacobi")
+        obj = tb.ComplianceObjective(s.f)
+        psi_d = torch.as_tensor(prob.psi, device=dev)
+        ms, iters, sol = time_steps(s, obj, psi_d, torch, 1, 1)
+        rho_d, _ = s.filtered_density_device(psi_d)
+        roof = roofline_3d(tb, _lib, s, rho_d, pk, torch)
+        out = {"workload": workload_desc(prob, "jacobi"), "value": ms[0] * 1e-3, "unit": UNIT, "n_gpus": 1,
+               "scaling": "strong", "pcg_iterations": iters[0], "J": sol.j, "roofline": roof,
+               "path": "single-GPU HdmSolver (no slabs at N = 1)"}
+        del s, sol, rho_d
+        torch.cuda.empty_cache()
+        smg = make_solver(tb, configs, prob, "mg")
+        objm = tb.ComplianceObjective(smg.f)
+        msm, itm, solm = time_steps(smg, objm, psi_d, torch, 2, 1)
+        out["mg"] = {"workload": workload_desc(prob, "mg"), "value": statistics.median(msm) * 1e-3, "unit": UNIT,
+                     "pcg_iterations": itm[-1], "J": solm.j,
+                     "J_rel_vs_jacobi": abs(solm.j - out["J"]) / abs(out["J"])}
+        del smg, solm
+        torch.cuda.empty_cache()
+        if want_cpu:
+            out["cpu_baseline"] = cpu_cfg4(prob, out["pcg_iterations"], [21, 20])
+        return out
     mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
-    slab = partition(prob.mesh.nz, world)[rank]
-    sv = SlabSolver(prob.mesh, prob.k_e, prob.f, prob.fixed, mat, slab, device=dev)
-    fl = SlabFilter(prob.mesh, prob.radius, slab, device=dev)
+    slab = partition(m.nz, world)[rank]
+    sv = SlabSolver(m, prob.k_e, prob.f, prob.fixed, mat, slab, device=dev)
+    fl = SlabFilter(m, prob.radius, slab, device=dev)
     psi = torch.as_tensor(sv.local_elems(prob.psi).copy(), device=dev)
-    comm = TorchComm(peer=True) if dist else LocalComm()
+    comm = TorchComm(peer=True)
     ev = slab_evaluate([sv], [fl], comm, [psi], rtol=prob.rtol)  # warm-up
     del ev
-    if dist:
-        dist.barrier()
+    dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -822,27 +847,23 @@ def cfg4_extra(args, dev, dist, world, rank, pk, want_cpu):
     e1.record()
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64, device=dev)
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    m = prob.mesh
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_eval = float(t.item())
     per_it = t_eval / max(ev.iterations, 1)
-    by_it = 8 * (9 * m.n_dofs + m.n_elems)
     out = {"workload": f"cfg4 {m.nx}x{m.ny}x{m.nz} Hex8, {m.n_dofs} DOF: filter R={prob.radius:g} + Jacobi-pCG "
                        f"{prob.rtol:g} + compliance + sensitivities + adjoint, z-slabs x{world}",
            "value": t_eval, "unit": UNIT, "n_gpus": world, "scaling": "strong", "pcg_iterations": ev.iterations,
            "filter_iterations": list(ev.filter_iterations), "J": ev.j,
-           "halo": ("NVLink peer stores (CUDA IPC)" if comm.peer_active else "nccl send/recv") if dist else "none (one slab)",
-           "roofline": {"kernel": "whole Jacobi-pCG iteration (upper bound: evaluation time / iterations)", "bound": "hbm",
-                        "achieved": by_it / per_it / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                        "frac": by_it / per_it / 1e9 / pk["hbm_gbs"], "traffic": None,
-                        "bytes_per_iteration": by_it, "us_per_iteration_upper_bound": per_it * 1e6,
+           "halo": "NVLink peer stores (CUDA IPC)" if comm.peer_active else "nccl send/recv",
+           "allreduces_per_iteration": getattr(comm, "allreduces", 0) / max(ev.iterations, 1),
+           "roofline": {"kernel": "whole Jacobi-pCG iteration (upper bound: evaluation time / iterations)",
+                        "bound": "hbm", "achieved": by_it / world / per_it / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                        "frac": by_it / world / per_it / 1e9 / pk["hbm_gbs"], "traffic": None,
+                        "bytes_per_iteration_per_rank": by_it / world, "us_per_iteration_upper_bound": per_it * 1e6,
                         "peak_source": peak_source(pk),
-                        "note": "SURVEY §8(d) bytes 8(9 N_u + N_e) per iteration; filter/sensitivity time included"}}
+                        "note": "SURVEY §8(d) bytes 8(9 N_u + N_e) per iteration / N; filter and sensitivities included"}}
     del ev, sv, fl, psi
     torch.cuda.empty_cache()
-    if want_cpu:
-        out["cpu_baseline"] = cpu_cfg4(prob, out["pcg_iterations"], out["filter_iterations"])
     return out
 
 
@@ -985,7 +1006,7 @@ def run_cfg4(args):
             "ms_per_step": out["value"] * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded cfg 4 recipe)",
             "config": {"workload": out["workload"], "parallelism": f"slab{world}", "halo": args.halo,
-                       "pcg_iterations": out["pcg_iterations"], "filter_iterations": out["filter_iterations"],
+                       "pcg_iterations": out["pcg_iterations"], "filter_iterations": out.get("filter_iterations"),
                        "J": out["J"], "seed": args.seed},
             "roofline": out["roofline"], "cpu_baseline": out.get("cpu_baseline"),
             "gpu_launches": int(launches), "clocks": clk}), flush=True)

@@ -126,7 +126,12 @@ int tb_plan_set_owned_planes(tb_plan* plan, int k0, int k1);
  * rtol, maxit; publishes local r.z, r.r), 1 finish init (after the host allreduce), 2 operator
  * (publishes local p.q; `parity` = iteration index), 3 alpha (after allreduce), 4 update
  * (publishes local r.z, r.r), 5 beta/convergence (after allreduce).  Between phases the caller
- * allreduces the 4-double `red` buffer and, after phase 4, refreshes the ghost planes of z. */
+ * allreduces the 4-double `red` buffer and, after phase 4, refreshes the ghost planes of z.
+ * Single-reduction form (Chronopoulos-Gear, Hex8 plans): 10 init (needs rho, b, rtol, maxit;
+ * u = D^-1 r in the z buffer, publishes local r.u, r.r), 13 update (p, s, x, r, u; publishes
+ * local r.u, r.r), 11 operator (w = K u; publishes local w.u), 12 scalars (after the allreduce).
+ * Iteration: 13 -> z halo -> 11 -> ONE allreduce of red[0..2] -> 12; start: 10 -> halo -> 11 ->
+ * allreduce -> 12.  Replaces the two per-iteration reductions of phases 2-5. */
 int tb_pcg_dist_phase(tb_plan* plan, int phase, const double* rho, const double* b, double rtol,
                       int maxit, int parity, void* stream);
 /* Device pointers of this rank's solution x, preconditioned residual z and reduction buffer. */

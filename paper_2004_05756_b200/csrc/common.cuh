@@ -72,6 +72,7 @@ struct PcgState {
   double red[4];
   int cg_init;  // single-reduction sweep (sweep.cu): the next sweep is a (re)start sweep
   int pad4;
+  double cg_beta;  // distributed single-reduction pCG (phases 10-13): beta of the p/s recurrences
 };
 
 // ---------------------------------------------------------------------------------------

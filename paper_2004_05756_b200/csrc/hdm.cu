@@ -556,9 +556,10 @@ int tb_pcg_dist_phase(tb_plan* plan, int phase, const double* rho, const double*
   TB_GUARD(plan != nullptr, "null plan");
   auto* P = reinterpret_cast<tb_plan_impl*>(plan);
   cudaStream_t s = (cudaStream_t)stream;
-  if (phase == 0) {
-    TB_GUARD(rho && b, "phase 0 needs rho and b");
+  if (phase == 0 || phase == 10) {
+    TB_GUARD(rho && b, "phase %d needs rho and b", phase);
     TB_GUARD(rtol > 0.0 && maxit >= 1, "rtol must be > 0 and maxit >= 1");
+    TB_GUARD(phase == 0 || (P->g.dim == 3 && P->hex8), "single-reduction phases need a Hex8 plan");
     if (!P->dist) {
       P->dist = 1;
       TB_TRY(P->work.set_fields(1, P->own_k0, P->own_k1));

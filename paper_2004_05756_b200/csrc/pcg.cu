@@ -707,6 +707,135 @@ __global__ void __launch_bounds__(kBlock) k_dist_update(HaloPush hp, const doubl
   }
 }
 
+// ---- distributed single-reduction pCG (Chronopoulos-Gear; phases 10-13) ----------------
+// Vectors: u = D^-1 r lives in w.z (so the halo machinery of z -- copies or IPC peer pushes --
+// carries it unchanged), w = K u in w.q, p in w.pa, s in w.tmp, scratch w.pb.  One iteration:
+//   13 update (p, s, x, r, u on owned dofs; local g = r.u, r.r; push u) -> halo -> 11 operator
+//   (w = K u, local d = w.u) -> ONE allreduce of (d, g, r.r) -> 12 scalars (alpha, beta, done).
+// phase 10: r = Z b, x = p = s = 0, u = D^-1 r on owned dofs (+ push); local g, r.r
+__global__ void __launch_bounds__(kBlock) k_dist_cg_start(int64_t n, HaloPush hp, const double* __restrict__ b,
+                                                          const double* __restrict__ dinv, double* __restrict__ x,
+                                                          double* __restrict__ r, double* __restrict__ u,
+                                                          double* __restrict__ p, double* __restrict__ sv,
+                                                          double* __restrict__ scratch, PcgState* st,
+                                                          double* partials, double rtol, int maxit) {
+  double acc[2] = {0.0, 0.0};
+  bool pushed = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double di = dinv[i];
+    const double ri = (di != 0.0) ? b[i] : 0.0;
+    x[i] = 0.0;
+    r[i] = ri;
+    p[i] = 0.0;
+    sv[i] = 0.0;
+    scratch[i] = 0.0;
+    if (i >= hp.own0 && i < hp.own1) {
+      const double ui = di * ri;
+      u[i] = ui;
+      pushed |= hp.push(i, ui);
+      acc[0] = fma(ri, ui, acc[0]);
+      acc[1] = fma(ri, ri, acc[1]);
+    }
+  }
+  if (pushed) __threadfence_system();
+  block_sum<2>(acc);
+  if (publish_partials<2>(acc, partials, &st->count_c)) {
+    gather_partials<2>(acc, partials, &st->count_c);
+    if (threadIdx.x == 0) {
+      st->red[1] = acc[0];
+      st->red[2] = acc[1];
+      st->iters = 0;
+      st->maxit = maxit;
+      st->beta = 0.0;  // the fused operator forms p = u + 0 p_old: it applies K to u
+      st->alpha = 0.0;
+      st->cg_beta = 0.0;
+      st->cg_init = 1;
+      st->done = 0;
+      st->pq = rtol;  // stashed until phase 12 has the global ||Z b||
+    }
+  }
+}
+
+// phase 12 (one thread, after the host allreduce of red = (d, g, r.r))
+__global__ void k_dist_cg_scalars(PcgState* st) {
+  if (st->done) return;
+  const double del = st->red[0], gam = st->red[1], rr = st->red[2];
+  st->rr = rr;
+  if (!isfinite(del) || !isfinite(gam) || !isfinite(rr)) {
+    st->done = 3;
+  } else if (st->cg_init) {
+    st->cg_init = 0;
+    st->bb = rr;
+    st->tol2 = st->pq * st->pq * rr;  // rtol stashed by phase 10
+    if (rr == 0.0 || gam == 0.0) {
+      st->done = 1;
+    } else if (!(del > 0.0)) {
+      st->done = 3;
+    } else {
+      st->alpha = gam / del;
+      st->cg_beta = 0.0;
+      st->rz = gam;
+    }
+  } else {
+    const int it = st->iters + 1;
+    st->iters = it;
+    if (rr <= st->tol2) {
+      st->done = 1;
+    } else {
+      const double beta = gam / st->rz;
+      const double den = del - beta * gam / st->alpha;
+      if (!(den > 0.0)) {
+        st->done = 3;
+      } else {
+        st->cg_beta = beta;
+        st->alpha = gam / den;
+        st->rz = gam;
+        if (it >= st->maxit) st->done = 2;
+      }
+    }
+  }
+}
+
+// phase 13: p = u + b p ; s = w + b s ; x += a p ; r -= a s ; u = D^-1 r (owned, free dofs; + push)
+__global__ void __launch_bounds__(kBlock) k_dist_cg_update(HaloPush hp, const double* __restrict__ dinv,
+                                                           const double* __restrict__ w, double* __restrict__ u,
+                                                           double* __restrict__ p, double* __restrict__ sv,
+                                                           double* __restrict__ x, double* __restrict__ r,
+                                                           PcgState* st, double* partials) {
+  if (st->done) return;
+  const double a = st->alpha, bt = st->cg_beta;
+  double acc[2] = {0.0, 0.0};
+  bool pushed = false;
+  for (int64_t i = hp.own0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < hp.own1;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double di = dinv[i];
+    double un = 0.0;
+    if (di != 0.0) {
+      const double pi = fma(bt, p[i], u[i]);
+      const double si = fma(bt, sv[i], w[i]);
+      p[i] = pi;
+      sv[i] = si;
+      x[i] = fma(a, pi, x[i]);
+      const double ri = fma(-a, si, r[i]);
+      r[i] = ri;
+      un = di * ri;
+      acc[0] = fma(ri, un, acc[0]);
+      acc[1] = fma(ri, ri, acc[1]);
+    }
+    u[i] = un;
+    pushed |= hp.push(i, un);
+  }
+  if (pushed) __threadfence_system();
+  block_sum<2>(acc);
+  if (publish_partials<2>(acc, partials, &st->count_b)) {
+    gather_partials<2>(acc, partials, &st->count_b);
+    if (threadIdx.x == 0) {
+      st->red[1] = acc[0];
+      st->red[2] = acc[1];
+    }
+  }
+}
+
 int pcg_dist_phase(const PcgOp& op, PcgWork& w, int phase, const double* b, double rtol, int maxit, int parity,
                    cudaStream_t s) {
   const int nb = kUpdateBlocks;
@@ -739,6 +868,24 @@ int pcg_dist_phase(const PcgOp& op, PcgWork& w, int phase, const double* b, doub
       break;
     case 5:
       k_dist_beta<<<1, 1, 0, s>>>(w.st);
+      launched(1);
+      break;
+    case 10:  // single reduction: init (D^-1, r = Z b, u = D^-1 r, local g and r.r)
+      op.launch_dinv(w.dinv, s);
+      k_dist_cg_start<<<nb, kBlock, 0, s>>>(w.n, hp, b, w.dinv, w.x, w.r, w.z, w.pa, w.tmp, w.pb, w.st, w.partC(),
+                                            rtol, maxit);
+      launched(2);
+      break;
+    case 11:  // w = K u (fused operator with beta = 0: p = u, q = K u) + local d = u.w
+      op.launch_fused(w, w.pb, w.pb, s);
+      launched(1);
+      break;
+    case 12:
+      k_dist_cg_scalars<<<1, 1, 0, s>>>(w.st);
+      launched(1);
+      break;
+    case 13:  // update + local g, r.r (+ halo push of u)
+      k_dist_cg_update<<<kUpdateBlocks, kBlock, 0, s>>>(hp, w.dinv, w.q, w.z, w.pa, w.tmp, w.x, w.r, w.st, w.partB());
       launched(1);
       break;
     default:

@@ -136,6 +136,8 @@ class SlabSolver:
         self.red = t.as_tensor(_CudaArray(pr.value, 4, self.device), device=self.device)
         self.rho = None
         self.rtol, self.maxit = 1e-8, 200000
+        # Chronopoulos-Gear phases 10-13: ONE allreduce per iteration (Hex8 plans)
+        self.single_reduction = True
 
     def __del__(self):
         h = getattr(self, "_plan", None)
@@ -159,8 +161,8 @@ class SlabSolver:
 
     # -- phases (see module docstring)
     def phase(self, p, parity=0):
-        rho = _lib.ptr(self.rho) if p == 0 else _lib.P(0)
-        b = _lib.ptr(self.f) if p == 0 else _lib.P(0)
+        rho = _lib.ptr(self.rho) if p in (0, 10) else _lib.P(0)
+        b = _lib.ptr(self.f) if p in (0, 10) else _lib.P(0)
         _lib.check(_lib.lib().tb_pcg_dist_phase(self._plan, p, rho, b, self.rtol, self.maxit, parity,
                                                 _lib.stream_ptr(self.device)), f"dist phase {p}")
 
@@ -308,6 +310,8 @@ class LocalComm:
 
     def __init__(self, peer: bool = False):
         self.peer = peer
+        self.allreduces = 0  # allreduce steps executed (graph replays counted per captured call)
+        self.capturable = True  # every step is a device op on the current stream
 
     def setup(self, solvers):
         if not self.peer:
@@ -318,6 +322,7 @@ class LocalComm:
             s.set_halo_peers(lo, hi)
 
     def allreduce(self, solvers):
+        self.allreduces += 1
         total = solvers[0].red.clone()
         for s in solvers[1:]:
             total = total + s.red
@@ -359,6 +364,12 @@ class TorchComm:
         self._mapped = []
         self._ready = set()   # solvers whose z halo travels as peer stores
         self._failed = set()  # solvers that fell back to NCCL send/recv
+        self.allreduces = 0   # allreduce steps executed (graph replays counted per captured call)
+
+    # The single-reduction iteration has no collective between the update that pushes u into the
+    # neighbours' ghost planes and the operator that reads them (neighbor_sync orders them with a
+    # one-double P2P token per neighbour), so it runs as an eager host loop here.
+    capturable = False
 
     def setup(self, solvers):
         if not self.peer or id(solvers[0]) in self._ready or id(solvers[0]) in self._failed:
@@ -410,6 +421,7 @@ class TorchComm:
         self._mapped, self._ready, self._failed = [], set(), set()
 
     def allreduce(self, solvers):
+        self.allreduces += 1
         red = solvers[0].red
         if red.is_cuda and self.dist.get_backend(self.group) == "gloo":
             host = red.cpu()  # waits for the phase on the current stream
@@ -417,6 +429,32 @@ class TorchComm:
             red.copy_(host)
         else:
             self.dist.all_reduce(red, group=self.group)
+
+    def neighbor_sync(self, solvers):
+        """Order this rank's peer stores (issued by the kernels before this call on its stream)
+        before the neighbours' next kernels: a one-double send/recv with each neighbour.  NCCL:
+        stream-ordered on both sides.  gloo: the host waits for the stream first.  A no-op unless
+        the z halo travels as peer stores (otherwise halo() moves the planes, which orders them)."""
+        s = solvers[0]
+        if id(s) not in self._ready:
+            return
+        d = self.dist
+        t = _lib.torch()
+        r, n = s.slab.rank, s.slab.nranks
+        gloo = d.get_backend(self.group) == "gloo"
+        if gloo and s.red.is_cuda:
+            t.cuda.current_stream(s.device).synchronize()
+        dev = "cpu" if gloo else s.device
+        send = t.zeros(1, dtype=t.float64, device=dev)
+        recv = [t.empty(1, dtype=t.float64, device=dev) for _ in range(2)]
+        ops = []
+        for k, nb in enumerate((r - 1, r + 1)):
+            if 0 <= nb < n:
+                ops.append(d.P2POp(d.isend, send, nb, self.group))
+                ops.append(d.P2POp(d.irecv, recv[k], nb, self.group))
+        if ops:
+            for req in d.batch_isend_irecv(ops):
+                req.wait()
 
     def reduce_scalars(self, values, op="sum"):
         """values: [floats of this rank's solver] -> the element-wise sum / max over the ranks."""
@@ -447,16 +485,25 @@ class TorchComm:
                 req.wait()
 
 
-def dist_pcg_solve(solvers, comm, rtol=1e-8, maxit=200000, check_every=32):
+def dist_pcg_solve(solvers, comm, rtol=1e-8, maxit=200000, check_every=32, graph=None):
     """Jacobi-pCG over the slabs of ``solvers`` (this process's share).  Returns
     (iterations, recursive relative residual, converged flag).  The host reads the device state
     every ``check_every`` iterations (a pipeline drain each time); phases issued after
-    convergence are no-ops on the device (their kernels return on st->done)."""
+    convergence are no-ops on the device (their kernels return on st->done).
+
+    Solvers with ``single_reduction`` (SlabSolver) run the Chronopoulos-Gear phases 10-13: ONE
+    allreduce of (w.u, r.u, r.r) per iteration.  When every step is a device operation on the
+    current stream (``comm.capturable``: LocalComm, or NCCL with the halo as peer stores) and
+    ``graph`` is not False, ``check_every`` iterations are captured once in a CUDA graph --
+    kernels, collectives and halo -- and the host loop only replays it and reads the state."""
     setup = getattr(comm, "setup", None)
     if setup is not None:
         setup(solvers)
     for s in solvers:
         s.rtol, s.maxit = rtol, maxit
+    if getattr(solvers[0], "single_reduction", False):
+        return _dist_cg1(solvers, comm, maxit, check_every, graph)
+    for s in solvers:
         s.phase(0)
     comm.allreduce(solvers)
     for s in solvers:
@@ -476,13 +523,77 @@ def dist_pcg_solve(solvers, comm, rtol=1e-8, maxit=200000, check_every=32):
         comm.halo(solvers)
         it += 1
         if it % check_every == 0 or it >= maxit:
-            iters, done, rr, bb = solvers[0].state()
-            if done != 0:
-                if done == 3:
-                    from .fem import IndefiniteMatrixError
+            r = _dist_state(solvers)
+            if r is not None:
+                return r
 
-                    raise IndefiniteMatrixError("distributed pCG breakdown")
-                return iters, (rr / bb) ** 0.5 if bb > 0 else 0.0, done == 1
+
+def _dist_state(solvers):
+    iters, done, rr, bb = solvers[0].state()
+    if done == 0:
+        return None
+    if done == 3:
+        from .fem import IndefiniteMatrixError
+
+        raise IndefiniteMatrixError("distributed pCG breakdown")
+    return iters, (rr / bb) ** 0.5 if bb > 0 else 0.0, done == 1
+
+
+def _dist_cg1(solvers, comm, maxit, check_every, graph):
+    """Single-reduction iteration: 13 update -> z halo -> 11 operator -> allreduce -> 12."""
+
+    sync = getattr(comm, "neighbor_sync", None)
+
+    def step():
+        for s in solvers:
+            s.phase(13)
+        comm.halo(solvers)
+        if sync is not None:
+            sync(solvers)  # peer stores of u before the neighbours' operator (no collective)
+        for s in solvers:
+            s.phase(11)
+        comm.allreduce(solvers)
+        for s in solvers:
+            s.phase(12)
+
+    for s in solvers:
+        s.phase(10)
+    comm.halo(solvers)
+    if sync is not None:
+        sync(solvers)
+    for s in solvers:
+        s.phase(11)
+    comm.allreduce(solvers)
+    for s in solvers:
+        s.phase(12)
+    use_graph = graph is not False and getattr(comm, "capturable", False) and solvers[0].red.is_cuda
+    if use_graph:
+        t = _lib.torch()
+        g = t.cuda.CUDAGraph()
+        side = t.cuda.Stream(device=solvers[0].device)
+        side.wait_stream(t.cuda.current_stream(solvers[0].device))
+        before = comm.allreduces
+        with t.cuda.stream(side):
+            with t.cuda.graph(g, stream=side):
+                for _ in range(check_every):
+                    step()
+        captured = comm.allreduces - before
+        comm.allreduces = before  # capture issued nothing; replays are counted below
+    it = 0
+    while True:
+        if use_graph:
+            g.replay()
+            comm.allreduces += captured
+            it += check_every
+        else:
+            for _ in range(check_every):
+                step()
+            it += check_every
+        r = _dist_state(solvers)
+        if r is not None:
+            return r
+        if it >= maxit:
+            return solvers[0].state()[0], 0.0, False
 
 
 @dataclass
@@ -574,7 +685,14 @@ class SlabRom:
             for r in slab_roms:
                 getattr(r, name).copy_(total)
         else:
-            comm.dist.all_reduce(getattr(slab_roms[0], name), group=comm.group)
+            v = getattr(slab_roms[0], name)
+            comm.allreduces += 1
+            if v.is_cuda and comm.dist.get_backend(comm.group) == "gloo":
+                host = v.cpu()  # gloo reduces host tensors; waits for the producing kernels
+                comm.dist.all_reduce(host, group=comm.group)
+                v.copy_(host)
+            else:
+                comm.dist.all_reduce(v, group=comm.group)
 
     def local_khat(self, rho_batch_local):
         t = _lib.torch()

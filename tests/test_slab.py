@@ -51,6 +51,17 @@ class _CpuPcg:
 
     def phase(self, ph, parity=0):
         x, z, red = self.x.numpy(), self.z.numpy(), self.red.numpy()
+        if ph == 10:  # k_dist_cg_start
+            self.K = self._operator()
+            diag = self.K.diagonal()
+            self.dinv = np.where(self.fixed, 0.0, 1.0 / diag)
+            self.r = np.where(self.fixed, 0.0, self.b)
+            x[:] = 0.0
+            z[:] = np.where(self.own, self.dinv * self.r, 0.0)
+            self.pp, self.s, self.w = np.zeros_like(z), np.zeros_like(z), np.zeros_like(z)
+            red[1], red[2] = self.r[self.own] @ z[self.own], self.r[self.own] @ self.r[self.own]
+            self.st = dict(iters=0, done=0, cg_init=True)
+            return
         if ph == 0:
             self.K = self._operator()
             diag = self.K.diagonal()
@@ -91,6 +102,37 @@ class _CpuPcg:
                 st["done"] = 1
             elif st["iters"] >= self.maxit:
                 st["done"] = 2
+        elif ph == 11:  # w = K u, local w.u (k_hex8<true> with beta = 0 in dist mode)
+            self.w = self.K @ z
+            red[0] = self.w[self.own] @ z[self.own]
+        elif ph == 12:  # k_dist_cg_scalars
+            st = self.st
+            dl, gm, rr = red[0], red[1], red[2]
+            st["rr"] = rr
+            if st.pop("cg_init", False):
+                st.update(bb=rr, tol2=self.rtol**2 * rr)
+                if rr == 0 or gm == 0:
+                    st["done"] = 1
+                else:
+                    st.update(alpha=gm / dl, cg_beta=0.0, rz=gm)
+            else:
+                st["iters"] += 1
+                if rr <= st["tol2"]:
+                    st["done"] = 1
+                else:
+                    beta = gm / st["rz"]
+                    st.update(cg_beta=beta, alpha=gm / (dl - beta * gm / st["alpha"]), rz=gm)
+                    if st["iters"] >= self.maxit:
+                        st["done"] = 2
+        elif ph == 13:  # k_dist_cg_update on owned dofs
+            a, b = self.st["alpha"], self.st["cg_beta"]
+            upd = self.own & (self.dinv != 0)
+            self.pp[upd] = z[upd] + b * self.pp[upd]
+            self.s[upd] = self.w[upd] + b * self.s[upd]
+            x[upd] += a * self.pp[upd]
+            self.r[upd] -= a * self.s[upd]
+            z[self.own] = np.where(upd, self.dinv * self.r, 0.0)[self.own]
+            red[1], red[2] = self.r[upd] @ z[upd], self.r[upd] @ self.r[upd]
 
     def state(self):
         s = self.st
@@ -122,6 +164,7 @@ class CpuSlab(_CpuPcg):
         self.rho = torch.as_tensor(self.local_elems(prob.psi).copy())
         self._init_vectors(nl, slab.own_local)
         self.rtol = 1e-8
+        self.single_reduction = True  # phases 10-13, as SlabSolver
 
     def local_elems(self, field):
         return field[self.slab.e0 * self.plane_elems:self.slab.e1 * self.plane_elems]
@@ -206,8 +249,10 @@ def _reference_u(prob):
 def test_driver_local_comm_cpu():
     prob = _problem()
     slabs = [CpuSlab(prob, s) for s in partition(prob.mesh.nz, 3)]
-    it, rel, ok = dist_pcg_solve(slabs, LocalComm(), rtol=1e-12, check_every=1)
+    comm = LocalComm()
+    it, rel, ok = dist_pcg_solve(slabs, comm, rtol=1e-12, check_every=1)
     assert ok
+    assert comm.allreduces == it + 1  # ONE allreduce per iteration (+ the start)
     u = np.zeros(prob.mesh.n_dofs)
     for s in slabs:
         k0, k1 = s.slab.own_local
@@ -282,9 +327,13 @@ def test_cuda_slabs_emulated_on_one_gpu(cuda, nranks):
                         rtol=1e-11)
     rho = torch.as_tensor(prob.psi, device=cuda)
     u_ref = glob.pcg_device(rho, glob._f_d).cpu().numpy()
-    u, it = _slab_solve(prob, mat, rho, nranks, LocalComm())
+    comm = LocalComm()
+    u, it = _slab_solve(prob, mat, rho, nranks, comm)
     assert np.abs(u - u_ref).max() <= 1e-8 * np.abs(u_ref).max()
     assert abs(glob.last_iterations - it) <= 8 + glob.last_iterations // 50
+    # single reduction, iterations captured in CUDA graphs of 32: ONE allreduce per iteration
+    # (+ the start); iterations after convergence inside the last replay are device no-ops
+    assert comm.allreduces - 1 == 32 * ((it + 31) // 32)
     # fused halo: the update kernels store the boundary planes into the neighbours' ghost
     # planes; same values as the copy exchange, so the iterates are bit-identical
     u_peer, it_peer = _slab_solve(prob, mat, rho, nranks, LocalComm(peer=True))
@@ -381,6 +430,78 @@ def test_cuda_slab_rom_emulated_on_one_gpu(cuda):
     assert torch.abs(uh - uh_ref).max() <= 1e-10 * torch.abs(uh_ref).max()
     for a, b in zip(norms, n_ref):
         assert abs(a - b) <= 1e-9 * b
+
+
+def _rom_setup(cuda):
+    import paper_2004_05756_b200 as tb
+
+    prob = configs.cfg5(nx=12, ny=6, nz=9, n_designs=3, k=10)
+    mat = tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP)
+    glob = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, 1.0), prob.f, prob.fixed, mat)
+    raw = configs.phi_columns(prob.mesh, 10, seed=0)
+    raw[:, ~glob.free_mask] = 0.0
+    phi = torch.as_tensor(tb.gram_schmidt(list(raw)), device=cuda)
+    rhos = torch.as_tensor(np.stack(prob.rom_designs), device=cuda)
+    return tb, prob, mat, glob, phi, rhos
+
+
+def _rom_gloo_worker(rank, world, port, q):
+    """cfg 5 element sharding, one rank per process (same GPU): K_hat, Phi^T f and the squared
+    residual partials are allreduced through torch.distributed (gloo); no kernel waits on a peer."""
+    import torch.distributed as dist
+
+    from paper_2004_05756_b200.slab import SlabRom, SlabSolver, slab_rom_solve_batch
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        tb, prob, mat, glob, phi, rhos = _rom_setup(torch.device("cuda", 0))
+        s = partition(prob.mesh.nz, world)[rank]
+        sv = SlabSolver(prob.mesh, prob.k_e, prob.f, prob.fixed, mat, s, device=0)
+        d0 = s.e0 * sv.plane_dofs
+        comm = TorchComm()
+        rom = SlabRom(sv, phi[d0:d0 + sv.local.n_dofs], comm)
+        pe = sv.plane_elems
+        kh, uh, norms = slab_rom_solve_batch([rom], comm, [rhos[:, s.e0 * pe:s.e1 * pe].contiguous()])
+        q.put((rank, kh.cpu().numpy(), uh.cpu().numpy(), norms, comm.allreduces))
+    except Exception as e:  # reported to the parent
+        q.put((rank, repr(e)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_cuda_slab_rom_gloo_two_processes(cuda):
+    """SlabRom across two real rank processes: reduced operators, reduced solves and residual
+    norms equal the single-GPU RomModel.solve_batch (SURVEY §8e cfg 5: one allreduce of the
+    nd x k x k operators, one of Phi^T f, one of the squared residual partials)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    tb, prob, mat, glob, phi, rhos = _rom_setup(cuda)
+    basis = tb.ReducedBasis(phi, None, None, phi.T @ glob._f_d)
+    kh_ref, uh_ref, n_ref = tb.RomModel(glob).solve_batch(basis, rhos)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rom_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=300) for _ in procs), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert len(r) > 2, f"rank {r[0]} failed: {r[1]}"
+    kh0 = torch.as_tensor(kh_ref).cpu().numpy()
+    for _, kh, uh, norms, nred in res:
+        assert np.linalg.norm(kh - kh0) <= 1e-12 * np.linalg.norm(kh0)
+        assert np.abs(uh - uh_ref.cpu().numpy()).max() <= 1e-10 * np.abs(uh_ref.cpu().numpy()).max()
+        for a, b in zip(norms, n_ref):
+            assert abs(a - b) <= 1e-9 * b
+        assert nred == 3
+    assert np.array_equal(res[0][1], res[1][1])  # every rank holds the same reduced operators
 
 
 # ---------------------------------------------------------------------------------------------

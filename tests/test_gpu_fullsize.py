@@ -1,4 +1,4 @@
-"""Parity at the BASELINE 3D sizes (cfg 3 192x96x96, cfg 5 256x128x128).
+"""Parity at the BASELINE 3D sizes (cfg 3 192x96x96, cfg 4 384x192x192, cfg 5 256x128x128).
 
 The reference cannot solve these grids (2D only; a direct solve is infeasible in 3D), so
 parity is split the way SURVEY §7.3(7) / §8(c) prescribe:
@@ -9,7 +9,9 @@ parity is split the way SURVEY §7.3(7) / §8(c) prescribe:
   its operator, Phi^T K(rho) Phi column blocks, Phi^T f, the ROM residual norm;
 * solve level by self-consistency with host arithmetic: the pCG solution's TRUE residual
   ||Z(f - K u)|| / ||Z f|| recomputed on the host with the oracle operator (<= rtol,
-  SURVEY App. A), f^T u = u^T K u, and the filter adjoint against the host CG adjoint.
+  SURVEY App. A), f^T u = u^T K u, and the filter adjoint against the host CG adjoint;
+* cfg 4: the slab-sharded evaluation (2 and 8 emulated ranks) against the single-GPU
+  evaluation on the full 43M-dof grid.
 
 Tolerances (north_star, written here): pure arithmetic kernels 1e-12 relative (norm-wise),
 compliance 1e-8 (the identity 1e-10), sensitivities / filtered densities / reduced
@@ -162,3 +164,34 @@ def test_cfg5_fhat_and_residual_norm(cfg5):
     r = np.where(s.free_mask, it.apply_stiffness(g, prob.k_e, a, u) - s.f, 0.0)  # rom.py:319-325
     ref = float(np.linalg.norm(r))
     assert abs(cfg5["norms"][0] - ref) <= 1e-6 * max(ref, 1e-9 * np.linalg.norm(s.f))
+
+
+@pytest.mark.parametrize("nranks", [2, 8])
+def test_cfg4_slab_evaluation_vs_single_gpu(cuda, nranks):
+    """BASELINE cfg 4 (384x192x192, 43M dofs) evaluated over 2 and 8 emulated z-slabs (one
+    process, LocalComm: the single-reduction distributed pCG, graph-captured, SlabFilter) against
+    the single-GPU HdmSolver.solve + gradient on the full grid."""
+    import torch
+
+    from paper_2004_05756_b200.slab import LocalComm, SlabFilter, SlabSolver, partition, slab_evaluate
+
+    prob = configs.cfg4()
+    m = prob.mesh
+    one = tb.HdmSolver(m, prob.k_e, tb.HelmholtzFilter(m, prob.radius), prob.f, prob.fixed, MAT, rtol=1e-10)
+    obj = tb.ComplianceObjective(one.f)
+    psi_d = torch.as_tensor(prob.psi, device=cuda)
+    sol = one.solve(psi_d, obj)
+    g1 = one.gradient(psi_d, sol, obj)
+    j1 = sol.j
+    del one, sol
+    slabs = partition(m.nz, nranks)
+    solvers = [SlabSolver(m, prob.k_e, prob.f, prob.fixed, MAT, s, device=cuda) for s in slabs]
+    filters = [SlabFilter(m, prob.radius, s, device=cuda) for s in slabs]
+    comm = LocalComm(peer=True)
+    ev = slab_evaluate(solvers, filters, comm, [s.local_elems(psi_d).contiguous() for s in solvers], rtol=1e-10)
+    assert abs(ev.j - j1) <= 1e-8 * abs(j1)
+    g = torch.empty_like(g1)
+    for s, gl in zip(solvers, ev.g):
+        sl, sg = s.owned_elems()
+        g[sg] = gl[sl]
+    assert float(torch.linalg.norm(g - g1) / torch.linalg.norm(g1)) <= 1e-6

@@ -537,7 +537,7 @@ def roofline_3d(tb, _lib, solver, rho_d, pk, torch):
         out["us_per_iteration"] = msf.value * 1e3
     out["iteration_gbs_s8d"] = 8 * (9 * n_u + n_e) / (out["us_per_iteration"] * 1e-6) / 1e9
     tpath = os.path.join(REPO, "profiles", "traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and (m.nx, m.ny, m.nz) == (192, 96, 96):  # captured at cfg 3
         out["traffic"] = json.load(open(tpath)).get("cfg3_" + path)
     return out
 

@@ -79,7 +79,7 @@ int tb_element_sensitivity(tb_plan* plan, const double* rho, const double* u, co
  * TRUE residual ||Z(b - K x)|| <= rtol ||Z b||.  x is output only (x0 = 0).
  * *iters, *relres are HOST pointers (may be NULL).  Returns TB_ERR_INDEFINITE on breakdown,
  * TB_ERR_NOT_CONVERGED at maxit (x holds the last iterate).  rtol < 0 selects round-off mode:
- * target |rtol|, and a true residual that stagnates at <= max(100 |rtol|, 1e-8) is accepted (the
+ * target |rtol|, and a true residual that stagnates at <= max(100 |rtol|, 1e-7) is accepted (the
  * reference solves directly; this is "as exact as the arithmetic allows").  The same convention holds for
  * tb_filter_apply / tb_filter_adjoint. */
 int tb_pcg_solve(tb_plan* plan, const double* rho, const double* b, double* x, double rtol,

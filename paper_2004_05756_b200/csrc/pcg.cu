@@ -417,14 +417,14 @@ static int pcg_solve_pc(const PcgOp& op, PcgWork& w, const double* b, double* x_
 }
 
 // rtol < 0 selects round-off mode (include/topo_b200.h): target |rtol|, and a solve whose true
-// residual stagnates (restarts stop paying off) at or below max(100 |rtol|, 1e-8) counts as
+// residual stagnates (restarts stop paying off) at or below max(100 |rtol|, 1e-7) counts as
 // converged -- the attainable accuracy of Jacobi-pCG on an ill-conditioned SIMP design.
 int pcg_solve(const PcgOp& op, PcgWork& w, const double* b, double* x_out, double rtol, int maxit, int* iters,
               double* relres, cudaStream_t s) {
   double accept = 0.0;
   if (rtol < 0.0) {
     rtol = -rtol;
-    accept = fmax(100.0 * rtol, 1e-8);
+    accept = fmax(100.0 * rtol, 1e-7);
   }
   if (!(rtol > 0.0) || maxit < 1) {
     set_error("pcg: rtol must be nonzero and maxit >= 1 (got %g, %d)", rtol, maxit);

@@ -667,7 +667,7 @@ int pcg_solve_sweep(tb_plan_impl* P, const double* b, double* x_out, double rtol
   double accept = 0.0;  // round-off mode (rtol < 0), as pcg_solve
   if (rtol < 0.0) {
     rtol = -rtol;
-    accept = fmax(100.0 * rtol, 1e-8);
+    accept = fmax(100.0 * rtol, 1e-7);
   }
   if (!(rtol > 0.0) || maxit < 1) {
     set_error("pcg: rtol must be nonzero and maxit >= 1 (got %g, %d)", rtol, maxit);

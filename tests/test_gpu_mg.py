@@ -186,19 +186,26 @@ def test_mg_gauss_jordan_coarsest_inverse(cuda, n):
 
 def test_mg_elongated_grid_vs_oracle(cuda):
     """A slender 400 x 17 cantilever (not a BASELINE config): in fp64 the attainable true
-    residual of an iterative solve stagnates near 1e-9 here (Jacobi-pCG near 1e-8), so the
-    solve asks for 1e-8; the multigrid answer matches the oracle's direct solve to the
-    accuracy that implies."""
+    residual stagnates near 1e-9 here for multigrid (Jacobi-pCG near 1.5e-8).  A solve asked for
+    less than that REPORTS it (NotConvergedError) instead of returning silently; a solve to 1e-8
+    meets the north_star tolerances against the oracle's direct solve (J 1e-8, g 1e-6), and so
+    does the drop-in's round-off mode (rtol=None)."""
     from oracle.fem import build_grid
     from oracle.hdm import Filter, Hdm, Material
 
     prob = configs.cfg1(seed=7, nx=400, ny=17)
-    s = build(prob, "mg", rtol=1e-8)
-    obj = tb.ComplianceObjective(s.f)
-    sol = s.solve(prob.psi, obj)
-    g = s.gradient(prob.psi, sol, obj)
     grid = build_grid(400, 17, 1.0)
     ora = Hdm(grid, prob.k_e, Filter(grid, prob.radius), prob.f, prob.fixed, Material(configs.RHO_L, configs.P_SIMP))
     ref = ora.solve(prob.psi)
-    assert abs(sol.j - ref["j"]) <= 1e-7 * abs(ref["j"])
-    assert nrel(g, ora.gradient(ref)) <= 1e-5
+    g_ref = ora.gradient(ref)
+    for rtol in (1e-8, None):
+        s = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, prob.radius), prob.f, prob.fixed, MAT,
+                         rtol=rtol, preconditioner="mg")  # None: round-off mode
+        obj = tb.ComplianceObjective(s.f)
+        sol = s.solve(prob.psi, obj)
+        g = s.gradient(prob.psi, sol, obj)
+        assert abs(sol.j - ref["j"]) <= 1e-8 * abs(ref["j"])
+        assert nrel(g, g_ref) <= 1e-6
+    s = build(prob, "mg", rtol=1e-10)
+    with pytest.raises(tb.NotConvergedError):
+        s.solve(prob.psi, tb.ComplianceObjective(s.f))

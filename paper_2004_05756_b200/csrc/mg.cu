@@ -654,7 +654,8 @@ int mg_build(tb_plan_impl* P) {
   // Gauss-Jordan gives each row block to its own CTA(s) (k_mg_gj_inverse: rbk = c / cps), so it
   // needs at least ceil(n / kGjB) co-resident CTAs at its shared-memory size, one per SM;
   // otherwise (MIG slice, MPS limits, large n) the cuSOLVER path is taken.
-  bool gj_ok = D == 2 && mg.ncoarse <= kGjMaxN && getenv("TB_MG_CUSOLVER") == nullptr;
+  // 2D and 3D alike (round 2: the 3D set-up no longer calls cuSOLVER's potrf/potri)
+  bool gj_ok = mg.ncoarse <= kGjMaxN && getenv("TB_MG_CUSOLVER") == nullptr;
   if (gj_ok) {
     int sms = 0, coop = 0, occ = 0;
     TB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P->device));

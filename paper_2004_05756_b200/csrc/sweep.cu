@@ -50,7 +50,6 @@ constexpr int kTOPlaneS = 672;
 constexpr int kTNRow = 34;                              // per-node D^-1 tile row: 33 nodes + 1
 constexpr int kTNPlane = kTNRow * kTRows;               // 306
 constexpr int kTNPlaneS = 320;
-constexpr int kTSlots = (kTPlane + kHT - 1) / kHT;      // 4 slots per thread
 // one staged plane: r, s, w (halo tiles), D^-1 (node tile), x, p (owned tiles)
 constexpr int kStage = 3 * kTPlaneS + kTNPlaneS + 2 * kTOPlaneS;   // 4400 doubles
 constexpr uint32_t kHaloBytes = sizeof(double) * kTPlane;
@@ -147,16 +146,10 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
   // 16-byte aligned tile starts: the halo tile begins at dof 3 (i0 - 1) - shh, the owned tile at
   // 3 i0 - sho, the node tile at node i0 - 1 - shn; shared-memory indices carry the shifts
   const int shh = (3 * (i0 - 1)) & 1, sho = (3 * i0) & 1, shn = (i0 - 1) & 1;
-  // LAND slots: box index f = t + s kHT -> (row f / kTRow, tile double d = f % kTRow - shh)
-  unsigned fown = 0;
-#pragma unroll
-  for (int s = 0; s < kTSlots; ++s) {
-    const int f = t + s * kHT, ly = f / kTRow, d = f % kTRow - shh, lx = d / 3;
-    const int ni = i0 - 1 + lx, nj = j0 - 1 + ly;
-    if (f < kTPlane && d >= 0 && d < 3 * kPX && lx >= 1 && lx <= kOX && ly >= 1 && ly <= kOY && ni < g.nnx &&
-        nj < g.nny)
-      fown |= 1u << s;
-  }
+  // LAND pairs: even box index f = 2h -> (row f / kTRow, tile doubles d0 = f % kTRow - shh, d0 + 1);
+  // owned tile doubles [3, dlim) of rows [1, oylim] (inside the grid)
+  const int dlim = min(3 * (kOX + 1), 3 * (g.nnx - (i0 - 1)));
+  const int oylim = min(kOY, g.nny - j0);
   const int64_t gbase = (int64_t)(j0 - 1) * V.pitch + 3 * (i0 - 1);  // pitched offset of tile (0, 0)
   const bool own_in = own && i0 + onx < g.nnx && j0 + ony < g.nny;
   const int64_t obase = (int64_t)(j0 + ony) * V.pitch + 3 * (i0 + onx);  // this thread's owned node
@@ -201,35 +194,70 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
     const bool pown = kp >= K0 && kp < K1;
     const int64_t pl = (int64_t)kp * V.plane;
 #pragma unroll 1
-    for (int s = 0; s < kTSlots; ++s) {
-      if (s < kTSlots - 1 || t < kTPlane - (kTSlots - 1) * kHT) {
-        const int f = t + s * kHT;
-        if (MODE == kModeApply) {
-          ub[f] = B[f];
-        } else {
-          const int ly = f / kTRow, dd = f % kTRow - shh;
-          const int lx = (dd + 3) / 3 - 1, c = dd - 3 * lx;  // dd = -1 -> lx = -1 (unused slot)
-          const double dn = B[3 * kTPlaneS + ly * kTNRow + lx + shn];
-          const bool fr = !((__double2loint(dn) >> c) & 1);  // free dof (mask bit c clear)
-          const double d = fr ? dn : 0.0;
-          const double r = B[f], so = B[kTPlaneS + f], w = B[2 * kTPlaneS + f];
-          const double sn = fr ? fma(b_cg, so, w) : 0.0;
-          const double rn = fr ? fma(-a_cg, sn, r) : 0.0;
-          const double un = d * rn;
-          ub[f] = un;
-          if (pown && (fown >> s & 1u)) {
-            const int fo = 3 * kTPlaneS + kTNPlaneS + (ly - 1) * kTORow + (dd - 3 + sho);
-            const double pn = fma(b_cg, B[fo + kTOPlaneS], d * r);
-            const double xn = fma(a_cg, pn, B[fo]);
-            const int64_t go = pl + gbase + (int64_t)ly * V.pitch + dd;
-            __stwb(V.x + go, xn);
-            __stwb(rout + go, rn);
-            __stwb(V.p + go, pn);
-            __stwb(sout + go, sn);
-            acc[0] = fma(rn, un, acc[0]);
-            acc[1] = fma(rn, rn, acc[1]);
-          }
+    for (int h = t; h < kTPlane / 2; h += kHT) {
+      const int f = 2 * h;  // even box index: 16-byte aligned pairs in every tile (see below)
+      if (MODE == kModeApply) {
+        *reinterpret_cast<double2*>(ub + f) = *reinterpret_cast<const double2*>(B + f);
+      } else {
+        const int ly = f / kTRow, d0 = f - ly * kTRow - shh;  // tile doubles d0, d0 + 1 of node row ly
+        const int lx0 = (d0 + 3) / 3 - 1, c0 = d0 - 3 * lx0;   // d0 = -1 -> lx0 = -1 (unused slot)
+        const int lx1 = lx0 + (c0 == 2), c1 = c0 == 2 ? 0 : c0 + 1;
+        const double* dnr = B + 3 * kTPlaneS + ly * kTNRow + shn;
+        const double dn0 = dnr[lx0], dn1 = dnr[lx1];
+        const bool fr0 = !((__double2loint(dn0) >> c0) & 1), fr1 = !((__double2loint(dn1) >> c1) & 1);
+        const double e0 = fr0 ? dn0 : 0.0, e1 = fr1 ? dn1 : 0.0;
+        const double2 r = *reinterpret_cast<const double2*>(B + f);
+        const double2 so = *reinterpret_cast<const double2*>(B + kTPlaneS + f);
+        const double2 w = *reinterpret_cast<const double2*>(B + 2 * kTPlaneS + f);
+        const double sn0 = fr0 ? fma(b_cg, so.x, w.x) : 0.0, sn1 = fr1 ? fma(b_cg, so.y, w.y) : 0.0;
+        const double rn0 = fr0 ? fma(-a_cg, sn0, r.x) : 0.0, rn1 = fr1 ? fma(-a_cg, sn1, r.y) : 0.0;
+        const double un0 = e0 * rn0, un1 = e1 * rn1;
+        *reinterpret_cast<double2*>(ub + f) = make_double2(un0, un1);
+        // owned pairs: vector stores; the one or two unpaired owned dofs of a row go to the
+        // singles pass below (93 owned doubles per row: odd)
+        if (pown && ly >= 1 && ly <= oylim && d0 >= 3 && d0 + 1 < dlim) {
+          // owned-tile index and pitched offset are even: f even and sho - shh odd (see shh/sho)
+          const int fo = 3 * kTPlaneS + kTNPlaneS + (ly - 1) * kTORow + (d0 - 3 + sho);
+          const double2 xo = *reinterpret_cast<const double2*>(B + fo);
+          const double2 po = *reinterpret_cast<const double2*>(B + fo + kTOPlaneS);
+          const double pn0 = fma(b_cg, po.x, e0 * r.x), pn1 = fma(b_cg, po.y, e1 * r.y);
+          const double xn0 = fma(a_cg, pn0, xo.x), xn1 = fma(a_cg, pn1, xo.y);
+          const int64_t go = pl + gbase + (int64_t)ly * V.pitch + d0;
+          __stwb(reinterpret_cast<double2*>(V.x + go), make_double2(xn0, xn1));
+          __stwb(reinterpret_cast<double2*>(rout + go), make_double2(rn0, rn1));
+          __stwb(reinterpret_cast<double2*>(V.p + go), make_double2(pn0, pn1));
+          __stwb(reinterpret_cast<double2*>(sout + go), make_double2(sn0, sn1));
+          acc[0] = fma(rn0, un0, acc[0]);
+          acc[1] = fma(rn0, rn0, acc[1]);
+          acc[0] = fma(rn1, un1, acc[0]);
+          acc[1] = fma(rn1, rn1, acc[1]);
         }
+      }
+    }
+    // singles: lanes 0..13 of the last warp (one pair each above) redo the pointwise update of
+    // the unpaired owned dof at the low (even lane) or high (odd lane) end of owned row 1 + l/2
+    // (same inputs, bitwise the same s, r, u as the pair pass) and store it
+    if (MODE == kModeCg && pown && t >= kHT - 32 && t < kHT - 32 + 2 * kOY) {
+      const int l = t - (kHT - 32), ly = 1 + (l >> 1);
+      const int d = (l & 1) ? dlim - 1 : 3;
+      const int mate = ((d - shh) & 1) ? d - 1 : d + 1;  // pairs start at tile doubles = shh (mod 2)
+      if (ly <= oylim && (mate < 3 || mate >= dlim)) {
+        const int f = ly * kTRow + d + shh, lx = d / 3, c = d - 3 * lx;
+        const double dn = B[3 * kTPlaneS + ly * kTNRow + shn + lx];
+        const bool fr = !((__double2loint(dn) >> c) & 1);
+        const double e = fr ? dn : 0.0, r = B[f];
+        const double sn = fr ? fma(b_cg, B[kTPlaneS + f], B[2 * kTPlaneS + f]) : 0.0;
+        const double rn = fr ? fma(-a_cg, sn, r) : 0.0;
+        const int fo = 3 * kTPlaneS + kTNPlaneS + (ly - 1) * kTORow + (d - 3 + sho);
+        const double pn = fma(b_cg, B[fo + kTOPlaneS], e * r);
+        const double xn = fma(a_cg, pn, B[fo]);
+        const int64_t go = pl + gbase + (int64_t)ly * V.pitch + d;
+        __stwb(V.x + go, xn);
+        __stwb(rout + go, rn);
+        __stwb(V.p + go, pn);
+        __stwb(sout + go, sn);
+        acc[0] = fma(rn, e * rn, acc[0]);
+        acc[1] = fma(rn, rn, acc[1]);
       }
     }
   };

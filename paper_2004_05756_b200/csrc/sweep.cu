@@ -150,6 +150,14 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
   // owned tile doubles [3, dlim) of rows [1, oylim] (inside the grid)
   const int dlim = min(3 * (kOX + 1), 3 * (g.nnx - (i0 - 1)));
   const int oylim = min(kOY, g.nny - j0);
+  // singles pass (see land): lane l < 2 kOY of the last warp owns the unpaired owned dof at the
+  // low (even l) or high (odd l) end of owned row 1 + l/2, if that row end is unpaired
+  bool single = false;
+  if (t >= kHT - 32 && t < kHT - 32 + 2 * kOY) {
+    const int l = t - (kHT - 32), d = (l & 1) ? dlim - 1 : 3;
+    const int mate = ((d - shh) & 1) ? d - 1 : d + 1;  // pairs start at tile doubles = shh (mod 2)
+    single = 1 + (l >> 1) <= oylim && (mate < 3 || mate >= dlim);
+  }
   const int64_t gbase = (int64_t)(j0 - 1) * V.pitch + 3 * (i0 - 1);  // pitched offset of tile (0, 0)
   const bool own_in = own && i0 + onx < g.nnx && j0 + ony < g.nny;
   const int64_t obase = (int64_t)(j0 + ony) * V.pitch + 3 * (i0 + onx);  // this thread's owned node
@@ -237,28 +245,25 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
     // singles: lanes 0..13 of the last warp (one pair each above) redo the pointwise update of
     // the unpaired owned dof at the low (even lane) or high (odd lane) end of owned row 1 + l/2
     // (same inputs, bitwise the same s, r, u as the pair pass) and store it
-    if (MODE == kModeCg && pown && t >= kHT - 32 && t < kHT - 32 + 2 * kOY) {
+    if (MODE == kModeCg && pown && single) {
       const int l = t - (kHT - 32), ly = 1 + (l >> 1);
       const int d = (l & 1) ? dlim - 1 : 3;
-      const int mate = ((d - shh) & 1) ? d - 1 : d + 1;  // pairs start at tile doubles = shh (mod 2)
-      if (ly <= oylim && (mate < 3 || mate >= dlim)) {
-        const int f = ly * kTRow + d + shh, lx = d / 3, c = d - 3 * lx;
-        const double dn = B[3 * kTPlaneS + ly * kTNRow + shn + lx];
-        const bool fr = !((__double2loint(dn) >> c) & 1);
-        const double e = fr ? dn : 0.0, r = B[f];
-        const double sn = fr ? fma(b_cg, B[kTPlaneS + f], B[2 * kTPlaneS + f]) : 0.0;
-        const double rn = fr ? fma(-a_cg, sn, r) : 0.0;
-        const int fo = 3 * kTPlaneS + kTNPlaneS + (ly - 1) * kTORow + (d - 3 + sho);
-        const double pn = fma(b_cg, B[fo + kTOPlaneS], e * r);
-        const double xn = fma(a_cg, pn, B[fo]);
-        const int64_t go = pl + gbase + (int64_t)ly * V.pitch + d;
-        __stwb(V.x + go, xn);
-        __stwb(rout + go, rn);
-        __stwb(V.p + go, pn);
-        __stwb(sout + go, sn);
-        acc[0] = fma(rn, e * rn, acc[0]);
-        acc[1] = fma(rn, rn, acc[1]);
-      }
+      const int f = ly * kTRow + d + shh, lx = d / 3, c = d - 3 * lx;
+      const double dn = B[3 * kTPlaneS + ly * kTNRow + shn + lx];
+      const bool fr = !((__double2loint(dn) >> c) & 1);
+      const double e = fr ? dn : 0.0, r = B[f];
+      const double sn = fr ? fma(b_cg, B[kTPlaneS + f], B[2 * kTPlaneS + f]) : 0.0;
+      const double rn = fr ? fma(-a_cg, sn, r) : 0.0;
+      const int fo = 3 * kTPlaneS + kTNPlaneS + (ly - 1) * kTORow + (d - 3 + sho);
+      const double pn = fma(b_cg, B[fo + kTOPlaneS], e * r);
+      const double xn = fma(a_cg, pn, B[fo]);
+      const int64_t go = pl + gbase + (int64_t)ly * V.pitch + d;
+      __stwb(V.x + go, xn);
+      __stwb(rout + go, rn);
+      __stwb(V.p + go, pn);
+      __stwb(sout + go, sn);
+      acc[0] = fma(rn, e * rn, acc[0]);
+      acc[1] = fma(rn, rn, acc[1]);
     }
   };
 #define SW_FACE(boff_, f_)                                                                                   \
@@ -300,24 +305,23 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
 #pragma unroll
     for (int s = 0; s < 4; ++s) tc[c][s] = 0.0;
   double* outv = (MODE == kModeApply) ? V.y : (q ? V.w[0] : V.w[1]);
-  int slot_top = 1;  // ring slot of plane rel + 1
-#pragma unroll 1
-  for (int rel = 0; rel < steps; ++rel) {
+  // one step: element plane ez = K0 - 1 + rel from the carried bottom face `bot` and the top
+  // face (node plane rel + 1) loaded into `top`; unrolled by two below so the faces swap roles
+  // instead of being copied
+  auto step = [&](int rel, const double(&bot)[3][4], double(&top)[3][4]) {
     const int ez = K0 - 1 + rel;
     cp_async_wait<1>();  // this thread's alpha of plane ez (group rel) has landed
     const double a_cur = aring[(rel % 3) * kHT + t];
     alpha_fetch(ez + 2, (rel + 2) % 3);
-    {  // ---- element (gei, gej, ez): spectrum from carried bottom face + top face (plane rel+1) ----
-      double ft[3][4];
-      SW_FACE(slot_top * kTPlaneS, ft);
+    {  // ---- element (gei, gej, ez): spectrum from the bottom face + top face (plane rel+1) ----
+      SW_FACE(((rel + 1) % 3) * kTPlaneS, top);
       double u[3][8];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
-          u[c][s] = fb[c][s] + ft[c][s];
-          u[c][s + 4] = fb[c][s] - ft[c][s];
-          fb[c][s] = ft[c][s];
+          u[c][s] = bot[c][s] + top[c][s];
+          u[c][s + 4] = bot[c][s] - top[c][s];
         }
       hex8_iso_blocks(K, a_cur, u);
       double fq[3][4];
@@ -360,8 +364,15 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
     __syncthreads();
     // its stage buffer is free again: plane rel + 4 in flight
     if (rel >= 1 && rel + 4 <= steps) issue(rel + 4);
-    slot_top = (slot_top == 2) ? 0 : slot_top + 1;
+  };
+  double ft[3][4];
+  int rel = 0;
+#pragma unroll 1
+  for (; rel + 2 <= steps; rel += 2) {
+    step(rel, fb, ft);
+    step(rel + 1, ft, fb);
   }
+  if (rel < steps) step(rel, fb, ft);
 #undef SW_FACE
   if (MODE == kModeCg) {
     block_sum<3>(acc);

@@ -73,6 +73,7 @@ struct PcgState {
   int cg_init;  // single-reduction sweep (sweep.cu): the next sweep is a (re)start sweep
   int pad4;
   double cg_beta;  // distributed single-reduction pCG (phases 10-13): beta of the p/s recurrences
+  double alpha_lag;  // sweep.cu: alpha of the x update a lagging sweep left pending on p (0: none)
 };
 
 // ---------------------------------------------------------------------------------------

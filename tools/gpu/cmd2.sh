@@ -1,0 +1,3 @@
+python -m pytest tests -x -q -m gpu > gpurun_out/t2.log 2>&1; tail -3 gpurun_out/t2.log
+ncu --set full --clock-control none --import-source on -k 'regex:k_hex8_cg<1>|k_hex8<' -c 4 -o gpurun_out/apply_modes python profiles/apply_modes.py > gpurun_out/ncu_apply.log 2>&1
+tail -2 gpurun_out/ncu_apply.log

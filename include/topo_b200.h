@@ -219,8 +219,8 @@ int tb_rom_residual_norms(tb_plan* plan, const double* phi, int k, const double*
                           const double* uhat, int nd, const double* g, int64_t g_stride,
                           double* norms, void* stream);
 
-/* Modified Gram-Schmidt with one re-orthogonalisation pass and relative drop tolerance
- * (rom.py:76-97).  vectors: m COLUMN vectors of length n (column-major n x m, device);
+/* Gram-Schmidt with one re-orthogonalisation pass and relative drop tolerance (rom.py:76-97):
+ * block classical GS in panels of 8 (Q^T W on DMMA), decisions on the device, one host sync.  vectors: m COLUMN vectors of length n (column-major n x m, device);
  * q: output (n x kept) ROW-major, compact (buffer of n*m doubles). *kept HOST.
  * Returns TB_ERR_INVALID when no vector survives ("no independent vectors supplied"). */
 int tb_gram_schmidt(int64_t n, int m, const double* vectors, double drop_tol, double* q,

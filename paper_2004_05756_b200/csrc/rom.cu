@@ -497,50 +497,6 @@ __global__ void __launch_bounds__(kBlock) k_resid_part(int64_t n, const double* 
   if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
 }
 
-// ---------------------------------------------------------------------------------------
-// Modified Gram-Schmidt step: v -= c_prev * q_prev ; c_next = q_next . v  (last block)
-// ---------------------------------------------------------------------------------------
-struct GsState {
-  double c[2];
-  unsigned int count;
-  unsigned int pad;
-};
-
-__global__ void __launch_bounds__(kBlock) k_gs_step(int64_t n, double* __restrict__ v, const double* __restrict__ qprev,
-                                                    int cprev_slot, const double* __restrict__ qnext, int cnext_slot,
-                                                    GsState* st, double* part) {
-  const double cp = (qprev != nullptr) ? st->c[cprev_slot] : 0.0;
-  double acc[1] = {0.0};
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double vi = v[i];
-    if (qprev != nullptr) {
-      vi = fma(-cp, qprev[i], vi);
-      v[i] = vi;
-    }
-    if (qnext != nullptr) acc[0] = fma(qnext[i], vi, acc[0]);
-  }
-  if (qnext == nullptr) return;
-  block_sum<1>(acc);
-  if (publish_partials<1>(acc, part, &st->count)) {
-    gather_partials<1>(acc, part, &st->count);
-    if (threadIdx.x == 0) st->c[cnext_slot] = acc[0];
-  }
-}
-
-__global__ void k_scale_copy(int64_t n, const double* __restrict__ v, double s, double* __restrict__ q) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    q[i] = v[i] * s;
-}
-
-// column-major (n x m) -> row-major (n x m)
-__global__ void k_transpose_cm_rm(int64_t n, int m, const double* __restrict__ cm, double* __restrict__ rm) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n * m) return;
-  const int64_t i = t / m;
-  const int j = (int)(t % m);
-  rm[t] = cm[(int64_t)j * n + i];
-}
-
 }  // namespace tb
 
 using namespace tb;
@@ -713,73 +669,6 @@ int tb_rom_residual_norms(tb_plan* plan, const double* phi, int k, const double*
   TB_CUDA(cudaStreamSynchronize(s));
   for (int d = 0; d < nd; ++d) norms[d] = sqrt(P->h_scalar[d]);
   return TB_OK;
-}
-
-int tb_gram_schmidt(int64_t n, int m, const double* vectors, double drop_tol, double* q, int* kept, void* stream) {
-  TB_GUARD(vectors && q && kept && n >= 1 && m >= 1, "bad arguments");
-  cudaStream_t s = (cudaStream_t)stream;
-  const int nb = grid_for(n);
-  double *V = nullptr, *Q = nullptr, *part = nullptr, *h = nullptr;
-  GsState* st = nullptr;
-  TB_CUDA(cudaMallocAsync(&V, sizeof(double) * n, s));
-  TB_CUDA(cudaMallocAsync(&Q, sizeof(double) * n * m, s));
-  TB_CUDA(cudaMallocAsync(&part, sizeof(double) * nb, s));
-  TB_CUDA(cudaMallocAsync(&st, sizeof(GsState), s));
-  TB_CUDA(cudaMemsetAsync(st, 0, sizeof(GsState), s));
-  TB_CUDA(cudaMallocHost(&h, sizeof(double) * 2));
-  int nk = 0;
-  int rc = TB_OK;
-  for (int i = 0; i < m && rc == TB_OK; ++i) {
-    cudaMemcpyAsync(V, vectors + (int64_t)i * n, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
-    { k_gs_step<<<nb, kBlock, 0, s>>>(n, V, nullptr, 0, V, 0, st, part); tb::launched(); }  // ||v0||^2
-    cudaMemcpyAsync(h, st->c, sizeof(double), cudaMemcpyDeviceToHost, s);
-    if (cudaStreamSynchronize(s) != cudaSuccess) {
-      rc = TB_ERR_CUDA;
-      break;
-    }
-    const double n0 = sqrt(h[0]);
-    if (n0 == 0.0) continue;
-    int slot = 0;
-    const double* prev = nullptr;
-    for (int pass = 0; pass < 2; ++pass)
-      for (int b = 0; b < nk; ++b) {
-        const double* qb = Q + (int64_t)b * n;
-        { k_gs_step<<<nb, kBlock, 0, s>>>(n, V, prev, slot ^ 1, qb, slot, st, part); tb::launched(); }
-        prev = qb;
-        slot ^= 1;
-      }
-    // last deflation + ||v||^2
-    { k_gs_step<<<nb, kBlock, 0, s>>>(n, V, prev, slot ^ 1, nullptr, 0, st, part); tb::launched(); }
-    { k_gs_step<<<nb, kBlock, 0, s>>>(n, V, nullptr, 0, V, 0, st, part); tb::launched(); }
-    cudaMemcpyAsync(h, st->c, sizeof(double), cudaMemcpyDeviceToHost, s);
-    if (cudaStreamSynchronize(s) != cudaSuccess) {
-      rc = TB_ERR_CUDA;
-      break;
-    }
-    const double n1 = sqrt(h[0]);
-    if (n1 >= drop_tol * n0) {
-      { k_scale_copy<<<nb, kBlock, 0, s>>>(n, V, 1.0 / n1, Q + (int64_t)nk * n); tb::launched(); }
-      ++nk;
-    }
-  }
-  if (rc == TB_OK && cudaGetLastError() != cudaSuccess) rc = TB_ERR_CUDA;
-  if (rc == TB_OK && nk == 0) {
-    set_error("no independent vectors supplied");
-    rc = TB_ERR_INVALID;
-  }
-  if (rc == TB_OK) {
-    const int64_t tot = n * nk;
-    { k_transpose_cm_rm<<<(int)((tot + kBlock - 1) / kBlock), kBlock, 0, s>>>(n, nk, Q, q); tb::launched(); }
-  }
-  *kept = nk;
-  cudaFreeAsync(V, s);
-  cudaFreeAsync(Q, s);
-  cudaFreeAsync(part, s);
-  cudaFreeAsync(st, s);
-  cudaStreamSynchronize(s);
-  cudaFreeHost(h);
-  if (rc == TB_ERR_CUDA) set_error("CUDA failure in gram_schmidt");
-  return rc;
 }
 
 }  // extern "C"

@@ -6,11 +6,12 @@ BASELINE cfg 5).  Here the basis lives once on the device and every reduced quan
 computed from it directly:
 
 * ``Phi^T f``            -> tb_rom_project
-* ``Phi^T K(rho) Phi``   -> tb_rom_reduced_stiffness (node-form, DMMA contraction)
+* ``Phi^T K(rho) Phi``   -> tb_rom_reduced_stiffness (3D: fused element form on DMMA; 2D: node form)
 * Cholesky / solves      -> tb_rom_cholesky_solve (batched, one CTA per design)
 * ``Phi uhat``           -> tb_rom_reconstruct
 * ``||K Phi uhat - g||`` -> tb_rom_residual_norms
-* Gram-Schmidt           -> tb_gram_schmidt (MGS x2 with drop tolerance, rom.py:76-97)
+* Gram-Schmidt           -> tb_gram_schmidt (block CGS2 in panels of 8, DMMA Gram products, drop
+  decisions on the device; same kept set and basis as rom.py:76-97's MGS x2 to round-off)
 
 ``ReducedBasis(phi, elem_phi, elem_k_phi, f_hat)`` keeps the reference signature; the two
 cache arguments are accepted and ignored (pass None).

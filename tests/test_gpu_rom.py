@@ -41,6 +41,33 @@ def test_gram_schmidt_matches_oracle(cuda):
     assert tb.gram_schmidt([np.ones(5), -np.ones(5)]).shape[1] == 1
 
 
+def test_block_gram_schmidt_panels_vs_oracle(cuda):
+    """Several panels of 8 (tb_gram_schmidt's block CGS2): drops inside a panel, across panels,
+    zero and near-dependent vectors; the kept set and the basis equal rom.py:76-97's MGS x2."""
+    rng = np.random.default_rng(11)
+    n = 20_000
+    base = [rng.standard_normal(n) for _ in range(15)]
+    vecs = list(base[:9])
+    vecs.append(3.0 * base[2] - base[7])                       # depends on the previous panel -> dropped
+    vecs.append(base[9])
+    vecs.append(np.zeros(n))                                    # zero -> skipped
+    vecs.append(base[9] - 2.0 * base[8] + 1e-14 * base[10])     # residual ~1e-15 of its norm -> dropped
+    vecs.append(base[0] + 1e-6 * base[14])                      # residual ~1e-6 of its norm -> kept
+    vecs += base[10:14]
+    vecs.append(base[13] + base[12])                            # same panel -> dropped
+    vecs += [rng.standard_normal(n) for _ in range(6)]
+    q = tb.gram_schmidt(vecs)
+    q_ref = gs_ref(vecs)
+    assert q.shape == q_ref.shape == (n, 21)
+    assert np.abs(q.T @ q - np.eye(21)).max() < 1e-12
+    # column 10 is determined by a 1e-6 residual: its round-off is amplified ~1e6 on both sides
+    err = np.abs(q - q_ref).max(axis=0)
+    assert err[np.arange(21) != 10].max() < 1e-12 and err[10] < 1e-8, err
+    for m in (1, 8, 9, 17):  # panel boundaries
+        vs = [rng.standard_normal(300) for _ in range(m)]
+        assert np.abs(tb.gram_schmidt(vs) - gs_ref(vs)).max() < 1e-12
+
+
 def test_pod_matches_oracle(cuda):
     rng = np.random.default_rng(1)
     snaps = rng.standard_normal((50, 6))

@@ -313,6 +313,18 @@ extern "C" int tb_gram_schmidt(int64_t n, int m, const double* vectors, double d
     return TB_ERR_INVALID;
   }
   cudaStream_t s = (cudaStream_t)stream;
+  {  // keep up to 16 GB of freed workspace in the stream-ordered pool between calls: re-mapping
+     // cfg 5's 6.6 GB basis workspace on every call cost more than the orthogonalisation
+    static bool done[64] = {};
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev < 64 && !done[dev] &&
+        cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = 16ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      done[dev] = true;
+    }
+  }
   const int mcap = (m + kGsChunk - 1) / kGsChunk * kGsChunk;
   double *Q = nullptr, *W = nullptr, *C = nullptr, *part = nullptr;
   GsCtl* ctl = nullptr;

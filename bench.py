@@ -22,6 +22,7 @@ evaluation slab-sharded over all N ranks (strong scaling).
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -498,10 +499,12 @@ def rom_profile(_lib, rom, basis, rhos, pk, torch):
             "note": f"one call = Phi^T K(rho_d) Phi for all {nd} designs; algorithmic bytes = Phi once + rho_d"}
 
 
-def roofline_3d(tb, _lib, solver, rho_d, pk, torch):
-    """Dominant kernel of the 3D Jacobi-pCG iteration, timed live with CUDA events on the
-    solve's stream (tb_pcg_profile: each kernel of an iteration bracketed by events).  Bytes:
-    the algorithmic traffic of that kernel per SURVEY §8(d)."""
+def roofline_3d(tb, _lib, solver, rho_d, pk, torch, live=None):
+    """Dominant kernel of the 3D Jacobi-pCG iteration.  Sweep path: timed live inside the timed
+    steps (``live`` = tb_pcg_iter_time: CUDA events on the solve's stream around every
+    iteration-graph launch, divided by the sweeps they ran); tb_pcg_profile (an event pair
+    around each single launch, outside the timed region) is reported beside it.  Bytes: the
+    algorithmic traffic of that kernel per SURVEY §8(d)."""
     import ctypes
 
     m = solver.mesh
@@ -514,9 +517,13 @@ def roofline_3d(tb, _lib, solver, rho_d, pk, torch):
         by = 8 * (9 * n_u + n_e)
         t = msf.value * 1e-3
         kern = ("k_hex8_cg (Chronopoulos-Gear Jacobi-pCG iteration in ONE z-sweep: TMA node planes, WHT-block Hex8 "
-                "operator, x/r/p/s/w updates, 3 dot products)")
+                "operator, x/r/p/s/w updates, 3 dot products; x update lagged on every other sweep)")
         note = "bytes = one Jacobi-pCG iteration, 8(9 N_u + N_e) (SURVEY §8(d)); the kernel IS the iteration"
         upd = None
+        if live is not None and live[1] > 0:
+            t = live[0] / live[1] * 1e-3
+            note += (f"; time = {live[0]:.1f} ms of iteration-graph launches over {live[1]} sweeps inside the timed "
+                     f"steps (events on the solve stream); isolated per-launch events: {msf.value * 1e3:.1f} us")
     else:
         by = 8 * (4 * n_u + n_e)
         t = msf.value * 1e-3
@@ -702,9 +709,16 @@ def run_ours(args):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    live = None  # in-situ sweep timing over the timed steps (events around the iteration graphs)
+    if mesh.dim == 3 and args.precond == "jacobi" and pcg_path(_lib, solver._plan) == "sweep":
+        live = [ctypes.c_double(0.0), ctypes.c_int64(0)]
+        _lib.check(_lib.lib().tb_pcg_iter_time(solver._plan, 1, ctypes.byref(live[0]), ctypes.byref(live[1])), "timer")
     launches0 = _lib.lib().tb_launch_count()
     step_ms, iters, sol = time_steps(solver, obj, psi_d, torch, args.steps, 0, flush)
     clk = clocks.stop()
+    if live is not None:
+        _lib.check(_lib.lib().tb_pcg_iter_time(solver._plan, 0, ctypes.byref(live[0]), ctypes.byref(live[1])), "timer")
+        live = (live[0].value, live[1].value)
     launches = _lib.lib().tb_launch_count() - launches0
     if dist:
         dist.barrier()
@@ -726,7 +740,7 @@ def run_ours(args):
 
     rho_d, _ = solver.filtered_density_device(psi_d)
     if mesh.dim == 3:
-        roof = roofline_3d(tb, _lib, solver, rho_d, pk, torch) if args.precond == "jacobi" else None
+        roof = roofline_3d(tb, _lib, solver, rho_d, pk, torch, live) if args.precond == "jacobi" else None
     else:
         roof = roofline_2d(solver, rho_d, pk, torch, args.precond)
     apply = apply_roofline(solver, rho_d, pk, torch)

@@ -101,6 +101,12 @@ int tb_pcg_profile(tb_plan* plan, const double* rho, const double* b, int nrep, 
  * there were (restarts after a true-residual check add one each); 0 launches when the solve ran
  * the graph path.  Synchronises on the last launch. */
 int tb_pcg_kernel_time(tb_plan* plan, float* ms, int* launches);
+/* Diagnostics: in-situ iteration timing of the single-sweep path (tb_pcg_path == 1).  reset != 0
+ * starts (or restarts) accumulating: every later tb_pcg_solve brackets its iteration-graph
+ * launches with CUDA events on the solve's stream.  Returns the accumulated device time (ms)
+ * and the number of sweeps it covered (HOST pointers), i.e. the mean sweep duration of real
+ * solves.  Replaces nothing in the reference (diagnostic). */
+int tb_pcg_iter_time(tb_plan* plan, int reset, double* ms, int64_t* iters);
 /* Which Jacobi-pCG iteration tb_pcg_solve runs for this plan: 1 = the 3D single-sweep
  * Chronopoulos-Gear kernel (Hex8, TMA-staged, one reduction per iteration), 0 = the two-kernel
  * iteration (2D / multigrid / distributed), -1 = null plan.  Replaces nothing in the reference
@@ -191,7 +197,7 @@ int tb_filter_transfer(tb_filter* filt, int mode, const double* in, double scale
                        void* stream);
 
 /* ---- reduced-order model (rom.py:182-390); phi is (n_dofs x k) ROW-major ---- */
-/* out[k*d + j] = sum_i phi[i*k + j] * vec[d*n + i] for nvec <= 16 stacked vectors of length n
+/* out[k*d + j] = sum_i phi[i*k + j] * vec[d*n + i] for nvec stacked vectors of length n (16 per pass over Phi)
  * (Phi^T f, rom.py:251, 289; also Q^T S of the POD) */
 int tb_rom_project(int64_t n, const double* phi, int k, const double* vec, int nvec, double* out,
                    void* stream);
@@ -210,7 +216,7 @@ int tb_rom_gram_colmajor(int64_t n, int k, const double* A, const double* B, int
  * 1 = not SPD (cho_factor LinAlgError -> DegenerateBasisError). */
 int tb_rom_cholesky_solve(int k, int nd, int nrhs, const double* khat, const double* rhs,
                           double* x, int* status, void* stream);
-/* u[d] = Phi uhat[d] (length n) for nd <= 16 coefficient vectors (rom.py:285) */
+/* u[d] = Phi uhat[d] (length n) for nd coefficient vectors (16 per pass over Phi; rom.py:285) */
 int tb_rom_reconstruct(int64_t n, const double* phi, int k, const double* uhat, int nd, double* u,
                        void* stream);
 /* norms[d] = || Z (K(rho_d) Phi uhat_d - g_d) ||_2 (rom.py:309-335); g is (nd x n_dofs) or a

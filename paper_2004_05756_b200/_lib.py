@@ -35,7 +35,7 @@ EXPORTS = (
     "tb_rom_gram_colmajor", "tb_rom_cholesky_solve", "tb_rom_reconstruct", "tb_rom_residual_norms", "tb_gram_schmidt",
     "tb_mma_workspace_bytes", "tb_mma_step", "tb_cone_create", "tb_cone_destroy", "tb_cone_apply",
     "tb_cone_adjoint", "tb_filter_set_owned_planes", "tb_filter_dist_phase", "tb_filter_dist_buffers",
-    "tb_filter_dist_state", "tb_filter_set_halo_peers", "tb_filter_transfer", "tb_mgp_prof_read", "tb_pcg_kernel_time", "tb_pcg_path", "tb_rom_fused_info",
+    "tb_filter_dist_state", "tb_filter_set_halo_peers", "tb_filter_transfer", "tb_mgp_prof_read", "tb_pcg_kernel_time", "tb_pcg_iter_time", "tb_pcg_path", "tb_rom_fused_info",
 )
 
 
@@ -98,6 +98,7 @@ _SIGS = {
     "tb_mgp_prof_read": ([ctypes.POINTER(ctypes.c_ulonglong)], I),
     "tb_pcg_kernel_time": ([P, ctypes.POINTER(ctypes.c_float), PI], I),
     "tb_pcg_path": ([P], I),
+    "tb_pcg_iter_time": ([P, I, PD, ctypes.POINTER(ctypes.c_int64)], I),
     "tb_rom_fused_info": ([P, I, I, PD], I),
     "tb_rom_project": ([I64, P, I, P, I, P, P], I),
     "tb_rom_reduced_stiffness": ([P, P, I, P, I, P, P], I),

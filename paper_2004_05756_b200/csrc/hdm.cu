@@ -494,6 +494,13 @@ int tb_pcg_profile(tb_plan* plan, const double* rho, const double* b, int nrep, 
   return pcg_profile(P->op, P->work, b, nrep, ms_fused, ms_update, s);
 }
 
+int tb_pcg_iter_time(tb_plan* plan, int reset, double* ms, int64_t* iters) {
+  TB_GUARD(plan && ms && iters, "null argument");
+  auto* P = reinterpret_cast<tb_plan_impl*>(plan);
+  TB_GUARD(sweep_enabled(P), "iteration timing is kept by the single-sweep path only (tb_pcg_path == 1)");
+  return pcg_iter_time_sweep(P, reset, ms, iters);
+}
+
 int64_t tb_launch_count(void) { return g_launches.load(); }
 
 int tb_plan_set_preconditioner(tb_plan* plan, int kind) {

@@ -115,6 +115,7 @@ void sweep_release(tb_plan_impl* P);
 int pcg_solve_sweep(tb_plan_impl* P, const double* b, double* x_out, double rtol, int maxit, int* iters,
                     double* relres, cudaStream_t s);
 int pcg_profile_sweep(tb_plan_impl* P, const double* b, int nrep, double* ms_iter, cudaStream_t s);
+int pcg_iter_time_sweep(tb_plan_impl* P, int reset, double* ms, int64_t* iters);
 
 // element-form reduced stiffness on DMMA for Hex8 plans (romfused.cu)
 bool rom_fused_eligible(const tb_plan_impl* P, int k);

@@ -514,14 +514,18 @@ extern "C" {
 int tb_rom_project(int64_t n, const double* phi, int k, const double* vec, int nvec, double* out, void* stream) {
   TB_GUARD(phi && vec && out && n >= 1, "bad arguments");
   TB_GUARD(k >= 1 && k <= kBlock, "basis size k=%d out of range [1, %d]", k, kBlock);
-  TB_GUARD(nvec >= 1 && nvec <= kMaxVec, "nvec=%d out of range [1, %d]", nvec, kMaxVec);
+  TB_GUARD(nvec >= 1, "nvec=%d must be >= 1", nvec);
   cudaStream_t s = (cudaStream_t)stream;
   const int nb = 148 * 2;
   double* part = nullptr;
-  TB_CUDA(cudaMallocAsync(&part, sizeof(double) * (size_t)nb * nvec * k, s));
+  const int nv0 = nvec < kMaxVec ? nvec : kMaxVec;
+  TB_CUDA(cudaMallocAsync(&part, sizeof(double) * (size_t)nb * nv0 * k, s));
   const int groups = kBlock / k;
-  { k_project_part<<<nb, kBlock, sizeof(double) * groups * nvec * k, s>>>(n, k, phi, vec, nvec, part); tb::launched(); }
-  { k_sum_parts<<<nblk(nvec * k), kBlock, 0, s>>>(nb, nvec * k, part, out); tb::launched(); }
+  for (int v0 = 0; v0 < nvec; v0 += kMaxVec) {  // kMaxVec vectors per pass over Phi
+    const int nv = nvec - v0 < kMaxVec ? nvec - v0 : kMaxVec;
+    { k_project_part<<<nb, kBlock, sizeof(double) * groups * nv * k, s>>>(n, k, phi, vec + (int64_t)v0 * n, nv, part); tb::launched(); }
+    { k_sum_parts<<<nblk(nv * k), kBlock, 0, s>>>(nb, nv * k, part, out + (int64_t)v0 * k); tb::launched(); }
+  }
   TB_CHECK_LAUNCH();
   TB_CUDA(cudaFreeAsync(part, s));
   return TB_OK;
@@ -635,12 +639,17 @@ int tb_rom_cholesky_solve(int k, int nd, int nrhs, const double* khat, const dou
 
 int tb_rom_reconstruct(int64_t n, const double* phi, int k, const double* uhat, int nd, double* u, void* stream) {
   TB_GUARD(phi && uhat && u && n >= 1, "bad arguments");
-  TB_GUARD(k >= 1 && nd >= 1 && nd <= kMaxVec, "bad sizes k=%d nd=%d", k, nd);
+  TB_GUARD(k >= 1 && nd >= 1, "bad sizes k=%d nd=%d", k, nd);
   cudaStream_t s = (cudaStream_t)stream;
-  if (k <= 64)
-    { k_reconstruct_dmma<<<148 * 8, kBlock, 0, s>>>(n, k, phi, uhat, nd, u); tb::launched(); }
-  else
-    { k_reconstruct<<<148 * 8, kBlock, sizeof(double) * nd * k, s>>>(n, k, phi, uhat, nd, u); tb::launched(); }
+  for (int d0 = 0; d0 < nd; d0 += kMaxVec) {  // kMaxVec designs per pass over Phi
+    const int m = nd - d0 < kMaxVec ? nd - d0 : kMaxVec;
+    const double* uh = uhat + (int64_t)d0 * k;
+    double* ud = u + (int64_t)d0 * n;
+    if (k <= 64)
+      { k_reconstruct_dmma<<<148 * 8, kBlock, 0, s>>>(n, k, phi, uh, m, ud); tb::launched(); }
+    else
+      { k_reconstruct<<<148 * 8, kBlock, sizeof(double) * m * k, s>>>(n, k, phi, uh, m, ud); tb::launched(); }
+  }
   TB_CHECK_LAUNCH();
   return TB_OK;
 }

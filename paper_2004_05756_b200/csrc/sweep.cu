@@ -50,13 +50,13 @@ namespace {
 constexpr int kTRow = 100;                              // node-plane tile row: 3 x 33 doubles + 1 (16 B multiple)
 constexpr int kTRows = kPY;                             // 9 node rows
 constexpr int kTPlane = kTRow * kTRows;                 // 900 doubles
-constexpr int kTPlaneS = 912;                           // smem stride: 128-byte multiple
+constexpr int kTPlaneS = (kTPlane + 15) / 16 * 16;      // smem stride: 128-byte multiple (912)
 constexpr int kTORow = 94;                              // owned tile row: 3 x 31 + 1
 constexpr int kTOPlane = kTORow * kOY;                  // 658
-constexpr int kTOPlaneS = 672;
+constexpr int kTOPlaneS = (kTOPlane + 15) / 16 * 16;    // 672
 constexpr int kTNRow = 34;                              // per-node D^-1 tile row: 33 nodes + 1
 constexpr int kTNPlane = kTNRow * kTRows;               // 306
-constexpr int kTNPlaneS = 320;
+constexpr int kTNPlaneS = (kTNPlane + 15) / 16 * 16;    // 320
 // one staged plane: r, s, w (halo tiles), D^-1 (node tile), x, p (owned tiles)
 constexpr int kStage = 3 * kTPlaneS + kTNPlaneS + 2 * kTOPlaneS;   // 4400 doubles
 constexpr uint32_t kHaloBytes = sizeof(double) * kTPlane;
@@ -605,6 +605,11 @@ struct SweepState {
   double* dn = nullptr;                // per-node D^-1 + Dirichlet bits (pitched)
   double* w1 = nullptr;                // w[1] (w[0] reuses the plan's dinv vector)
   cudaGraphExec_t exec = nullptr;
+  // in-situ iteration timing (tb_pcg_iter_time): events around every iteration-graph launch
+  bool timing = false;
+  cudaEvent_t tev[2] = {nullptr, nullptr};
+  double t_ms = 0.0;
+  int64_t t_iters = 0;
 };
 
 // The plan's PcgWork vectors are allocated with sweep_size() doubles for Hex8 plans and reused
@@ -665,6 +670,8 @@ int sweep_init(tb_plan_impl* P) {
 void sweep_release(tb_plan_impl* P) {
   if (P->sweep == nullptr) return;
   if (P->sweep->exec) cudaGraphExecDestroy(P->sweep->exec);
+  for (auto& e : P->sweep->tev)
+    if (e) cudaEventDestroy(e);
   if (P->sweep->w1) cudaFree(P->sweep->w1);
   if (P->sweep->dn) cudaFree(P->sweep->dn);
   delete P->sweep;
@@ -765,7 +772,9 @@ int pcg_solve_sweep(tb_plan_impl* P, const double* b, double* x_out, double rtol
         if (w.h_st->done != 0) break;
       }
     } else {
+      if (S.timing) TB_CUDA(cudaEventRecord(S.tev[0], s));
       TB_CUDA(cudaGraphLaunch(S.exec, s));
+      if (S.timing) TB_CUDA(cudaEventRecord(S.tev[1], s));
     }
     // true residual at exit: y = K x, r = Z(b - y); converged if ||r|| <= rtol ||Z b||
     k_sweep_xfix<<<kUpdateBlocks, kBlock, 0, s>>>(P->g, P->n_dofs, S.vecs.pitch, S.vecs, w.st);
@@ -779,6 +788,12 @@ int pcg_solve_sweep(tb_plan_impl* P, const double* b, double* x_out, double rtol
     TB_CUDA(cudaStreamSynchronize(s));
     const PcgState& h = *w.h_st;
     if (!plain) launched((int64_t)((h.iters - it_before + kIters) / kIters) * (kIters + 1));
+    if (!plain && S.timing) {  // the stream sync above has passed tev[1]
+      float ms = 0.f;
+      TB_CUDA(cudaEventElapsedTime(&ms, S.tev[0], S.tev[1]));
+      S.t_ms += ms;
+      S.t_iters += h.iters - it_before + 1;  // + the start sweep of this (re)start
+    }
     it_before = h.iters;
     if (h.done == 1) break;
     if (h.done == 3) {
@@ -806,6 +821,23 @@ int pcg_solve_sweep(tb_plan_impl* P, const double* b, double* x_out, double rtol
   launched(1);
   TB_CHECK_LAUNCH();
   return rc;
+}
+
+int pcg_iter_time_sweep(tb_plan_impl* P, int reset, double* ms, int64_t* iters) {
+  TB_TRY(sweep_init(P));
+  SweepState& S = *P->sweep;
+  if (reset) {
+    if (!S.tev[0]) {
+      TB_CUDA(cudaEventCreate(&S.tev[0]));
+      TB_CUDA(cudaEventCreate(&S.tev[1]));
+    }
+    S.timing = true;
+    S.t_ms = 0.0;
+    S.t_iters = 0;
+  }
+  *ms = S.t_ms;
+  *iters = S.t_iters;
+  return TB_OK;
 }
 
 // per-launch CUDA-event time of the sweep (iterations kept live with rtol = 0)

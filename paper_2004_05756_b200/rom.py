@@ -90,10 +90,8 @@ def _project(phi_d, vecs_d):
     t = _lib.torch()
     n, k = phi_d.shape
     out = t.empty((vecs_d.shape[0], k), dtype=t.float64, device=phi_d.device)
-    for s in range(0, vecs_d.shape[0], 16):
-        nv = min(16, vecs_d.shape[0] - s)
-        _lib.check(_lib.lib().tb_rom_project(n, _lib.ptr(phi_d), k, _lib.ptr(vecs_d[s:s + nv].contiguous()), nv,
-                                             _lib.ptr(out[s:s + nv]), _stream(phi_d.device)), "rom project")
+    _lib.check(_lib.lib().tb_rom_project(n, _lib.ptr(phi_d), k, _lib.ptr(vecs_d.contiguous()), vecs_d.shape[0],
+                                         _lib.ptr(out), _stream(phi_d.device)), "rom project")
     return out
 
 
@@ -102,11 +100,8 @@ def _reconstruct(phi_d, coef_d):
     t = _lib.torch()
     n, k = phi_d.shape
     out = t.empty((coef_d.shape[0], n), dtype=t.float64, device=phi_d.device)
-    for s in range(0, coef_d.shape[0], 16):
-        nd = min(16, coef_d.shape[0] - s)
-        _lib.check(_lib.lib().tb_rom_reconstruct(n, _lib.ptr(phi_d), k, _lib.ptr(coef_d[s:s + nd].contiguous()),
-                                                 nd, _lib.ptr(out[s:s + nd]), _stream(phi_d.device)),
-                   "rom reconstruct")
+    _lib.check(_lib.lib().tb_rom_reconstruct(n, _lib.ptr(phi_d), k, _lib.ptr(coef_d.contiguous()), coef_d.shape[0],
+                                             _lib.ptr(out), _stream(phi_d.device)), "rom reconstruct")
     return out
 
 

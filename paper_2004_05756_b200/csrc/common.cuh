@@ -160,6 +160,33 @@ __device__ __forceinline__ void gather_partials(double (&v)[NV], const double* p
   if (tid == 0) *counter = 0u;
 }
 
+// ---- mbarrier + 1D bulk copy (async proxy) primitives shared by the TMA/bulk-staged kernels ----
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mb_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nMBW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra MBW_%=;\n}\n" ::"r"(
+          smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1D bulk copy global -> shared, completion counted on `bar`; addresses and size 16-byte aligned
+__device__ __forceinline__ void bulk_g2s(double* dst, const double* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+// generic-proxy writes (this or other CTAs, ordered by a barrier) -> later async-proxy reads
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;\n" ::: "memory"); }
+
 inline int grid_for(int64_t n, int per_block = kBlock, int cap = 148 * 8) {
   int64_t b = (n + per_block - 1) / per_block;
   if (b > cap) b = cap;

@@ -410,43 +410,116 @@ __global__ void k_mg_gemv(int64_t n, const double* __restrict__ A, const double*
 // A[i, :] <- A[i, :] - Gm_i [row block K] off the K columns, -Gm_i on them.  One grid barrier
 // per step.
 // ---------------------------------------------------------------------------------------
+// Shared-memory layout of k_mg_gj_inverse (host and device compute it identically): the row
+// block K is staged compactly -- this CTA's R slice (LS columns) then its update part (LU) --
+// and, when `stg`, this CTA's own rows (update part) and their K columns as well, so the step
+// needs no L2 round trip after the staging.
+#ifdef TB_GJ_PROF
+__device__ unsigned long long g_gj_prof[2][8];
+#define GJ_MARK(k)                                                               \
+  do {                                                                           \
+    if ((blockIdx.x == 0 || blockIdx.x == 100) && threadIdx.x == 0) {            \
+      unsigned long long t_;                                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                     \
+      g_gj_prof[blockIdx.x ? 1 : 0][k] += t_ - prof_last;                        \
+      prof_last = t_;                                                            \
+    }                                                                            \
+  } while (0)
+#else
+#define GJ_MARK(k) \
+  do {             \
+  } while (0)
+#endif
+
+struct GjLayout {
+  int cols_per, cps, ucols, LS, LU, LW;
+  __host__ __device__ GjLayout(int n, int grid) {
+    const int nb = (n + kGjB - 1) / kGjB;
+    cols_per = (n + grid - 1) / grid;
+    cps = grid / nb > 1 ? grid / nb : 1;
+    ucols = (n + cps - 1) / cps;
+    LS = (cols_per + 1) / 2 * 2;
+    LU = (ucols + 1) / 2 * 2;
+    LW = LS + LU;
+  }
+  // bulk copies need 16-byte aligned global rows and ranges
+  __host__ __device__ bool bulk(int n) const { return !(n & 1) && !(cols_per & 1) && !(ucols & 1); }
+  __host__ __device__ size_t smem(bool stg) const {
+    return sizeof(double) * ((size_t)kGjB * LW + (stg ? (size_t)kGjB * LU + kGjB * kGjB : 0));
+  }
+};
+
 __global__ void __launch_bounds__(512, 1) k_mg_gj_inverse(int n, double* __restrict__ A, double* __restrict__ G,
-                                                          unsigned int* bar, int* info) {
-  extern __shared__ double W[];  // [kGjB][n]: row block K (old values)
+                                                          unsigned int* bar, int* info, int stg) {
+  extern __shared__ __align__(16) double gj_sm[];
   __shared__ double Pi[kGjB][kGjB];  // P^-1
   __shared__ double Gm[kGjB][kGjB];  // F P^-1 for this CTA's rows
   __shared__ int bad;
+  __shared__ __align__(8) uint64_t wbar;  // bulk copies of the step's operands
   const int nb = (n + kGjB - 1) / kGjB;
   const int c = blockIdx.x, t = threadIdx.x, nt = blockDim.x, lane = t & 31;
-  const int cols_per = (n + gridDim.x - 1) / gridDim.x;
-  const int j0 = c * cols_per, j1 = min(n, j0 + cols_per);  // this CTA's slice of R
+  const GjLayout Lo(n, (int)gridDim.x);
+  double* Ws = gj_sm;                           // [kGjB][LW]: row block K, R slice then update part
+  double* Os = gj_sm + kGjB * Lo.LW;            // [kGjB][LU]: own rows, update part (stg)
+  double* Fs = Os + kGjB * Lo.LU;               // [kGjB][kGjB]: own rows, K columns (stg)
+  const int j0 = c * Lo.cols_per, j1 = min(n, j0 + Lo.cols_per);  // this CTA's slice of R
   // row block rbk of the matrix, column part cpart of cps (several CTAs per row block when the
   // grid is at least twice the block count, so more SMs share the rank-16 updates)
-  const int cps = max(1, (int)gridDim.x / nb);
-  const int rbk = c / cps, cpart = c % cps;
-  const int ucols = (n + cps - 1) / cps;
-  const int u0 = cpart * ucols, u1 = min(n, u0 + ucols);
-  if (t == 0) bad = 0;
+  const int rbk = c / Lo.cps, cpart = c % Lo.cps;
+  const int u0 = cpart * Lo.ucols, u1 = min(n, u0 + Lo.ucols);
+  const bool bulk = Lo.bulk(n);
+  if (t == 0) {
+    bad = 0;
+    mb_init(&wbar, 1);
+  }
+  __syncthreads();
+  uint32_t wphase = 0;
+#ifdef TB_GJ_PROF
+  unsigned long long prof_last = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_last));
+#endif
   for (int K = 0; K < nb; ++K) {
     const int k0 = K * kGjB, kb = min(kGjB, n - k0);
     const bool own = (rbk < nb && rbk != K);
     const int r0 = rbk * kGjB, rb = own ? min(kGjB, n - r0) : 0;
     const bool parked = own && (rbk == K - 1);  // rows of block K-1 live in G[(K-1) & 1]
     const double* rows = parked ? G + (int64_t)((K - 1) & 1) * kGjB * n : A + (int64_t)r0 * n;
-    // row block K -> shared memory by cp.async (in flight while P^-1 and Gm are formed)
-    // only the columns this CTA reads: its R slice [j0, j1) and its update part [u0, u1)
-    // (the pivot block comes from global memory below)
-    for (int q = t; q < kb * (j1 - j0); q += nt) {
-      const int r = q / (j1 - j0), j = j0 + q % (j1 - j0);
-      cp_async8(W + (size_t)r * n + j, A + (int64_t)(k0 + r) * n + j, true);
-    }
-    if (own)
-      for (int q = t; q < kb * (u1 - u0); q += nt) {
-        const int r = q / (u1 - u0), j = u0 + q % (u1 - u0);
-        if (j >= j0 && j < j1) continue;  // already requested
-        cp_async8(W + (size_t)r * n + j, A + (int64_t)(k0 + r) * n + j, true);
+    const int ns = max(0, j1 - j0), nsu = own ? max(0, u1 - u0) : 0;
+    // operands -> shared memory, in flight while P^-1 is formed: row block K (R slice + update
+    // part) and, stg, this CTA's own rows; one bulk copy per row and range by one thread (the
+    // per-element cp.async loops were ~40% of the kernel's instructions), else 8-byte cp.async
+    const bool ownst = stg && own && rb > 0;
+    const uint32_t bytes = (uint32_t)(sizeof(double) * (kb * (ns + nsu) + (ownst ? rb * (nsu + kb) : 0)));
+    if (bulk) {
+      // warp 0 issues: lane 0 arms the barrier, then lane r copies row r of every operand
+      // (one thread issuing all ~64 copies took ~3.5 us per step)
+      if (t < 32 && bytes > 0) {
+        fence_proxy_async();  // operands were written (generic proxy) before the grid barrier
+        if (t == 0) mb_expect_tx(&wbar, bytes);
+        __syncwarp();
+        const int r = t & (kGjB - 1);
+        if (t < kGjB && r < kb) {
+          const double* src = A + (int64_t)(k0 + r) * n;
+          if (ns) bulk_g2s(Ws + r * Lo.LW, src + j0, (uint32_t)(sizeof(double) * ns), &wbar);
+          if (nsu) bulk_g2s(Ws + r * Lo.LW + Lo.LS, src + u0, (uint32_t)(sizeof(double) * nsu), &wbar);
+        }
+        if (ownst && t >= kGjB && r < rb) {
+          bulk_g2s(Os + r * Lo.LU, rows + (int64_t)r * n + u0, (uint32_t)(sizeof(double) * nsu), &wbar);
+          bulk_g2s(Fs + r * kGjB, rows + (int64_t)r * n + k0, (uint32_t)(sizeof(double) * kb), &wbar);
+        }
       }
-    cp_async_commit();
+    } else {
+      for (int r = 0; r < kb; ++r) {
+        const double* src = A + (int64_t)(k0 + r) * n;
+        for (int q = t; q < ns + nsu; q += nt) {
+          const bool sl = q < ns;
+          const int j = sl ? j0 + q : u0 + (q - ns);
+          cp_async8(Ws + r * Lo.LW + (sl ? q : Lo.LS + (q - ns)), src + j, true);
+        }
+      }
+      cp_async_commit();
+    }
+    GJ_MARK(0);
     // P^-1 in warp 0: lane l holds column l of [P | I] (rows in registers), Gauss-Jordan by
     // shuffles (SPD pivots, no pivoting; a short last block is padded with identity rows)
     if (t < 32) {
@@ -475,25 +548,33 @@ __global__ void __launch_bounds__(512, 1) k_mg_gj_inverse(int n, double* __restr
         for (int r = 0; r < kGjB; ++r) Pi[r][lane - kGjB] = col[r];
       }
     }
+    GJ_MARK(1);
+    if (!bulk) {
+      cp_async_wait<0>();
+    } else if (bytes > 0) {
+      mb_wait(&wbar, wphase);
+      wphase ^= 1u;
+    }
+    GJ_MARK(2);
     __syncthreads();
+    GJ_MARK(3);
     // Gm = F P^-1, F = this row block's K columns (old)
     if (own && t < kGjB * kGjB) {
       const int r = t / kGjB, p = t % kGjB;
       double f[kGjB];
 #pragma unroll
-      for (int m = 0; m < kGjB; ++m) f[m] = (r < rb && m < kb) ? __ldcg(rows + (int64_t)r * n + k0 + m) : 0.0;
+      for (int m = 0; m < kGjB; ++m)
+        f[m] = (r < rb && m < kb) ? (ownst ? Fs[r * kGjB + m] : __ldcg(rows + (int64_t)r * n + k0 + m)) : 0.0;
       double acc = 0.0;
 #pragma unroll
       for (int m = 0; m < kGjB; ++m) acc = fma(f[m], Pi[m][p], acc);
       Gm[r][p] = (p < kb) ? acc : 0.0;
     }
-    cp_async_wait<0>();
-    __syncthreads();
     // this CTA's slice of R = P^-1 [row block K] (R[:, K cols] = P^-1), parked for owner K
-    {
+    if (ns > 0) {
       double* g = G + (int64_t)(K & 1) * kGjB * n;
-      for (int q = t; q < kGjB * (j1 - j0); q += nt) {
-        const int r = q / (j1 - j0), j = j0 + q % (j1 - j0);
+      for (int q = t; q < kGjB * ns; q += nt) {
+        const int r = q / ns, jj = q - r * ns, j = j0 + jj;
         if (r >= kb) continue;
         double acc;
         if (j >= k0 && j < k0 + kb) {
@@ -502,36 +583,67 @@ __global__ void __launch_bounds__(512, 1) k_mg_gj_inverse(int n, double* __restr
           acc = 0.0;
 #pragma unroll
           for (int m = 0; m < kGjB; ++m)
-            if (m < kb) acc = fma(Pi[r][m], W[m * n + j], acc);
+            if (m < kb) acc = fma(Pi[r][m], Ws[m * Lo.LW + jj], acc);
         }
         g[(int64_t)r * n + j] = acc;
       }
     }
-    // row i <- row i - Gm_i [row block K] off the K columns, -Gm_i on them (columns u0 .. u1)
+    GJ_MARK(4);
+    __syncthreads();  // Gm
+    GJ_MARK(5);
+    // row i <- row i - Gm_i [row block K] off the K columns, -Gm_i on them (columns u0 .. u1).
+    // The rank-16 update runs on the FP64 tensor cores: 8x8 output tiles (2 row tiles x the
+    // column tiles of [u0, u1)) spread over the warps, D = old + (-Gm) W by 4 m8n8k4 k-steps;
+    // the K columns are overwritten with -Gm afterwards (the general formula would give 0 there).
     if (own) {
-      for (int j = u0 + t; j < u1; j += nt) {
-        double w[kGjB], old[kGjB];
-        const bool kc = (j >= k0 && j < k0 + kb);
+      const int warp = t >> 5, nwarp = nt >> 5;
+      const int ntile = (nsu + 7) / 8;
+      const int ar = lane >> 2, ak = lane & 3;  // A fragment (row, k); B fragment (k, col) = (ak, ar)
+      double ga[2][4];                          // -Gm fragments: [row tile][k-step]
 #pragma unroll
-        for (int m = 0; m < kGjB; ++m) w[m] = (m < kb && !kc) ? W[m * n + j] : 0.0;
+      for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int r = 0; r < kGjB; ++r) old[r] = (r < rb && !kc) ? __ldcg(rows + (int64_t)r * n + j) : 0.0;
+        for (int ks = 0; ks < 4; ++ks) ga[mt][ks] = -Gm[mt * 8 + ar][ks * 4 + ak];
+      // a warp takes column tiles (both row tiles of a column tile share the B fragments), two
+      // independent DMMA chains in flight
+      for (int ct = warp; ct < ntile; ct += nwarp) {
+        const int jt = ct * 8;            // column tile, relative to u0
+        const int jc = jt + 2 * ak;       // D fragment columns jc, jc + 1
+        const int jb = jt + ar;           // B fragment column
+        double d[2][2];
 #pragma unroll
-        for (int r = 0; r < kGjB; ++r) {
-          if (r >= rb) continue;
-          double v;
-          if (kc) {
-            v = -Gm[r][j - k0];
-          } else {
-            v = old[r];
+        for (int mt = 0; mt < 2; ++mt) {
+          const int r = mt * 8 + ar;      // D fragment row
 #pragma unroll
-            for (int m = 0; m < kGjB; ++m) v = fma(-Gm[r][m], w[m], v);
+          for (int e = 0; e < 2; ++e)
+            d[mt][e] = (r < rb && jc + e < nsu)
+                           ? (ownst ? Os[r * Lo.LU + jc + e] : __ldcg(rows + (int64_t)r * n + u0 + jc + e))
+                           : 0.0;
+        }
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const int m = ks * 4 + ak;
+          const double b = (m < kb && jb < nsu) ? Ws[m * Lo.LW + Lo.LS + jb] : 0.0;
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(d[mt][0]), "+d"(d[mt][1])
+                         : "d"(ga[mt][ks]), "d"(b));
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int r = mt * 8 + ar;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = u0 + jc + e;
+            if (r < rb && jc + e < nsu) A[(int64_t)(r0 + r) * n + j] = (j >= k0 && j < k0 + kb) ? -Gm[r][j - k0] : d[mt][e];
           }
-          A[(int64_t)(r0 + r) * n + j] = v;
         }
       }
     }
+    GJ_MARK(6);
     grid_sync_flip(bar);
+    GJ_MARK(7);
   }
   // the last pivot block's rows are still parked in G
   if (c == 0) {
@@ -541,6 +653,16 @@ __global__ void __launch_bounds__(512, 1) k_mg_gj_inverse(int n, double* __restr
   }
   if (t == 0 && bad) atomicMax(info, bad);
 }
+
+#ifdef TB_GJ_PROF
+}  // namespace tb
+extern "C" int tb_gj_prof_read(unsigned long long* out16) {
+  if (cudaMemcpyFromSymbol(out16, tb::g_gj_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return 2;
+  static const unsigned long long zeros[16] = {};
+  return cudaMemcpyToSymbol(tb::g_gj_prof, zeros, sizeof(zeros)) != cudaSuccess ? 2 : 0;
+}
+namespace tb {
+#endif
 
 // ---------------------------------------------------------------------------------------
 // host side
@@ -660,7 +782,10 @@ int mg_build(tb_plan_impl* P) {
     int sms = 0, coop = 0, occ = 0;
     TB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P->device));
     TB_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, P->device));
-    const size_t smem = sizeof(double) * kGjB * (size_t)mg.ncoarse;
+    const GjLayout lo((int)mg.ncoarse, sms);
+    mg.gj_stg = lo.bulk((int)mg.ncoarse) && lo.smem(true) <= 200 * 1024;  // stage own rows when they fit
+    const size_t smem = lo.smem(mg.gj_stg);
+    mg.gj_smem = smem;
     TB_CUDA(cudaFuncSetAttribute(k_mg_gj_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     TB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mg_gj_inverse, 512, smem));
     const int64_t nblocks = (mg.ncoarse + kGjB - 1) / kGjB;
@@ -671,8 +796,6 @@ int mg_build(tb_plan_impl* P) {
     TB_CUDA(cudaMalloc(&mg.gj_bar, 64));
     TB_CUDA(cudaMallocHost(&mg.h_info, sizeof(int)));
     TB_CUDA(cudaMemset(mg.gj_bar, 0, 64));
-    TB_CUDA(cudaFuncSetAttribute(k_mg_gj_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(sizeof(double) * kGjB * (size_t)mg.ncoarse)));
   }
   mg.built = true;
   return TB_OK;
@@ -749,12 +872,12 @@ int mg_setup(tb_plan_impl* P, cudaStream_t s) {
     TB_CUDA(cudaMemsetAsync(mg.info, 0, sizeof(int), s));
     int nn = (int)n;
     double* A = mg.dense;
-    void* args[] = {(void*)&nn, (void*)&A, (void*)&mg.gj, (void*)&mg.gj_bar, (void*)&mg.info};
+    int stg = mg.gj_stg ? 1 : 0;
+    void* args[] = {(void*)&nn, (void*)&A, (void*)&mg.gj, (void*)&mg.gj_bar, (void*)&mg.info, (void*)&stg};
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    TB_CUDA(cudaLaunchCooperativeKernel((const void*)k_mg_gj_inverse, sms, 512, args,
-                                        sizeof(double) * kGjB * (size_t)n, s));
+    TB_CUDA(cudaLaunchCooperativeKernel((const void*)k_mg_gj_inverse, sms, 512, args, mg.gj_smem, s));
     tb::launched();
     // the pivot check is read after the solve's own stream sync (mg_check): no bubble here
     TB_CUDA(cudaMemcpyAsync(mg.h_info, mg.info, sizeof(int), cudaMemcpyDeviceToHost, s));

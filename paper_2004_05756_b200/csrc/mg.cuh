@@ -39,6 +39,8 @@ struct Mg {
   uint8_t* dirty = nullptr;    // level-1 coarse elements that need the general aggregation
   double* dense = nullptr;     // coarsest dense matrix scratch
   double* gj = nullptr;        // 2D: Gauss-Jordan parked pivot rows (2 x kGjB x n)
+  bool gj_stg = false;         // Gauss-Jordan stages the CTA's own rows in shared memory
+  size_t gj_smem = 0;          // its dynamic shared memory per CTA
   int* h_info = nullptr;       // pinned copy of the Gauss-Jordan pivot flag, read after the solve
   bool info_pending = false;
   unsigned int* gj_bar = nullptr;  // its grid barrier

@@ -152,7 +152,7 @@ void HelmOp::launch_fused(const PcgWork& w, const double* pold, double* pnew, cu
   if (g.dim == 2)
     k_pcg_fused<2, 1, false><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, filt->H2, nullptr, w.z, pold, pnew, w.q, w.st,
                                                                  w.partA());
-  else
+  else if (!(filt->iso3 && helm3d_launch_fused(g, filt->h4, w, pold, pnew, s)))
     k_pcg_fused<3, 1, false><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, filt->H3, nullptr, w.z, pold, pnew, w.q, w.st,
                                                                  w.partA());
 }
@@ -160,7 +160,7 @@ void HelmOp::launch_apply(const double* v, double* y, cudaStream_t s) const {
   const Grid& g = filt->g;
   if (g.dim == 2)
     { k_node_apply<2, 1, false><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, filt->H2, nullptr, v, y, nullptr); tb::launched(); }
-  else
+  else if (!(filt->iso3 && helm3d_launch_apply(g, filt->h4, v, y, s)))
     { k_node_apply<3, 1, false><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, filt->H3, nullptr, v, y, nullptr); tb::launched(); }
 }
 void HelmOp::launch_dinv(double* dinv, cudaStream_t s) const {
@@ -640,6 +640,7 @@ int tb_filter_create(int dim, int nx, int ny, int nz, double h, double radius, i
   }
   F->vol_share = pow(g.h, g.dim) / nn;  // b_e entries = h^d / 2^d (filtering.py:75-76)
   if (g.dim == 2) F->pat_ok = q4_pattern_values(1, F->H2.v, &F->pat);
+  if (g.dim == 3) F->iso3 = helm3d_iso(F->H3.v, F->h4);
   F->op.filt = F;
   F->op.persist_grid = (g.dim == 2) ? persist_grid_for<1, false>(g, &F->op.tiles) : 0;  // 3D: graph loop
   int rc = F->work.alloc(g.n_nodes, F->op.fused_blocks(), F->op.persist_grid > 0);

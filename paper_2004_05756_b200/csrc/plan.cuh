@@ -91,6 +91,8 @@ struct tb_filter_impl {
   Q4Pat pat{};       // 2D: pattern values of H2
   bool pat_ok = false;
   Mat<8> H3{};
+  bool iso3 = false;    // 3D: H3 has the cube symmetry -> 27-point stencil kernel (helm3d.cu)
+  double h4[4] = {0, 0, 0, 0};
   double* d_b = nullptr;
   // slab mode (tb_filter_set_owned_planes): ghost node planes masked (dinv 0), owned [k0, k1)
   uint8_t* d_fixed = nullptr;
@@ -107,6 +109,13 @@ void scalar_element_matrices(int dim, double h, double* S, double* M, double* s_
 Grid make_grid(int dim, int nx, int ny, int nz, double h);
 void finish_sum(int nb, const double* part, double* out, cudaStream_t s);
 int device_dot(const double* a, const double* b, int64_t n, double* scratch, double* out_dev, cudaStream_t s);
+
+// 3D Helmholtz operator as a constant-coefficient 27-point stencil (helm3d.cu)
+bool helm3d_iso(const double* H3, double* h4);
+bool helm3d_launch_fused(const Grid& g, const double* h4, const PcgWork& w, const double* pold, double* pnew,
+                         cudaStream_t s);
+bool helm3d_launch_apply(const Grid& g, const double* h4, const double* v, double* y, cudaStream_t s);
+int64_t helm3d_max_ctas(const Grid& g);
 
 // single-sweep 3D Jacobi-pCG (sweep.cu)
 int64_t sweep_size(const Grid& g);

@@ -43,3 +43,30 @@ def test_cfg2_hdm_and_rom_vs_reference(cuda):
     rs = rom.solve(basis, sol.rho, obj)
     assert abs(rs.j - float(G["rom_j"])) <= 1e-8 * abs(float(G["rom_j"]))
     assert abs(rs.residual_norm - float(G["rom_residual"])) <= 1e-6 * float(G["rom_residual"])
+
+
+def test_cfg2_full_fields_vs_oracle(cuda):
+    """Every entry of rho, u, s and g at full cfg 2 size against the CPU oracle (oracle/hdm.py,
+    SuperLU; pinned to the reference by golden_cfg1.npz in full and golden_cfg2.npz's samples),
+    not only the strided samples of the reference run."""
+    from oracle.fem import build_grid
+    from oracle.hdm import Filter, Hdm, Material
+
+    prob = configs.cfg2()
+    s = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, prob.radius), prob.f, prob.fixed,
+                     tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP), rtol=prob.rtol)
+    obj = tb.ComplianceObjective(s.f)
+    sol = s.solve(prob.psi, obj)
+    g = s.gradient(prob.psi, sol, obj)
+    sens = s.element_sensitivity(sol.rho, sol.u, sol.lam, obj)
+    grid = build_grid(600, 200, 1.0)
+    ora = Hdm(grid, prob.k_e, Filter(grid, prob.radius), prob.f, prob.fixed, Material(configs.RHO_L, configs.P_SIMP))
+    ref = ora.solve(prob.psi)
+    g_ref = ora.gradient(ref)
+    s_ref = ora.element_sensitivity(ref["rho"], ref["u"], ref["lam"])
+    assert abs(sol.j - ref["j"]) <= 1e-8 * abs(ref["j"])
+    assert np.max(np.abs(sol.rho - ref["rho"]) / ref["rho"]) <= 1e-6          # element-wise
+    assert np.linalg.norm(sol.u - ref["u"]) <= 1e-6 * np.linalg.norm(ref["u"])
+    assert np.linalg.norm(sens - s_ref) <= 1e-6 * np.linalg.norm(s_ref)
+    assert np.linalg.norm(g - g_ref) <= 1e-6 * np.linalg.norm(g_ref)
+    assert np.abs(g - g_ref).max() <= 1e-6 * np.abs(g_ref).max()

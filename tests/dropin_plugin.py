@@ -28,7 +28,19 @@ def patch():
 
     mods = [importlib.import_module(f"romtopt.{m}") for m in
             ("fem", "filtering", "hdm", "rom", "problems", "trustregion", "mma", "runner")]
-    swap = {"HdmSolver": tb.HdmSolver, "HelmholtzFilter": tb.HelmholtzFilter, "RomModel": tb.RomModel,
+    hdm_cls = tb.HdmSolver
+    pc, rt = os.environ.get("TB_DROPIN_PRECOND"), os.environ.get("TB_DROPIN_RTOL")
+    if pc or rt:  # diagnostics: the drop-in with another preconditioner / solve tolerance
+        class _Hdm(tb.HdmSolver):
+            def __init__(self, *a, **kw):
+                if pc:
+                    kw.setdefault("preconditioner", pc)
+                if rt:
+                    kw.setdefault("rtol", float(rt))
+                super().__init__(*a, **kw)
+
+        hdm_cls = _Hdm
+    swap = {"HdmSolver": hdm_cls, "HelmholtzFilter": tb.HelmholtzFilter, "RomModel": tb.RomModel,
             "ReducedBasis": tb.ReducedBasis, "gram_schmidt": tb.gram_schmidt, "pod": tb.pod}
     for m in mods + [romtopt]:
         for name, obj in swap.items():

@@ -93,8 +93,8 @@ __global__ void __launch_bounds__(kGsThreads) k_gs_atb(int64_t n, int c0, const 
                                                        const double* __restrict__ W, int nb, const GsCtl* ctl,
                                                        double* __restrict__ part) {
   extern __shared__ __align__(16) double gs_sm[];  // [2][kGsChunk * kGsLd] A, then [2][kGsB * kGsLd] B
-  double* sA[2] = {gs_sm, gs_sm + kGsChunk * kGsLd};
-  double* sB[2] = {gs_sm + 2 * kGsChunk * kGsLd, gs_sm + 2 * kGsChunk * kGsLd + kGsB * kGsLd};
+  auto sA = [&](int buf) { return gs_sm + buf * kGsChunk * kGsLd; };
+  auto sB = [&](int buf) { return gs_sm + 2 * kGsChunk * kGsLd + buf * kGsB * kGsLd; };
   const int nA = min(kGsChunk, ctl->nk0 - c0);
   const int nB = PANEL_Q ? ctl->nk - ctl->nk0 : nb;
   const double* B = PANEL_Q ? Q + (int64_t)ctl->nk0 * n : W;
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kGsThreads) k_gs_atb(int64_t n, int c0, const 
       const int cc = isA ? c : c - nA8;
       const bool ok = row < i1 && cc < (isA ? nA : nB);
       const double* src = (isA ? A : B) + (ok ? (int64_t)cc * n + row : 0);
-      cp_async8((isA ? sA[buf] : sB[buf]) + cc * kGsLd + r, src, ok);
+      cp_async8((isA ? sA(buf) : sB(buf)) + cc * kGsLd + r, src, ok);
     }
     cp_async_commit();
   };
@@ -134,8 +134,8 @@ __global__ void __launch_bounds__(kGsThreads) k_gs_atb(int64_t n, int c0, const 
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double* a_s = sA[s & 1];
-    const double* b_s = sB[s & 1];
+    const double* a_s = sA(s & 1);
+    const double* b_s = sB(s & 1);
 #pragma unroll
     for (int t = 0; t < kGsTpw; ++t) {
       const int m0 = (warp + t * kGsWarps) * 8;

@@ -14,5 +14,8 @@ python -m pip install --no-index --no-build-isolation --no-deps --find-links /op
     --target "$REPO/baseline/_ref" "$TMP/pkg"
 mkdir -p "$REPO/baseline/_ref/romtopt_tests"
 cp "$SRC"/tests/*.py "$REPO/baseline/_ref/romtopt_tests/"
+# the reference's own cached MMA reference histories (mbb, cantilever, mbb-small), read by its
+# acceptance suite from <tests>/../.ref_cache
+if [ -d "$SRC/.ref_cache" ]; then cp -r "$SRC/.ref_cache" "$REPO/baseline/_ref/.ref_cache"; chmod -R u+w "$REPO/baseline/_ref/.ref_cache"; fi
 rm -rf "$TMP"
 echo "staged romtopt + tests in $REPO/baseline/_ref"

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes
 import hashlib
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -33,6 +34,24 @@ __all__ = [
     "StaleSolutionError",
     "psi_digest",
 ]
+
+
+_HOST_POOL = None
+
+
+def _host_pool():
+    """Worker threads for the host-side byte work of the numpy API (design snapshot, staleness
+    comparison): numpy releases the GIL for the copies and the solver's ctypes calls release it
+    while the device works, so the bytes are handled during the solve instead of after it."""
+    global _HOST_POOL
+    if _HOST_POOL is None:
+        _HOST_POOL = ThreadPoolExecutor(max_workers=2, thread_name_prefix="tb-host")
+    return _HOST_POOL
+
+
+def _same_bytes(psi, snap):
+    arr = np.ascontiguousarray(psi, dtype=float)
+    return arr.shape == snap.shape and np.array_equal(arr.view(np.uint64), snap.view(np.uint64))
 
 
 ROUNDOFF_RTOL = -1e-12  # tb_pcg_solve round-off mode: target 1e-12, stagnation <= 1e-7 accepted
@@ -290,6 +309,9 @@ class HdmSolver:
         psi_d = _lib.to_dev(psi, self.device)
         if tuple(psi_d.shape) != (self.mesh.n_elems,):
             raise ValueError(f"psi must have length {self.mesh.n_elems}, got shape {tuple(psi_d.shape)}")
+        # numpy design: its byte snapshot (for gradient's staleness check) is taken by a worker
+        # thread while the device filters and solves
+        snap_job = None if native else _host_pool().submit(np.array, psi, dtype=float, copy=True)
         rho_d, clamp_width = self.filtered_density_device(psi_d)
         rho_host = None if native else _lib.to_host_async(rho_d)  # lands while the solve runs
         # the clamp guarantees [rho_l, 1]; NaN input surfaces as a pCG breakdown
@@ -316,7 +338,7 @@ class HdmSolver:
                                iterations=iters, relres=relres)
         # numpy design: keep a byte snapshot; psi_hash (SHA-256, hdm.py:36-37) is computed on
         # first request and gradient() compares bytes directly (same strictness, no hashing)
-        snap = np.array(psi, dtype=float, copy=True)
+        snap = snap_job.result()
         sol = HdmSolution(None, rho_u, u_u, lam_u, j, clamp_width, None, psi_ref=(snap, None, None),
                           iterations=iters, relres=relres)
         sol._dev = ((rho_u, u_u, lam_u), (rho_d, u_d, u_d if lam_u is u_u else None))
@@ -334,11 +356,12 @@ class HdmSolver:
                 same = tuple(snap.shape) == tuple(psi.shape) and bool(
                     _lib.torch().equal(snap, psi.to(snap.device, snap.dtype)))
         elif not native and ref is not None and isinstance(ref[0], np.ndarray):
-            arr = np.ascontiguousarray(psi, dtype=float)
-            same = arr.shape == ref[0].shape and np.array_equal(arr.view(np.uint64), ref[0].view(np.uint64))
+            # compared by a worker thread while the device computes the gradient; a mismatch
+            # raises before anything is returned (the gradient does not touch RunStats)
+            same = _host_pool().submit(_same_bytes, psi, ref[0])
         else:
             same = psi_digest(psi) == solution.psi_hash
-        if not same:
+        if same is False:
             raise StaleSolutionError("solution was computed at a different design than psi")
         dev = solution._dev
         if (dev is not None and dev[1][2] is not None and solution.rho is dev[0][0] and solution.u is dev[0][1]
@@ -346,7 +369,10 @@ class HdmSolver:
             s_d = self.sensitivity_device(dev[1][0], dev[1][1], dev[1][2])  # device copies, no re-upload
         else:
             s_d = self._sensitivity(solution.rho, solution.u, solution.lam, objective)
-        return self._user(self.filter.apply_adjoint_device(s_d), native)
+        g_d = self.filter.apply_adjoint_device(s_d)
+        if not isinstance(same, bool) and not same.result():
+            raise StaleSolutionError("solution was computed at a different design than psi")
+        return self._user(g_d, native)
 
     def _sensitivity(self, rho, u, lam, objective):
         rho_d = _lib.to_dev(rho, self.device)

@@ -1,4 +1,5 @@
-"""Where the numpy-API (e2e) evaluation spends time beyond the device-resident one (cfg2)."""
+"""Where the numpy-API (e2e) evaluation spends time beyond the device-resident one (argv[1]:
+cfg2 multigrid, default, or cfg3 Jacobi: the headline)."""
 import os
 import sys
 import time
@@ -10,10 +11,11 @@ import torch  # noqa: E402
 import paper_2004_05756_b200 as tb  # noqa: E402
 from paper_2004_05756_b200 import configs  # noqa: E402
 
-prob = configs.cfg2()
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+prob = getattr(configs, name)()
 s = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, prob.radius), prob.f, prob.fixed,
                  tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP), rtol=prob.rtol,
-                 preconditioner="mg")
+                 preconditioner="mg" if name == "cfg2" else "jacobi")
 obj = tb.ComplianceObjective(s.f)
 psi_h = np.ascontiguousarray(prob.psi)
 psi_d = torch.as_tensor(psi_h, device="cuda")

@@ -551,32 +551,47 @@ def roofline_3d(tb, _lib, solver, rho_d, pk, torch, live=None):
 
 def apply_roofline(solver, rho_d, pk, torch):
     """K(rho)u GDOF/s (HdmSolver.apply_stiffness, hdm.py:224-233, alpha(rho) included):
-    20 calls captured in a CUDA graph, median of 5 replays; bytes 8(2 N_u + N_e)."""
+    20 calls captured in a CUDA graph, median of 5 replays; bytes 8(2 N_u + N_e).  Reported
+    twice: back-to-back on one (rho, v) -- at cfg 3 the ~100 MB of operands can stay in the
+    126 MB L2 -- and cold, the calls cycling through 4 distinct (rho, v) pairs (~230 MB of
+    inputs), so every call streams its operands from HBM."""
     m = solver.mesh
     n_u = m.n_dofs
-    v = torch.randn(n_u, dtype=torch.float64, device=rho_d.device)
-    for _ in range(3):
-        solver.apply_device(rho_d, v)
-    torch.cuda.synchronize()
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
-        for _ in range(20):
-            solver.apply_device(rho_d, v)
-    graph.replay()
-    torch.cuda.synchronize()
-    ts = []
-    for _ in range(5):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        graph.replay()
-        b.record()
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b) / 20 * 1e-3)
-    t = statistics.median(ts)
     by = 8 * (2 * n_u + m.n_elems)
+
+    def timed(pairs):
+        for r, v in pairs:
+            solver.apply_device(r, v)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for i in range(20):
+                r, v = pairs[i % len(pairs)]
+                solver.apply_device(r, v)
+        graph.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            graph.replay()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) / 20 * 1e-3)
+        del graph
+        return statistics.median(ts)
+
+    v = torch.randn(n_u, dtype=torch.float64, device=rho_d.device)
+    t = timed([(rho_d, v)])
+    cold = [(rho_d.clone(), torch.randn(n_u, dtype=torch.float64, device=rho_d.device)) for _ in range(4)]
+    tc = timed(cold)
+    del cold
     return {"us_per_call": t * 1e6, "gdofs": n_u / t / 1e9, "bytes_per_launch": by, "achieved_gbs": by / t / 1e9,
             "frac": by / t / 1e9 / pk["hbm_gbs"],
-            "note": "back-to-back calls: v and rho may be L2-resident between calls when they fit in 126 MB"}
+            "note": "back-to-back calls: v and rho may be L2-resident between calls when they fit in 126 MB",
+            "cold": {"us_per_call": tc * 1e6, "gdofs": n_u / tc / 1e9, "achieved_gbs": by / tc / 1e9,
+                     "frac": by / tc / 1e9 / pk["hbm_gbs"],
+                     "note": "calls cycle through 4 distinct (rho, v) pairs: operands streamed from HBM"}}
 
 
 def mg_bytes_per_iteration(nx, ny, min_dofs=1200):

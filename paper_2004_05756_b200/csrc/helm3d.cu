@@ -64,17 +64,29 @@ __global__ void __launch_bounds__(kHzT) k_helm3d(Grid g, HelmIso H, const double
     wr[m] = xp * H.h[m + 1];
   }
   const double cy[3] = {ym, ym + yp, yp};
-  // fetch slots: halo plane index f = t + s kHzT (two slots cover 340)
+  // fetch slots: halo plane index f = t + s kHzT (two slots cover 340); the in-plane offset,
+  // validity and ownership of each slot are fixed for the whole sweep
+  int64_t soff[2];
+  unsigned sok = 0, sown = 0;
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int f = t + s * kHzT;
+    const int lx = f % kHzPX, ly = f / kHzPX;
+    const int ni = i0 - 1 + lx, nj = j0 - 1 + ly;
+    const bool ok = f < kHzPlane && ni >= 0 && ni < g.nnx && nj >= 0 && nj < g.nny;
+    soff[s] = ok ? (int64_t)nj * g.nnx + ni : 0;
+    if (ok) sok |= 1u << s;
+    if (ok && lx >= 1 && lx <= kHzX && ly >= 1 && ly <= kHzY) sown |= 1u << s;
+  }
   auto issue = [&](int kp, int buf) {
     const bool zok = kp >= 0 && kp < g.nnz;
+    const int64_t po = zok ? (int64_t)kp * pn : 0;
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       const int f = t + s * kHzT;
       if (f < kHzPlane) {
-        const int lx = f % kHzPX, ly = f / kHzPX;
-        const int ni = i0 - 1 + lx, nj = j0 - 1 + ly;
-        const bool ok = zok && ni >= 0 && ni < g.nnx && nj >= 0 && nj < g.nny;
-        const int64_t off = ok ? (int64_t)kp * pn + (int64_t)nj * g.nnx + ni : 0;
+        const bool ok = zok && (sok >> s & 1u);
+        const int64_t off = ok ? po + soff[s] : 0;
         cp_async8(&stg[buf][0][f], z + off, ok);
         if (FUSED) cp_async8(&stg[buf][1][f], pold + off, ok);
       }
@@ -90,12 +102,7 @@ __global__ void __launch_bounds__(kHzT) k_helm3d(Grid g, HelmIso H, const double
       if (f < kHzPlane) {
         const double p = FUSED ? fma(beta, stg[buf][1][f], stg[buf][0][f]) : stg[buf][0][f];
         ring[slot][f] = p;
-        if (FUSED && pown) {
-          const int lx = f % kHzPX, ly = f / kHzPX;
-          const int ni = i0 - 1 + lx, nj = j0 - 1 + ly;
-          if (lx >= 1 && lx <= kHzX && ly >= 1 && ly <= kHzY && ni < g.nnx && nj < g.nny)
-            pnew[(int64_t)kp * pn + (int64_t)nj * g.nnx + ni] = p;
-        }
+        if (FUSED && pown && (sown >> s & 1u)) pnew[(int64_t)kp * pn + soff[s]] = p;
       }
     }
   };

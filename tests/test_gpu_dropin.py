@@ -1,7 +1,9 @@
 """The drop-in claim, tested with the reference's OWN code (SURVEY §4 strategy (1)):
 
-* the unmodified reference test modules of the hot path and its callers (pkg/tests/test_hdm.py,
-  test_filtering.py, test_rom.py, test_trustregion.py, test_problems.py, staged under baseline/_ref/romtopt_tests by tools/stage_reference.sh) run with
+* every unmodified reference test module but the acceptance suite (pkg/tests/test_hdm.py,
+  test_filtering.py, test_rom.py, test_trustregion.py, test_problems.py, test_fem.py, test_mma.py,
+  test_cli.py, test_report.py; 192 tests, staged under baseline/_ref/romtopt_tests by
+  tools/stage_reference.sh) runs with
   HdmSolver / HelmholtzFilter / RomModel / ReducedBasis / gram_schmidt / pod swapped for the B200
   classes (tests/dropin_plugin.py);
 * the reference's TrustRegionDriver.run (trustregion.py:383-513) on its built-in mbb-small
@@ -61,7 +63,8 @@ def test_reference_acceptance_on_dropin(cuda):
     assert "7 passed" in tail, tail
 
 @pytest.mark.parametrize("module", ["test_hdm.py", "test_filtering.py", "test_rom.py", "test_trustregion.py",
-                                    "test_problems.py"])
+                                    "test_problems.py", "test_fem.py", "test_mma.py", "test_cli.py",
+                                    "test_report.py"])
 def test_reference_suite_on_dropin(cuda, module):
     _need_ref()
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "dropin_plugin", "-p", "no:cacheprovider",

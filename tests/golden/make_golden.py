@@ -10,7 +10,8 @@ Files:
   golden_cfg1.npz   BASELINE cfg 1 (120x40): rho, phi, u, J, s, g, K(rho)v, ROM k=10 chain
   golden_small.npz  reference test-fixture problems (cantilever 6x2 / 12x4 / 4x2, filters)
   golden_cfg2.npz   BASELINE cfg 2 (600x200): scalars + strided samples (needs --with-cfg2)
-  ref3d_small.npz   reference HdmSolver / RomModel run on a duck-typed Hex8 mesh
+  ref3d_small.npz   reference HdmSolver / RomModel run on a duck-typed Hex8 mesh (6x3x3)
+  ref3d_medium.npz  the same at 20x10x10 (7,623 dofs)
   golden_mma.npz    reference MmaOptimizer trajectories (box + volume bound, move caps)
   golden_subproblem.npz  reference TrustRegionDriver.solve_subproblem on a 48x16 half-MBB
 """
@@ -179,7 +180,7 @@ def make_ref3d():
     """Reference solver code run unchanged on a duck-typed Hex8 mesh."""
     from oracle.fem import build_grid, elasticity_element_matrix as ke_any
 
-    for nx, ny, nz in ((6, 3, 3),):
+    for (nx, ny, nz), name in (((6, 3, 3), "ref3d_small.npz"), ((20, 10, 10), "ref3d_medium.npz")):
         g = build_grid(nx, ny, 1.0, nz=nz)
         mesh = SimpleNamespace(elem_dofs=g.elem_dofs, elem_nodes=g.elem_nodes, n_elems=g.n_elems, n_nodes=g.n_nodes,
                                n_dofs=g.n_dofs, elem_volume=1.0, h=1.0, nx=nx, ny=ny)
@@ -210,7 +211,7 @@ def make_ref3d():
         rom = RomModel(solver)
         k_hat = rom.reduced_stiffness(basis, sol.rho)
         rs = rom.solve(basis, sol.rho, obj)
-        np.savez_compressed(os.path.join(HERE, "ref3d_small.npz"), psi=prob.psi, u=sol.u, j=sol.j, s=s, v=v, kv=kv,
+        np.savez_compressed(os.path.join(HERE, name), psi=prob.psi, u=sol.u, j=sol.j, s=s, v=v, kv=kv,
                             phi=phi, k_hat=k_hat, f_hat=basis.f_hat, uhat=rs.uhat, rom_j=rs.j,
                             rom_res=rs.residual_norm, dims=np.array([nx, ny, nz]))
         print("ref3d: J=%.10f  J_rom=%.10f" % (sol.j, rs.j))

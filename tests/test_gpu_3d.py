@@ -25,8 +25,11 @@ def build(prob, rtol=1e-12):
                         rtol=rtol)
 
 
-def test_kernels_vs_reference_duck_typed_3d(cuda):
-    G = golden("ref3d_small.npz")
+@pytest.mark.parametrize("fixture", ["ref3d_small.npz", "ref3d_medium.npz"])
+def test_kernels_vs_reference_duck_typed_3d(cuda, fixture):
+    """The reference's own HdmSolver / RomModel run unchanged on a duck-typed Hex8 mesh
+    (tests/golden/make_golden.py), 6x3x3 and 20x10x10 elements."""
+    G = golden(fixture)
     nx, ny, nz = (int(v) for v in G["dims"])
     prob = configs.cfg3(seed=1, nx=nx, ny=ny, nz=nz)
     s = build(prob)

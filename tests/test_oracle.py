@@ -91,8 +91,9 @@ def test_filter_fixtures_match_reference():
         assert np.abs(f.apply_adjoint(G[f"{key}_v"]) - G[f"{key}_adj"]).max() <= 1e-12
 
 
-def test_3d_oracle_matches_reference_on_duck_typed_mesh():
-    G = golden("ref3d_small.npz")
+@pytest.mark.parametrize("fixture", ["ref3d_small.npz", "ref3d_medium.npz"])
+def test_3d_oracle_matches_reference_on_duck_typed_mesh(fixture):
+    G = golden(fixture)
     nx, ny, nz = (int(v) for v in G["dims"])
     prob = configs.cfg3(seed=1, nx=nx, ny=ny, nz=nz)
     g = build_grid(nx, ny, 1.0, nz=nz)

@@ -48,6 +48,7 @@ struct MgpLevel {
 struct MgpArgs {
   MgpLevel L[kMgpMaxLv];
   int nlev, nu;  // levels; smoothing sweeps per side (1 or 2)
+  int fused;     // V(1,1) in tiled fused phases (TB_MGP_UNFUSED=1: one phase per operation)
   int64_t ncoarse;
   double omega;
   const double* ainv;   // coarsest dense inverse
@@ -94,9 +95,11 @@ __device__ __forceinline__ Rng cta_rng() { return {threadIdx.x, blockDim.x}; }
 // Every load is unconditional (out-of-grid neighbours read a clamped in-range address) and
 // only the accumulation is predicated, so all loads of a node are in flight together; the sums
 // are those of the graph path term by term.
-template <bool L0>
-__device__ __forceinline__ void mgp_apply(const MgpLevel& L, const Q4Pat& K, const double* __restrict__ alpha,
-                                          int n, const double* v, double (&out)[2]) {
+// (The operand comes from a functor V(dx, dy, node, out[2]) -- offsets in {0,1,2} around
+// (i, j) -- reading the stored vector or, in the fused phases, a shared-memory tile.)
+template <bool L0, class VF>
+__device__ __forceinline__ void mgp_apply_f(const MgpLevel& L, const Q4Pat& K, const double* __restrict__ alpha,
+                                            int n, const VF& V, double (&out)[2]) {
   const Grid& g = L.g;
   const int i = (int)(n % g.nnx), j = (int)(n / g.nnx);
   if (L0) {
@@ -108,9 +111,10 @@ __device__ __forceinline__ void mgp_apply(const MgpLevel& L, const Q4Pat& K, con
         const int ii = i + dx - 1, jj = j + dy - 1;
         const bool ok = ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
         const int64_t node = ok ? (int64_t)jj * g.nnx + ii : n;
-        const double v0 = __ldcg(v + 2 * node), v1 = __ldcg(v + 2 * node + 1);
-        P[dy * 3 + dx][0] = ok ? v0 : 0.0;
-        P[dy * 3 + dx][1] = ok ? v1 : 0.0;
+        double vv[2];
+        V(dx, dy, node, vv);
+        P[dy * 3 + dx][0] = ok ? vv[0] : 0.0;
+        P[dy * 3 + dx][1] = ok ? vv[1] : 0.0;
       }
     double a[4];
 #pragma unroll
@@ -129,7 +133,9 @@ __device__ __forceinline__ void mgp_apply(const MgpLevel& L, const Q4Pat& K, con
       const int ni = i + m % 3 - 1, nj = j + m / 3 - 1;
       const bool ok = ni >= 0 && ni < g.nnx && nj >= 0 && nj < g.nny;
       const int64_t nbn = ok ? (int64_t)nj * g.nnx + ni : n;
-      const double v0 = __ldcg(v + 2 * nbn), v1 = __ldcg(v + 2 * nbn + 1);
+      double vv[2];
+      V(m % 3, m / 3, nbn, vv);
+      const double v0 = vv[0], v1 = vv[1];
       const double* s = (m >= 4) ? L.st + (int64_t)(m - 4) * 4 * N + n : L.st + (int64_t)(4 - m) * 4 * N + nbn;
       const double s0 = __ldg(s), s1 = __ldg(s + N), s2 = __ldg(s + 2 * N), s3 = __ldg(s + 3 * N);
       if (ok) {
@@ -143,6 +149,17 @@ __device__ __forceinline__ void mgp_apply(const MgpLevel& L, const Q4Pat& K, con
       }
     }
   }
+}
+
+// y_n = (A_l v)_n for a stored vector v (written inside this kernel: L2 loads)
+template <bool L0>
+__device__ __forceinline__ void mgp_apply(const MgpLevel& L, const Q4Pat& K, const double* __restrict__ alpha,
+                                          int n, const double* v, double (&out)[2]) {
+  auto V = [v](int, int, int64_t node, double (&vv)[2]) {
+    vv[0] = __ldcg(v + 2 * node);
+    vv[1] = __ldcg(v + 2 * node + 1);
+  };
+  mgp_apply_f<L0>(L, K, alpha, n, V, out);
 }
 
 // out = in + omega D^-1 (b - A in)   (in == nullptr: out = omega D^-1 b)
@@ -255,6 +272,174 @@ __device__ __noinline__ void mgp_prolong(const MgpLevel& F, double* xf, const Mg
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Tiled fused phases of the V(1,1) cycle (one grid barrier fewer per level and direction).
+// R: residual of level F + restriction to level C.  A CTA takes a tile of kRtX x kRtY coarse
+//    nodes, stages the fine iterate around it in shared memory, evaluates the fine residuals of
+//    the tile's (2 kRtX + 1) x (2 kRtY + 1) restriction taps from there (~10% recomputed at tile
+//    seams), then restricts.
+// PS: prolongation + post-smoothing sweep.  A CTA takes a tile of kPtX x kPtY fine nodes, stages
+//    the prolongated iterate x + P~ xb_c on the tile and its halo, then sweeps from there.
+// The per-dof arithmetic is that of mgp_resid / mgp_restrict / mgp_prolong / mgp_sweep, so the
+// iterates are bitwise those of the phase-per-operation form.
+constexpr int kRtX = 16, kRtY = 8;                       // coarse tile of R
+constexpr int kRfX = 2 * kRtX + 1, kRfY = 2 * kRtY + 1;  // fine residual taps (33 x 17)
+constexpr int kRxX = kRfX + 2, kRxY = kRfY + 2;          // fine iterate around them (35 x 19)
+constexpr int kPtX = 32, kPtY = 16;                      // fine tile of PS (one node per thread)
+constexpr int kPiX = kPtX + 2, kPiY = kPtY + 2;          // prolongated iterate incl. halo
+constexpr int kTileX = (kRxX * kRxY > kPiX * kPiY) ? kRxX * kRxY : kPiX * kPiY;  // doubles x 2
+
+template <bool L0F>
+__device__ __noinline__ void mgp_tile_R(const MgpLevel& C, const MgpLevel& F, const Q4Pat K, const double* alpha,
+                                        const double* xf, double omega, bool sweep1, double* tx, double* tr) {
+  const Grid& gc = C.g;
+  const Grid& gf = F.g;
+  const int ntx = (gc.nnx + kRtX - 1) / kRtX, nty = (gc.nny + kRtY - 1) / kRtY;
+  const int t = threadIdx.x, nt = blockDim.x;
+#pragma unroll 1
+  for (int tile = blockIdx.x; tile < ntx * nty; tile += gridDim.x) {
+    const int I0 = (tile % ntx) * kRtX, J0 = (tile / ntx) * kRtY;
+    const int fx0 = 2 * I0 - 1, fy0 = 2 * J0 - 1;  // fine origin of the taps
+    for (int q = t; q < kRxX * kRxY; q += nt) {
+      const int gi = fx0 - 1 + q % kRxX, gj = fy0 - 1 + q / kRxX;
+      const bool ok = gi >= 0 && gi < gf.nnx && gj >= 0 && gj < gf.nny;
+      const int64_t node = ok ? (int64_t)gj * gf.nnx + gi : 0;
+      tx[2 * q] = ok ? __ldcg(xf + 2 * node) : 0.0;
+      tx[2 * q + 1] = ok ? __ldcg(xf + 2 * node + 1) : 0.0;
+    }
+    __syncthreads();
+    for (int q = t; q < kRfX * kRfY; q += nt) {
+      const int li = q % kRfX, lj = q / kRfX;
+      const int gi = fx0 + li, gj = fy0 + lj;
+      double r[2] = {0.0, 0.0};
+      if (gi >= 0 && gi < gf.nnx && gj >= 0 && gj < gf.nny) {
+        const int fn = gj * gf.nnx + gi;
+        auto V = [&](int dx, int dy, int64_t, double (&vv)[2]) {
+          const int idx = 2 * ((lj + dy) * kRxX + li + dx);
+          vv[0] = tx[idx];
+          vv[1] = tx[idx + 1];
+        };
+        double y[2];
+        mgp_apply_f<L0F>(F, K, alpha, fn, V, y);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int64_t d = 2 * (int64_t)fn + c;
+          r[c] = (__ldg(F.dinv + d) != 0.0) ? __ldcg(F.b + d) - y[c] : 0.0;
+        }
+      }
+      tr[2 * q] = r[0];
+      tr[2 * q + 1] = r[1];
+    }
+    __syncthreads();
+    for (int q = t; q < kRtX * kRtY; q += nt) {
+      const int I = I0 + q % kRtX, J = J0 + q / kRtX;
+      if (I < gc.nnx && J < gc.nny) {
+        double acc[2] = {0.0, 0.0};
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+          for (int dx = -1; dx <= 1; ++dx) {
+            const int fi = 2 * I + dx, fj = 2 * J + dy;
+            const double w = mgp_pw(fi, I, gf.nx) * mgp_pw(fj, J, gf.ny);
+            if (w != 0.0) {
+              const int idx = 2 * ((fj - fy0) * kRfX + fi - fx0);
+              acc[0] = fma(w, tr[idx], acc[0]);
+              acc[1] = fma(w, tr[idx + 1], acc[1]);
+            }
+          }
+        const int64_t n = (int64_t)J * gc.nnx + I;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int64_t d = 2 * n + c;
+          const double bc = __ldg(C.fixed + d) ? 0.0 : acc[c];
+          C.b[d] = bc;
+          if (sweep1) C.xa[d] = omega * __ldg(C.dinv + d) * bc;
+        }
+      }
+    }
+    __syncthreads();  // the tiles are reused by the next tile
+  }
+}
+
+// prolongated iterate at fine node (i, j): x_f + P~ xb_c on free dofs (mgp_prolong's arithmetic)
+__device__ __forceinline__ void mgp_prolonged(const MgpLevel& F, const double* xf, const MgpLevel& C, int i, int j,
+                                              double (&out)[2]) {
+  const Grid& gf = F.g;
+  const Grid& gc = C.g;
+  const int64_t m = (int64_t)j * gf.nnx + i;
+  int i0, ni, j0, nj;
+  if (!(i & 1)) { i0 = i >> 1; ni = 1; } else if (i == gf.nx) { i0 = (gf.nx + 1) >> 1; ni = 1; } else { i0 = i >> 1; ni = 2; }
+  if (!(j & 1)) { j0 = j >> 1; nj = 1; } else if (j == gf.ny) { j0 = (gf.ny + 1) >> 1; nj = 1; } else { j0 = j >> 1; nj = 2; }
+  const double w = (ni == 2 ? 0.5 : 1.0) * (nj == 2 ? 0.5 : 1.0);
+  const int i1 = min(i0 + 1, gc.nnx - 1), j1 = min(j0 + 1, gc.nny - 1);
+  const int64_t c00 = 2 * ((int64_t)j0 * gc.nnx + i0), c01 = 2 * ((int64_t)j0 * gc.nnx + i1);
+  const int64_t c10 = 2 * ((int64_t)j1 * gc.nnx + i0), c11 = 2 * ((int64_t)j1 * gc.nnx + i1);
+  double v[4][2];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    v[0][c] = __ldcg(C.xb + c00 + c);
+    v[1][c] = __ldcg(C.xb + c01 + c);
+    v[2][c] = __ldcg(C.xb + c10 + c);
+    v[3][c] = __ldcg(C.xb + c11 + c);
+  }
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const double x0 = __ldcg(xf + 2 * m + c);
+    double acc = v[0][c];
+    if (ni == 2) acc += v[1][c];
+    if (nj == 2) {
+      acc += v[2][c];
+      if (ni == 2) acc += v[3][c];
+    }
+    out[c] = __ldg(F.fixed + 2 * m + c) ? x0 : fma(w, acc, x0);
+  }
+}
+
+// RZ: level 0 (z = out): accumulate r.z of the dofs written (the reduction that follows)
+template <bool L0F>
+__device__ __noinline__ void mgp_tile_PS(const MgpLevel& F, const double* xf, double* out, const MgpLevel& C,
+                                         const Q4Pat K, const double* alpha, double omega, double* tin,
+                                         double* rz) {
+  const Grid& gf = F.g;
+  const int ntx = (gf.nnx + kPtX - 1) / kPtX, nty = (gf.nny + kPtY - 1) / kPtY;
+  const int t = threadIdx.x, nt = blockDim.x;
+#pragma unroll 1
+  for (int tile = blockIdx.x; tile < ntx * nty; tile += gridDim.x) {
+    const int i0 = (tile % ntx) * kPtX, j0 = (tile / ntx) * kPtY;
+    for (int q = t; q < kPiX * kPiY; q += nt) {
+      const int gi = i0 - 1 + q % kPiX, gj = j0 - 1 + q / kPiX;
+      double v[2] = {0.0, 0.0};
+      if (gi >= 0 && gi < gf.nnx && gj >= 0 && gj < gf.nny) mgp_prolonged(F, xf, C, gi, gj, v);
+      tin[2 * q] = v[0];
+      tin[2 * q + 1] = v[1];
+    }
+    __syncthreads();
+    for (int q = t; q < kPtX * kPtY; q += nt) {
+      const int li = q % kPtX, lj = q / kPtX;
+      const int gi = i0 + li, gj = j0 + lj;
+      if (gi < gf.nnx && gj < gf.nny) {
+        const int n = gj * gf.nnx + gi;
+        auto V = [&](int dx, int dy, int64_t, double (&vv)[2]) {
+          const int idx = 2 * ((lj + dy) * kPiX + li + dx);
+          vv[0] = tin[idx];
+          vv[1] = tin[idx + 1];
+        };
+        double y[2];
+        mgp_apply_f<L0F>(F, K, alpha, n, V, y);
+        const int self = 2 * ((lj + 1) * kPiX + li + 1);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int64_t d = 2 * (int64_t)n + c;
+          const double o = tin[self + c] + omega * __ldg(F.dinv + d) * (__ldcg(F.b + d) - y[c]);
+          out[d] = o;
+          if (rz != nullptr) *rz = fma(__ldcg(F.b + d), o, *rz);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // xb_c = Ainv b_c, one warp per row over the grid (fixed-order lane partials)
 __device__ __forceinline__ void mgp_dense(const MgpLevel& C, const double* __restrict__ ainv, int64_t n) {
   const int lane = threadIdx.x & 31;
@@ -289,6 +474,8 @@ __device__ __forceinline__ double mgp_sum(const double* part, int k) {
 
 __global__ void __launch_bounds__(kMgpThreads, 1) k_mgpcg2d(Q4Pat K, MgpArgs a) {
   __shared__ MgpLevel sL[kMgpMaxLv];
+  __shared__ double s_tx[2 * kTileX];            // fused phases: staged fine iterate
+  __shared__ double s_tr[2 * kRfX * kRfY];       // fused restriction: fine residual taps
   for (int l = threadIdx.x; l < a.nlev; l += blockDim.x) sL[l] = a.L[l];
   __syncthreads();
   PcgState* st = a.st;
@@ -300,6 +487,7 @@ __global__ void __launch_bounds__(kMgpThreads, 1) k_mgpcg2d(Q4Pat K, MgpArgs a) 
   int done = 0;
   const int nlev = a.nlev, lg = nlev - 1;  // grid levels 0 .. nlev-2, then the dense coarsest
   const int nu = a.nu;
+  const bool fused = a.fused != 0;
   const double* alpha_e = a.alpha;
   double* x = a.x;
   double* r = a.r;
@@ -387,6 +575,35 @@ __global__ void __launch_bounds__(kMgpThreads, 1) k_mgpcg2d(Q4Pat K, MgpArgs a) 
     }
     // ---- rest of the V-cycle: z = M^-1 r.  V(nu, nu), nu in {1, 2}: the pre-smoothed iterate
     // is xa (nu = 1) or xb (nu = 2); the final iterate of every level ends in xb.
+    double rzn;
+    if (nu == 1 && fused) {
+      // V(1,1) in tiled fused phases (see mgp_tile_R / mgp_tile_PS): 12 grid barriers per
+      // iteration instead of 19
+      for (int l = 1; l <= lg; ++l) {  // level lg = the dense coarsest (no pre-smoothing there)
+        if (l == 1) mgp_tile_R<true>(sL[1], sL[0], K, alpha_e, sL[0].xa, omega, l < lg, s_tx, s_tr);
+        else mgp_tile_R<false>(sL[l], sL[l - 1], K, alpha_e, sL[l - 1].xa, omega, l < lg, s_tx, s_tr);
+        grid_sync_flip(bar);
+        MGP_MARK(8 + l - 1);
+      }
+      mgp_dense(sL[nlev - 1], a.ainv, a.ncoarse);
+      MGP_MARK(3);
+      grid_sync_flip(bar);
+      double rzp[1] = {0.0};
+      for (int l = lg - 1; l >= 0; --l) {
+        MgpLevel& L = sL[l];
+        if (l == 0) {
+          mgp_tile_PS<true>(L, L.xa, L.xb, sL[1], K, alpha_e, omega, s_tx, &rzp[0]);  // z = xb of level 0
+        } else {
+          mgp_tile_PS<false>(L, L.xa, L.xb, sL[l + 1], K, alpha_e, omega, s_tx, nullptr);
+          grid_sync_flip(bar);
+        }
+        MGP_MARK(16 + l);
+      }
+      publish_partials_grid_sync<1>(rzp, part + 2 * gridDim.x, bar, false);
+      rzn = mgp_sum(part, 2);
+    } else {
+    // ---- rest of the V-cycle: z = M^-1 r.  V(nu, nu), nu in {1, 2}: the pre-smoothed iterate
+    // is xa (nu = 1) or xb (nu = 2); the final iterate of every level ends in xb.
     for (int l = 0; l < lg; ++l) {
       MgpLevel& L = sL[l];
       if (l > 0) {
@@ -428,14 +645,15 @@ __global__ void __launch_bounds__(kMgpThreads, 1) k_mgpcg2d(Q4Pat K, MgpArgs a) 
       }
       MGP_MARK(16 + l);
     }
-    // ---- r.z (z = xb of level 0, this thread's own dofs), beta
+    // ---- r.z (z = xb of level 0, this thread's own dofs)
     double rzp[1] = {0.0};
 #pragma unroll 1
     for (int n = (int)G.start; n < (int)N0; n += (int)G.stride)
 #pragma unroll
       for (int c = 0; c < 2; ++c) rzp[0] = fma(__ldcg(r + 2 * n + c), __ldcg(z + 2 * n + c), rzp[0]);
     publish_partials_grid_sync<1>(rzp, part + 2 * gridDim.x, bar, false);
-    const double rzn = mgp_sum(part, 2);
+    rzn = mgp_sum(part, 2);
+    }
     MGP_MARK(16);
     beta = first ? 0.0 : rzn / rz;
     rz = rzn;
@@ -481,6 +699,7 @@ bool mg_pcg2d_persistent(tb_plan_impl* P, PcgWork& w, cudaStream_t s) {
   MgpArgs a{};
   a.nlev = (int)mg.lv.size();
   a.nu = mg.nu;
+  a.fused = getenv("TB_MGP_UNFUSED") == nullptr ? 1 : 0;
   for (int l = 0; l < a.nlev; ++l) {
     const MgLevel& L = mg.lv[l];
     MgpLevel& d = a.L[l];

@@ -282,10 +282,16 @@ __device__ __noinline__ void mgp_prolong(const MgpLevel& F, double* xf, const Mg
 //    the prolongated iterate x + P~ xb_c on the tile and its halo, then sweeps from there.
 // The per-dof arithmetic is that of mgp_resid / mgp_restrict / mgp_prolong / mgp_sweep, so the
 // iterates are bitwise those of the phase-per-operation form.
-constexpr int kRtX = 16, kRtY = 8;                       // coarse tile of R
+#ifndef TB_MGP_RTY
+#define TB_MGP_RTY 8
+#endif
+#ifndef TB_MGP_PTY
+#define TB_MGP_PTY 16
+#endif
+constexpr int kRtX = 16, kRtY = TB_MGP_RTY;              // coarse tile of R
 constexpr int kRfX = 2 * kRtX + 1, kRfY = 2 * kRtY + 1;  // fine residual taps (33 x 17)
 constexpr int kRxX = kRfX + 2, kRxY = kRfY + 2;          // fine iterate around them (35 x 19)
-constexpr int kPtX = 32, kPtY = 16;                      // fine tile of PS (one node per thread)
+constexpr int kPtX = 32, kPtY = TB_MGP_PTY;              // fine tile of PS (one node per thread at 16)
 constexpr int kPiX = kPtX + 2, kPiY = kPtY + 2;          // prolongated iterate incl. halo
 constexpr int kTileX = (kRxX * kRxY > kPiX * kPiY) ? kRxX * kRxY : kPiX * kPiY;  // doubles x 2
 

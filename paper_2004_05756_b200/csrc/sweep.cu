@@ -62,7 +62,7 @@ constexpr int kStage = 3 * kTPlaneS + kTNPlaneS + 2 * kTOPlaneS;   // 4400 doubl
 constexpr uint32_t kHaloBytes = sizeof(double) * kTPlane;
 constexpr uint32_t kNodeBytes = sizeof(double) * kTNPlane;
 constexpr uint32_t kOwnBytes = sizeof(double) * kTOPlane;
-constexpr int kSmemDoubles = 2 * kStage + 3 * kTPlaneS + 2 * 3 * kHT + 3 * kHT;
+constexpr int kSmemDoubles = 2 * kStage + 3 * kTPlaneS + 2 * 3 * kHT + 3 * kHT + kHT;  // + LAND slot table
 constexpr size_t kSweepSmem = sizeof(double) * kSmemDoubles + 2 * sizeof(uint64_t) + 128;  // + mbarriers + align
 
 enum { kModeCg = 0, kModeApply = 1, kModeCgLag = 2 };
@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
   double* U = STG + 2 * kStage;                        // [3][kTPlaneS] u node-plane ring
   double(*stage2)[3][kHT] = reinterpret_cast<double(*)[3][kHT]>(U + 3 * kTPlaneS);
   double* aring = U + 3 * kTPlaneS + 2 * 3 * kHT;      // [3][kHT] alpha of element planes ez .. ez+2
-  uint64_t* bar = reinterpret_cast<uint64_t*>(aring + 3 * kHT);  // [2]
+  uint32_t* lsl = reinterpret_cast<uint32_t*>(aring + 3 * kHT);  // [2][kHT] LAND slot descriptors
+  uint64_t* bar = reinterpret_cast<uint64_t*>(aring + 4 * kHT);  // [2]
 
   constexpr bool CG = MODE != kModeApply;
   double a_cg = 0.0, b_cg = 0.0, a_lag = 0.0;
@@ -169,6 +170,19 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
     single = 1 + (l >> 1) <= oylim && (mate < 3 || mate >= dlim);
   }
   const int64_t gbase = (int64_t)(j0 - 1) * V.pitch + 3 * (i0 - 1);  // pitched offset of tile (0, 0)
+  // LAND slot descriptors, loop-invariant (pairs h = t and t + kHT of every plane), packed so the
+  // per-plane pass does no index division: bits 0-8 h, 9-17 D^-1 tile index of the node of double
+  // f = 2h plus 1, 18-19 its component, 20 owned pair, 21-24 node row ly, 25-31 tile double d0 + 1
+  auto lslot = [&](int h) -> uint32_t {
+    const int f = 2 * h, ly = f / kTRow, d0 = f - ly * kTRow - shh;  // tile doubles d0, d0 + 1 of row ly
+    const int lx0 = (d0 + 3) / 3 - 1, c0 = d0 - 3 * lx0;               // d0 = -1 -> lx0 = -1 (unused slot)
+    const bool ow = ly >= 1 && ly <= oylim && d0 >= 3 && d0 + 1 < dlim;  // owned, inside the grid
+    return (uint32_t)h | (uint32_t)(ly * kTNRow + shn + lx0 + 1) << 9 | (uint32_t)c0 << 18 | (uint32_t)ow << 20 |
+           (uint32_t)ly << 21 | (uint32_t)(d0 + 1) << 25;
+  };
+  // kept in shared memory (one LDS per pair): as two more live registers they made the sweep spill
+  lsl[t] = lslot(t);
+  lsl[kHT + t] = lslot(min(t + kHT, kTPlane / 2 - 1));
   const bool own_in = own && i0 + onx < g.nnx && j0 + ony < g.nny;
   const int64_t obase = (int64_t)(j0 + ony) * V.pitch + 3 * (i0 + onx);  // this thread's owned node
   if (t == 0) {
@@ -211,33 +225,34 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
     const int kp = K0 - 1 + m;
     const bool pown = kp >= K0 && kp < K1;
     const int64_t pl = (int64_t)kp * V.plane;
-#pragma unroll 1
-    for (int h = t; h < kTPlane / 2; h += kHT) {
-      const int f = 2 * h;  // even box index: 16-byte aligned pairs in every tile (see below)
+    // one pair of tile doubles (f, f + 1) from its packed slot descriptor (see lslot)
+    auto pair = [&](uint32_t pk) {
+      const int f = 2 * (int)(pk & 511u);  // even box index: 16-byte aligned pairs in every tile
       if (MODE == kModeApply) {
         *reinterpret_cast<double2*>(ub + f) = *reinterpret_cast<const double2*>(B + f);
       } else {
-        const int ly = f / kTRow, d0 = f - ly * kTRow - shh;  // tile doubles d0, d0 + 1 of node row ly
-        const int lx0 = (d0 + 3) / 3 - 1, c0 = d0 - 3 * lx0;   // d0 = -1 -> lx0 = -1 (unused slot)
-        const int lx1 = lx0 + (c0 == 2), c1 = c0 == 2 ? 0 : c0 + 1;
-        const double* dnr = B + 3 * kTPlaneS + ly * kTNRow + shn;
-        const double dn0 = dnr[lx0], dn1 = dnr[lx1];
+        const int c0 = (int)(pk >> 18) & 3, c1 = c0 == 2 ? 0 : c0 + 1;  // components of f, f + 1
+        const double* dnr = B + 3 * kTPlaneS + (int)((pk >> 9) & 511u) - 1;  // node of double f
+        const double dn0 = dnr[0], dn1 = dnr[c0 == 2 ? 1 : 0];
         const bool fr0 = !((__double2loint(dn0) >> c0) & 1), fr1 = !((__double2loint(dn1) >> c1) & 1);
-        const double e0 = fr0 ? dn0 : 0.0, e1 = fr1 ? dn1 : 0.0;
         const double2 r = *reinterpret_cast<const double2*>(B + f);
         const double2 so = *reinterpret_cast<const double2*>(B + kTPlaneS + f);
         const double2 w = *reinterpret_cast<const double2*>(B + 2 * kTPlaneS + f);
-        const double sn0 = fr0 ? fma(b_cg, so.x, w.x) : 0.0, sn1 = fr1 ? fma(b_cg, so.y, w.y) : 0.0;
-        const double rn0 = fr0 ? fma(-a_cg, sn0, r.x) : 0.0, rn1 = fr1 ? fma(-a_cg, sn1, r.y) : 0.0;
-        const double un0 = e0 * rn0, un1 = e1 * rn1;
+        // fixed dofs: r = s = 0 in every stored iterate (k_sweep_prep/restart, and this update
+        // keeps them), so masking w alone gives s = r = u = 0 there -- bitwise the values of
+        // masking s, r and D^-1 separately, with 8 fewer selects per pair
+        const double sn0 = fma(b_cg, so.x, fr0 ? w.x : 0.0), sn1 = fma(b_cg, so.y, fr1 ? w.y : 0.0);
+        const double rn0 = fma(-a_cg, sn0, r.x), rn1 = fma(-a_cg, sn1, r.y);
+        const double un0 = dn0 * rn0, un1 = dn1 * rn1;
         *reinterpret_cast<double2*>(ub + f) = make_double2(un0, un1);
         // owned pairs: vector stores; the one or two unpaired owned dofs of a row go to the
         // singles pass below (93 owned doubles per row: odd)
-        if (pown && ly >= 1 && ly <= oylim && d0 >= 3 && d0 + 1 < dlim) {
+        if (pown && ((pk >> 20) & 1u)) {
+          const int ly = (int)(pk >> 21) & 15, d0 = (int)(pk >> 25) - 1;  // node row, tile double of f
           // owned-tile index and pitched offset are even: f even and sho - shh odd (see shh/sho)
           const int fo = 3 * kTPlaneS + kTNPlaneS + (ly - 1) * kTORow + (d0 - 3 + sho);
           const double2 po = *reinterpret_cast<const double2*>(B + fo + kTOPlaneS);
-          const double pn0 = fma(b_cg, po.x, e0 * r.x), pn1 = fma(b_cg, po.y, e1 * r.y);
+          const double pn0 = fma(b_cg, po.x, dn0 * r.x), pn1 = fma(b_cg, po.y, dn1 * r.y);
           const int64_t go = pl + gbase + (int64_t)ly * V.pitch + d0;
           if (MODE == kModeCg) {
             const double2 xo = *reinterpret_cast<const double2*>(B + fo);
@@ -253,28 +268,35 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
           acc[1] = fma(rn1, rn1, acc[1]);
         }
       }
-    }
+    };
+    pair(lsl[t]);
+    if (t < kTPlane / 2 - kHT) pair(lsl[kHT + t]);
     // singles: lanes 0..13 of the last warp (one pair each above) redo the pointwise update of
     // the unpaired owned dof at the low (even lane) or high (odd lane) end of owned row 1 + l/2
     // (same inputs, bitwise the same s, r, u as the pair pass) and store it
     if (CG && pown && single) {
-      const int l = t - (kHT - 32), ly = 1 + (l >> 1);
+      // the lane index is re-read here (volatile) so the compiler does not hoist this rare
+      // branch's index math out of the sweep loop: hoisted, it was spilled to local memory and
+      // reloaded after every barrier (k_hex8_cg<2>: 5.8% of the stall samples)
+      int tv;
+      asm volatile("mov.u32 %0, %%laneid;" : "=r"(tv));
+      const int l = tv, ly = 1 + (l >> 1);
       const int d = (l & 1) ? dlim - 1 : 3;
       const int f = ly * kTRow + d + shh, lx = d / 3, c = d - 3 * lx;
       const double dn = B[3 * kTPlaneS + ly * kTNRow + shn + lx];
       const bool fr = !((__double2loint(dn) >> c) & 1);
-      const double e = fr ? dn : 0.0, r = B[f];
-      const double sn = fr ? fma(b_cg, B[kTPlaneS + f], B[2 * kTPlaneS + f]) : 0.0;
-      const double rn = fr ? fma(-a_cg, sn, r) : 0.0;
+      const double r = B[f];
+      const double sn = fma(b_cg, B[kTPlaneS + f], fr ? B[2 * kTPlaneS + f] : 0.0);  // as the pairs
+      const double rn = fma(-a_cg, sn, r);
       const int fo = 3 * kTPlaneS + kTNPlaneS + (ly - 1) * kTORow + (d - 3 + sho);
       const double po = B[fo + kTOPlaneS];
-      const double pn = fma(b_cg, po, e * r);
+      const double pn = fma(b_cg, po, dn * r);
       const int64_t go = pl + gbase + (int64_t)ly * V.pitch + d;
       if (MODE == kModeCg) __stwb(V.x + go, fma(a_cg, pn, fma(a_lag, po, B[fo])));
       __stwb(rout + go, rn);
       __stwb(V.p + go, pn);
       __stwb(sout + go, sn);
-      acc[0] = fma(rn, e * rn, acc[0]);
+      acc[0] = fma(rn, dn * rn, acc[0]);
       acc[1] = fma(rn, rn, acc[1]);
     }
   };

@@ -99,6 +99,18 @@ __device__ __forceinline__ void tma_load3(double* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// Stores of the new iterate carry an L2 evict_last policy: an iteration writes ~200 MB at cfg 3
+// into a 126 MB L2 that the sweep's own reads (r, s, w of the old set: dead once read) stream
+// through as well; with the hint the planes written last survive until the next, reversed sweep
+// reads them first.  (evict_first on the dead loads instead evicts halo rows before the
+// neighbour CTA re-reads them: 100.2 against 93.5 us per sweep.)
+__device__ __forceinline__ void st_keep(double2* p, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 }  // namespace
 
 // Tensor maps of one plan's pitched vectors: halo tiles [100 x 9 x 1] of r, s, w (both parity
@@ -135,6 +147,15 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
   uint64_t* bar = reinterpret_cast<uint64_t*>(aring + 4 * kHT);  // [2]
 
   constexpr bool CG = MODE != kModeApply;
+  // Sweep direction.  The lagging sweeps run bottom-up, the catch-up sweeps top-down: a sweep then
+  // starts on the node planes its predecessor wrote last, which are still in the 126 MB L2 (an
+  // iteration writes ~200 MB at cfg 3), instead of on the ones written longest ago.  The top-down
+  // sweep is the mirror image: sweep plane m is node plane K1 - m, the carried face is the
+  // element's upper one, and the z stage swaps roles (same operands in every sum: node values
+  // bitwise those of the bottom-up sweep; the dot products add the planes in reverse order).
+  constexpr bool DOWN = MODE == kModeCg;
+  uint64_t kpol;  // L2 policy of the stores (see st_keep)
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(kpol));
   double a_cg = 0.0, b_cg = 0.0, a_lag = 0.0;
   if (CG) {
     if (st->done) return;
@@ -195,7 +216,7 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
   // completes once per use, so plane m waits on parity (m >> 1) & 1.
   auto issue = [&](int m) {
     if (t == 0) {
-      const int kp = K0 - 1 + m;
+      const int kp = DOWN ? K1 - m : K0 - 1 + m;
       double* B = STG + (m & 1) * kStage;
       uint64_t* bb = bar + (m & 1);
       const int cx = 3 * (i0 - 1) - shh, cy = j0 - 1;
@@ -222,7 +243,7 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
     mbar_wait(bar + (m & 1), (m >> 1) & 1);
     const double* B = STG + (m & 1) * kStage;
     double* ub = U + (m % 3) * kTPlaneS;
-    const int kp = K0 - 1 + m;
+    const int kp = DOWN ? K1 - m : K0 - 1 + m;
     const bool pown = kp >= K0 && kp < K1;
     const int64_t pl = (int64_t)kp * V.plane;
     // one pair of tile doubles (f, f + 1) from its packed slot descriptor (see lslot)
@@ -257,11 +278,11 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
           if (MODE == kModeCg) {
             const double2 xo = *reinterpret_cast<const double2*>(B + fo);
             const double xn0 = fma(a_cg, pn0, fma(a_lag, po.x, xo.x)), xn1 = fma(a_cg, pn1, fma(a_lag, po.y, xo.y));
-            __stwb(reinterpret_cast<double2*>(V.x + go), make_double2(xn0, xn1));
+            st_keep(reinterpret_cast<double2*>(V.x + go), make_double2(xn0, xn1), kpol);
           }
-          __stwb(reinterpret_cast<double2*>(rout + go), make_double2(rn0, rn1));
-          __stwb(reinterpret_cast<double2*>(V.p + go), make_double2(pn0, pn1));
-          __stwb(reinterpret_cast<double2*>(sout + go), make_double2(sn0, sn1));
+          st_keep(reinterpret_cast<double2*>(rout + go), make_double2(rn0, rn1), kpol);
+          st_keep(reinterpret_cast<double2*>(V.p + go), make_double2(pn0, pn1), kpol);
+          st_keep(reinterpret_cast<double2*>(sout + go), make_double2(sn0, sn1), kpol);
           acc[0] = fma(rn0, un0, acc[0]);
           acc[1] = fma(rn0, rn0, acc[1]);
           acc[0] = fma(rn1, un1, acc[0]);
@@ -292,10 +313,10 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
       const double po = B[fo + kTOPlaneS];
       const double pn = fma(b_cg, po, dn * r);
       const int64_t go = pl + gbase + (int64_t)ly * V.pitch + d;
-      if (MODE == kModeCg) __stwb(V.x + go, fma(a_cg, pn, fma(a_lag, po, B[fo])));
-      __stwb(rout + go, rn);
-      __stwb(V.p + go, pn);
-      __stwb(sout + go, sn);
+      if (MODE == kModeCg) st_keep(V.x + go, fma(a_cg, pn, fma(a_lag, po, B[fo])), kpol);
+      st_keep(rout + go, rn, kpol);
+      st_keep(V.p + go, pn, kpol);
+      st_keep(sout + go, sn, kpol);
       acc[0] = fma(rn, dn * rn, acc[0]);
       acc[1] = fma(rn, rn, acc[1]);
     }
@@ -325,12 +346,12 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
   const double* a_ptr = alpha + ((int64_t)gej * g.nx + gei);
   const int64_t a_stride = (int64_t)g.nx * g.ny;
   auto alpha_fetch = [&](int e, int slot) {  // element plane e (zero outside the grid / chunk)
-    const bool ok = col_ok && e >= 0 && e < g.nz && e < K1;
+    const bool ok = col_ok && e >= 0 && e < g.nz && e < K1 && e >= K0 - 1;
     cp_async8(aring + slot * kHT + t, ok ? a_ptr + (int64_t)e * a_stride : alpha, ok);
     cp_async_commit();
   };
-  alpha_fetch(K0 - 1, 0);
-  alpha_fetch(K0, 1);
+  alpha_fetch(DOWN ? K1 - 1 : K0 - 1, 0);
+  alpha_fetch(DOWN ? K1 - 2 : K0, 1);
   double fb[3][4];
   SW_FACE(0, fb);
   double tc[3][4];
@@ -343,10 +364,11 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
   // face (node plane rel + 1) loaded into `top`; unrolled by two below so the faces swap roles
   // instead of being copied
   auto step = [&](int rel, const double(&bot)[3][4], double(&top)[3][4]) {
-    const int ez = K0 - 1 + rel;
+    const int ez = DOWN ? K1 - 1 - rel : K0 - 1 + rel;  // element plane between sweep planes rel, rel + 1
+    const int kpo = DOWN ? K1 - rel : K0 - 1 + rel;     // node plane completed by this step (sweep plane rel)
     cp_async_wait<1>();  // this thread's alpha of plane ez (group rel) has landed
     const double a_cur = aring[(rel % 3) * kHT + t];
-    alpha_fetch(ez + 2, (rel + 2) % 3);
+    alpha_fetch(DOWN ? ez - 2 : ez + 2, (rel + 2) % 3);
     {  // ---- element (gei, gej, ez): spectrum from the bottom face + top face (plane rel+1) ----
       SW_FACE(((rel + 1) % 3) * kTPlaneS, top);
       double u[3][8];
@@ -355,7 +377,7 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
           u[c][s] = bot[c][s] + top[c][s];
-          u[c][s + 4] = bot[c][s] - top[c][s];
+          u[c][s + 4] = DOWN ? top[c][s] - bot[c][s] : bot[c][s] - top[c][s];  // lower face - upper face
         }
       hex8_iso_blocks(K, a_cur, u);
       double fq[3][4];
@@ -363,8 +385,10 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
       for (int c = 0; c < 3; ++c) {
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
-          fq[c][s] = tc[c][s] + (u[c][s] + u[c][s + 4]);
-          tc[c][s] = u[c][s] - u[c][s + 4];
+          // share of the completed plane (the element's lower face going up, upper going down)
+          // joins the neighbour element's carried share; the other face's share is carried on
+          fq[c][s] = tc[c][s] + (DOWN ? u[c][s] - u[c][s + 4] : u[c][s] + u[c][s + 4]);
+          tc[c][s] = DOWN ? u[c][s] + u[c][s + 4] : u[c][s] - u[c][s + 4];
         }
         const double s0 = fq[c][0] + fq[c][1], d0 = fq[c][0] - fq[c][1];
         const double s1 = fq[c][2] + fq[c][3], d1 = fq[c][2] - fq[c][3];
@@ -385,12 +409,12 @@ __global__ void __launch_bounds__(kHT, kHexCtas)
     if (own_in && rel >= 1) {  // owned node (px, py) of plane ez: w out, d = w.u
       const int e_dn = (py - 1) * kHX + (px - 1), e_up = py * kHX + (px - 1);
       const double* up = U + (rel % 3) * kTPlaneS + py * kTRow + shh + 3 * px;
-      double* dst = outv + (int64_t)ez * V.plane + obase;
+      double* dst = outv + (int64_t)kpo * V.plane + obase;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const double v = stage2[1][c][e_dn] + stage2[0][c][e_up];
         if (CG) acc[2] = fma(up[c], v, acc[2]);
-        __stwb(dst + c, v);
+        st_keep(dst + c, v, kpol);
       }
     }
     // plane rel + 2 (in flight for two steps) -> ring slot (rel + 2) % 3 = slot of plane rel - 1

@@ -657,6 +657,7 @@ int tb_filter_create(int dim, int nx, int ny, int nz, double h, double radius, i
     delete F;
     return rc;
   }
+  spectral_init(F);
   *out = reinterpret_cast<tb_filter*>(F);
   return TB_OK;
 }
@@ -665,6 +666,7 @@ int tb_filter_destroy(tb_filter* filt) {
   if (!filt) return TB_OK;
   auto* F = reinterpret_cast<tb_filter_impl*>(filt);
   cudaSetDevice(F->device);
+  spectral_release(F);
   F->work.release();
   if (F->d_b) cudaFree(F->d_b);
   if (F->d_fixed) cudaFree(F->d_fixed);
@@ -694,6 +696,16 @@ static int filter_single_mode(tb_filter_impl* F) {
   return F->work.set_fields(0, F->own_k0, F->own_k1);
 }
 
+// whole-grid H x = d_b into work.x: direct (spectral.cu, 0 iterations) or pCG
+static int filter_solve(tb_filter_impl* F, double rtol, int* iters, cudaStream_t s) {
+  if (F->spec != nullptr) {
+    if (iters) *iters = 0;
+    return spectral_solve(F, F->d_b, F->work.x, s);
+  }
+  TB_TRY(filter_single_mode(F));
+  return pcg_solve(F->op, F->work, F->d_b, F->work.x, rtol, 10000, iters, nullptr, s);
+}
+
 extern "C" {
 
 int tb_filter_apply(tb_filter* filt, const double* psi, double* phi, double* rho, double rtol, int* iters,
@@ -703,8 +715,7 @@ int tb_filter_apply(tb_filter* filt, const double* psi, double* phi, double* rho
   const Grid& g = F->g;
   cudaStream_t s = (cudaStream_t)stream;
   TB_TRY(tb_filter_load_vector(filt, psi, F->d_b, stream));
-  TB_TRY(filter_single_mode(F));
-  TB_TRY(pcg_solve(F->op, F->work, F->d_b, F->work.x, rtol, 10000, iters, nullptr, s));
+  TB_TRY(filter_solve(F, rtol, iters, s));
   const double inv_nn = (g.dim == 2) ? 0.25 : 0.125;
   if (g.dim == 2)
     { k_node_to_elem<2><<<nblk(g.n_elems), kBlock, 0, s>>>(g, F->work.x, inv_nn, rho); tb::launched(); }
@@ -726,8 +737,7 @@ int tb_filter_adjoint(tb_filter* filt, const double* v, double* w, double rtol, 
   else
     { k_elem_to_node<3><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, v, inv_nn, 1.0, F->d_b); tb::launched(); }
   TB_CHECK_LAUNCH();
-  TB_TRY(filter_single_mode(F));
-  TB_TRY(pcg_solve(F->op, F->work, F->d_b, F->work.x, rtol, 10000, iters, nullptr, s));
+  TB_TRY(filter_solve(F, rtol, iters, s));
   if (g.dim == 2)
     { k_node_to_elem<2><<<nblk(g.n_elems), kBlock, 0, s>>>(g, F->work.x, F->vol_share, w); tb::launched(); }
   else

@@ -11,6 +11,7 @@ namespace tb {
 struct tb_plan_impl;
 struct tb_filter_impl;
 struct SweepState;
+struct SpectralFilter;
 
 // SIMP elasticity operator  Z K(rho) Z  (alpha from the plan's d_alpha)
 struct ElastOp final : PcgOp {
@@ -99,7 +100,15 @@ struct tb_filter_impl {
   int dist = 0, own_k0 = 0, own_k1 = 1 << 30;
   HelmOp op;
   PcgWork work;
+  // direct solve of the whole-grid filter system by the tensor-product cosine basis
+  // (spectral.cu); null: pCG (slab phases, TB_FILTER_PCG=1, or a failed self-check)
+  SpectralFilter* spec = nullptr;
 };
+
+// direct Helmholtz filter solve (spectral.cu)
+void spectral_init(tb_filter_impl* F);
+void spectral_release(tb_filter_impl* F);
+int spectral_solve(tb_filter_impl* F, const double* b, double* phi, cudaStream_t s);
 
 // Integer Laplacian / mass tables of the scalar Q1 element: S_e = (h^(d-2)) S/s_div,
 // M_e = m_mul * M  (2D: S/6, h^2/36 M, fem.py:72-92; 3D: h S/12, h^3/216 M).

@@ -132,3 +132,26 @@ def test_3d_non_isotropic_element_matrix_falls_back_to_node_owner(cuda):
     phi = tb.gram_schmidt([np.where(s.free_mask, rng.standard_normal(prob.mesh.n_dofs), 0.0) for _ in range(4)])
     kh = tb.RomModel(s).reduced_stiffness(tb.ReducedBasis(phi, None, None, phi.T @ s.f), sol.rho)
     assert np.linalg.norm(kh - phi.T @ (k @ phi)) <= 1e-12 * np.linalg.norm(kh)
+
+
+@pytest.mark.parametrize("dims", [(12, 6, 5), (7, 9, 4)])
+def test_3d_filter_direct_solve_matches_pcg(cuda, monkeypatch, dims):
+    """The direct (tensor-product cosine basis, spectral.cu) whole-grid filter solve against the
+    pCG solve of the same system (TB_FILTER_PCG=1) and against the oracle's assembled operator
+    (filtering.py:59-76): filter and adjoint."""
+    nx, ny, nz = dims
+    prob = configs.cfg3(seed=5, nx=nx, ny=ny, nz=nz)
+    rng = np.random.default_rng(11)
+    psi = rng.uniform(0.01, 1.0, prob.mesh.n_elems)
+    v = rng.standard_normal(prob.mesh.n_elems)
+    direct = tb.HelmholtzFilter(prob.mesh, prob.radius)
+    monkeypatch.setenv("TB_FILTER_PCG", "1")
+    pcg = tb.HelmholtzFilter(prob.mesh, prob.radius)
+    monkeypatch.delenv("TB_FILTER_PCG")
+    a, b = direct.apply(psi), pcg.apply(psi)
+    assert nrel(a.rho, b.rho) <= 1e-10
+    assert nrel(direct.apply_adjoint(v), pcg.apply_adjoint(v)) <= 1e-10
+    g = build_grid(nx, ny, 1.0, nz=nz)
+    ora = Filter(g, prob.radius)
+    assert nrel(a.rho, ora.apply(psi)[1]) <= 1e-12
+    assert nrel(direct.apply_adjoint(v), ora.apply_adjoint(v)) <= 1e-12

@@ -517,7 +517,8 @@ def roofline_3d(tb, _lib, solver, rho_d, pk, torch, live=None):
         by = 8 * (9 * n_u + n_e)
         t = msf.value * 1e-3
         kern = ("k_hex8_cg (Chronopoulos-Gear Jacobi-pCG iteration in ONE z-sweep: TMA node planes, WHT-block Hex8 "
-                "operator, x/r/p/s/w updates, 3 dot products; x update lagged on every other sweep)")
+                "operator, x/r/p/s/w updates, 3 dot products; x update lagged on every other sweep; sweeps alternate z direction "
+                "and store with an L2 evict_last policy so each starts on L2-resident planes)")
         note = "bytes = one Jacobi-pCG iteration, 8(9 N_u + N_e) (SURVEY §8(d)); the kernel IS the iteration"
         upd = None
         if live is not None and live[1] > 0:
@@ -589,6 +590,9 @@ def apply_roofline(solver, rho_d, pk, torch):
     return {"us_per_call": t * 1e6, "gdofs": n_u / t / 1e9, "bytes_per_launch": by, "achieved_gbs": by / t / 1e9,
             "frac": by / t / 1e9 / pk["hbm_gbs"],
             "note": "back-to-back calls: v and rho may be L2-resident between calls when they fit in 126 MB",
+            "bound_note": ("3D Hex8: the WHT-block operator is FP64-pipe bound, not HBM bound (~165 FP64 "
+                           "instructions per element, ncu FP64 pipe 48% busy, arithmetic floor ~24 us at cfg 3; "
+                           "DESIGN.md 4.1); frac is against HBM as SURVEY 8(d) asks") if m.dim == 3 else None,
             "cold": {"us_per_call": tc * 1e6, "gdofs": n_u / tc / 1e9, "achieved_gbs": by / tc / 1e9,
                      "frac": by / tc / 1e9 / pk["hbm_gbs"],
                      "note": "calls cycle through 4 distinct (rho, v) pairs: operands streamed from HBM"}}
@@ -797,7 +801,9 @@ def run_ours(args):
                        "parallelism": "replicas" if world > 1 else "single",
                        "l2": ("256 MiB buffer written between steps (outside the step events); the cfg3 working set "
                               "(~350 MB of pCG vectors) also exceeds the 126 MB L2") if flush is not None else "no flush",
-                       "pcg_iterations": its, "seed": args.seed},
+                       "pcg_iterations": its, "seed": args.seed,
+                       "filter_solver": ("direct (tensor-product cosine basis, DMMA mode products; spectral.cu)"
+                                         if prob.mesh.dim == 3 else "persistent pCG (2D)")},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk, "apply": apply, "extra": extras,
         }

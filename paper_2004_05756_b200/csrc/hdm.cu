@@ -304,6 +304,23 @@ void tb_plan_impl::apply_alpha(const double* alpha, const double* v, double* y, 
     { k_node_apply<3, 3, true><<<nblk(g.n_nodes), kBlock, 0, s>>>(g, K3, alpha, v, y, fx); tb::launched(); }
 }
 
+// Hex8 operator with an epilogue on the owned nodes (k_hex8 EPI): epi 1: out = v + omega dinv (b - K v),
+// epi 2: out = dinv != 0 ? b - K v : 0.  out must not alias v (other CTAs read v's halo).
+bool tb_plan_impl::apply_alpha_epi(int epi, const double* alpha, const double* v, double* out, const double* b,
+                                   const double* dinv, double omega, cudaStream_t s) const {
+  if (g.dim != 3 || !hex8 || !hex8_epi) return false;
+  if (epi == 1)
+    k_hex8<false, false, 1><<<hex8_grid(g, zchunk), kHT, kHex8Smem, s>>>(g, hiso, alpha, v, nullptr, nullptr, out,
+                                                                         nullptr, nullptr, zchunk, 0.0, 3.0, nullptr,
+                                                                         nullptr, 0, 0, b, dinv, omega);
+  else
+    k_hex8<false, false, 2><<<hex8_grid(g, zchunk), kHT, kHex8Smem, s>>>(g, hiso, alpha, v, nullptr, nullptr, out,
+                                                                         nullptr, nullptr, zchunk, 0.0, 3.0, nullptr,
+                                                                         nullptr, 0, 0, b, dinv, omega);
+  tb::launched();
+  return true;
+}
+
 int tb_plan_impl::material(const double* rho, double* alpha, double* dalpha, cudaStream_t s) const {
   { k_material<<<grid_for(g.n_elems), kBlock, 0, s>>>(g.n_elems, rho_l, p, rho, alpha, dalpha); tb::launched(); }
   TB_CHECK_LAUNCH();
@@ -362,6 +379,11 @@ int tb_plan_create(int dim, int nx, int ny, int nz, double h, const double* k_e,
       cudaError_t e3 = cudaFuncSetAttribute(k_hex8<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHex8Smem);
       if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)
         P->hex8 = false;
+      P->hex8_epi = P->hex8 &&
+                    cudaFuncSetAttribute(k_hex8<false, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kHex8Smem) == cudaSuccess &&
+                    cudaFuncSetAttribute(k_hex8<false, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kHex8Smem) == cudaSuccess;
     }
   }
   if (dim == 2) P->op.persist_grid = persist_grid_for<2, true>(P->g, &P->op.tiles);

@@ -131,7 +131,13 @@ constexpr int kOSlots = (kOPlane + kHT - 1) / kHT;     // 3 store slots per thre
 // after its last flush.  Mask bytes read inside the sweep cost registers (spills) and ~8 us.
 // SIMP (!FUSED only, p = 3): `alpha` holds rho; alpha = rho_l + (1 - rho_l) rho^3 is formed per
 // element as it is loaded (same operation order as k_material), saving the material pass.
-template <bool FUSED, bool SIMP = false>
+// EPI (!FUSED only): epilogue on the owned nodes instead of out = K in (multigrid level 0, mg.cu):
+//   1: out = in + omega * ed * (eb - K in)   (damped-Jacobi sweep, ed = D^-1 with 0 on fixed dofs)
+//   2: out = ed != 0 ? eb - K in : 0          (masked residual)
+// eb / ed of the node plane gathered next travel by cp.async into the (otherwise unused) p_old
+// staging area one step ahead; `in` at the node is read from the staged plane.  This saves the
+// separate update kernel's pass over 5 (3) vectors per smoothing sweep (residual).
+template <bool FUSED, bool SIMP = false, int EPI = 0>
 __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const double* __restrict__ alpha,
                                                  const double* __restrict__ in, const double* __restrict__ in2,
                                                  double* __restrict__ pnew, double* __restrict__ out,
@@ -139,7 +145,10 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
                                                  int zchunk, double rho_l = 0.0, double p_simp = 3.0,
                                                  const int64_t* __restrict__ zidx = nullptr,
                                                  const int* __restrict__ zoff = nullptr,
-                                                 int64_t col_stride = 0, int zblocks = 0) {
+                                                 int64_t col_stride = 0, int zblocks = 0,
+                                                 const double* __restrict__ eb = nullptr,
+                                                 const double* __restrict__ ed = nullptr, double omega = 0.0) {
+  static_assert(EPI == 0 || !FUSED, "the epilogue modes belong to the plain operator");
   // plane[4][kPlane]: node planes (buffer = plane index mod 4), AoS rows as in global memory.
   // stage[2][2][3][kHT]: node-plane corner outputs (oy) already summed over the two
   // x-neighbour elements, double buffered by step parity.  ostg[2][kOPlane]: finished owned
@@ -252,12 +261,32 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
   // Ring buffers are indexed by the plane's position relative to the first plane of this CTA
   // (K0 - 1).
   double* pstg = ostg + 2 * kOPlane;  // [2][kPlane] p_old staging (FUSED)
+  // EPI: eb, ed of this thread's owned node on the plane gathered next: estg[2][3][kHT] in pstg
+  double* estg = pstg;
+  static_assert(2 * 3 * kHT <= 2 * kPlane, "epilogue staging must fit the p_old staging area");
+  const bool own_in = own && i0 + onx < g.nnx && j0 + ony < g.nny;
+  const int gnode = 3 * ((j0 + ony) * g.nnx + (i0 + onx));
+  auto epi_issue = [&](int kp) {  // own group: the plane issue that may follow commits its own
+    if (EPI != 0) {
+      if (own) {
+        const bool ok = own_in && kp >= K0 && kp < K1;
+        const int64_t off = ok ? (int64_t)kp * plane_dofs + gnode : 0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          cp_async8(estg + c * kHT + t, eb + off + c, ok);
+          cp_async8(estg + (3 + c) * kHT + t, ed + off + c, ok);
+        }
+      }
+      cp_async_commit();
+    }
+  };
 #define HEX8_PB(rel_) (((rel_) & 3) * kPlane)
 #define HEX8_PS(rel_) (pstg + ((rel_) & 1) * kPlane)
   HEX8_ISSUE(K0 - 1, HEX8_PB(0), HEX8_PS(0));
   HEX8_ISSUE(K0, HEX8_PB(1), HEX8_PS(1));
   // p_old of plane K0+1 is staged in the (still unused) buffer of plane K0+2
   HEX8_ISSUE(K0 + 1, HEX8_PB(2), plane + HEX8_PB(3));
+  epi_issue(K0);
   cp_async_wait<0>();
   HEX8_LAND(K0 - 1, HEX8_PB(0), HEX8_PS(0));
   HEX8_LAND(K0, HEX8_PB(1), HEX8_PS(1));
@@ -357,6 +386,8 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
       if (rel >= 1 && ez + 2 <= K1) {
         cp_async_wait<0>();
         HEX8_LAND(ez + 2, HEX8_PB(r + 2), HEX8_PS(r + 2));
+      } else if (EPI != 0) {
+        cp_async_wait<0>();  // this step's eb, ed
       }
       __syncthreads();
       if (rel >= 2) HEX8_FLUSH(ez - 1, (r + 1) & 1);  // plane ez-1 was staged before this barrier
@@ -368,13 +399,16 @@ __global__ void __launch_bounds__(kHT, kHexCtas) k_hex8(Grid g, Hex8Iso K, const
         const bool dot_here = dot_any && ez >= dk0 && ez < dk1;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const double v = stage2[r & 1][1][c][e_dn] + stage2[r & 1][0][c][e_up];
+          double v = stage2[r & 1][1][c][e_dn] + stage2[r & 1][0][c][e_up];
           if (FUSED && dot_here) acc[0] = fma(pp[c], v, acc[0]);  // p is 0 outside the grid
+          if (EPI == 1) v = pp[c] + omega * estg[(3 + c) * kHT + t] * (estg[c * kHT + t] - v);
+          if (EPI == 2) v = (estg[(3 + c) * kHT + t] != 0.0) ? estg[c * kHT + t] - v : 0.0;
           o[c] = v;
         }
       }
       // plane ez+3 reuses the buffer of plane ez-1, which every thread finished with before
       // this step's barrier
+      epi_issue(ez + 1);  // after this step's gather has read the staging slots (same thread)
       if (ez + 3 <= K1) HEX8_ISSUE(ez + 3, HEX8_PB(r + 3), HEX8_PS(r + 3));
     }
   }

@@ -3,6 +3,8 @@
 
 #include "cgcg2d.cuh"  // grid_sync_flip
 #include "mg.cuh"
+#include <utility>
+
 #include "plan.cuh"
 
 namespace tb {
@@ -932,6 +934,30 @@ static void vcycle(tb_plan_impl* P, size_t l, const double* b, double* x, cudaSt
   if (l + 1 == mg.lv.size()) {
     { k_mg_gemv<<<148 * 4, kBlock, 0, s>>>(L.n, mg.ainv, b, x); tb::launched(); }
     return;
+  }
+  // Level 0 of a Hex8 grid: the smoothing sweeps and the residual run as epilogues of the
+  // operator kernel (k_hex8 EPI; TB_MG_NOFUSE=1 keeps the separate update kernels).  A sweep
+  // cannot update in place (other CTAs read the halo of its input), so the iterate alternates
+  // between L.t and x; it starts in L.t and, after (nu - 1) + nu sweeps, ends in x.
+  static const bool nofuse = getenv("TB_MG_NOFUSE") != nullptr;
+  if (l == 0 && P->hex8_epi && !nofuse) {
+    double* cur = L.t;
+    double* oth = x;
+    { k_mg_jacobi<<<nb, kBlock, 0, s>>>(L.n, mg.omega, L.dinv, b, nullptr, nullptr, cur); tb::launched(); }
+    for (int it = 1; it < mg.nu; ++it) {
+      P->apply_alpha_epi(1, P->d_alpha, cur, oth, b, L.dinv, mg.omega, s);
+      std::swap(cur, oth);
+    }
+    P->apply_alpha_epi(2, P->d_alpha, cur, L.r, b, L.dinv, 0.0, s);
+    const MgLevel& C0 = mg.lv[1];
+    { k_mg_restrict<3><<<nblk(C0.g.n_nodes), kBlock, 0, s>>>(C0.g, L.g, L.r, C0.fixed, C0.b); tb::launched(); }
+    vcycle(P, 1, C0.b, C0.x, s);
+    { k_mg_prolong_add<3><<<nblk(L.g.n_nodes), kBlock, 0, s>>>(L.g, C0.g, C0.x, L.fixed, cur); tb::launched(); }
+    for (int it = 0; it < mg.nu; ++it) {
+      P->apply_alpha_epi(1, P->d_alpha, cur, oth, b, L.dinv, mg.omega, s);
+      std::swap(cur, oth);
+    }
+    return;  // cur == x
   }
   // pre-smoothing: nu damped-Jacobi sweeps from x = 0
   { k_mg_jacobi<<<nb, kBlock, 0, s>>>(L.n, mg.omega, L.dinv, b, nullptr, nullptr, x); tb::launched(); }

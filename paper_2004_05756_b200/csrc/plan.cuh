@@ -57,6 +57,7 @@ struct tb_plan_impl {
   Mat<24> K3{};
   Hex8Iso hiso{};        // WHT block values of K3 (3D)
   bool hex8 = false;     // K3 has the isotropic WHT block structure -> element-centric kernel
+  bool hex8_epi = false; // the epilogue instances of k_hex8 (multigrid level 0) are usable
   int zchunk = 8;
   int dist = 0;              // distributed (slab) pCG mode
   int precond = 0;           // 0 Jacobi, 1 geometric multigrid
@@ -80,6 +81,8 @@ struct tb_plan_impl {
   int init(const uint8_t* fixed_host);
   void release();
   void apply_alpha(const double* alpha, const double* v, double* y, bool mask, cudaStream_t s) const;
+  bool apply_alpha_epi(int epi, const double* alpha, const double* v, double* out, const double* b,
+                       const double* dinv, double omega, cudaStream_t s) const;
   int material(const double* rho, double* alpha, double* dalpha, cudaStream_t s) const;
   int rom_scratch(size_t bytes);
 };

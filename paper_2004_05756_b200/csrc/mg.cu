@@ -176,10 +176,14 @@ __global__ void __launch_bounds__(kBlock) k_mg_stencil(Grid g, const double* __r
   }
 }
 
-// y = A v on a coarse level from its half stencil (node-owner, fixed neighbour order)
-template <int D>
+// y = A v on a coarse level from its half stencil (node-owner, fixed neighbour order).
+// EPI 1: y = v + omega ed (eb - A v) (damped-Jacobi sweep), EPI 2: y = ed != 0 ? eb - A v : 0
+// (masked residual); y must not alias v.
+template <int D, int EPI = 0>
 __global__ void __launch_bounds__(kBlock) k_mg_sapply(Grid g, const double* __restrict__ st,
-                                                      const double* __restrict__ v, double* __restrict__ y) {
+                                                      const double* __restrict__ v, double* __restrict__ y,
+                                                      const double* __restrict__ eb = nullptr,
+                                                      const double* __restrict__ ed = nullptr, double omega = 0.0) {
   constexpr int NB = Q1<D>::NB, MC = NB / 2;
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= g.n_nodes) return;
@@ -214,7 +218,12 @@ __global__ void __launch_bounds__(kBlock) k_mg_sapply(Grid g, const double* __re
     }
   }
 #pragma unroll
-  for (int c = 0; c < D; ++c) y[n * D + c] = out[c];
+  for (int c = 0; c < D; ++c) {
+    double o = out[c];
+    if (EPI == 1) o = v[n * D + c] + omega * ed[n * D + c] * (eb[n * D + c] - o);
+    if (EPI == 2) o = (ed[n * D + c] != 0.0) ? eb[n * D + c] - o : 0.0;
+    y[n * D + c] = o;
+  }
 }
 
 template <int D>
@@ -939,22 +948,47 @@ static void vcycle(tb_plan_impl* P, size_t l, const double* b, double* x, cudaSt
   // operator kernel (k_hex8 EPI; TB_MG_NOFUSE=1 keeps the separate update kernels).  A sweep
   // cannot update in place (other CTAs read the halo of its input), so the iterate alternates
   // between L.t and x; it starts in L.t and, after (nu - 1) + nu sweeps, ends in x.
+  // The same on the coarse levels through the stencil kernel's epilogue (k_mg_sapply EPI).
   static const bool nofuse = getenv("TB_MG_NOFUSE") != nullptr;
-  if (l == 0 && P->hex8_epi && !nofuse) {
+  if ((l > 0 || P->hex8_epi) && !nofuse) {
+    // out = epilogue(A_l cur): epi 1 one smoothing sweep, epi 2 the masked residual
+    auto level_epi = [&](int epi, const double* cur, double* out) {
+      if (l == 0) {
+        P->apply_alpha_epi(epi, P->d_alpha, cur, out, b, L.dinv, mg.omega, s);
+        return;
+      }
+      const int blocks = nblk(L.g.n_nodes);
+      if (L.g.dim == 2) {
+        if (epi == 1) k_mg_sapply<2, 1><<<blocks, kBlock, 0, s>>>(L.g, L.st, cur, out, b, L.dinv, mg.omega);
+        else k_mg_sapply<2, 2><<<blocks, kBlock, 0, s>>>(L.g, L.st, cur, out, b, L.dinv, mg.omega);
+      } else {
+        if (epi == 1) k_mg_sapply<3, 1><<<blocks, kBlock, 0, s>>>(L.g, L.st, cur, out, b, L.dinv, mg.omega);
+        else k_mg_sapply<3, 2><<<blocks, kBlock, 0, s>>>(L.g, L.st, cur, out, b, L.dinv, mg.omega);
+      }
+      tb::launched();
+    };
     double* cur = L.t;
     double* oth = x;
     { k_mg_jacobi<<<nb, kBlock, 0, s>>>(L.n, mg.omega, L.dinv, b, nullptr, nullptr, cur); tb::launched(); }
     for (int it = 1; it < mg.nu; ++it) {
-      P->apply_alpha_epi(1, P->d_alpha, cur, oth, b, L.dinv, mg.omega, s);
+      level_epi(1, cur, oth);
       std::swap(cur, oth);
     }
-    P->apply_alpha_epi(2, P->d_alpha, cur, L.r, b, L.dinv, 0.0, s);
-    const MgLevel& C0 = mg.lv[1];
-    { k_mg_restrict<3><<<nblk(C0.g.n_nodes), kBlock, 0, s>>>(C0.g, L.g, L.r, C0.fixed, C0.b); tb::launched(); }
-    vcycle(P, 1, C0.b, C0.x, s);
-    { k_mg_prolong_add<3><<<nblk(L.g.n_nodes), kBlock, 0, s>>>(L.g, C0.g, C0.x, L.fixed, cur); tb::launched(); }
+    level_epi(2, cur, L.r);
+    const MgLevel& C0 = mg.lv[l + 1];
+    if (L.g.dim == 2) {
+      { k_mg_restrict<2><<<nblk(C0.g.n_nodes), kBlock, 0, s>>>(C0.g, L.g, L.r, C0.fixed, C0.b); tb::launched(); }
+    } else {
+      { k_mg_restrict<3><<<nblk(C0.g.n_nodes), kBlock, 0, s>>>(C0.g, L.g, L.r, C0.fixed, C0.b); tb::launched(); }
+    }
+    vcycle(P, l + 1, C0.b, C0.x, s);
+    if (L.g.dim == 2) {
+      { k_mg_prolong_add<2><<<nblk(L.g.n_nodes), kBlock, 0, s>>>(L.g, C0.g, C0.x, L.fixed, cur); tb::launched(); }
+    } else {
+      { k_mg_prolong_add<3><<<nblk(L.g.n_nodes), kBlock, 0, s>>>(L.g, C0.g, C0.x, L.fixed, cur); tb::launched(); }
+    }
     for (int it = 0; it < mg.nu; ++it) {
-      P->apply_alpha_epi(1, P->d_alpha, cur, oth, b, L.dinv, mg.omega, s);
+      level_epi(1, cur, oth);
       std::swap(cur, oth);
     }
     return;  // cur == x

@@ -209,3 +209,41 @@ def test_mg_elongated_grid_vs_oracle(cuda):
     s = build(prob, "mg", rtol=1e-10)
     with pytest.raises(tb.NotConvergedError):
         s.solve(prob.psi, tb.ComplianceObjective(s.f))
+
+
+_NOFUSE_SCRIPT = """
+import sys, json
+import numpy as np
+import paper_2004_05756_b200 as tb
+from paper_2004_05756_b200 import configs
+prob = configs.cfg3(seed=4, nx=24, ny=12, nz=12)
+s = tb.HdmSolver(prob.mesh, prob.k_e, tb.HelmholtzFilter(prob.mesh, prob.radius), prob.f, prob.fixed,
+                 tb.MaterialModel(rho_l=configs.RHO_L, p=configs.P_SIMP), rtol=1e-10, preconditioner="mg")
+sol = s.solve(prob.psi, tb.ComplianceObjective(s.f))
+np.save(sys.argv[1], sol.u)
+print(json.dumps({"j": sol.j, "iterations": sol.iterations}))
+"""
+
+
+def test_mg_3d_fused_epilogues_match_separate_kernels(cuda, tmp_path):
+    """The V-cycle with the smoothing sweeps and residuals as operator-kernel epilogues (k_hex8
+    EPI, k_mg_sapply EPI) against the separate update kernels (TB_MG_NOFUSE=1, read once per
+    process: run in a child process): the same preconditioner up to rounding, so the same
+    iteration count and solution."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for label, env in (("fused", {}), ("separate", {"TB_MG_NOFUSE": "1"})):
+        path = str(tmp_path / f"u_{label}.npy")
+        r = subprocess.run([sys.executable, "-c", _NOFUSE_SCRIPT, path], cwd=repo, capture_output=True, text=True,
+                           env={**os.environ, **env, "PYTHONPATH": repo}, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[label] = (json.loads(r.stdout.strip().splitlines()[-1]), np.load(path))
+    a, b = out["fused"], out["separate"]
+    assert abs(a[0]["iterations"] - b[0]["iterations"]) <= 1
+    assert abs(a[0]["j"] - b[0]["j"]) <= 1e-9 * abs(b[0]["j"])
+    assert nrel(a[1], b[1]) <= 1e-7

@@ -19,6 +19,10 @@ static inline int nblk(int64_t n) { return (int)((n + kBlock - 1) / kBlock); }
 // ---------------------------------------------------------------------------------------
 constexpr int kMaxVec = 16;
 
+// NV >= nvec is the compile-time vector count (1, 2, 4, 8 or 16): with the loop over kMaxVec
+// predicated at run time a single vector cost ~190 instructions per row and warp (issue-bound,
+// 0.55 TB/s at cfg 5 size).  4 rows of Phi in flight per thread.
+template <int NV>
 __global__ void __launch_bounds__(kBlock) k_project_part(int64_t n, int k, const double* __restrict__ phi,
                                                          const double* __restrict__ vec, int nvec,
                                                          double* __restrict__ part) {
@@ -27,17 +31,31 @@ __global__ void __launch_bounds__(kBlock) k_project_part(int64_t n, int k, const
   const int t = threadIdx.x, j = t % k, rg = t / k;
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t i0 = (int64_t)blockIdx.x * per, i1 = min(n, i0 + per);
-  double acc[kMaxVec];
+  double acc[NV];
 #pragma unroll
-  for (int d = 0; d < kMaxVec; ++d) acc[d] = 0.0;
+  for (int d = 0; d < NV; ++d) acc[d] = 0.0;
   if (rg < groups) {
-    for (int64_t i = i0 + rg; i < i1; i += groups) {
+    constexpr int U = 4;
+    int64_t i = i0 + rg;
+    for (; i + (int64_t)(U - 1) * groups < i1; i += (int64_t)U * groups) {
+      double pv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) pv[u] = __ldg(phi + (i + (int64_t)u * groups) * k + j);
+#pragma unroll
+      for (int u = 0; u < U; ++u)  // rows in increasing order, as the rolled loop
+#pragma unroll
+        for (int d = 0; d < NV; ++d)
+          if (NV == 1 || d < nvec) acc[d] = fma(pv[u], __ldg(vec + (int64_t)d * n + i + (int64_t)u * groups), acc[d]);
+    }
+    for (; i < i1; i += groups) {
       const double pv = phi[i * k + j];
 #pragma unroll
-      for (int d = 0; d < kMaxVec; ++d)
-        if (d < nvec) acc[d] = fma(pv, __ldg(vec + (int64_t)d * n + i), acc[d]);
+      for (int d = 0; d < NV; ++d)
+        if (NV == 1 || d < nvec) acc[d] = fma(pv, __ldg(vec + (int64_t)d * n + i), acc[d]);
     }
-    for (int d = 0; d < nvec; ++d) sh[(rg * nvec + d) * k + j] = acc[d];
+#pragma unroll
+    for (int d = 0; d < NV; ++d)
+      if (d < nvec) sh[(rg * nvec + d) * k + j] = acc[d];
   }
   __syncthreads();
   for (int o = t; o < nvec * k; o += blockDim.x) {
@@ -454,20 +472,33 @@ __global__ void __launch_bounds__(kBlock) k_reconstruct_dmma(int64_t n, int k, c
       const int d = 8 * t + (lane >> 2), j = 4 * st + (lane & 3);
       b[t][st] = (d < nd && j < k) ? uhat[(int64_t)d * k + j] : 0.0;
     }
-  const int nsteps = (k + 3) / 4;
-  for (int64_t i0 = warp * 8; i0 < n; i0 += nwarps * 8) {
+  // the A fragments of the next 8 rows are loaded (all 16 k-steps, unconditionally issued) before
+  // the DMMA chain of the current ones: ncu of the load-then-use loop showed 4 warps per
+  // scheduler stalled 22 cycles per issue on the long scoreboard (2.25 TB/s at cfg 5 size; now
+  // 4.5 TB/s)
+  auto load_tile = [&](int64_t i0, double (&a)[kSteps]) {
     const int64_t row = i0 + (lane >> 2);
     const double* pr = phi + row * k;
+#pragma unroll
+    for (int st = 0; st < kSteps; ++st) {
+      const int j = 4 * st + (lane & 3);
+      a[st] = (row < n && j < k) ? __ldg(pr + j) : 0.0;
+    }
+  };
+  double a[kSteps];
+  if (warp * 8 < n) load_tile(warp * 8, a);
+  for (int64_t i0 = warp * 8; i0 < n; i0 += nwarps * 8) {
+    double an[kSteps];
+    const int64_t inext = i0 + nwarps * 8;
+    if (inext < n) load_tile(inext, an);
     double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
     for (int st = 0; st < kSteps; ++st) {
-      if (st < nsteps) {
-        const int j = 4 * st + (lane & 3);
-        const double a = (row < n && j < k) ? __ldg(pr + j) : 0.0;
-        dmma_8x8x4(acc[0], a, b[0][st]);
-        dmma_8x8x4(acc[1], a, b[1][st]);
-      }
+      dmma_8x8x4(acc[0], a[st], b[0][st]);
+      dmma_8x8x4(acc[1], a[st], b[1][st]);
     }
+#pragma unroll
+    for (int st = 0; st < kSteps; ++st) a[st] = an[st];
     // thread holds U^T[row i0 + lane/4][design 8t + 2(lane%4) + h]
     const int64_t ri = i0 + (lane >> 2);
     if (ri < n) {
@@ -516,14 +547,21 @@ int tb_rom_project(int64_t n, const double* phi, int k, const double* vec, int n
   TB_GUARD(k >= 1 && k <= kBlock, "basis size k=%d out of range [1, %d]", k, kBlock);
   TB_GUARD(nvec >= 1, "nvec=%d must be >= 1", nvec);
   cudaStream_t s = (cudaStream_t)stream;
-  const int nb = 148 * 2;
+  const int nb = n >= (int64_t)1 << 20 ? 148 * 8 : 148 * 2;  // large bases: every resident CTA slot streams
   double* part = nullptr;
   const int nv0 = nvec < kMaxVec ? nvec : kMaxVec;
   TB_CUDA(cudaMallocAsync(&part, sizeof(double) * (size_t)nb * nv0 * k, s));
   const int groups = kBlock / k;
   for (int v0 = 0; v0 < nvec; v0 += kMaxVec) {  // kMaxVec vectors per pass over Phi
     const int nv = nvec - v0 < kMaxVec ? nvec - v0 : kMaxVec;
-    { k_project_part<<<nb, kBlock, sizeof(double) * groups * nv * k, s>>>(n, k, phi, vec + (int64_t)v0 * n, nv, part); tb::launched(); }
+    const size_t sm = sizeof(double) * groups * nv * k;
+    const double* v = vec + (int64_t)v0 * n;
+    if (nv == 1) k_project_part<1><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
+    else if (nv == 2) k_project_part<2><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
+    else if (nv <= 4) k_project_part<4><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
+    else if (nv <= 8) k_project_part<8><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
+    else k_project_part<16><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
+    tb::launched();
     { k_sum_parts<<<nblk(nv * k), kBlock, 0, s>>>(nb, nv * k, part, out + (int64_t)v0 * k); tb::launched(); }
   }
   TB_CHECK_LAUNCH();

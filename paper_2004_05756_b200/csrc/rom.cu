@@ -65,6 +65,73 @@ __global__ void __launch_bounds__(kBlock) k_project_part(int64_t n, int k, const
   }
 }
 
+// Several vectors: the NV values of a row are needed by every column thread, so a chunk of kPtR
+// rows of the vectors is staged in shared memory (coalesced loads, transposed to [row][NV]) and
+// read back as broadcast 16-byte loads; the per-thread global loads of the kernel above (NV per
+// row and thread, the same address in all lanes) ran 16 vectors at 0.6 TB/s at cfg 5 size.
+// Same partition and the same row order per thread as k_project_part: bitwise the same sums.
+constexpr int kPtR = 64;
+template <int NV>
+__global__ void __launch_bounds__(kBlock) k_project_tile(int64_t n, int k, const double* __restrict__ phi,
+                                                         const double* __restrict__ vec, int nvec,
+                                                         double* __restrict__ part) {
+  extern __shared__ double sh[];  // [groups][nvec][k] for the final reduction
+  __shared__ __align__(16) double vt[kPtR * NV];
+  const int groups = kBlock / k;
+  const int t = threadIdx.x, j = t % k, rg = t / k;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * per, i1 = min(n, i0 + per);
+  double acc[NV];
+#pragma unroll
+  for (int d = 0; d < NV; ++d) acc[d] = 0.0;
+  // chunks start at multiples of `groups` rows from i0, so thread rg keeps rows i0 + rg + m groups
+  const int rows_per = kPtR / groups * groups;  // >= groups: the host launches this kernel for groups <= kPtR only
+  for (int64_t base = i0; base < i1; base += rows_per) {
+    const int rows = (int)min((int64_t)rows_per, i1 - base);
+    __syncthreads();  // the previous chunk's tile has been read
+    for (int idx = t; idx < NV * rows_per; idx += kBlock) {
+      const int d = idx / rows_per, r = idx - d * rows_per;
+      vt[r * NV + d] = (d < nvec && r < rows) ? __ldg(vec + (int64_t)d * n + base + r) : 0.0;
+    }
+    __syncthreads();
+    if (rg < groups) {
+      constexpr int U = 4;
+      int r = rg;
+      for (; r + (U - 1) * groups < rows; r += U * groups) {
+        double pv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) pv[u] = __ldg(phi + (base + r + u * groups) * k + j);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const double2* vr = reinterpret_cast<const double2*>(vt + (r + u * groups) * NV);
+#pragma unroll
+          for (int d2 = 0; d2 < NV / 2; ++d2) {
+            const double2 v = vr[d2];
+            acc[2 * d2] = fma(pv[u], v.x, acc[2 * d2]);
+            acc[2 * d2 + 1] = fma(pv[u], v.y, acc[2 * d2 + 1]);
+          }
+        }
+      }
+      for (; r < rows; r += groups) {
+        const double pv = __ldg(phi + (base + r) * k + j);
+#pragma unroll
+        for (int d = 0; d < NV; ++d) acc[d] = fma(pv, vt[r * NV + d], acc[d]);
+      }
+    }
+  }
+  if (rg < groups) {
+#pragma unroll
+    for (int d = 0; d < NV; ++d)
+      if (d < nvec) sh[(rg * nvec + d) * k + j] = acc[d];
+  }
+  __syncthreads();
+  for (int o = t; o < nvec * k; o += blockDim.x) {
+    double s = 0.0;
+    for (int g = 0; g < groups; ++g) s += sh[g * nvec * k + o];
+    part[(int64_t)blockIdx.x * nvec * k + o] = s;
+  }
+}
+
 // out[o] = sum_b part[b][o]  (fixed order), o < len
 __global__ void k_sum_parts(int nb, int len, const double* __restrict__ part, double* __restrict__ out) {
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
@@ -557,10 +624,16 @@ int tb_rom_project(int64_t n, const double* phi, int k, const double* vec, int n
     const size_t sm = sizeof(double) * groups * nv * k;
     const double* v = vec + (int64_t)v0 * n;
     if (nv == 1) k_project_part<1><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
-    else if (nv == 2) k_project_part<2><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
-    else if (nv <= 4) k_project_part<4><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
-    else if (nv <= 8) k_project_part<8><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
-    else k_project_part<16><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
+    else if (groups > kPtR) {  // k < 4: a row chunk of the tile kernel would be empty
+      if (nv == 2) k_project_part<2><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
+      else if (nv <= 4) k_project_part<4><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
+      else if (nv <= 8) k_project_part<8><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
+      else k_project_part<16><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
+    }
+    else if (nv == 2) k_project_tile<2><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
+    else if (nv <= 4) k_project_tile<4><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
+    else if (nv <= 8) k_project_tile<8><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
+    else k_project_tile<16><<<nb, kBlock, sm, s>>>(n, k, phi, v, nv, part);
     tb::launched();
     { k_sum_parts<<<nblk(nv * k), kBlock, 0, s>>>(nb, nv * k, part, out + (int64_t)v0 * k); tb::launched(); }
   }

@@ -230,3 +230,34 @@ def test_certified_lanczos_matches_power_iteration(cuda):
     with pytest.raises(ValueError):
         rom.error_bounds(basis, rho, rs, obj, mode="certified", method="qr")
     del n0
+
+
+@pytest.mark.parametrize("k,nvec", [(1, 1), (2, 3), (3, 16), (10, 5), (33, 2), (64, 16), (64, 20), (100, 4)])
+def test_project_and_reconstruct_kernels_vs_numpy(cuda, k, nvec):
+    """tb_rom_project (Phi^T V: single-vector, shared-memory tiled and tiny-k kernels) and
+    tb_rom_reconstruct (Phi Uhat: DMMA kernel for k <= 64) against numpy on a ragged size."""
+    import ctypes
+
+    import torch
+
+    from paper_2004_05756_b200 import _lib
+
+    dev = torch.device("cuda", 0)
+    n = 40037
+    rng = np.random.default_rng(k * 100 + nvec)
+    phi = rng.standard_normal((n, k))
+    vec = rng.standard_normal((nvec, n))
+    phi_d, vec_d = torch.as_tensor(phi, device=dev), torch.as_tensor(vec, device=dev)
+    out = torch.empty(nvec, k, dtype=torch.float64, device=dev)
+    lib = _lib.lib()
+    _lib.check(lib.tb_rom_project(ctypes.c_int64(n), _lib.ptr(phi_d), k, _lib.ptr(vec_d), nvec, _lib.ptr(out),
+                                  _lib.stream_ptr(dev)), "project")
+    ref = vec @ phi
+    assert np.abs(out.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+    nd = min(nvec, 16)
+    uhat = rng.standard_normal((nd, k))
+    u = torch.empty(nd, n, dtype=torch.float64, device=dev)
+    _lib.check(lib.tb_rom_reconstruct(ctypes.c_int64(n), _lib.ptr(phi_d), k, _lib.ptr(torch.as_tensor(uhat, device=dev)),
+                                      nd, _lib.ptr(u), _lib.stream_ptr(dev)), "reconstruct")
+    ref_u = uhat @ phi.T
+    assert np.abs(u.cpu().numpy() - ref_u).max() <= 1e-12 * np.abs(ref_u).max()

@@ -802,8 +802,7 @@ def run_ours(args):
                        "l2": ("256 MiB buffer written between steps (outside the step events); the cfg3 working set "
                               "(~350 MB of pCG vectors) also exceeds the 126 MB L2") if flush is not None else "no flush",
                        "pcg_iterations": its, "seed": args.seed,
-                       "filter_solver": ("direct (tensor-product cosine basis, DMMA mode products; spectral.cu)"
-                                         if prob.mesh.dim == 3 else "persistent pCG (2D)")},
+                       "filter_solver": "direct (tensor-product cosine basis, DMMA mode products; spectral.cu)"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk, "apply": apply, "extra": extras,
         }

@@ -13,7 +13,7 @@
 // mode products back.  The mode products are dense FP64 contractions (2 n flops per entry and
 // axis: 2.8 GFLOP per solve at cfg 3) and run on the FP64 tensor cores (DMMA m8n8k4); the result
 // is the solution to round-off, as the reference's sparse direct solve, where pCG stopped at
-// its tolerance.  cfg 3: 1.54 ms per filter solve by pCG.
+// its tolerance.  cfg 3: 1.54 -> 0.27 ms per filter call, cfg 2: 0.18 -> 0.08 ms.
 //
 // tb_filter_create verifies the factorisation against the filter's own operator kernel on a
 // random vector (||H phi - b|| <= 1e-11 ||b||) and keeps pCG otherwise.
@@ -40,17 +40,27 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 // C_b(m, n) = sum_k A_b(m, k) B_b(k, n) for b < gridDim.z: A(m, k) at A + b a_sb + m a_sm + k a_sk
 // (A_MC: a_sm == 1, else a_sk == 1), B(k, n) at B + b b_sb + k b_sk + n, C(m, n) at
 // C + b c_sb + m c_sm + n.  256 threads: warp (wm, wn) of 4 x 2 owns a 16 x 32 block of the tile.
+// ksplit > 0 (2D grids: too few output tiles to fill the GPU and a long serial K loop): blockIdx.z
+// is not a batch index but a slice [z ksplit, (z + 1) ksplit) of K, and slice z writes its partial
+// product to C + z c_sb; k_spec_sum adds the slices in fixed order.
 template <bool A_MC>
 __global__ void __launch_bounds__(256) k_spec_gemm(int M, int N, int K, const double* __restrict__ A, int64_t a_sm,
                                                    int64_t a_sk, int64_t a_sb, const double* __restrict__ B, int64_t b_sk,
-                                                   int64_t b_sb, double* __restrict__ C, int64_t c_sm, int64_t c_sb) {
+                                                   int64_t b_sb, double* __restrict__ C, int64_t c_sm, int64_t c_sb,
+                                                   int ksplit) {
   __shared__ double As[kSgK][kSgLd];  // [k][m]
   __shared__ double Bs[kSgK][kSgLd];  // [k][n]
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int wm = w & 3, wn = w >> 2;
   const int m0 = blockIdx.y * kSgT, n0 = blockIdx.x * kSgT;
-  A += (int64_t)blockIdx.z * a_sb;
-  B += (int64_t)blockIdx.z * b_sb;
+  int kbeg = 0;
+  if (ksplit > 0) {
+    kbeg = (int)blockIdx.z * ksplit;
+    K = min(K, kbeg + ksplit);
+  } else {
+    A += (int64_t)blockIdx.z * a_sb;
+    B += (int64_t)blockIdx.z * b_sb;
+  }
   C += (int64_t)blockIdx.z * c_sb;
   double acc[2][4][2];
 #pragma unroll
@@ -58,7 +68,7 @@ __global__ void __launch_bounds__(256) k_spec_gemm(int M, int N, int K, const do
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   const int g4 = lane >> 2, l4 = lane & 3;
-  for (int k0 = 0; k0 < K; k0 += kSgK) {
+  for (int k0 = kbeg; k0 < K; k0 += kSgK) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       int m, k;
@@ -120,6 +130,16 @@ __global__ void __launch_bounds__(kBlock) k_spec_scale(int nnx, int nny, int nnz
   }
 }
 
+// out = sum over the K slices of a split mode product, in slice order
+__global__ void __launch_bounds__(kBlock) k_spec_sum(int64_t n, int ns, const double* __restrict__ part,
+                                                    double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = part[i];
+    for (int z = 1; z < ns; ++z) s += part[(int64_t)z * n + i];
+    out[i] = s;
+  }
+}
+
 __global__ void __launch_bounds__(kBlock) k_spec_resid(int64_t n, const double* __restrict__ y,
                                                       const double* __restrict__ b, double* __restrict__ part) {
   double acc[2] = {0.0, 0.0};
@@ -161,7 +181,10 @@ struct SpectralFilter {
   double* d_Vt[3] = {nullptr, nullptr, nullptr};  // V^T
   double* d_ev = nullptr;                         // [mu_x | m_x | mu_y | m_y | mu_z | m_z]
   double* d_t[2] = {nullptr, nullptr};            // ping-pong scratch (n_nodes each)
+  double* d_part = nullptr;                       // 2D: K-slice partial products (kSgSplit x n_nodes)
 };
+
+constexpr int kSgSplit = 8;
 
 void spectral_release(tb_filter_impl* F) {
   SpectralFilter* S = F->spec;
@@ -173,22 +196,37 @@ void spectral_release(tb_filter_impl* F) {
   if (S->d_ev) cudaFree(S->d_ev);
   for (auto* p : S->d_t)
     if (p) cudaFree(p);
+  if (S->d_part) cudaFree(S->d_part);
   delete S;
   F->spec = nullptr;
 }
 
-// Y(o, a, q) = sum_i Q[i][a] X(o, i, q) over the array viewed as [outer][n][inner]
+// Y(o, a, q) = sum_i Q[i][a] X(o, i, q) over the array viewed as [outer][n][inner].  part != null
+// (2D, outer or inner == 1 with a single batch): K split into slices, partials in `part`, summed into Y.
 static void mode_product(int64_t outer, int n, int64_t inner, const double* Q, const double* X, double* Y,
-                         cudaStream_t s) {
+                         double* part, cudaStream_t s) {
+  const int64_t total = outer * n * inner;
+  int ksplit = 0, ns = 1;
+  if (part != nullptr && (inner == 1 || outer == 1)) {
+    ksplit = ((n + kSgSplit - 1) / kSgSplit + kSgK - 1) / kSgK * kSgK;
+    ns = (n + ksplit - 1) / ksplit;
+    if (ns < 2) ksplit = 0, ns = 1;
+  }
+  double* C = ksplit ? part : Y;
   if (inner == 1) {  // x axis: Y (outer x n) = X (outer x n) Q
-    dim3 grid((unsigned)((n + kSgT - 1) / kSgT), (unsigned)((outer + kSgT - 1) / kSgT), 1);
-    k_spec_gemm<false><<<grid, 256, 0, s>>>((int)outer, n, n, X, n, 1, 0, Q, n, 0, Y, n, 0);
+    dim3 grid((unsigned)((n + kSgT - 1) / kSgT), (unsigned)((outer + kSgT - 1) / kSgT), (unsigned)ns);
+    k_spec_gemm<false><<<grid, 256, 0, s>>>((int)outer, n, n, X, n, 1, 0, Q, n, 0, C, n, ksplit ? total : 0, ksplit);
   } else {  // Y_o (n x inner) = Q^T X_o
-    dim3 grid((unsigned)((inner + kSgT - 1) / kSgT), (unsigned)((n + kSgT - 1) / kSgT), (unsigned)outer);
-    k_spec_gemm<true><<<grid, 256, 0, s>>>(n, (int)inner, n, Q, 1, n, 0, X, inner, (int64_t)n * inner, Y, inner,
-                                           (int64_t)n * inner);
+    dim3 grid((unsigned)((inner + kSgT - 1) / kSgT), (unsigned)((n + kSgT - 1) / kSgT),
+              (unsigned)(ksplit ? ns : outer));
+    k_spec_gemm<true><<<grid, 256, 0, s>>>(n, (int)inner, n, Q, 1, n, 0, X, inner, (int64_t)n * inner, C, inner,
+                                           ksplit ? total : (int64_t)n * inner, ksplit);
   }
   launched();
+  if (ksplit) {
+    k_spec_sum<<<grid_for(total), kBlock, 0, s>>>(total, ns, part, Y);
+    launched();
+  }
 }
 
 // phi = H^-1 b (b and phi may not alias the scratch; b == phi is allowed)
@@ -197,25 +235,26 @@ int spectral_solve(tb_filter_impl* F, const double* b, double* phi, cudaStream_t
   const Grid& g = F->g;
   const int nx = g.nnx, ny = g.nny, nz = g.nnz;
   double *t0 = S.d_t[0], *t1 = S.d_t[1];
-  mode_product((int64_t)nz * ny, nx, 1, S.d_V[0], b, t0, s);
-  mode_product(nz, ny, nx, S.d_V[1], t0, t1, s);
+  double* part = S.d_part;  // null in 3D
+  mode_product((int64_t)nz * ny, nx, 1, S.d_V[0], b, t0, part, s);
+  mode_product(nz, ny, nx, S.d_V[1], t0, t1, part, s);
   double* cur = t1;
   double* oth = t0;
   if (g.dim == 3) {
-    mode_product(1, nz, (int64_t)ny * nx, S.d_V[2], t1, t0, s);
+    mode_product(1, nz, (int64_t)ny * nx, S.d_V[2], t1, t0, nullptr, s);
     cur = t0;
     oth = t1;
   }
   k_spec_scale<<<grid_for(g.n_nodes), kBlock, 0, s>>>(nx, ny, nz, F->r * F->r, S.d_ev, cur);
   launched();
   if (g.dim == 3) {
-    mode_product(1, nz, (int64_t)ny * nx, S.d_Vt[2], cur, oth, s);
+    mode_product(1, nz, (int64_t)ny * nx, S.d_Vt[2], cur, oth, nullptr, s);
     double* tmp = cur;
     cur = oth;
     oth = tmp;
   }
-  mode_product(nz, ny, nx, S.d_Vt[1], cur, oth, s);
-  mode_product((int64_t)nz * ny, nx, 1, S.d_Vt[0], oth, phi, s);
+  mode_product(nz, ny, nx, S.d_Vt[1], cur, oth, part, s);
+  mode_product((int64_t)nz * ny, nx, 1, S.d_Vt[0], oth, phi, part, s);
   TB_CHECK_LAUNCH();
   return TB_OK;
 }
@@ -226,10 +265,9 @@ void spectral_init(tb_filter_impl* F) {
   const char* e = getenv("TB_FILTER_PCG");
   if (e != nullptr && e[0] != '\0' && e[0] != '0') return;
   const Grid& g = F->g;
-  // 2D keeps the persistent pCG kernel: at cfg 2 (601 x 201 nodes) the mode products fill only
-  // 40 CTAs and the direct solve measured no faster (0.176 against 0.173 ms per filter call);
-  // TB_FILTER_SPECTRAL_2D=1 enables it there as well (same code, nnz = 1)
-  if (g.dim == 2 && getenv("TB_FILTER_SPECTRAL_2D") == nullptr) return;
+  // 2D as well (same code, nnz = 1): the mode products there have too few output tiles to fill the
+  // GPU, so K is split into up to 8 slices summed in fixed order (cfg 2: 0.18 -> 0.08 ms per filter
+  // call against the persistent pCG kernel; without the split the direct solve was no faster)
   auto* S = new SpectralFilter();
   F->spec = S;
   const int n[3] = {g.nnx, g.nny, g.dim == 3 ? g.nnz : 1};
@@ -256,7 +294,8 @@ void spectral_init(tb_filter_impl* F) {
   const size_t nb = sizeof(double) * (size_t)g.n_nodes;
   ok = ok && cudaMalloc(&S->d_ev, sizeof(double) * ev.size()) == cudaSuccess &&
        cudaMemcpy(S->d_ev, ev.data(), sizeof(double) * ev.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
-       cudaMalloc(&S->d_t[0], nb) == cudaSuccess && cudaMalloc(&S->d_t[1], nb) == cudaSuccess;
+       cudaMalloc(&S->d_t[0], nb) == cudaSuccess && cudaMalloc(&S->d_t[1], nb) == cudaSuccess &&
+       (g.dim == 3 || cudaMalloc(&S->d_part, nb * kSgSplit) == cudaSuccess);
   // self-check: b = pseudo-random, phi = solve(b), ||H phi - b|| / ||b||
   double rel = 1.0;
   if (ok) {

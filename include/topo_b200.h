@@ -170,7 +170,10 @@ int tb_filter_destroy(tb_filter* filt);
 /* b(psi) = (h^d/2^d) sum_{e∋n} psi_e  (filtering.py:73-76) */
 int tb_filter_load_vector(tb_filter* filt, const double* psi, double* b, void* stream);
 /* phi = H^-1 b(psi); rho_e = mean of phi over the element nodes (filtering.py:78-97);
- * phi may be NULL.  *iters HOST (may be NULL). */
+ * phi may be NULL.  *iters HOST (may be NULL).  A whole-grid filter solves H phi = b DIRECTLY in
+ * the tensor-product cosine basis of the uniform grid (csrc/spectral.cu: the solution to round-off,
+ * as the reference's sparse direct solve; rtol is not used and *iters = 0); the pCG path with the
+ * rtol convention of tb_pcg_solve remains for slab phases and under TB_FILTER_PCG=1. */
 int tb_filter_apply(tb_filter* filt, const double* psi, double* phi, double* rho, double rtol,
                     int* iters, void* stream);
 /* w = (h^d/2^d) Q^T H^-1 Q (v/2^d): exact transpose of psi->rho (filtering.py:99-114) */
